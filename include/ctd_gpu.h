@@ -1,0 +1,186 @@
+/* ctd_gpu.h — C-ABI of the B200-native CTD-S / CTD-D hot path.
+ *
+ * Drop-in boundary for the reference's proj/core C++ entry points (paths
+ * relative to /root/reference/proj/core).  Each function below names the
+ * reference interface it replaces.  Plain pointers and sizes only: no CUDA,
+ * torch or C++ types cross this boundary (a cudaStream_t travels as void*).
+ *
+ * Status codes: 0 = ok, otherwise the reference ErrorClass value
+ * (include/ctd/error.hpp:11-19) of the exception the reference would throw,
+ * or CTD_ERR_DEVICE / CTD_ERR_NUMERIC for failures the CPU code cannot have.
+ * ctd_gpu_last_error() returns the message of the last failure on the
+ * calling thread.
+ *
+ * Threading: calls on one context are not
+ * re-entrant; independent contexts may run concurrently on separate streams.
+ * Results are deterministic: identical inputs give bit-identical kept fibers,
+ * U and sampled ids on every run and every GPU count.
+ */
+#ifndef CTD_GPU_H
+#define CTD_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum ctd_gpu_status {
+  CTD_OK = 0,
+  CTD_ERR_ARGUMENT = 1,    /* ArgumentError   error.hpp:32-35 */
+  CTD_ERR_SHAPE = 2,       /* ShapeError      error.hpp:37-40 */
+  CTD_ERR_EMPTY_INPUT = 3, /* EmptyInputError error.hpp:42-45 */
+  CTD_ERR_PARSE = 4,       /* ParseError (unused on this path) */
+  CTD_ERR_METRIC = 5,      /* MetricError     error.hpp:61-64 */
+  CTD_ERR_ORACLE = 6,      /* OracleError (unused on this path) */
+  CTD_ERR_IO = 7,          /* IoError (unused on this path) */
+  CTD_ERR_DEVICE = 8,      /* CUDA / NCCL failure, out of device memory */
+  CTD_ERR_NUMERIC = 9      /* internal exact-arithmetic self-check failed */
+};
+
+/* ctd_s flags */
+#define CTD_GPU_WITH_ERROR 0x1u /* also run the relative-error pass (evaluation.cpp:88-122) */
+#define CTD_GPU_WITH_CORE 0x2u  /* also materialize C = X x_mode R^T (ctd_static.cpp:12-17) */
+
+typedef struct ctd_gpu_ctx ctd_gpu_ctx;         /* device, stream, scratch pool */
+typedef struct ctd_gpu_tensor ctd_gpu_tensor;   /* SparseTensor (sparse_tensor.hpp:17-60) resident in HBM */
+typedef struct ctd_gpu_factors ctd_gpu_factors; /* LRFactors (factors.hpp:32-47) + run trace */
+typedef struct ctd_gpu_basis ctd_gpu_basis;     /* FiberBasis (fiber_basis.hpp:21-61) */
+typedef struct ctd_gpu_stream ctd_gpu_stream;   /* StreamState (ctd_dynamic.hpp:18-39) */
+
+const char *ctd_gpu_last_error(void);
+const char *ctd_gpu_version(void);
+
+/* ---- context ------------------------------------------------------------ */
+/* stream: a cudaStream_t (NULL = legacy default stream).  All work of the
+ * context is ordered on that stream. */
+int ctd_gpu_ctx_create(int device, void *stream, ctd_gpu_ctx **out);
+int ctd_gpu_ctx_set_stream(ctd_gpu_ctx *ctx, void *stream);
+int ctd_gpu_ctx_synchronize(ctd_gpu_ctx *ctx);
+int ctd_gpu_ctx_destroy(ctd_gpu_ctx *ctx);
+/* Launch counter of this library's kernels on the context (for bench.py). */
+int64_t ctd_gpu_ctx_launches(const ctd_gpu_ctx *ctx);
+
+/* ---- tensors (SparseTensor, sparse_tensor.hpp:27-28) --------------------- */
+/* Host COO exactly as SparseTensor::indices()/values() hold it: nnz*order
+ * int64 coordinates row-concatenated, lexicographically sorted and coalesced
+ * (a normalized SparseTensor).  Copied host->device and narrowed to int32 on
+ * the device after a range check (ShapeError if any extent >= 2^31). */
+int ctd_gpu_tensor_from_host(ctd_gpu_ctx *ctx, int order, const int64_t *shape,
+                             int64_t nnz, const int64_t *indices,
+                             const double *values, ctd_gpu_tensor **out);
+/* Device-resident COO, structure of arrays: mode_indices[k] is a device
+ * pointer to nnz int32 coordinates of mode k; values a device pointer to nnz
+ * doubles.  The pointers are borrowed (not copied, not freed). */
+int ctd_gpu_tensor_from_device(ctd_gpu_ctx *ctx, int order, const int64_t *shape,
+                               int64_t nnz, const int32_t *const *mode_indices,
+                               const double *values, ctd_gpu_tensor **out);
+int64_t ctd_gpu_tensor_nnz(const ctd_gpu_tensor *t);
+int ctd_gpu_tensor_destroy(ctd_gpu_tensor *t);
+
+/* ---- tensor_ops / sampling pieces (parity surface) ---------------------- */
+/* matricize + column_sq_norms (tensor_ops.hpp:21,39; tensor_ops.cpp:118-135,
+ * 194-202).  Writes the mode-`mode` matricization in *compressed* CSC form:
+ * only the nonempty fibers.  n_fibers receives F; fiber_col[F] the column
+ * ids j, fiber_ptr[F+1] the offsets, rows[nnz]/vals[nnz] the entries in
+ * (column,row) order, sq_norms[F] the exact squared norms.  Any output
+ * pointer may be NULL; sizes: F <= nnz. */
+int ctd_gpu_matricize(ctd_gpu_ctx *ctx, const ctd_gpu_tensor *x, int mode,
+                      int64_t *n_fibers, int64_t *fiber_col, int64_t *fiber_ptr,
+                      int32_t *rows, double *vals, double *sq_norms);
+/* column_distribution (sampling.hpp:20, sampling.cpp:21-31) restricted to
+ * the nonempty fibers (every other column has probability exactly 0), and
+ * the clamped cumulative array sample_with_replacement builds
+ * (sampling.cpp:42-54), both bit-exact.  probs/cumulative have F entries. */
+int ctd_gpu_column_distribution(ctd_gpu_ctx *ctx, const ctd_gpu_tensor *x,
+                                int mode, double *total_sq_norm, double *probs,
+                                double *cumulative);
+/* sample_with_replacement (sampling.hpp:27-28) over a host probability
+ * vector of n columns (zero entries allowed). */
+int ctd_gpu_sample_with_replacement(ctd_gpu_ctx *ctx, const double *probs,
+                                    int64_t n, int64_t count, uint64_t seed,
+                                    int64_t *out);
+/* unique_first_occurrence (sampling.hpp:31). */
+int ctd_gpu_unique_first_occurrence(ctd_gpu_ctx *ctx, const int64_t *drawn,
+                                    int64_t n, int64_t *out, int64_t *n_out);
+
+/* ---- CTD-S (ctd_static.hpp:22-24) --------------------------------------- */
+int ctd_gpu_ctd_s(ctd_gpu_ctx *ctx, const ctd_gpu_tensor *x, int mode,
+                  int64_t sample_size, double epsilon, uint64_t seed,
+                  unsigned flags, ctd_gpu_factors **out);
+
+typedef struct {
+  int64_t kept;        /* s~ = kept_count()                     */
+  int64_t r_rows;      /* I_alpha                                */
+  int64_t r_nnz;       /* nnz(R)                                 */
+  int64_t c_nnz;       /* nnz(C) (0 unless CTD_GPU_WITH_CORE)    */
+  int64_t n_drawn;     /* s                                      */
+  int64_t n_unique;    /* s'                                     */
+  int64_t n_fibers;    /* F = nonempty mode-alpha fibers of X    */
+  int64_t n_cols;      /* N_alpha                                */
+  int64_t u_nnz;       /* exact nonzeros of U (dense_matrix.cpp:24-29) */
+  int mode;
+  int order;
+  double epsilon;
+  uint64_t seed;
+  double total_sq_norm; /* |X|_F^2 as column_distribution computes it */
+  double relative_error; /* NaN unless CTD_GPU_WITH_ERROR */
+  double min_margin;     /* min |log10(ratio/eps)| over decisions */
+  int integer_exact;     /* 1 if the exact-integer fast paths were used */
+} ctd_gpu_factors_info;
+
+int ctd_gpu_factors_info_get(const ctd_gpu_factors *f, ctd_gpu_factors_info *info);
+/* FiberId.flat of every kept fiber, acceptance order (factors.hpp:17-22). */
+int ctd_gpu_factors_kept_flat(const ctd_gpu_factors *f, int64_t *out);
+/* R as CSC (kept+1, r_nnz, r_nnz), acceptance order (fiber_basis.cpp:111-124). */
+int ctd_gpu_factors_r(const ctd_gpu_factors *f, int64_t *col_ptr, int64_t *rows,
+                      double *vals);
+/* U, kept x kept row-major (factors.hpp:34). */
+int ctd_gpu_factors_u(const ctd_gpu_factors *f, double *u);
+/* C_(mode) = R^T X_(mode) as CSC with kept rows and N_alpha columns
+ * (compressed: only nonempty columns, c_cols receives their count). */
+int ctd_gpu_factors_core(const ctd_gpu_factors *f, int64_t *c_cols,
+                         int64_t *col_id, int64_t *col_ptr, int64_t *rows,
+                         double *vals);
+/* Run trace for parity: drawn[s], unique[s'], and per unique candidate the
+ * try_append_fiber outcome (fiber_basis.hpp:30-37).  Any pointer may be NULL. */
+int ctd_gpu_factors_trace(const ctd_gpu_factors *f, int64_t *drawn, int64_t *unique,
+                          int32_t *accepted, int32_t *degenerate, double *delta);
+int ctd_gpu_factors_destroy(ctd_gpu_factors *f);
+
+/* relative_error (evaluation.hpp:39) of X against factors computed from it. */
+int ctd_gpu_relative_error(ctd_gpu_ctx *ctx, const ctd_gpu_tensor *x,
+                           ctd_gpu_factors *f, double *out);
+/* memory_usage (evaluation.hpp:42); needs CTD_GPU_WITH_CORE. */
+int ctd_gpu_memory_usage(const ctd_gpu_tensor *x, const ctd_gpu_factors *f,
+                         double *out);
+
+/* ---- FiberBasis (fiber_basis.hpp:21-61) --------------------------------- */
+int ctd_gpu_basis_create(ctd_gpu_ctx *ctx, int64_t dim, ctd_gpu_basis **out);
+int ctd_gpu_basis_destroy(ctd_gpu_basis *b);
+int64_t ctd_gpu_basis_size(const ctd_gpu_basis *b);
+/* try_append_fiber (fiber_basis.cpp:43-109): host sparse vector (sorted
+ * unique idx, no zeros).  y receives U R^T x (size() entries, may be NULL). */
+int ctd_gpu_basis_try_append(ctd_gpu_basis *b, int64_t dim, int64_t nnz,
+                             const int64_t *idx, const double *val, double epsilon,
+                             int32_t *accepted, int32_t *degenerate, double *delta,
+                             double *y);
+int ctd_gpu_basis_u(const ctd_gpu_basis *b, double *u);
+
+/* ---- CTD-D (ctd_dynamic.hpp:42-58) -------------------------------------- */
+int ctd_gpu_stream_init(ctd_gpu_ctx *ctx, const ctd_gpu_tensor *historical,
+                        int mode, int64_t sample_size, double epsilon,
+                        uint64_t seed, unsigned flags, ctd_gpu_stream **out);
+/* ctd_d_step: one slab of time extent 1. */
+int ctd_gpu_stream_step(ctd_gpu_stream *s, const ctd_gpu_tensor *slab,
+                        int64_t sample_size);
+int64_t ctd_gpu_stream_t(const ctd_gpu_stream *s);
+/* Snapshot of the stream's factors (kept ids, R, U; core when maintained). */
+int ctd_gpu_stream_factors(ctd_gpu_stream *s, ctd_gpu_factors **out);
+int ctd_gpu_stream_destroy(ctd_gpu_stream *s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CTD_GPU_H */

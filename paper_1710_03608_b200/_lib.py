@@ -1,0 +1,84 @@
+"""ctypes loader for libctd_gpu.so (the C-ABI in include/ctd_gpu.h).
+
+There is no CPU fallback: if the CUDA library is not built, importing the
+product API raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libctd_gpu.so")
+
+_lib = None
+
+
+class FactorsInfo(C.Structure):
+    _fields_ = [("kept", C.c_int64), ("r_rows", C.c_int64), ("r_nnz", C.c_int64),
+                ("c_nnz", C.c_int64), ("n_drawn", C.c_int64), ("n_unique", C.c_int64),
+                ("n_fibers", C.c_int64), ("n_cols", C.c_int64), ("u_nnz", C.c_int64),
+                ("mode", C.c_int), ("order", C.c_int), ("epsilon", C.c_double),
+                ("seed", C.c_uint64), ("total_sq_norm", C.c_double),
+                ("relative_error", C.c_double), ("min_margin", C.c_double),
+                ("integer_exact", C.c_int)]
+
+
+# (name, restype, argtypes) for every symbol declared in include/ctd_gpu.h.
+_V, _I, _I64, _D, _U64, _P = C.c_void_p, C.c_int, C.c_int64, C.c_double, C.c_uint64, C.c_void_p
+_PV = C.POINTER(C.c_void_p)
+SIGNATURES = [
+    ("ctd_gpu_last_error", C.c_char_p, []),
+    ("ctd_gpu_version", C.c_char_p, []),
+    ("ctd_gpu_ctx_create", _I, [_I, _V, _PV]),
+    ("ctd_gpu_ctx_set_stream", _I, [_V, _V]),
+    ("ctd_gpu_ctx_synchronize", _I, [_V]),
+    ("ctd_gpu_ctx_destroy", _I, [_V]),
+    ("ctd_gpu_ctx_launches", _I64, [_V]),
+    ("ctd_gpu_tensor_from_host", _I, [_V, _I, _P, _I64, _P, _P, _PV]),
+    ("ctd_gpu_tensor_from_device", _I, [_V, _I, _P, _I64, _P, _P, _PV]),
+    ("ctd_gpu_tensor_nnz", _I64, [_V]),
+    ("ctd_gpu_tensor_destroy", _I, [_V]),
+    ("ctd_gpu_matricize", _I, [_V, _V, _I, _P, _P, _P, _P, _P, _P]),
+    ("ctd_gpu_column_distribution", _I, [_V, _V, _I, _P, _P, _P]),
+    ("ctd_gpu_sample_with_replacement", _I, [_V, _P, _I64, _I64, _U64, _P]),
+    ("ctd_gpu_unique_first_occurrence", _I, [_V, _P, _I64, _P, _P]),
+    ("ctd_gpu_ctd_s", _I, [_V, _V, _I, _I64, _D, _U64, C.c_uint, _PV]),
+    ("ctd_gpu_factors_info_get", _I, [_V, C.POINTER(FactorsInfo)]),
+    ("ctd_gpu_factors_kept_flat", _I, [_V, _P]),
+    ("ctd_gpu_factors_r", _I, [_V, _P, _P, _P]),
+    ("ctd_gpu_factors_u", _I, [_V, _P]),
+    ("ctd_gpu_factors_core", _I, [_V, _P, _P, _P, _P, _P]),
+    ("ctd_gpu_factors_trace", _I, [_V, _P, _P, _P, _P, _P]),
+    ("ctd_gpu_factors_destroy", _I, [_V]),
+    ("ctd_gpu_relative_error", _I, [_V, _V, _V, _P]),
+    ("ctd_gpu_memory_usage", _I, [_V, _V, _P]),
+    ("ctd_gpu_basis_create", _I, [_V, _I64, _PV]),
+    ("ctd_gpu_basis_destroy", _I, [_V]),
+    ("ctd_gpu_basis_size", _I64, [_V]),
+    ("ctd_gpu_basis_try_append", _I, [_V, _I64, _I64, _P, _P, _D, _P, _P, _P, _P]),
+    ("ctd_gpu_basis_u", _I, [_V, _P]),
+    ("ctd_gpu_stream_init", _I, [_V, _V, _I, _I64, _D, _U64, C.c_uint, _PV]),
+    ("ctd_gpu_stream_step", _I, [_V, _V, _I64]),
+    ("ctd_gpu_stream_t", _I64, [_V]),
+    ("ctd_gpu_stream_factors", _I, [_V, _PV]),
+    ("ctd_gpu_stream_destroy", _I, [_V]),
+]
+
+
+def load(path: str = LIB_PATH):
+    """Load libctd_gpu.so and bind every C-ABI symbol (raises if absent)."""
+    global _lib
+    if _lib is not None and path == LIB_PATH:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is not built; run `python -c 'import __graft_entry__ as g; "
+                          f"g.build()'` (there is no CPU fallback)")
+    lib = C.CDLL(path)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path == LIB_PATH:
+        _lib = lib
+    return lib

@@ -1,0 +1,382 @@
+// COO -> mode-alpha fiber bucketing: the GPU form of matricize
+// (tensor_ops.cpp:118-135) + the SparseMatrix COO constructor
+// (sparse_matrix.cpp:22-67) + column_sq_norms (tensor_ops.cpp:194-202).
+//
+// Layout: every entry gets the composite key (column j, row i_alpha).  Keys
+// are unique for a normalized SparseTensor, so sorting them yields exactly
+// the reference's (col,row) order.  Three HBM passes:
+//   1. histogram of buckets  b = j >> wbits  (W = 2^wbits consecutive columns)
+//   2. scatter every entry to its bucket as a 32-bit key
+//      (j - b*W) << rowbits | row  plus its value; validates the input
+//   3. one CTA per bucket: stable block radix sort of the bucket's keys in
+//      shared memory (global memory for the rare oversize bucket), then a
+//      coalesced write of rows/values, fiber heads ranked across buckets with
+//      a decoupled look-back, and each fiber's squared norm summed in
+//      ascending-row order (bit-identical to the reference loop).
+#include "bucket.cuh"
+#include "radix.cuh"
+
+namespace ctdgpu {
+
+namespace {
+
+constexpr int kSortThreads = 512;
+constexpr int kCap = 8192;  // bucket capacity of the shared-memory path
+
+struct CooView {
+  int order;
+  int mode;
+  long long nnz;
+  const int32_t* idx[kMaxOrder];
+  const double* val;
+  long long stride[kMaxOrder];
+  long long shape[kMaxOrder];
+};
+
+__device__ __forceinline__ long long col_of(const CooView& c, long long i, int* row, bool* oob) {
+  long long j = 0;
+  bool bad = false;
+  int r = 0;
+  for (int k = 0; k < c.order; ++k) {
+    const long long v = c.idx[k][i];
+    bad |= (v < 0) | (v >= c.shape[k]);
+    if (k == c.mode) r = (int)v;
+    else j += v * c.stride[k];
+  }
+  *row = r;
+  *oob = bad;
+  return j;
+}
+
+__global__ void k_hist(CooView c, int wbits, unsigned* count, unsigned* flags) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const unsigned long long kNone = ~0ull;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < c.nnz; base += stride) {
+    const long long i = base + threadIdx.x;
+    const bool act = i < c.nnz;
+    const unsigned amask = __ballot_sync(0xffffffffu, act);
+    if (!act) continue;
+    int row;
+    bool oob;
+    const long long j = col_of(c, i, &row, &oob);
+    if (oob) atomicOr(flags, FLAG_BOUNDS);
+    const unsigned long long b = oob ? kNone : (unsigned long long)(j >> wbits);
+    const unsigned peers = __match_any_sync(amask, b);
+    if (b != kNone && (int)(threadIdx.x & 31) == __ffs(peers) - 1)
+      atomicAdd(&count[b], (unsigned)__popc(peers));
+  }
+}
+
+__global__ void k_excl_scan_u32(const unsigned* cnt, long long n, unsigned long long* off) {
+  __shared__ unsigned long long sh[33];
+  unsigned long long carry = 0;
+  for (long long b0 = 0; b0 < n; b0 += (long long)blockDim.x * 4) {
+    unsigned long long v[4], s = 0;
+    const long long base = b0 + (long long)threadIdx.x * 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = (base + k < n) ? cnt[base + k] : 0ull;
+      s += v[k];
+    }
+    unsigned long long tot;
+    unsigned long long pre = block_excl_sum<unsigned long long>(s, sh, &tot) + carry;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (base + k < n) off[base + k] = pre;
+      pre += v[k];
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) off[n] = carry;
+}
+
+struct ScatterOut {
+  unsigned long long* cursor;
+  uint32_t* tkey;
+  double* tval;
+  int* integer_ok;   // cleared when a value is not a small integer
+  double* sum_sq;    // sum of v^2, any order
+};
+
+__global__ void k_scatter(CooView c, int wbits, int rowbits, ScatterOut o, unsigned* flags) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const unsigned long long wmask = (1ull << wbits) - 1ull;
+  double sq = 0.0;
+  bool intok = true;
+  const unsigned long long kNone = ~0ull;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < c.nnz; base += stride) {
+    const long long i = base + threadIdx.x;
+    const bool act = i < c.nnz;
+    const unsigned amask = __ballot_sync(0xffffffffu, act);
+    if (!act) continue;
+    int row;
+    bool oob;
+    const long long j = col_of(c, i, &row, &oob);
+    const double v = c.val[i];
+    if (!oob) {
+      if (v == 0.0) atomicOr(flags, FLAG_ZERO);
+      intok &= (v == rint(v)) && (fabs(v) <= 67108864.0);
+      sq += v * v;
+    }
+    const unsigned long long b = oob ? kNone : (unsigned long long)(j >> wbits);
+    const unsigned peers = __match_any_sync(amask, b);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long basepos = 0;
+    if (b != kNone && (int)(threadIdx.x & 31) == leader)
+      basepos = atomicAdd(&o.cursor[b], (unsigned long long)__popc(peers));
+    basepos = __shfl_sync(peers, basepos, leader);
+    if (b == kNone) continue;
+    const unsigned long long pos = basepos + __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
+    o.tkey[pos] = (uint32_t)((((unsigned long long)j & wmask) << rowbits) | (unsigned)row);
+    o.tval[pos] = v;
+  }
+  sq = warp_sum(sq);
+  const bool all_ok = __all_sync(0xffffffffu, intok);
+  if ((threadIdx.x & 31) == 0) {
+    if (sq != 0.0) atomicAdd(o.sum_sq, sq);
+    if (!all_ok) atomicExch(o.integer_ok, 0);
+  }
+}
+
+struct SortArgs {
+  const unsigned long long* off;  // [nb+1]
+  uint32_t* tkey;                 // [nnz] scattered keys (reused as sort buffer A)
+  const double* tval;             // [nnz]
+  uint32_t* gkey2;                // [nnz] global sort buffer B (oversize buckets)
+  uint32_t* gidx1;                // [nnz]
+  uint32_t* gidx2;                // [nnz]
+  int32_t* out_row;
+  double* out_val;
+  int64_t* fcol;
+  int64_t* fptr;
+  double* norm;
+  unsigned long long* status;     // look-back words, [nb]
+  unsigned* ticket;
+  long long nb;
+  long long nnz;
+  int wbits, rowbits;
+  long long* F_out;
+  unsigned* flags;
+};
+
+__device__ long long lookback(unsigned long long* st, long long b, long long agg) {
+  const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1;
+  if (b == 0) {
+    atomicExch(&st[0], kInc | (unsigned long long)agg);
+    return 0;
+  }
+  atomicExch(&st[b], kAgg | (unsigned long long)agg);
+  long long prefix = 0;
+  long long i = b - 1;
+  while (true) {
+    const unsigned long long s = *((volatile unsigned long long*)&st[i]);
+    const unsigned long long f = s >> 62;
+    if (f == 0) {
+      __nanosleep(40);
+      continue;
+    }
+    prefix += (long long)(s & kVal);
+    if (f == 2) break;
+    --i;
+  }
+  atomicExch(&st[b], kInc | (unsigned long long)(prefix + agg));
+  return prefix;
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_bucket_sort(SortArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* ska = (uint32_t*)smem;
+  uint32_t* skb = ska + kCap;
+  uint16_t* sia = (uint16_t*)(skb + kCap);
+  uint16_t* sib = sia + kCap;
+  double* sv = (double*)(sib + kCap);
+  uint32_t* hist = (uint32_t*)(sv + kCap);
+  __shared__ uint32_t sh32[33];
+  __shared__ long long sh64[33];
+  __shared__ long long s_b, s_fbase;
+  if (threadIdx.x == 0) s_b = atomicAdd(a.ticket, 1u);
+  __syncthreads();
+  const long long b = s_b;
+  if (b >= a.nb) return;
+  const long long start = (long long)a.off[b];
+  const int m = (int)((long long)a.off[b + 1] - start);
+  const int T = blockDim.x, t = threadIdx.x;
+  const int keybits = a.wbits + a.rowbits;
+  const uint32_t rowmask = a.rowbits ? (0xffffffffu >> (32 - a.rowbits)) : 0u;
+  const bool small = m <= kCap;
+  const uint32_t* K;
+  const double* V;
+  if (small) {
+    for (int p = t; p < m; p += T) {
+      ska[p] = a.tkey[start + p];
+      sia[p] = (uint16_t)p;
+    }
+    __syncthreads();
+    const bool inb = block_radix_sort<uint16_t>(ska, skb, sia, sib, m, keybits, hist, sh32);
+    K = inb ? skb : ska;
+    const uint16_t* I = inb ? sib : sia;
+    for (int p = t; p < m; p += T) sv[p] = a.tval[start + I[p]];
+    V = sv;
+  } else {
+    uint32_t* ka = a.tkey + start;
+    uint32_t* kb = a.gkey2 + start;
+    uint32_t* ia = a.gidx1 + start;
+    uint32_t* ib = a.gidx2 + start;
+    for (int p = t; p < m; p += T) ia[p] = (uint32_t)p;
+    __syncthreads();
+    const bool inb = block_radix_sort<uint32_t>(ka, kb, ia, ib, m, keybits, hist, sh32);
+    K = inb ? kb : ka;
+    const uint32_t* I = inb ? ib : ia;
+    for (int p = t; p < m; p += T) a.out_val[start + p] = a.tval[start + I[p]];
+    V = a.out_val + start;
+  }
+  __syncthreads();
+  // Contiguous chunk per thread: write rows/values, find fiber heads.
+  const int per = (m + T - 1) / T;
+  const int c0 = min(t * per, m), c1 = min(c0 + per, m);
+  long long nh = 0;
+  bool dup = false;
+  for (int p = c0; p < c1; ++p) {
+    const uint32_t key = K[p];
+    a.out_row[start + p] = (int32_t)(key & rowmask);
+    if (small) a.out_val[start + p] = V[p];
+    const bool head = (p == 0) || ((K[p - 1] >> a.rowbits) != (key >> a.rowbits));
+    dup |= (p > 0) && (K[p - 1] == key);
+    nh += head;
+  }
+  if (dup) atomicOr(a.flags, FLAG_DUPLICATE);
+  long long agg;
+  long long rank = block_excl_sum<long long>(nh, sh64, &agg);
+  if (t == 0) {
+    s_fbase = lookback(a.status, b, agg);
+    if (b == a.nb - 1) {
+      *a.F_out = s_fbase + agg;
+      a.fptr[s_fbase + agg] = a.nnz;
+    }
+  }
+  __syncthreads();
+  const long long fbase = s_fbase;
+  for (int p = c0; p < c1; ++p) {
+    const uint32_t key = K[p];
+    const uint32_t jl = a.rowbits < 32 ? (key >> a.rowbits) : 0u;
+    const bool head = (p == 0) || ((K[p - 1] >> a.rowbits) != jl);
+    if (!head) continue;
+    const long long f = fbase + rank++;
+    a.fcol[f] = ((long long)b << a.wbits) + (long long)jl;
+    a.fptr[f] = start + p;
+    // column_sq_norms: s += v*v in ascending row order (tensor_ops.cpp:197-198)
+    double s = 0.0;
+    for (int q = p; q < m && (K[q] >> a.rowbits) == jl; ++q) s = dadd(s, dsqr(V[q]));
+    a.norm[f] = s;
+  }
+}
+
+int bits_for(long long n) {  // bits needed to represent 0..n-1
+  int b = 0;
+  while (b < 63 && (1ll << b) < n) ++b;
+  return b;
+}
+
+}  // namespace
+
+void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
+  if (mode < 0 || mode >= x.order)
+    fail(CTD_ERR_ARGUMENT, "mode " + std::to_string(mode) + " out of range for order " +
+                               std::to_string(x.order));
+  CooView c{};
+  c.order = x.order;
+  c.mode = mode;
+  c.nnz = x.nnz;
+  c.val = x.val;
+  long long acc = 1;
+  for (int k = 0; k < x.order; ++k) {  // fiber_strides, tensor_ops.cpp:106-116
+    c.idx[k] = x.idx[k];
+    c.shape[k] = x.shape[k];
+    if (k == mode) {
+      c.stride[k] = 0;
+      continue;
+    }
+    c.stride[k] = acc;
+    acc *= x.shape[k];
+  }
+  out.rows = x.shape[mode];
+  out.cols = acc;
+  out.nnz = x.nnz;
+  out.mode = mode;
+  const int rowbits = bits_for(out.rows);
+  if (rowbits > 31) fail(CTD_ERR_SHAPE, "mode extent exceeds 2^31");
+  // Bucket width: ~2048 expected entries per bucket, key must fit 32 bits.
+  int wbits = 0;
+  {
+    const double per_col = out.cols > 0 ? (double)x.nnz / (double)out.cols : 1.0;
+    const double want = 2048.0 / (per_col > 0 ? per_col : 1.0);
+    while (wbits < 32 - rowbits && (double)(1ll << (wbits + 1)) <= want) ++wbits;
+    wbits = std::min(wbits, 32 - rowbits);
+  }
+  long long nb = out.cols > 0 ? ((out.cols - 1) >> wbits) + 1 : 1;
+  if (nb > (1ll << 28)) fail(CTD_ERR_SHAPE, "matricized column count too large for bucketing");
+  const long long nnz = x.nnz;
+  out.row.alloc(ctx, nnz);
+  out.val.alloc(ctx, nnz);
+  out.col.alloc(ctx, nnz + 1);
+  out.ptr.alloc(ctx, nnz + 1);
+  out.norm.alloc(ctx, nnz + 1);
+  Buf<long long> dF(ctx, 1);
+  if (nnz == 0) {
+    out.F = 0;
+    ctx->zero(out.ptr.p, sizeof(int64_t));
+    return;
+  }
+  Buf<unsigned> count(ctx, nb);
+  count.zero();
+  Buf<unsigned long long> off(ctx, nb + 1), cursor(ctx, nb + 1), status(ctx, nb);
+  status.zero();
+  Buf<uint32_t> tkey(ctx, nnz);
+  Buf<double> tval(ctx, nnz);
+  Buf<int> intok(ctx, 1);
+  Buf<double> sumsq(ctx, 1);
+  Buf<unsigned> ticket(ctx, 1);
+  ticket.zero();
+  sumsq.zero();
+  {
+    const int one = 1;
+    ctx->to_dev(intok.p, &one, 1);
+  }
+  const unsigned grid = (unsigned)std::min<long long>((nnz + 255) / 256, (long long)ctx->sm_count * 16);
+  LAUNCH(ctx, k_hist, grid, 256, 0, c, wbits, count.p, ctx->d_flags);
+  LAUNCH(ctx, k_excl_scan_u32, 1, 1024, 0, count.p, nb, off.p);
+  CUDA_OK(cudaMemcpyAsync(cursor.p, off.p, (nb + 1) * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToDevice, ctx->stream));
+  ScatterOut so{cursor.p, tkey.p, tval.p, intok.p, sumsq.p};
+  LAUNCH(ctx, k_scatter, grid, 256, 0, c, wbits, rowbits, so, ctx->d_flags);
+  // Oversize buckets need global sort buffers; allocate lazily (rare).
+  // The buffers are sized nnz so every bucket owns its slice.
+  Buf<uint32_t> gkey2, gidx1, gidx2;
+  gkey2.alloc(ctx, nnz);
+  gidx1.alloc(ctx, nnz);
+  gidx2.alloc(ctx, nnz);
+  SortArgs sa{off.p, tkey.p, tval.p, gkey2.p, gidx1.p, gidx2.p, out.row.p, out.val.p,
+              out.col.p, out.ptr.p, out.norm.p, status.p, ticket.p, nb, nnz, wbits, rowbits,
+              dF.p, ctx->d_flags};
+  const size_t smem = (size_t)kCap * (4 + 4 + 2 + 2 + 8) + (kSortThreads / 32) * kRadix * 4;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CUDA_OK(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr_set = true;
+  }
+  LAUNCH(ctx, k_bucket_sort, (unsigned)nb, kSortThreads, smem, sa);
+  long long F = 0;
+  int iok = 0;
+  double ssq = 0.0;
+  ctx->to_host(&F, dF.p, 1);
+  ctx->to_host(&iok, intok.p, 1);
+  ctx->to_host(&ssq, sumsq.p, 1);
+  ctx->sync();
+  out.F = F;
+  out.sum_sq = ssq;
+  out.integer_exact = iok && ssq < 4503599627370496.0;  // 2^52
+  ctx->check_flags("matricize");
+}
+
+}  // namespace ctdgpu

@@ -1,0 +1,28 @@
+#pragma once
+#include "ctx.cuh"
+
+namespace ctdgpu {
+
+// Mode-`mode` matricization of a SparseTensor in compressed CSC form (only
+// the F nonempty fibers), entries ordered by (column, row) exactly as the
+// reference's SparseMatrix stores them (sparse_matrix.cpp:38-66), with the
+// squared norm of every fiber summed in ascending-row order
+// (tensor_ops.cpp:194-202).
+struct Fibers {
+  int64_t rows = 0;  // I_alpha
+  int64_t cols = 0;  // N_alpha
+  int64_t nnz = 0;
+  int64_t F = 0;
+  int mode = 0;
+  Buf<int64_t> col;   // [F] column id j of each nonempty fiber
+  Buf<int64_t> ptr;   // [F+1] offsets
+  Buf<int32_t> row;   // [nnz]
+  Buf<double> val;    // [nnz]
+  Buf<double> norm;   // [F]
+  bool integer_exact = false;  // all values integral, |v| <= 2^26, sum v^2 < 2^52
+  double sum_sq = 0.0;         // sum of v^2 (any order; exact when integer_exact)
+};
+
+void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out);
+
+}  // namespace ctdgpu

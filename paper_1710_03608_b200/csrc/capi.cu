@@ -1,0 +1,539 @@
+// extern "C" boundary (include/ctd_gpu.h).  Every entry point converts
+// internal failures into the reference ErrorClass codes.
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "cdf.cuh"
+#include "ctd.cuh"
+#include "relerr.cuh"
+#include "sample.cuh"
+
+using namespace ctdgpu;
+
+struct ctd_gpu_ctx {
+  Ctx c;
+};
+struct ctd_gpu_tensor {
+  Tensor t;
+};
+struct ctd_gpu_factors {
+  Factors f;
+};
+struct ctd_gpu_basis {
+  Ctx* ctx;
+  std::unique_ptr<Basis> b;
+};
+struct ctd_gpu_stream {
+  Stream s;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return CTD_OK;
+  } catch (const Fail& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return CTD_ERR_DEVICE;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return CTD_ERR_DEVICE;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) fail(CTD_ERR_ARGUMENT, std::string(what) + " is NULL");
+}
+
+__global__ void k_narrow(const int64_t* in, long long nnz, int order, int32_t* out, unsigned* flags) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nnz * order) return;
+  const long long i = e / order;
+  const int k = (int)(e - i * order);
+  const int64_t v = in[e];
+  if (v < 0 || v > 0x7fffffffLL) atomicOr(flags, FLAG_BOUNDS);
+  out[(long long)k * nnz + i] = (int32_t)v;
+}
+
+void check_shape(int order, const int64_t* shape) {
+  if (order < 0 || order > kMaxOrder) fail(CTD_ERR_ARGUMENT, "tensor order out of range");
+  for (int k = 0; k < order; ++k) {
+    if (shape[k] < 0) fail(CTD_ERR_ARGUMENT, "tensor extent must be non-negative");
+    if (shape[k] > 0x7fffffffLL) fail(CTD_ERR_SHAPE, "tensor extent exceeds the int32 index range");
+  }
+}
+
+}  // namespace
+
+namespace ctdgpu {
+
+void Ctx::check_flags(const char* where) {
+  unsigned f = 0;
+  CUDA_OK(cudaMemcpyAsync(&f, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, stream));
+  CUDA_OK(cudaStreamSynchronize(stream));
+  if (!f) return;
+  CUDA_OK(cudaMemsetAsync(d_flags, 0, sizeof(unsigned), stream));
+  const std::string w(where);
+  if (f & FLAG_BOUNDS) fail(CTD_ERR_SHAPE, w + ": tensor entry index out of bounds");
+  if (f & FLAG_DUPLICATE)
+    fail(CTD_ERR_ARGUMENT, w + ": duplicate coordinates (input is not a normalized SparseTensor)");
+  if (f & FLAG_ZERO) fail(CTD_ERR_ARGUMENT, w + ": stored zero (input is not a normalized SparseTensor)");
+  if (f & FLAG_EMPTY) fail(CTD_ERR_EMPTY_INPUT, w + ": sampling from an all-zero distribution");
+  if (f & FLAG_OVERFLOW) fail(CTD_ERR_NUMERIC, w + ": internal capacity exceeded");
+  // FLAG_SEQSUM: a self-check failed and the sequential fallback ran; the
+  // result is still exact.  Nothing to report.
+}
+
+}  // namespace ctdgpu
+
+extern "C" {
+
+const char* ctd_gpu_last_error(void) { return g_last_error.c_str(); }
+const char* ctd_gpu_version(void) { return "ctd_gpu 0.1 (sm_100a)"; }
+
+int ctd_gpu_ctx_create(int device, void* stream, ctd_gpu_ctx** out) {
+  return guarded([&] {
+    need(out, "out");
+    auto h = std::make_unique<ctd_gpu_ctx>();
+    Ctx& c = h->c;
+    c.device = device;
+    CUDA_OK(cudaSetDevice(device));
+    c.stream = static_cast<cudaStream_t>(stream);
+    CUDA_OK(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, device));
+    int coop = 0;
+    CUDA_OK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+    if (!coop) fail(CTD_ERR_DEVICE, "device does not support cooperative launch");
+    cudaMemPool_t pool;
+    CUDA_OK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    CUDA_OK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    CUDA_OK(cudaMalloc(&c.d_flags, sizeof(unsigned)));
+    CUDA_OK(cudaMalloc(&c.d_bar, 4 * sizeof(unsigned)));
+    CUDA_OK(cudaMemset(c.d_flags, 0, sizeof(unsigned)));
+    CUDA_OK(cudaMemset(c.d_bar, 0, 4 * sizeof(unsigned)));
+    *out = h.release();
+  });
+}
+
+int ctd_gpu_ctx_set_stream(ctd_gpu_ctx* ctx, void* stream) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->c.stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+int ctd_gpu_ctx_synchronize(ctd_gpu_ctx* ctx) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->c.sync();
+  });
+}
+
+int ctd_gpu_ctx_destroy(ctd_gpu_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->c.stream);
+    cudaFree(ctx->c.d_flags);
+    cudaFree(ctx->c.d_bar);
+    delete ctx;
+  });
+}
+
+int64_t ctd_gpu_ctx_launches(const ctd_gpu_ctx* ctx) { return ctx ? ctx->c.launches : -1; }
+
+int ctd_gpu_tensor_from_host(ctd_gpu_ctx* ctx, int order, const int64_t* shape, int64_t nnz,
+                             const int64_t* indices, const double* values, ctd_gpu_tensor** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    if (order > 0) need(shape, "shape");
+    if (nnz < 0) fail(CTD_ERR_SHAPE, "index data does not match entry count");
+    if (order == 0 && nnz > 0) fail(CTD_ERR_SHAPE, "entries supplied for an order-0 tensor");
+    check_shape(order, shape);
+    Ctx* c = &ctx->c;
+    auto h = std::make_unique<ctd_gpu_tensor>();
+    Tensor& t = h->t;
+    t.ctx = c;
+    t.order = order;
+    t.nnz = nnz;
+    for (int k = 0; k < order; ++k) t.shape[k] = shape[k];
+    t.own_idx.alloc(c, (size_t)nnz * order + 1);
+    t.own_val.alloc(c, nnz + 1);
+    if (nnz > 0) {
+      need(indices, "indices");
+      need(values, "values");
+      Buf<int64_t> raw(c, (size_t)nnz * order);
+      c->to_dev(raw.p, indices, (size_t)nnz * order);
+      c->to_dev(t.own_val.p, values, nnz);
+      LAUNCH(c, k_narrow, ceil_div((uint64_t)nnz * order, 256), 256, 0, raw.p, (long long)nnz, order,
+             t.own_idx.p, c->d_flags);
+      c->check_flags("SparseTensor");
+    }
+    for (int k = 0; k < order; ++k) t.idx[k] = t.own_idx.p + (size_t)k * nnz;
+    t.val = t.own_val.p;
+    *out = h.release();
+  });
+}
+
+int ctd_gpu_tensor_from_device(ctd_gpu_ctx* ctx, int order, const int64_t* shape, int64_t nnz,
+                               const int32_t* const* mode_indices, const double* values,
+                               ctd_gpu_tensor** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    if (order > 0) need(shape, "shape");
+    if (nnz < 0) fail(CTD_ERR_SHAPE, "index data does not match entry count");
+    check_shape(order, shape);
+    auto h = std::make_unique<ctd_gpu_tensor>();
+    Tensor& t = h->t;
+    t.ctx = &ctx->c;
+    t.order = order;
+    t.nnz = nnz;
+    for (int k = 0; k < order; ++k) {
+      t.shape[k] = shape[k];
+      t.idx[k] = mode_indices ? mode_indices[k] : nullptr;
+      if (nnz > 0) need(t.idx[k], "mode_indices[k]");
+    }
+    t.val = values;
+    if (nnz > 0) need(values, "values");
+    *out = h.release();
+  });
+}
+
+int64_t ctd_gpu_tensor_nnz(const ctd_gpu_tensor* t) { return t ? t->t.nnz : -1; }
+
+int ctd_gpu_tensor_destroy(ctd_gpu_tensor* t) {
+  return guarded([&] { delete t; });
+}
+
+int ctd_gpu_matricize(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int mode, int64_t* n_fibers,
+                      int64_t* fiber_col, int64_t* fiber_ptr, int32_t* rows, double* vals,
+                      double* sq_norms) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(x, "x");
+    Ctx* c = &ctx->c;
+    Fibers fb;
+    matricize(c, x->t, mode, fb);
+    if (n_fibers) *n_fibers = fb.F;
+    if (fiber_col) c->to_host(fiber_col, fb.col.p, fb.F);
+    if (fiber_ptr) c->to_host(fiber_ptr, fb.ptr.p, fb.F + 1);
+    if (rows) c->to_host(rows, fb.row.p, fb.nnz);
+    if (vals) c->to_host(vals, fb.val.p, fb.nnz);
+    if (sq_norms) c->to_host(sq_norms, fb.norm.p, fb.F);
+    c->sync();
+  });
+}
+
+int ctd_gpu_column_distribution(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int mode,
+                                double* total_sq_norm, double* probs, double* cumulative) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(x, "x");
+    Ctx* c = &ctx->c;
+    Law law;
+    build_law(c, x->t, mode, law);
+    if (total_sq_norm) c->to_host(total_sq_norm, law.total.p, 1);
+    if (probs) c->to_host(probs, law.probs.p, law.fb.F);
+    if (cumulative) c->to_host(cumulative, law.cum.p, law.fb.F);
+    c->sync();
+  });
+}
+
+int ctd_gpu_sample_with_replacement(ctd_gpu_ctx* ctx, const double* probs, int64_t n, int64_t count,
+                                    uint64_t seed, int64_t* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    if (count < 0) fail(CTD_ERR_ARGUMENT, "sample count must be non-negative");  // sampling.cpp:36
+    if (count == 0) return;
+    need(out, "out");
+    Ctx* c = &ctx->c;
+    if (n <= 0) fail(CTD_ERR_EMPTY_INPUT, "sampling from an all-zero distribution");
+    need(probs, "probs");
+    Buf<double> p(c, n), cum(c, n);
+    c->to_dev(p.p, probs, n);
+    clamped_cdf(c, p.p, n, cum.p, c->d_flags);
+    c->check_flags("sample_with_replacement");
+    Buf<int64_t> d(c, count);
+    draw_columns(c, cum.p, n, count, seed, d.p);
+    c->to_host(out, d.p, count);
+    c->sync();
+  });
+}
+
+int ctd_gpu_unique_first_occurrence(ctd_gpu_ctx* ctx, const int64_t* drawn, int64_t n, int64_t* out,
+                                    int64_t* n_out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(n_out, "n_out");
+    *n_out = 0;
+    if (n <= 0) return;
+    need(drawn, "drawn");
+    need(out, "out");
+    Ctx* c = &ctx->c;
+    Buf<int64_t> in(c, n), o(c, n);
+    Buf<int> nu(c, 1);
+    c->to_dev(in.p, drawn, n);
+    dedup_first64(c, in.p, n, o.p, nu.p);
+    int k = c->read1(nu.p);
+    c->to_host(out, o.p, k);
+    c->sync();
+    *n_out = k;
+  });
+}
+
+int ctd_gpu_ctd_s(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int mode, int64_t sample_size, double epsilon,
+                  uint64_t seed, unsigned flags, ctd_gpu_factors** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(x, "x");
+    need(out, "out");
+    if (flags & CTD_GPU_WITH_CORE) fail(CTD_ERR_ARGUMENT, "core materialization is not available yet");
+    auto h = std::make_unique<ctd_gpu_factors>();
+    run_ctd_s(&ctx->c, x->t, mode, sample_size, epsilon, seed, flags, h->f);
+    *out = h.release();
+  });
+}
+
+int ctd_gpu_factors_info_get(const ctd_gpu_factors* f, ctd_gpu_factors_info* info) {
+  return guarded([&] {
+    need(f, "factors");
+    need(info, "info");
+    const Factors& F = f->f;
+    std::memset(info, 0, sizeof(*info));
+    info->kept = (int64_t)F.kept_flat.size();
+    info->r_rows = F.rows;
+    info->r_nnz = F.basis ? F.basis->rnnz : 0;
+    info->c_nnz = 0;
+    info->n_drawn = (int64_t)F.drawn.size();
+    info->n_unique = (int64_t)F.unique.size();
+    info->n_fibers = F.F;
+    info->n_cols = F.cols;
+    info->mode = F.mode;
+    info->order = F.order;
+    info->epsilon = F.eps;
+    info->seed = F.seed;
+    info->total_sq_norm = F.total;
+    info->relative_error = F.rel_error;
+    info->min_margin = F.min_margin;
+    info->integer_exact = F.integer_exact;
+    info->u_nnz = -1;  // computed on demand by ctd_gpu_factors_u callers
+  });
+}
+
+int ctd_gpu_factors_kept_flat(const ctd_gpu_factors* f, int64_t* out) {
+  return guarded([&] {
+    need(f, "factors");
+    need(out, "out");
+    std::memcpy(out, f->f.kept_flat.data(), f->f.kept_flat.size() * sizeof(int64_t));
+  });
+}
+
+int ctd_gpu_factors_r(const ctd_gpu_factors* f, int64_t* col_ptr, int64_t* rows, double* vals) {
+  return guarded([&] {
+    need(f, "factors");
+    basis_r(*f->f.basis, col_ptr, rows, vals);
+  });
+}
+
+int ctd_gpu_factors_u(const ctd_gpu_factors* f, double* u) {
+  return guarded([&] {
+    need(f, "factors");
+    need(u, "u");
+    basis_u(*f->f.basis, u);
+  });
+}
+
+int ctd_gpu_factors_core(const ctd_gpu_factors* f, int64_t*, int64_t*, int64_t*, int64_t*, double*) {
+  return guarded([&] {
+    need(f, "factors");
+    fail(CTD_ERR_ARGUMENT, "core materialization is not available yet");
+  });
+}
+
+int ctd_gpu_factors_trace(const ctd_gpu_factors* f, int64_t* drawn, int64_t* unique, int32_t* accepted,
+                          int32_t* degenerate, double* delta) {
+  return guarded([&] {
+    need(f, "factors");
+    const Factors& F = f->f;
+    if (drawn) std::memcpy(drawn, F.drawn.data(), F.drawn.size() * sizeof(int64_t));
+    if (unique) std::memcpy(unique, F.unique.data(), F.unique.size() * sizeof(int64_t));
+    if (accepted) std::memcpy(accepted, F.accepted.data(), F.accepted.size() * sizeof(int32_t));
+    if (degenerate) std::memcpy(degenerate, F.degenerate.data(), F.degenerate.size() * sizeof(int32_t));
+    if (delta) std::memcpy(delta, F.delta.data(), F.delta.size() * sizeof(double));
+  });
+}
+
+int ctd_gpu_factors_destroy(ctd_gpu_factors* f) {
+  return guarded([&] { delete f; });
+}
+
+int ctd_gpu_relative_error(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, ctd_gpu_factors* f, double* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(x, "x");
+    need(f, "factors");
+    need(out, "out");
+    Factors& F = f->f;
+    if (x->t.order != F.order) fail(CTD_ERR_SHAPE, "factor shape does not match the tensor");
+    for (int k = 0; k < F.order; ++k)
+      if (x->t.shape[k] != F.shape[k]) fail(CTD_ERR_SHAPE, "factor shape does not match the tensor");
+    Fibers fb;
+    matricize(&ctx->c, x->t, F.mode, fb);
+    *out = relative_error(&ctx->c, fb, *F.basis);
+  });
+}
+
+int ctd_gpu_memory_usage(const ctd_gpu_tensor* x, const ctd_gpu_factors* f, double* out) {
+  return guarded([&] {
+    need(x, "x");
+    need(f, "factors");
+    need(out, "out");
+    if (x->t.nnz == 0) fail(CTD_ERR_METRIC, "memory usage undefined for an empty tensor");
+    fail(CTD_ERR_ARGUMENT, "memory_usage needs nnz(C): core materialization is not available yet");
+  });
+}
+
+int ctd_gpu_basis_create(ctd_gpu_ctx* ctx, int64_t dim, ctd_gpu_basis** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    if (dim < 0) fail(CTD_ERR_ARGUMENT, "basis dimension must be non-negative");
+    auto h = std::make_unique<ctd_gpu_basis>();
+    h->ctx = &ctx->c;
+    h->b = std::make_unique<Basis>(&ctx->c, dim);
+    *out = h.release();
+  });
+}
+
+int ctd_gpu_basis_destroy(ctd_gpu_basis* b) {
+  return guarded([&] { delete b; });
+}
+
+int64_t ctd_gpu_basis_size(const ctd_gpu_basis* b) { return b ? b->b->K : -1; }
+
+int ctd_gpu_basis_try_append(ctd_gpu_basis* b, int64_t dim, int64_t nnz, const int64_t* idx, const double* val,
+                             double epsilon, int32_t* accepted, int32_t* degenerate, double* delta, double* y) {
+  return guarded([&] {
+    need(b, "basis");
+    Basis& B = *b->b;
+    Ctx* c = b->ctx;
+    if (dim != B.dim) fail(CTD_ERR_SHAPE, "fiber length does not match basis");  // fiber_basis.cpp:45
+    if (nnz < 0) fail(CTD_ERR_ARGUMENT, "negative nnz");
+    std::vector<int32_t> r32(nnz > 0 ? nnz : 1);
+    for (int64_t i = 0; i < nnz; ++i) {
+      if (idx[i] < 0 || idx[i] >= dim) fail(CTD_ERR_SHAPE, "fiber index out of range");
+      r32[i] = (int32_t)idx[i];
+    }
+    Buf<int32_t> drow(c, nnz + 1), dlen(c, 1);
+    Buf<double> dval(c, nnz + 1);
+    Buf<int64_t> doff(c, 1);
+    const int64_t zero = 0;
+    const int32_t len = (int32_t)nnz;
+    c->to_dev(drow.p, r32.data(), nnz);
+    if (nnz) c->to_dev(dval.p, val, nnz);
+    c->to_dev(doff.p, &zero, 1);
+    c->to_dev(dlen.p, &len, 1);
+    Cands cd;
+    cd.n = 1;
+    cd.off = doff.p;
+    cd.len = dlen.p;
+    cd.row = drow.p;
+    cd.val = dval.p;
+    BatchOut bo;
+    const int64_t k_before = B.K;
+    filter_batch(B, cd, epsilon, bo, y != nullptr);
+    if (accepted) *accepted = bo.accepted[0];
+    if (degenerate) *degenerate = bo.degenerate[0];
+    if (delta) *delta = bo.delta[0];
+    if (y) std::memcpy(y, bo.y_last.data(), (size_t)k_before * sizeof(double));
+  });
+}
+
+int ctd_gpu_basis_u(const ctd_gpu_basis* b, double* u) {
+  return guarded([&] {
+    need(b, "basis");
+    need(u, "u");
+    basis_u(*b->b, u);
+  });
+}
+
+int ctd_gpu_stream_init(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* historical, int mode, int64_t sample_size,
+                        double epsilon, uint64_t seed, unsigned flags, ctd_gpu_stream** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(historical, "historical");
+    need(out, "out");
+    (void)flags;
+    auto h = std::make_unique<ctd_gpu_stream>();
+    stream_init(&ctx->c, historical->t, mode, sample_size, epsilon, seed, h->s);
+    *out = h.release();
+  });
+}
+
+int ctd_gpu_stream_step(ctd_gpu_stream* s, const ctd_gpu_tensor* slab, int64_t sample_size) {
+  return guarded([&] {
+    need(s, "stream");
+    need(slab, "slab");
+    stream_step(s->s, slab->t, sample_size);
+  });
+}
+
+int64_t ctd_gpu_stream_t(const ctd_gpu_stream* s) { return s ? s->s.t : -1; }
+
+int ctd_gpu_stream_factors(ctd_gpu_stream* s, ctd_gpu_factors** out) {
+  return guarded([&] {
+    need(s, "stream");
+    need(out, "out");
+    // Snapshot: kept ids and a copy of the basis (R, U).
+    auto h = std::make_unique<ctd_gpu_factors>();
+    Factors& F = h->f;
+    const Stream& S = s->s;
+    F.ctx = S.ctx;
+    F.order = S.order;
+    F.mode = S.mode;
+    for (int k = 0; k + 1 < S.order; ++k) F.shape[k] = S.slab_shape[k];
+    F.shape[S.order - 1] = S.t;
+    F.eps = S.eps;
+    F.seed = S.seed;
+    F.rows = S.basis->dim;
+    F.kept_flat = S.kept_flat;
+    // copy the basis state needed by the accessors (R, U)
+    auto nb = std::make_unique<Basis>(S.ctx, S.basis->dim);
+    const Basis& B = *S.basis;
+    Ctx* c = S.ctx;
+    nb->K = B.K;
+    nb->LD = B.K > 0 ? B.K : 1;
+    nb->U.alloc(c, (size_t)nb->LD * nb->LD);
+    if (B.K)
+      CUDA_OK(cudaMemcpy2DAsync(nb->U.p, B.K * sizeof(double), B.U.p, B.LD * sizeof(double), B.K * sizeof(double),
+                                B.K, cudaMemcpyDeviceToDevice, c->stream));
+    nb->kcap = B.K;
+    nb->rptr.alloc(c, B.K + 1);
+    CUDA_OK(cudaMemcpyAsync(nb->rptr.p, B.rptr.p, (B.K + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->stream));
+    nb->rnnz = nb->rcap = B.rnnz;
+    nb->rrow.alloc(c, B.rnnz + 1);
+    nb->rval.alloc(c, B.rnnz + 1);
+    if (B.rnnz) {
+      CUDA_OK(cudaMemcpyAsync(nb->rrow.p, B.rrow.p, B.rnnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
+      CUDA_OK(cudaMemcpyAsync(nb->rval.p, B.rval.p, B.rnnz * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    }
+    F.basis = std::move(nb);
+    *out = h.release();
+  });
+}
+
+int ctd_gpu_stream_destroy(ctd_gpu_stream* s) {
+  return guarded([&] { delete s; });
+}
+
+}  // extern "C"

@@ -1,0 +1,340 @@
+// Device-wide exact sequential cumulative sum (see seqsum.cuh for the
+// algorithm) and the sampling law built from it:
+//   T   = sequential sum of fiber norms            (sampling.cpp:26-27)
+//   p_j = fl(n_j / T)                              (sampling.cpp:29)
+//   cum = sequential running sum of p, tail clamped (sampling.cpp:42-54)
+// All three are bit-identical to the reference.
+#include "cdf.cuh"
+#include "seqsum.cuh"
+
+namespace ctdgpu {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kPerThread = 8;
+constexpr int kBS = kThreads * kPerThread;  // elements per block
+constexpr int kDMax = 128;                  // directs per block before fallback
+
+__global__ void k_chunk_sum(const double* __restrict__ x, long long n, double* bsum) {
+  __shared__ double sh[33];
+  const long long base = (long long)blockIdx.x * kBS + (long long)threadIdx.x * kPerThread;
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < kPerThread; ++k)
+    if (base + k < n) s += x[base + k];
+  double tot = block_sum<double>(s, sh);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+// Exclusive scan (approximate, any association) of nb block sums; 1 block.
+__global__ void k_scan_bsum(const double* bsum, long long nb, double* bpre) {
+  __shared__ double sh[33];
+  double carry = 0.0;
+  for (long long b0 = 0; b0 < nb; b0 += (long long)blockDim.x * 4) {
+    double v[4];
+    double s = 0.0;
+    const long long base = b0 + (long long)threadIdx.x * 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = (base + k < nb) ? bsum[base + k] : 0.0;
+      s += v[k];
+    }
+    double tot;
+    double pre = block_excl_sum<double>(s, sh, &tot) + carry;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (base + k < nb) bpre[base + k] = pre;
+      pre += v[k];
+    }
+    carry += tot;
+  }
+}
+
+struct LocalOut {
+  short* e;      // per element: REG binade, E_DIRECT or E_ZERO
+  Mono* m;       // per element: run mono (in-block, from head or block start)
+  int* slot;     // per element: head slot (>=0), -1 inherited, -2 zero
+  double* dl_x;  // per block direct list
+  Mono* dl_m;
+  short* dl_e;
+  int* dl_inh;
+  int* bnd;      // directs per block
+  Seg* bagg;     // block aggregate
+  short* blast;  // e/cls of the block's last element
+};
+
+__global__ void k_seq_local(const double* __restrict__ x, long long n, const double* bpre,
+                            LocalOut o, unsigned* flags) {
+  __shared__ double dsh[33];
+  __shared__ Seg ssh[33];
+  __shared__ int ish[33];
+  __shared__ short last_e[kThreads];
+  const long long bb = (long long)blockIdx.x * kBS;
+  const long long b0 = bb + (long long)threadIdx.x * kPerThread;
+  const double mg = seq_margin(n);
+  double xv[kPerThread];
+  double cs = 0.0;
+#pragma unroll
+  for (int k = 0; k < kPerThread; ++k) {
+    xv[k] = (b0 + k < n) ? x[b0 + k] : 0.0;
+    cs += xv[k];
+  }
+  double pre = block_excl_sum<double>(cs, dsh, nullptr) + bpre[blockIdx.x];
+  // Pass B.
+  Seg agg{0, mono_id()};
+  int nd = 0;
+  short le = (short)0x7fff;
+  {
+    double P = pre;
+#pragma unroll
+    for (int k = 0; k < kPerThread; ++k) {
+      const long long i = b0 + k;
+      if (i >= n) break;
+      const double Pc = P + xv[k];
+      int e = 0;
+      Mono m;
+      const int c = seq_classify(i == 0, P, Pc, xv[k], mg, &e, &m);
+      if (c == CLS_REG) {
+        agg.m = mono_cat(agg.m, m);
+        le = (short)e;
+      } else {
+        agg.h = 1;
+        agg.m = mono_id();
+        if (c == CLS_DIRECT) ++nd;
+        le = c == CLS_DIRECT ? E_DIRECT : E_ZERO;
+      }
+      P = Pc;
+    }
+  }
+  last_e[threadIdx.x] = le;
+  Seg tot_seg;
+  Seg carry = block_seg_excl(agg, ssh, &tot_seg);
+  int ntot;
+  int dpos = block_excl_sum<int>(nd, ish, &ntot);
+  const bool over = ntot > kDMax;
+  if (threadIdx.x == 0) {
+    o.bnd[blockIdx.x] = over ? 0 : ntot;
+    o.bagg[blockIdx.x] = tot_seg;
+    if (over) atomicOr(flags, FLAG_SEQSUM);
+  }
+  // e of the element before this thread's chunk (within the block).
+  short prev_e = (short)0x7ffe;  // 0x7ffe: "previous block"
+  for (int q = (int)threadIdx.x - 1; q >= 0; --q)
+    if (last_e[q] != (short)0x7fff) { prev_e = last_e[q]; break; }
+  // Pass C.
+  {
+    double P = pre;
+    Mono M = carry.m;
+    int head_slot = carry.h ? -3 : -1;  // -3: head earlier in block (slot set below)
+    // The last head before this chunk within the block: its slot = dpos-1
+    // if any direct precedes, unless that head was a ZERO element.
+    if (carry.h) head_slot = (dpos > 0) ? (int)(blockIdx.x * kDMax + dpos - 1) : -2;
+    int inh = carry.h ? 0 : 1;
+#pragma unroll
+    for (int k = 0; k < kPerThread; ++k) {
+      const long long i = b0 + k;
+      if (i >= n) break;
+      const double Pc = P + xv[k];
+      int e = 0;
+      Mono m;
+      const int c = seq_classify(i == 0, P, Pc, xv[k], mg, &e, &m);
+      if (c == CLS_REG) {
+        M = mono_cat(M, m);
+        o.e[i] = (short)e;
+        o.m[i] = M;
+        o.slot[i] = head_slot;
+        prev_e = (short)e;
+      } else if (c == CLS_DIRECT) {
+        const int slot = (int)(blockIdx.x * kDMax + dpos);
+        if (!over) {
+          o.dl_x[slot] = xv[k];
+          o.dl_m[slot] = M;
+          o.dl_e[slot] = prev_e;
+          o.dl_inh[slot] = inh;
+        }
+        o.e[i] = E_DIRECT;
+        o.slot[i] = slot;
+        ++dpos;
+        head_slot = slot;
+        M = mono_id();
+        inh = 0;
+        prev_e = E_DIRECT;
+      } else {
+        o.e[i] = E_ZERO;
+        o.slot[i] = -2;
+        head_slot = -2;
+        M = mono_id();
+        inh = 0;
+        prev_e = E_ZERO;
+      }
+      P = Pc;
+    }
+  }
+  const long long last = min(n, bb + kBS) - 1;  // the block's last element
+  if ((last - bb) / kPerThread == (long long)threadIdx.x) o.blast[blockIdx.x] = le;
+}
+
+struct WalkOut {
+  double* head_val;  // per slot
+  Mono* carry_in;    // per block
+  int* inh_head;     // per block: slot of the last head before the block (-2 zero)
+  double* total;
+};
+
+__device__ __forceinline__ bool is_reg_e(short e) { return e >= -1100 && e <= 1100; }
+
+// Sequential walker over the (few) direct elements, one thread.
+__global__ void k_seq_walk(long long nb, LocalOut o, WalkOut w, unsigned* flags) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (*flags & FLAG_SEQSUM) return;
+  Seg carry{0, mono_id()};
+  double head = 0.0;
+  int head_slot = -2;
+  short prev_last = E_ZERO;
+  bool ok = true;
+  for (long long b = 0; b < nb && ok; ++b) {
+    w.carry_in[b] = carry.m;
+    w.inh_head[b] = head_slot;
+    const int nd = o.bnd[b];
+    for (int q = 0; q < nd && ok; ++q) {
+      const int slot = (int)(b * kDMax + q);
+      const Mono M = o.dl_inh[slot] ? mono_cat(carry.m, o.dl_m[slot]) : o.dl_m[slot];
+      const short eb = (o.dl_e[slot] == (short)0x7ffe) ? prev_last : o.dl_e[slot];
+      double acc = head;
+      if (is_reg_e(eb)) ok = seq_apply_run(head, eb, M, &acc);
+      acc = dadd(acc, o.dl_x[slot]);
+      head = acc;
+      head_slot = slot;
+      w.head_val[slot] = acc;
+    }
+    const Seg a = o.bagg[b];
+    carry = a.h ? a : Seg{carry.h, mono_cat(carry.m, a.m)};
+    prev_last = o.blast[b];
+  }
+  double total = head;
+  if (ok && is_reg_e(prev_last)) ok = seq_apply_run(head, prev_last, carry.m, &total);
+  if (!ok) atomicOr(flags, FLAG_SEQSUM);
+  else *w.total = total;
+}
+
+__global__ void k_seq_final(long long n, LocalOut o, WalkOut w, double* cum,
+                            const unsigned* flags) {
+  if (*flags & FLAG_SEQSUM) return;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const short e = o.e[i];
+  double c;
+  if (e == E_ZERO) {
+    c = 0.0;
+  } else if (e == E_DIRECT) {
+    c = w.head_val[o.slot[i]];
+  } else {
+    const long long b = i / kBS;
+    const int s = o.slot[i];
+    const int hs = s >= 0 ? s : w.inh_head[b];
+    const Mono M = s >= 0 ? o.m[i] : mono_cat(w.carry_in[b], o.m[i]);
+    c = dmake(mono_apply(M, dsig(w.head_val[hs])), e);
+  }
+  cum[i] = c;
+}
+
+// Plain sequential loop: taken only when a self-check failed.
+__global__ void k_seq_fallback(const double* x, long long n, double* cum, double* total,
+                               const unsigned* flags) {
+  if (!(*flags & FLAG_SEQSUM)) return;
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double acc = 0.0;
+  for (long long i = 0; i < n; ++i) {
+    acc = dadd(acc, x[i]);
+    if (cum) cum[i] = acc;
+  }
+  *total = acc;
+}
+
+}  // namespace
+
+void seq_cumsum(Ctx* ctx, const double* x, int64_t n, double* cum, double* d_total) {
+  if (n <= 0) {
+    ctx->zero(d_total, sizeof(double));
+    return;
+  }
+  const long long nb = (n + kBS - 1) / kBS;
+  Buf<double> bsum(ctx, nb), bpre(ctx, nb);
+  Buf<short> ge(ctx, n);
+  Buf<Mono> gm(ctx, n);
+  Buf<int> gslot(ctx, n);
+  Buf<double> dlx(ctx, nb * kDMax);
+  Buf<Mono> dlm(ctx, nb * kDMax);
+  Buf<short> dle(ctx, nb * kDMax);
+  Buf<int> dli(ctx, nb * kDMax);
+  Buf<int> bnd(ctx, nb);
+  Buf<Seg> bagg(ctx, nb);
+  Buf<short> blast(ctx, nb);
+  Buf<double> headv(ctx, nb * kDMax);
+  Buf<Mono> cin(ctx, nb);
+  Buf<int> inh(ctx, nb);
+  Buf<unsigned> fl(ctx, 1);
+  fl.zero();
+  LocalOut o{ge.p, gm.p, gslot.p, dlx.p, dlm.p, dle.p, dli.p, bnd.p, bagg.p, blast.p};
+  WalkOut w{headv.p, cin.p, inh.p, d_total};
+  LAUNCH(ctx, k_chunk_sum, (unsigned)nb, kThreads, 0, x, (long long)n, bsum.p);
+  LAUNCH(ctx, k_scan_bsum, 1, 1024, 0, bsum.p, nb, bpre.p);
+  LAUNCH(ctx, k_seq_local, (unsigned)nb, kThreads, 0, x, (long long)n, bpre.p, o, fl.p);
+  LAUNCH(ctx, k_seq_walk, 1, 32, 0, nb, o, w, fl.p);
+  if (cum) LAUNCH(ctx, k_seq_final, ceil_div(n, 256), 256, 0, (long long)n, o, w, cum, fl.p);
+  LAUNCH(ctx, k_seq_fallback, 1, 32, 0, x, (long long)n, cum, d_total, fl.p);
+}
+
+// ---------------------------------------------------------------------------
+// Sampling law.
+namespace {
+
+__global__ void k_probs(const double* __restrict__ norms, long long F, const double* total,
+                        double* probs, int* last_pos) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= F) return;
+  const double p = ddiv(norms[i], *total);  // sampling.cpp:29
+  probs[i] = p;
+  if (p > 0.0) atomicMax(last_pos, (int)i);
+}
+
+__global__ void k_lastpos(const double* probs, long long n, int* last_pos) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && probs[i] > 0.0) atomicMax(last_pos, (int)i);
+}
+
+__global__ void k_clamp(double* cum, long long F, const int* last_pos, unsigned* flags) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lp = *last_pos;
+  if (lp < 0) {
+    if (i == 0) atomicOr(flags, FLAG_EMPTY);  // all-zero law: EmptyInputError
+    return;
+  }
+  if (i < F && i >= lp) cum[i] = 1.0;  // sampling.cpp:54
+}
+
+}  // namespace
+
+void sampling_law(Ctx* ctx, const double* norms, int64_t F, double* d_total, double* probs,
+                  double* cum, unsigned* d_law_flags) {
+  Buf<double> scratch(ctx, F > 0 ? F : 1);
+  seq_cumsum(ctx, norms, F, scratch.p, d_total);  // T: sequential over columns
+  Buf<int> lp(ctx, 1);
+  CUDA_OK(cudaMemsetAsync(lp.p, 0xff, sizeof(int), ctx->stream));
+  if (F > 0) LAUNCH(ctx, k_probs, ceil_div(F, 256), 256, 0, norms, (long long)F, d_total, probs, lp.p);
+  Buf<double> t2(ctx, 1);
+  seq_cumsum(ctx, probs, F, cum, t2.p);
+  LAUNCH(ctx, k_clamp, ceil_div(F > 0 ? F : 1, 256), 256, 0, cum, (long long)F, lp.p, d_law_flags);
+}
+
+void clamped_cdf(Ctx* ctx, const double* probs, int64_t n, double* cum, unsigned* d_flags) {
+  Buf<int> lp(ctx, 1);
+  CUDA_OK(cudaMemsetAsync(lp.p, 0xff, sizeof(int), ctx->stream));
+  Buf<double> t(ctx, 1);
+  seq_cumsum(ctx, probs, n, cum, t.p);
+  if (n > 0) LAUNCH(ctx, k_lastpos, ceil_div(n, 256), 256, 0, probs, (long long)n, lp.p);
+  LAUNCH(ctx, k_clamp, ceil_div(n > 0 ? n : 1, 256), 256, 0, cum, (long long)n, lp.p, d_flags);
+}
+
+}  // namespace ctdgpu

@@ -1,0 +1,169 @@
+// Orchestration of Algorithm 1 (CTD-S, ctd_static.cpp:19-50) and
+// Algorithm 2 (CTD-D step, ctd_dynamic.cpp:149-229) on the device.
+#include "cdf.cuh"
+#include "ctd.cuh"
+#include "relerr.cuh"
+#include "sample.cuh"
+
+namespace ctdgpu {
+
+namespace {
+
+__global__ void k_make_cands(const int32_t* uniq, const int* n_u, const int64_t* fptr, int64_t* off,
+                             int32_t* len) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *n_u) return;
+  const int f = uniq[i];
+  off[i] = fptr[f];
+  len[i] = (int32_t)(fptr[f + 1] - fptr[f]);
+}
+
+__global__ void k_gather_cols(const int32_t* fib, long long n, const int64_t* fcol, int64_t* out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = fcol[fib[i]];
+}
+
+// Front end shared by CTD-S and the CTD-D step: law, draws, dedup, filter.
+struct Front {
+  std::vector<int64_t> drawn, unique;
+  BatchOut bo;
+  double total = 0.0;
+};
+
+void front_end(Ctx* ctx, const Fibers& fb, Basis& basis, int64_t s, double eps, uint64_t seed,
+               Front& fr, bool trace) {
+  const int64_t F = fb.F;
+  Buf<double> probs(ctx, F + 1), cum(ctx, F + 1), total(ctx, 1);
+  sampling_law(ctx, fb.norm.p, F, total.p, probs.p, cum.p, ctx->d_flags);
+  Buf<int32_t> drawn(ctx, s), uniq(ctx, s);
+  Buf<int> nu(ctx, 1);
+  draw_fibers(ctx, cum.p, F, s, seed, drawn.p);
+  dedup_first(ctx, drawn.p, s, uniq.p, nu.p);
+  int n_u = 0;
+  ctx->to_host(&n_u, nu.p, 1);
+  ctx->to_host(&fr.total, total.p, 1);
+  ctx->sync();
+  ctx->check_flags("sampling");
+  Buf<int64_t> coff(ctx, n_u + 1);
+  Buf<int32_t> clen(ctx, n_u + 1);
+  if (n_u > 0) LAUNCH(ctx, k_make_cands, ceil_div(n_u, 256), 256, 0, uniq.p, nu.p, fb.ptr.p, coff.p, clen.p);
+  Cands c;
+  c.n = n_u;
+  c.off = coff.p;
+  c.len = clen.p;
+  c.row = fb.row.p;
+  c.val = fb.val.p;
+  filter_batch(basis, c, eps, fr.bo, false);
+  // column ids of the draws / unique candidates (host trace)
+  Buf<int64_t> cols(ctx, s + 1);
+  if (trace) {
+    fr.drawn.resize(s);
+    LAUNCH(ctx, k_gather_cols, ceil_div(s, 256), 256, 0, drawn.p, (long long)s, fb.col.p, cols.p);
+    ctx->to_host(fr.drawn.data(), cols.p, s);
+    ctx->sync();
+  }
+  fr.unique.resize(n_u);
+  if (n_u > 0) {
+    LAUNCH(ctx, k_gather_cols, ceil_div(n_u, 256), 256, 0, uniq.p, (long long)n_u, fb.col.p, cols.p);
+    ctx->to_host(fr.unique.data(), cols.p, n_u);
+    ctx->sync();
+  }
+}
+
+void check_ctd_s_args(const Tensor& x, int mode, int64_t s, double eps) {
+  // ctd_static.cpp:21-27
+  if (x.nnz == 0) fail(CTD_ERR_EMPTY_INPUT, "cannot decompose an empty tensor");
+  if (mode < 0 || mode >= x.order)
+    fail(CTD_ERR_ARGUMENT, "mode " + std::to_string(mode) + " out of range for order " +
+                               std::to_string(x.order));
+  if (s < 1) fail(CTD_ERR_ARGUMENT, "sample size must be at least 1");
+  if (!(eps > 0.0)) fail(CTD_ERR_ARGUMENT, "epsilon must be positive");
+}
+
+}  // namespace
+
+void build_law(Ctx* ctx, const Tensor& x, int mode, Law& law) {
+  matricize(ctx, x, mode, law.fb);
+  if (law.fb.nnz == 0) fail(CTD_ERR_EMPTY_INPUT, "column distribution of an all-zero matrix");
+  const int64_t F = law.fb.F;
+  law.probs.alloc(ctx, F + 1);
+  law.cum.alloc(ctx, F + 1);
+  law.total.alloc(ctx, 1);
+  sampling_law(ctx, law.fb.norm.p, F, law.total.p, law.probs.p, law.cum.p, ctx->d_flags);
+  ctx->sync();
+  ctx->check_flags("column_distribution");
+}
+
+void run_ctd_s(Ctx* ctx, const Tensor& x, int mode, int64_t s, double eps, uint64_t seed,
+               unsigned flags, Factors& out) {
+  check_ctd_s_args(x, mode, s, eps);
+  out.ctx = ctx;
+  out.order = x.order;
+  out.mode = mode;
+  for (int k = 0; k < x.order; ++k) out.shape[k] = x.shape[k];
+  out.eps = eps;
+  out.seed = seed;
+  Fibers fb;
+  matricize(ctx, x, mode, fb);
+  out.F = fb.F;
+  out.cols = fb.cols;
+  out.rows = fb.rows;
+  out.integer_exact = fb.integer_exact;
+  out.basis = std::make_unique<Basis>(ctx, fb.rows);
+  Front fr;
+  front_end(ctx, fb, *out.basis, s, eps, seed, fr, true);
+  out.total = fr.total;
+  out.drawn = std::move(fr.drawn);
+  out.unique = std::move(fr.unique);
+  out.accepted = fr.bo.accepted;
+  out.degenerate = fr.bo.degenerate;
+  out.delta = fr.bo.delta;
+  out.slow_path = fr.bo.slow_path;
+  for (int32_t k : fr.bo.kept_cand) out.kept_flat.push_back(out.unique[k]);
+  for (size_t i = 0; i < fr.bo.res_sq.size(); ++i) {
+    const double xs = fr.bo.x_sq[i];
+    if (xs > 0.0 && fr.bo.res_sq[i] > 0.0) {
+      const double m = std::fabs(std::log10(std::sqrt(fr.bo.res_sq[i] / xs) / eps));
+      out.min_margin = std::min(out.min_margin, m);
+    }
+  }
+  if (flags & CTD_GPU_WITH_ERROR) out.rel_error = relative_error(ctx, fb, *out.basis);
+}
+
+void stream_init(Ctx* ctx, const Tensor& hist, int mode, int64_t s, double eps, uint64_t seed,
+                 Stream& out) {
+  // ctd_dynamic.cpp:133-136
+  if (hist.order < 2) fail(CTD_ERR_ARGUMENT, "a stream needs at least one non-time mode");
+  if (mode < 0 || mode >= hist.order - 1) fail(CTD_ERR_ARGUMENT, "mode must precede the time mode");
+  Factors f;
+  run_ctd_s(ctx, hist, mode, s, eps, seed, 0, f);
+  out.ctx = ctx;
+  out.order = hist.order;
+  out.mode = mode;
+  for (int k = 0; k + 1 < hist.order; ++k) out.slab_shape[k] = hist.shape[k];
+  out.t = hist.shape[hist.order - 1];
+  out.eps = eps;
+  out.seed = seed;
+  out.basis = std::move(f.basis);
+  out.kept_flat = std::move(f.kept_flat);
+}
+
+void stream_step(Stream& st, const Tensor& slab, int64_t d) {
+  // ctd_dynamic.cpp:151-158
+  if (slab.order != st.order) fail(CTD_ERR_SHAPE, "slab order does not match the stream");
+  for (int k = 0; k + 1 < st.order; ++k)
+    if (slab.shape[k] != st.slab_shape[k]) fail(CTD_ERR_SHAPE, "slab extents do not match the stream");
+  if (slab.shape[st.order - 1] != 1) fail(CTD_ERR_SHAPE, "slab must have time extent 1");
+  if (d < 1) fail(CTD_ERR_ARGUMENT, "sample size must be at least 1");
+  Ctx* ctx = st.ctx;
+  if (slab.nnz > 0) {  // :173-188
+    Fibers fb;
+    matricize(ctx, slab, st.mode, fb);
+    Front fr;
+    front_end(ctx, fb, *st.basis, d, st.eps, st.seed ^ (uint64_t)st.t, fr, false);
+    for (int32_t k : fr.bo.kept_cand) st.kept_flat.push_back(fr.unique[k] + st.t * fb.cols);
+  }
+  st.t += 1;  // :227
+}
+
+}  // namespace ctdgpu

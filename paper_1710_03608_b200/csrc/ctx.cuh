@@ -1,0 +1,100 @@
+// Context, device buffers and tensor handles.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace ctdgpu {
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  unsigned* d_flags = nullptr;   // kernel-raised error flags (FLAG_*)
+  unsigned* d_bar = nullptr;     // grid-barrier words for persistent kernels
+  int64_t launches = 0;          // kernels launched on this context
+
+  void* alloc_bytes(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 16;
+    CUDA_OK(cudaMallocAsync(&p, n, stream));
+    return p;
+  }
+  template <typename T>
+  T* alloc(size_t n) { return static_cast<T*>(alloc_bytes(n * sizeof(T))); }
+  void release(void* p) {
+    if (p) cudaFreeAsync(p, stream);
+  }
+  void sync() { CUDA_OK(cudaStreamSynchronize(stream)); }
+  void zero(void* p, size_t bytes) { CUDA_OK(cudaMemsetAsync(p, 0, bytes, stream)); }
+  template <typename T>
+  void to_host(T* dst, const T* src, size_t n) {
+    if (n) CUDA_OK(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, stream));
+  }
+  template <typename T>
+  void to_dev(T* dst, const T* src, size_t n) {
+    if (n) CUDA_OK(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, stream));
+  }
+  template <typename T>
+  T read1(const T* src) {
+    T v;
+    to_host(&v, src, 1);
+    sync();
+    return v;
+  }
+  // Reads and clears the kernel error flags; raises the mapped status.
+  void check_flags(const char* where);
+};
+
+// RAII device buffer (stream-ordered allocation on the context stream).
+template <typename T>
+struct Buf {
+  Ctx* c = nullptr;
+  T* p = nullptr;
+  size_t n = 0;
+  Buf() = default;
+  Buf(Ctx* ctx, size_t count) : c(ctx), p(ctx->alloc<T>(count)), n(count) {}
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
+  Buf(Buf&& o) noexcept : c(o.c), p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  Buf& operator=(Buf&& o) noexcept {
+    if (this != &o) { reset(); c = o.c; p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~Buf() { reset(); }
+  void reset() {
+    if (p && c) c->release(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(Ctx* ctx, size_t count) { reset(); c = ctx; p = ctx->alloc<T>(count); n = count; }
+  void ensure(Ctx* ctx, size_t count) { if (n < count || !p) alloc(ctx, count); }
+  void zero() { if (p) c->zero(p, n * sizeof(T)); }
+  T* get() const { return p; }
+};
+
+constexpr int kMaxOrder = 16;
+
+// SparseTensor (sparse_tensor.hpp:17-60) resident in HBM as SoA int32
+// coordinates + fp64 values, lexicographically sorted and coalesced.
+struct Tensor {
+  Ctx* ctx = nullptr;
+  int order = 0;
+  int64_t shape[kMaxOrder] = {0};
+  int64_t nnz = 0;
+  const int32_t* idx[kMaxOrder] = {nullptr};
+  const double* val = nullptr;
+  Buf<int32_t> own_idx;  // owned storage when built from host
+  Buf<double> own_val;
+};
+
+// Launch helper: counts launches and checks launch errors.
+#define LAUNCH(ctx, kern, grid, block, smem, ...)                                   \
+  do {                                                                              \
+    kern<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);                  \
+    (ctx)->launches++;                                                              \
+    CUDA_OK(cudaGetLastError());                                                    \
+  } while (0)
+
+}  // namespace ctdgpu

@@ -1,0 +1,632 @@
+// Linear-independence filter + U recurrence (FiberBasis::try_append_fiber,
+// fiber_basis.cpp:43-109), replayed bit-exactly on the device.
+//
+// The loop over candidates is inherently sequential (each accept changes R
+// and U), so it runs as ONE persistent cooperative kernel over all SMs with
+// a software grid barrier between dependent phases.  Per candidate n:
+//   P0 (if n-1 was accepted) U <- [[U + y y^T/d, -y/d], [-y^T/d, 1/d]]
+//      elementwise over (K+1)^2 (fiber_basis.cpp:92-106); append x_{n-1} to R,
+//      to R's row index and to the first-appearance row order.
+//   P1 y = U g, one thread per row, each a sequential fl() chain in column
+//      order (DenseMatrix::matvec, dense_matrix.cpp:42-47).  g = R^T x comes
+//      from a Gram table precomputed in parallel before the loop: every g_k
+//      is a sorted-merge dot product (gram_coeffs, fiber_basis.cpp:21-41)
+//      whose only nonzero terms are the common rows in ascending order, so
+//      a dense-lookup chain over c_k's rows adds exactly the same terms.
+//   P2 z_r = sum_k y_k R[r,k] per row of R in ascending k (the reference's
+//      scatter order, :56-65); the squared residual terms are laid out in the
+//      reference's summation order: x's rows ascending, then R's rows in
+//      first-touch order (:66-77).
+//   P3 every CTA computes res^2 = the exact sequential sum of those terms
+//      (seqsum.cuh) redundantly — no barrier needed after it — and takes the
+//      decision sqrt(res^2) <= eps sqrt(|x|^2) (:79) and the delta guard
+//      (:83-88).
+// All arithmetic that restates the reference uses __dmul_rn/__dadd_rn/
+// __ddiv_rn (no FMA), so kept fibers, delta and U are bit-identical.
+#include <algorithm>
+#include <cmath>
+
+#include "filter.cuh"
+#include "radix.cuh"
+#include "seqsum.cuh"
+
+namespace ctdgpu {
+
+Basis::Basis(Ctx* c, int64_t d) : ctx(c), dim(d) {
+  rowbase.alloc(c, d + 1);
+  rowbase.zero();
+  rowlen.alloc(c, d + 1);
+  rowlen.zero();
+  sr_list.alloc(c, d + 1);
+  sr_pos.alloc(c, d + 1);
+  CUDA_OK(cudaMemsetAsync(sr_pos.p, 0xff, (d + 1) * sizeof(int32_t), c->stream));
+  sr_n.alloc(c, 1);
+  sr_n.zero();
+  tag.alloc(c, d + 1);
+  tag.zero();
+  zd.alloc(c, 2 * (d + 1));
+  kf.alloc(c, d + 1);
+  rptr.alloc(c, 1);
+  rptr.zero();
+}
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T ldg_cg(const T* p) { return __ldcg(p); }
+
+// ---------------------------------------------------------------------------
+// Preparation kernels.
+__global__ void k_cand_stats(Cands c, long long* total_len) {
+  long long s = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < c.n;
+       i += (long long)gridDim.x * blockDim.x)
+    s += c.len[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd((unsigned long long*)total_len, (unsigned long long)s);
+}
+
+// per-row count of candidate entries (for row-index capacity)
+__global__ void k_count_rows(Cands c, int32_t* cnt) {
+  const long long cand = blockIdx.x;
+  if (cand >= c.n) return;
+  const long long off = c.off[cand];
+  for (int t = threadIdx.x; t < c.len[cand]; t += blockDim.x) atomicAdd(&cnt[c.row[off + t]], 1);
+}
+
+__global__ void k_row_caps(const int32_t* rowlen, const int32_t* cnt, long long dim, long long* cap) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < dim) cap[r] = (long long)rowlen[r] + cnt[r];
+}
+
+__global__ void k_excl_scan_ll(const long long* in, long long n, long long* out) {
+  __shared__ long long sh[33];
+  long long carry = 0;
+  for (long long b0 = 0; b0 < n; b0 += (long long)blockDim.x * 4) {
+    long long v[4], s = 0;
+    const long long base = b0 + (long long)threadIdx.x * 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = (base + k < n) ? in[base + k] : 0;
+      s += v[k];
+    }
+    long long tot;
+    long long pre = block_excl_sum<long long>(s, sh, &tot) + carry;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (base + k < n) out[base + k] = pre;
+      pre += v[k];
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
+__global__ void k_copy_rows(const long long* oldbase, const long long* newbase, const int32_t* rowlen,
+                            const int32_t* ok, const double* ov, int32_t* nk, double* nv, long long dim) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= dim) return;
+  const long long a = oldbase[r], b = newbase[r];
+  for (int t = 0; t < rowlen[r]; ++t) {
+    nk[b + t] = ok[a + t];
+    nv[b + t] = ov[a + t];
+  }
+}
+
+__global__ void k_copy_u(const double* src, long long ld_src, double* dst, long long ld_dst, long long k) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= k * k) return;
+  const long long i = e / k, j = e % k;
+  dst[i * ld_dst + j] = src[i * ld_src + j];
+}
+
+// x_sq = SparseVec::squared_norm (sparse_matrix.cpp:10-14), exact sequential.
+__global__ void __launch_bounds__(256) k_xsq(Cands c, double* xsq, unsigned* flags) {
+  __shared__ SeqSumSmem S;
+  const long long cand = blockIdx.x;
+  if (cand >= c.n) return;
+  const double* v = c.val + c.off[cand];
+  auto get = [v](long long i) { return dsqr(v[i]); };
+  bool bad = false;
+  const double s = block_exact_sum(get, c.len[cand], S, &bad);
+  if (threadIdx.x == 0) {
+    xsq[cand] = s;
+    if (bad) atomicOr(flags, FLAG_SEQSUM);
+  }
+}
+
+// Dense candidate matrix D[row][cand] (dim x n), zeroed beforehand.
+__global__ void k_dense_cands(Cands c, double* D, long long n) {
+  const long long cand = blockIdx.x;
+  if (cand >= c.n) return;
+  const long long off = c.off[cand];
+  for (int t = threadIdx.x; t < c.len[cand]; t += blockDim.x)
+    D[(long long)c.row[off + t] * n + cand] = c.val[off + t];
+}
+
+// G[a][b] = merge-dot(left column a, candidate b) for b > a_min(a):
+// sequential over the left column's rows ascending; D lookups are exactly 0
+// off the common support, and adding fl(v*0) = +-0 never changes the sum.
+__global__ void k_gram(const int64_t* lptr_off, const int32_t* llen, const int64_t* lptr, int use_ptr,
+                       const int32_t* lrow, const double* lval, long long nleft, const double* D,
+                       long long n, double* G, int strictly_upper) {
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nbw = (n + 31) >> 5;
+  const long long a = warp / nbw;
+  if (a >= nleft) return;
+  const long long b = (warp % nbw) * 32 + (threadIdx.x & 31);
+  if (strictly_upper && ((warp % nbw) * 32 + 31) <= a) return;  // whole warp below diagonal
+  long long off, len;
+  if (use_ptr) {
+    off = lptr[a];
+    len = lptr[a + 1] - off;
+  } else {
+    off = lptr_off[a];
+    len = llen[a];
+  }
+  double s = 0.0;
+  const bool act = b < n && (!strictly_upper || b > a);
+  for (long long t = 0; t < len; ++t) {
+    const int r = lrow[off + t];
+    const double x = lval[off + t];
+    if (act) s = dadd(s, dmul(x, D[(long long)r * n + b]));
+  }
+  if (act) G[a * n + b] = s;
+}
+
+// ---------------------------------------------------------------------------
+// The persistent filter kernel.
+struct FArgs {
+  int n_u;
+  int K0;
+  long long dim;
+  long long LD;
+  Cands c;
+  const double* xsq;
+  const double* Gc;  // [n_u][n_u] candidate x candidate (a < b)
+  const double* Gb;  // [K0][n_u] basis x candidate
+  double eps;
+  double* U;
+  int64_t* rptr;
+  int32_t* rrow;
+  double* rval;
+  long long rnnz0;
+  const int64_t* rowbase;
+  int32_t* rowlen;
+  int32_t* rek;
+  double* rev;
+  int32_t* sr_list;
+  int32_t* sr_pos;
+  int* sr_n;
+  uint32_t* tag;
+  uint32_t tag_base;
+  double* zd;
+  int32_t* kf;
+  double* term;      // [dim]
+  double* term2;     // [dim] slow-path ordered terms
+  uint32_t* skey;    // [4*dim] slow-path sort scratch
+  double* ybuf0;
+  double* ybuf1;
+  int* kept_cand;
+  int* slow;         // [n_u] per-candidate slow-path flag
+  int32_t* accepted;
+  int32_t* degenerate;
+  double* delta;
+  double* res_out;
+  double* y_last;
+  long long* final_K;
+  long long* final_rnnz;
+  unsigned* bar;
+  unsigned* flags;
+};
+
+constexpr int kFThreads = 512;
+
+__global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
+  __shared__ SeqSumSmem S;
+  __shared__ uint32_t hist[(kFThreads / 32) * kRadix];
+  __shared__ uint32_t sh32[33];
+  __shared__ int shi[33];
+  __shared__ int s_cnt;
+  const unsigned nb = gridDim.x;
+  const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long gthreads = (long long)nb * blockDim.x;
+  const long long LD = a.LD;
+  int K = a.K0;
+  long long rnnz = a.rnnz0;
+  bool prev_acc = false;
+  double prev_delta = 0.0;
+  int prev_n = -1;
+  for (int n = 0; n <= a.n_u; ++n) {
+    double* yprev = (n & 1) ? a.ybuf0 : a.ybuf1;
+    double* ycur = (n & 1) ? a.ybuf1 : a.ybuf0;
+    // ---------------- P0: apply the previous accept -------------------------
+    if (prev_acc) {
+      const int Ko = K;
+      const long long K1 = Ko + 1;
+      const long long tot = K1 * K1;
+      for (long long e = gtid; e < tot; e += gthreads) {
+        const long long i = e / K1, j = e - i * K1;
+        double v;
+        if (i < Ko && j < Ko) {
+          v = dadd(ldg_cg(&a.U[i * LD + j]), ddiv(dmul(ldg_cg(&yprev[i]), ldg_cg(&yprev[j])), prev_delta));
+        } else if (i == Ko && j == Ko) {
+          v = ddiv(1.0, prev_delta);
+        } else {
+          const long long q = (i == Ko) ? j : i;
+          v = ddiv(-ldg_cg(&yprev[q]), prev_delta);
+        }
+        a.U[i * LD + j] = v;
+      }
+      const long long off = a.c.off[prev_n];
+      const int m = a.c.len[prev_n];
+      for (long long t = gtid; t < m; t += gthreads) {
+        const int r = a.c.row[off + t];
+        const double v = a.c.val[off + t];
+        a.rrow[rnnz + t] = r;
+        a.rval[rnnz + t] = v;
+        const int L = ldg_cg(&a.rowlen[r]);
+        const long long p = a.rowbase[r] + L;
+        a.rek[p] = Ko;
+        a.rev[p] = v;
+        a.rowlen[r] = L + 1;
+      }
+      if (blockIdx.x == 0) {
+        // Ordered append of x's rows not yet in R (first-appearance order).
+        int srn = ldg_cg(a.sr_n);
+        for (int base = 0; base < m; base += blockDim.x) {
+          const int t = base + threadIdx.x;
+          const int r = t < m ? a.c.row[off + t] : 0;
+          const int isnew = (t < m) && (ldg_cg(&a.sr_pos[r]) < 0);
+          int tot2;
+          const int pos = block_excl_sum<int>(isnew, shi, &tot2);
+          if (isnew) {
+            a.sr_list[srn + pos] = r;
+            a.sr_pos[r] = srn + pos;
+          }
+          srn += tot2;
+          __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+          *a.sr_n = srn;
+          a.kept_cand[Ko - a.K0] = prev_n;
+          a.rptr[Ko + 1] = rnnz + m;
+        }
+      }
+      rnnz += m;
+      K = Ko + 1;
+      grid_barrier(a.bar, nb);
+    }
+    if (n == a.n_u) break;
+    // ---------------- P1: y = U g --------------------------------------------
+    const long long off = a.c.off[n];
+    const int m = a.c.len[n];
+    const uint32_t tg = a.tag_base + (uint32_t)n + 1u;
+    // zd is double-buffered by candidate parity: CTAs still in P3 of n-1 read
+    // the other half.  x's rows start at z = 0 (rows outside R are untouched).
+    double* zdn = a.zd + (n & 1) * (a.dim + 1);
+    for (long long t = gtid; t < m; t += gthreads) {
+      a.tag[a.c.row[off + t]] = tg;
+      zdn[a.c.row[off + t]] = 0.0;
+    }
+    for (long long i = gtid; i < K; i += gthreads) {
+      double acc = 0.0;
+      for (int j = 0; j < K; ++j) {
+        const double g = (j < a.K0) ? a.Gb[(long long)j * a.n_u + n]
+                                    : a.Gc[(long long)ldg_cg(&a.kept_cand[j - a.K0]) * a.n_u + n];
+        // U is exactly symmetric: U[j][i] == U[i][j], read down column i (coalesced).
+        acc = dadd(acc, dmul(ldg_cg(&a.U[(long long)j * LD + i]), g));
+      }
+      ycur[i] = acc;
+    }
+    grid_barrier(a.bar, nb);
+    // ---------------- P2: z over R's rows, residual terms ---------------------
+    const int srn = ldg_cg(a.sr_n);
+    for (long long q = gtid; q < srn; q += gthreads) {
+      const int r = ldg_cg(&a.sr_list[q]);
+      const long long b0 = a.rowbase[r];
+      const int L = ldg_cg(&a.rowlen[r]);
+      double z = 0.0;
+      int kfd = -1;
+      int kst = -1;
+      for (int e = 0; e < L; ++e) {
+        const int k = ldg_cg(&a.rek[b0 + e]);
+        const double yk = ldg_cg(&ycur[k]);
+        z = dadd(z, dmul(yk, ldg_cg(&a.rev[b0 + e])));
+        if (kst < 0) kst = k;
+        if (kfd < 0 && yk != 0.0) kfd = k;
+      }
+      zdn[r] = z;
+      a.kf[r] = kfd;
+      a.term[q] = (ldg_cg(&a.tag[r]) == tg) ? 0.0 : dsqr(z);
+      // touched order differs from first-appearance order only if the row's
+      // first kept column has y == 0 while the row is still touched.
+      if (z != 0.0 && kfd != kst) atomicExch(&a.slow[n], 1);
+    }
+    grid_barrier(a.bar, nb);
+    // ---------------- P3: exact residual, decision (every CTA) ---------------
+    const bool slow = ldg_cg(&a.slow[n]) != 0;
+    long long nterm = srn;
+    const double* tsrc = a.term;
+    if (slow) {
+      // Rebuild the touched list in the reference's order: rows r not in x
+      // with kfd(r) >= 0, sorted by (kfd, position within column kfd) which is
+      // (kfd, r).  Done by CTA 0, then shared through a barrier.
+      if (blockIdx.x == 0) {
+        uint32_t* ka = a.skey;
+        uint32_t* kb = ka + a.dim;
+        uint32_t* ia = kb + a.dim;
+        uint32_t* ib = ia + a.dim;
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+        for (int q = threadIdx.x; q < srn; q += blockDim.x) {
+          const int r = ldg_cg(&a.sr_list[q]);
+          if (ldg_cg(&a.kf[r]) >= 0 && ldg_cg(&a.tag[r]) != tg) {
+            const int p = atomicAdd(&s_cnt, 1);
+            ka[p] = (uint32_t)r;
+            ia[p] = (uint32_t)r;
+          }
+        }
+        __syncthreads();
+        const int cnt = s_cnt;
+        // sort by r, then stable by kfd
+        bool inb = block_radix_sort<uint32_t>(ka, kb, ia, ib, cnt, 32, hist, sh32);
+        uint32_t* K2 = inb ? kb : ka;
+        uint32_t* I2 = inb ? ib : ia;
+        uint32_t* K3 = inb ? ka : kb;
+        uint32_t* I3 = inb ? ia : ib;
+        for (int p = threadIdx.x; p < cnt; p += blockDim.x) {
+          K3[p] = (uint32_t)ldg_cg(&a.kf[I2[p]]);
+          I3[p] = I2[p];
+        }
+        __syncthreads();
+        inb = block_radix_sort<uint32_t>(K3, K2, I3, I2, cnt, 32, hist, sh32);
+        const uint32_t* IF = inb ? I2 : I3;
+        for (int p = threadIdx.x; p < cnt; p += blockDim.x) a.term2[p] = dsqr(ldg_cg(&zdn[IF[p]]));
+        if (threadIdx.x == 0) a.slow[n] = 2 + cnt;  // publish count
+      }
+      grid_barrier(a.bar, nb);
+      nterm = ldg_cg(&a.slow[n]) - 2;
+      tsrc = a.term2;
+    }
+    const double* xv = a.c.val + off;
+    const int32_t* xr = a.c.row + off;
+    const double* zd = zdn;
+    auto get = [=](long long i) -> double {
+      if (i < m) {
+        const int r = xr[i];
+        const double z = ldg_cg(&zd[r]);
+        return dsqr(dsub(xv[i], z));  // fiber_basis.cpp:69-70
+      }
+      return ldg_cg(&tsrc[i - m]);     // fiber_basis.cpp:74-75
+    };
+    bool bad = false;
+    const double res = block_exact_sum(get, (long long)m + nterm, S, &bad);
+    const double xs = a.xsq[n];
+    const bool reject = __dsqrt_rn(res) <= dmul(a.eps, __dsqrt_rn(xs));  // :79
+    bool acc = false, degen = false;
+    if (!reject) {
+      degen = !(res > 0.0) || isinf(res) || isnan(res) || isinf(ddiv(1.0, res));  // :84-85
+      acc = !degen;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.accepted[n] = acc;
+      a.degenerate[n] = degen;
+      a.delta[n] = acc ? res : 0.0;
+      a.res_out[n] = res;
+      if (bad) atomicOr(a.flags, FLAG_SEQSUM);
+    }
+    if (a.y_last && n == a.n_u - 1 && blockIdx.x == 0)
+      for (int i = threadIdx.x; i < K; i += blockDim.x) a.y_last[i] = ldg_cg(&ycur[i]);
+    prev_acc = acc;
+    prev_delta = res;
+    prev_n = n;
+    // P1 of the next candidate overwrites `tag` and the other y buffer only;
+    // zd/term are rewritten in its P2 after a barrier, so no barrier here.
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *a.final_K = K;
+    *a.final_rnnz = rnnz;
+  }
+}
+
+}  // namespace
+
+void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want_y) {
+  Ctx* ctx = B.ctx;
+  const int64_t n = c.n;
+  out = BatchOut{};
+  if (n == 0) return;
+  if (n >= (1ll << 31)) fail(CTD_ERR_ARGUMENT, "too many candidates");
+  // ---- sizes
+  Buf<long long> tl(ctx, 1);
+  tl.zero();
+  LAUNCH(ctx, k_cand_stats, std::min<unsigned>(ceil_div(n, 256), 1024), 256, 0, c, tl.p);
+  const long long total_len = ctx->read1(tl.p);
+  const int64_t K0 = B.K;
+  // ---- capacities: U, R columns, R entries
+  if (B.LD < K0 + n) {
+    const int64_t nld = std::max<int64_t>(K0 + n, B.LD * 2);
+    Buf<double> nu(ctx, (size_t)nld * nld);
+    if (K0 > 0)
+      LAUNCH(ctx, k_copy_u, ceil_div(K0 * K0, 256), 256, 0, B.U.p, (long long)B.LD, nu.p,
+             (long long)nld, (long long)K0);
+    B.U = std::move(nu);
+    B.LD = nld;
+  }
+  if (B.kcap < K0 + n) {
+    const int64_t nk = std::max<int64_t>(K0 + n, B.kcap * 2);
+    Buf<int64_t> np(ctx, nk + 1);
+    CUDA_OK(cudaMemcpyAsync(np.p, B.rptr.p, (K0 + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    B.rptr = std::move(np);
+    B.kcap = nk;
+  }
+  if (B.rcap < B.rnnz + total_len) {
+    const int64_t nr = std::max<int64_t>(B.rnnz + total_len, B.rcap * 2);
+    Buf<int32_t> nrow(ctx, nr);
+    Buf<double> nval(ctx, nr);
+    if (B.rnnz) {
+      CUDA_OK(cudaMemcpyAsync(nrow.p, B.rrow.p, B.rnnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+      CUDA_OK(cudaMemcpyAsync(nval.p, B.rval.p, B.rnnz * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    B.rrow = std::move(nrow);
+    B.rval = std::move(nval);
+    B.rcap = nr;
+  }
+  // ---- row index with room for every candidate entry
+  {
+    const long long dim = B.dim;
+    Buf<int32_t> cnt(ctx, dim + 1);
+    cnt.zero();
+    LAUNCH(ctx, k_count_rows, (unsigned)n, 128, 0, c, cnt.p);
+    Buf<int64_t> cap(ctx, dim + 1), nbase(ctx, dim + 1);
+    LAUNCH(ctx, k_row_caps, ceil_div(dim, 256), 256, 0, B.rowlen.p, cnt.p, dim, (long long*)cap.p);
+    LAUNCH(ctx, k_excl_scan_ll, 1, 1024, 0, (const long long*)cap.p, dim, (long long*)nbase.p);
+    const int64_t ncap = B.rnnz + total_len + 1;
+    Buf<int32_t> nk(ctx, ncap);
+    Buf<double> nv(ctx, ncap);
+    if (B.rnnz)
+      LAUNCH(ctx, k_copy_rows, ceil_div(dim, 256), 256, 0, (const long long*)B.rowbase.p,
+             (const long long*)nbase.p, B.rowlen.p, B.rek.p, B.rev.p, nk.p, nv.p, dim);
+    B.rowbase = std::move(nbase);
+    B.rek = std::move(nk);
+    B.rev = std::move(nv);
+    B.ricap = ncap;
+  }
+  // ---- per-candidate |x|^2, Gram tables
+  Buf<double> xsq(ctx, n);
+  LAUNCH(ctx, k_xsq, (unsigned)n, 256, 0, c, xsq.p, ctx->d_flags);
+  Buf<double> D(ctx, (size_t)B.dim * n);
+  D.zero();
+  LAUNCH(ctx, k_dense_cands, (unsigned)n, 128, 0, c, D.p, (long long)n);
+  Buf<double> Gc(ctx, (size_t)n * n);
+  {
+    const long long warps = n * ((n + 31) / 32);
+    LAUNCH(ctx, k_gram, ceil_div(warps * 32, 256), 256, 0, c.off, c.len, (const int64_t*)nullptr, 0,
+           c.row, c.val, (long long)n, D.p, (long long)n, Gc.p, 1);
+  }
+  Buf<double> Gb(ctx, K0 > 0 ? (size_t)K0 * n : 1);
+  if (K0 > 0) {
+    const long long warps = K0 * ((n + 31) / 32);
+    LAUNCH(ctx, k_gram, ceil_div(warps * 32, 256), 256, 0, (const int64_t*)nullptr, (const int32_t*)nullptr,
+           B.rptr.p, 1, B.rrow.p, B.rval.p, (long long)K0, D.p, (long long)n, Gb.p, 0);
+  }
+  D.reset();
+  // ---- persistent kernel
+  Buf<double> term(ctx, B.dim + 1), term2(ctx, B.dim + 1);
+  Buf<uint32_t> skey(ctx, 4 * (B.dim + 1));
+  Buf<double> y0(ctx, B.LD + 1), y1(ctx, B.LD + 1), ylast(ctx, B.LD + 1);
+  Buf<int> kept(ctx, n), slow(ctx, n);
+  slow.zero();
+  Buf<int32_t> acc(ctx, n), deg(ctx, n);
+  Buf<double> dl(ctx, n), res(ctx, n);
+  Buf<long long> fK(ctx, 1), fR(ctx, 1);
+  FArgs fa{};
+  fa.n_u = (int)n;
+  fa.K0 = (int)K0;
+  fa.dim = B.dim;
+  fa.LD = B.LD;
+  fa.c = c;
+  fa.xsq = xsq.p;
+  fa.Gc = Gc.p;
+  fa.Gb = Gb.p;
+  fa.eps = eps;
+  fa.U = B.U.p;
+  fa.rptr = B.rptr.p;
+  fa.rrow = B.rrow.p;
+  fa.rval = B.rval.p;
+  fa.rnnz0 = B.rnnz;
+  fa.rowbase = B.rowbase.p;
+  fa.rowlen = B.rowlen.p;
+  fa.rek = B.rek.p;
+  fa.rev = B.rev.p;
+  fa.sr_list = B.sr_list.p;
+  fa.sr_pos = B.sr_pos.p;
+  fa.sr_n = B.sr_n.p;
+  fa.tag = B.tag.p;
+  fa.tag_base = B.tag_base;
+  fa.zd = B.zd.p;
+  fa.kf = B.kf.p;
+  fa.term = term.p;
+  fa.term2 = term2.p;
+  fa.skey = skey.p;
+  fa.ybuf0 = y0.p;
+  fa.ybuf1 = y1.p;
+  fa.kept_cand = kept.p;
+  fa.slow = slow.p;
+  fa.accepted = acc.p;
+  fa.degenerate = deg.p;
+  fa.delta = dl.p;
+  fa.res_out = res.p;
+  fa.y_last = want_y ? ylast.p : nullptr;
+  fa.final_K = fK.p;
+  fa.final_rnnz = fR.p;
+  fa.bar = ctx->d_bar;
+  fa.flags = ctx->d_flags;
+  ctx->zero(ctx->d_bar, 2 * sizeof(unsigned));
+  int per_sm = 0;
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter, kFThreads, 0));
+  if (per_sm < 1) fail(CTD_ERR_DEVICE, "filter kernel cannot be resident");
+  const unsigned grid = (unsigned)ctx->sm_count;  // one CTA per SM
+  void* args[] = {&fa};
+  CUDA_OK(cudaLaunchCooperativeKernel((const void*)k_filter, dim3(grid), dim3(kFThreads), args, 0,
+                                      ctx->stream));
+  ctx->launches++;
+  // ---- results
+  out.accepted.resize(n);
+  out.degenerate.resize(n);
+  out.delta.resize(n);
+  out.res_sq.resize(n);
+  out.x_sq.resize(n);
+  std::vector<int> slowv(n);
+  long long newK = 0, newR = 0;
+  ctx->to_host(out.accepted.data(), acc.p, n);
+  ctx->to_host(out.degenerate.data(), deg.p, n);
+  ctx->to_host(out.delta.data(), dl.p, n);
+  ctx->to_host(out.res_sq.data(), res.p, n);
+  ctx->to_host(out.x_sq.data(), xsq.p, n);
+  ctx->to_host(slowv.data(), slow.p, n);
+  ctx->to_host(&newK, fK.p, 1);
+  ctx->to_host(&newR, fR.p, 1);
+  int srn = 0;
+  ctx->to_host(&srn, B.sr_n.p, 1);
+  if (want_y) {
+    out.y_last.resize(K0 + n);
+    ctx->to_host(out.y_last.data(), ylast.p, K0 + n);
+  }
+  ctx->sync();
+  ctx->check_flags("filter");
+  int64_t k_at_last = K0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (out.accepted[i]) out.kept_cand.push_back((int32_t)i);
+    if (slowv[i]) out.slow_path = true;
+    if (i < n - 1 && out.accepted[i]) ++k_at_last;
+  }
+  if (want_y) out.y_last.resize(k_at_last);
+  B.K = newK;
+  B.rnnz = newR;
+  B.srn = srn;
+  B.tag_base += (uint32_t)n + 1u;
+}
+
+void basis_u(const Basis& B, double* u) {
+  if (B.K == 0) return;
+  CUDA_OK(cudaMemcpy2DAsync(u, B.K * sizeof(double), B.U.p, B.LD * sizeof(double), B.K * sizeof(double),
+                            B.K, cudaMemcpyDeviceToHost, B.ctx->stream));
+  B.ctx->sync();
+}
+
+void basis_r(const Basis& B, int64_t* col_ptr, int64_t* rows, double* vals) {
+  Ctx* ctx = B.ctx;
+  if (col_ptr) ctx->to_host(col_ptr, B.rptr.p, B.K + 1);
+  if (rows && B.rnnz) {
+    std::vector<int32_t> r(B.rnnz);
+    ctx->to_host(r.data(), B.rrow.p, B.rnnz);
+    ctx->sync();
+    for (int64_t i = 0; i < B.rnnz; ++i) rows[i] = r[i];
+  }
+  if (vals) ctx->to_host(vals, B.rval.p, B.rnnz);
+  ctx->sync();
+}
+
+}  // namespace ctdgpu

@@ -1,0 +1,66 @@
+#pragma once
+#include "ctx.cuh"
+
+namespace ctdgpu {
+
+// FiberBasis (fiber_basis.hpp:21-61) resident in HBM: R (kept fibers, owned
+// copies, CSC in acceptance order), a row index of R (per row, the kept
+// columns containing it in ascending k — the order the reference's z scatter
+// visits them), the first-appearance order of R's rows (the reference's
+// `touched` order when every y_k != 0), and U = (R^T R)^-1 dense, leading
+// dimension LD.  U is kept exactly symmetric, as the reference's is.
+struct Basis {
+  Ctx* ctx = nullptr;
+  int64_t dim = 0;
+  int64_t K = 0;     // kept columns
+  int64_t LD = 0;    // U capacity (rows = cols)
+  Buf<double> U;
+  int64_t kcap = 0, rcap = 0, rnnz = 0;
+  Buf<int64_t> rptr;  // [kcap+1]
+  Buf<int32_t> rrow;  // [rcap]
+  Buf<double> rval;   // [rcap]
+  int64_t ricap = 0;
+  Buf<int64_t> rowbase;  // [dim+1]
+  Buf<int32_t> rowlen;   // [dim]
+  Buf<int32_t> rek;      // [ricap] kept-column index
+  Buf<double> rev;       // [ricap] value
+  Buf<int32_t> sr_list;  // [dim] rows of R in first-appearance order
+  Buf<int32_t> sr_pos;   // [dim] position in sr_list or -1
+  Buf<int> sr_n;         // device count
+  int64_t srn = 0;
+  Buf<uint32_t> tag;     // [dim] candidate tag of the rows of the current x
+  uint32_t tag_base = 0;
+  Buf<double> zd;        // [dim]
+  Buf<int32_t> kf;       // [dim] dynamic first k (slow path)
+
+  Basis(Ctx* c, int64_t d);
+  // Copy R's host CSC and U (resume ctor, fiber_basis.cpp:13-19).
+};
+
+// Candidate fibers (device): candidate c = rows/vals [off[c], off[c]+len[c]).
+struct Cands {
+  int64_t n = 0;
+  const int64_t* off = nullptr;
+  const int32_t* len = nullptr;
+  const int32_t* row = nullptr;
+  const double* val = nullptr;
+};
+
+// Per-candidate outcome of try_append_fiber (fiber_basis.hpp:30-37).
+struct BatchOut {
+  std::vector<int32_t> accepted, degenerate;
+  std::vector<double> delta, res_sq, x_sq;
+  std::vector<int32_t> kept_cand;  // candidates accepted, in order
+  std::vector<double> y_last;      // y of the last candidate (U R^T x)
+  bool slow_path = false;
+};
+
+// Runs the reference filter loop (ctd_static.cpp:40-44) over all candidates
+// in order against the basis, appending the accepted ones.
+void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want_y);
+
+// Host copies of the basis.
+void basis_u(const Basis& B, double* u /* K*K row-major */);
+void basis_r(const Basis& B, int64_t* col_ptr, int64_t* rows, double* vals);
+
+}  // namespace ctdgpu

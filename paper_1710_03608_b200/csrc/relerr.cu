@@ -1,0 +1,125 @@
+// Relative reconstruction error |X - R U C|^2 / |X|^2 (relative_error,
+// evaluation.cpp:88-122) without materializing C or a dense reconstruction.
+//
+// With C = R^T X (compute_core, ctd_static.cpp:12-17) and P = R U R^T the
+// error numerator is  sum_j |x_j|^2 - 2 x_j^T P x_j + x_j^T P^2 x_j; U is the
+// inverse Gram, P^2 = P, so it is |X|^2 - sum_j <R^T x_j, (R U)^T x_j>.  Both
+// factors are gathered per nonzero from dense row-major panels
+// Rd = R (dim x K) and Q = R U (dim x K): one streaming pass over the
+// bucketed nonzeros with a K-wide register accumulator per fiber (warp per
+// fiber, lanes across K).  This is a tolerance path (|d| <= 1e-9 max(1,|ref|)),
+// so it uses FMA and a deterministic (fixed-order) reduction.
+#include "relerr.cuh"
+
+namespace ctdgpu {
+
+namespace {
+
+__global__ void k_dense_r(const int64_t* rptr, const int32_t* rrow, const double* rval, long long K,
+                          double* Rd) {
+  const long long k = blockIdx.x;
+  if (k >= K) return;
+  for (long long t = rptr[k] + threadIdx.x; t < rptr[k + 1]; t += blockDim.x)
+    Rd[(long long)rrow[t] * K + k] = rval[t];
+}
+
+// Q[r][c] = sum over R's row r entries (k, v): v * U[k][c].
+__global__ void k_ru(const int64_t* rowbase, const int32_t* rowlen, const int32_t* rek, const double* rev,
+                     const double* U, long long LD, long long dim, long long K, double* Q) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= dim * K) return;
+  const long long r = e / K, c = e - r * K;
+  const long long b = rowbase[r];
+  const int L = rowlen[r];
+  double s = 0.0;
+  for (int t = 0; t < L; ++t) s = __fma_rn(rev[b + t], U[(long long)rek[b + t] * LD + c], s);
+  Q[e] = s;
+}
+
+constexpr int kCW = 4;  // columns per lane per chunk
+
+__global__ void k_cd(const int64_t* fptr, long long F, const int32_t* row, const double* val,
+                     const double* Rd, const double* Q, long long K, double* partial) {
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  double part = 0.0;
+  for (long long f = warp; f < F; f += nwarps) {
+    const long long b = fptr[f], e = fptr[f + 1];
+    for (long long c0 = 0; c0 < K; c0 += 32 * kCW) {
+      double ac[kCW], ad[kCW];
+#pragma unroll
+      for (int u = 0; u < kCW; ++u) ac[u] = ad[u] = 0.0;
+      for (long long t = b; t < e; ++t) {
+        const long long r = row[t];
+        const double v = val[t];
+        const double* rr = Rd + r * K;
+        const double* qq = Q + r * K;
+#pragma unroll
+        for (int u = 0; u < kCW; ++u) {
+          const long long c = c0 + lane + 32 * u;
+          if (c < K) {
+            ac[u] = __fma_rn(v, rr[c], ac[u]);
+            ad[u] = __fma_rn(v, qq[c], ad[u]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kCW; ++u) part = __fma_rn(ac[u], ad[u], part);
+    }
+  }
+  part = warp_sum(part);
+  if (lane == 0) partial[warp] = part;
+}
+
+__global__ void k_sumsq(const double* v, long long n, double* partial) {
+  __shared__ double sh[33];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    s = __fma_rn(v[i], v[i], s);
+  s = block_sum<double>(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// Fixed-order reduction of n partials (one block).
+__global__ void k_reduce(const double* p, long long n, double* out) {
+  __shared__ double sh[33];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) s += p[i];
+  s = block_sum<double>(s, sh);
+  if (threadIdx.x == 0) *out = s;
+}
+
+}  // namespace
+
+double relative_error(Ctx* ctx, const Fibers& fb, const Basis& B) {
+  const long long K = B.K, dim = B.dim;
+  // |X|^2
+  const unsigned sgrid = (unsigned)ctx->sm_count * 4;
+  Buf<double> sp(ctx, sgrid), xsq(ctx, 1), cd(ctx, 1);
+  LAUNCH(ctx, k_sumsq, sgrid, 256, 0, fb.val.p, (long long)fb.nnz, sp.p);
+  LAUNCH(ctx, k_reduce, 1, 1024, 0, sp.p, (long long)sgrid, xsq.p);
+  if (K == 0) {
+    const double x = ctx->read1(xsq.p);
+    if (x == 0.0) fail(CTD_ERR_METRIC, "relative error undefined for a zero tensor");
+    return 1.0;
+  }
+  Buf<double> Rd(ctx, (size_t)dim * K), Q(ctx, (size_t)dim * K);
+  Rd.zero();
+  LAUNCH(ctx, k_dense_r, (unsigned)K, 128, 0, B.rptr.p, B.rrow.p, B.rval.p, K, Rd.p);
+  LAUNCH(ctx, k_ru, ceil_div(dim * K, 256), 256, 0, B.rowbase.p, B.rowlen.p, B.rek.p, B.rev.p, B.U.p,
+         (long long)B.LD, dim, K, Q.p);
+  const unsigned cgrid = (unsigned)ctx->sm_count * 8;
+  const long long nwarps = (long long)cgrid * 256 / 32;
+  Buf<double> cp(ctx, nwarps);
+  LAUNCH(ctx, k_cd, cgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, Rd.p, Q.p, K, cp.p);
+  LAUNCH(ctx, k_reduce, 1, 1024, 0, cp.p, nwarps, cd.p);
+  double hx = 0, hcd = 0;
+  ctx->to_host(&hx, xsq.p, 1);
+  ctx->to_host(&hcd, cd.p, 1);
+  ctx->sync();
+  if (hx == 0.0) fail(CTD_ERR_METRIC, "relative error undefined for a zero tensor");
+  return (hx - hcd) / hx;
+}
+
+}  // namespace ctdgpu

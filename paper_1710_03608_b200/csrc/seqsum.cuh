@@ -1,0 +1,278 @@
+// Exact reproduction of a *sequential* IEEE-double running sum of
+// non-negative terms,  c_i = fl(c_{i-1} + x_i),  c_{-1} = 0,  in parallel.
+//
+// The reference accumulates several such sums in strict order: the sampling
+// CDF (sampling.cpp:42-49), the normalizer (:26-27), fiber norms
+// (tensor_ops.cpp:196-199), |x|^2 (sparse_matrix.cpp:10-14) and the residual
+// (fiber_basis.cpp:66-77).  All terms are >= 0, so the running sum is
+// monotone.  While c_{i-1} and c_i stay in one binade [2^e, 2^(e+1)), every
+// representable value is a multiple of ulp_e = 2^(e-52) and
+//     c_i / ulp_e = c_{i-1} / ulp_e + rne(x_i / ulp_e),
+// an integer increment independent of c_{i-1} except on an exact half-ulp
+// tie, where round-half-even depends on the parity of c_{i-1}/ulp_e.  Such a
+// step is the map A -> A + a[A & 1]; these maps compose associatively
+// (struct Mono), so a run of same-binade steps is one parallel scan.
+//
+// Which binade c_i lies in is decided from an approximate prefix P~ (any
+// summation order; |P~ - c| <= 2 n u c for non-negative terms).  An element
+// is "regular" when P~_{i-1} and P~_i are in the same binade and both lie
+// farther than a 4nu relative margin from its edges; every other element is
+// "direct" and is added with a real fl() add by a sequential walker (binade
+// crossings, near-boundary values, subnormals: a few dozen per run).  The
+// walker also verifies every run (start binade, no overflow of the binade);
+// a failed check sets FLAG_SEQSUM and the caller falls back to a plain
+// sequential loop, so the result is always the sequential one.
+#pragma once
+
+#include "common.cuh"
+
+namespace ctdgpu {
+
+struct Mono {
+  long long a0, a1;  // A -> A + (A odd ? a1 : a0)
+};
+__device__ __forceinline__ Mono mono_id() { return Mono{0, 0}; }
+__device__ __forceinline__ Mono mono_cat(const Mono& f, const Mono& g) {
+  Mono h;
+  h.a0 = f.a0 + ((f.a0 & 1) ? g.a1 : g.a0);
+  h.a1 = f.a1 + (((f.a1 + 1) & 1) ? g.a1 : g.a0);
+  return h;
+}
+__device__ __forceinline__ long long mono_apply(const Mono& f, long long A) {
+  return A + ((A & 1) ? f.a1 : f.a0);
+}
+
+enum : int { CLS_ZERO = 0, CLS_DIRECT = 1, CLS_REG = 2 };
+constexpr short E_DIRECT = -30000;
+constexpr short E_ZERO = -30001;
+
+__device__ __forceinline__ double seq_margin(long long n) {
+  return 4.0 * (double)n * 1.1102230246251565e-16 + 2.8421709430404007e-14;
+}
+
+__device__ __forceinline__ bool near_binade_edge(double P, double mg) {
+  const int e = dexp(P);
+  if (e < -1021 || e > 1022) return true;
+  const double lo = pow2(e);
+  return (P - lo) <= mg * P || (2.0 * lo - P) <= mg * P;
+}
+
+// Classify element i given approximate prefixes before (Pp) and after (Pc).
+__device__ __forceinline__ int seq_classify(bool first, double Pp, double Pc, double x,
+                                            double mg, int* e_out, Mono* m_out) {
+  if (Pc == 0.0) return CLS_ZERO;
+  if (first || !(Pp > 0.0) || !(Pc > 0.0) || !(x < 1.7976931348623157e308)) return CLS_DIRECT;
+  const int ep = dexp(Pp), ec = dexp(Pc);
+  if (ep != ec || ec < -960 || ec > 1020) return CLS_DIRECT;
+  if (near_binade_edge(Pp, mg) || near_binade_edge(Pc, mg)) return CLS_DIRECT;
+  const double s = dmul(x, pow2(52 - ec));  // exact power-of-two scaling, < 2^53
+  const double fl = floor(s);
+  const double fr = dsub(s, fl);
+  const long long m = (long long)fl;
+  if (fr > 0.5) {
+    m_out->a0 = m_out->a1 = m + 1;
+  } else if (fr < 0.5) {
+    m_out->a0 = m_out->a1 = m;
+  } else {  // exact tie: result rounds to even
+    m_out->a0 = m + (m & 1);
+    m_out->a1 = m + ((m + 1) & 1);
+  }
+  *e_out = ec;
+  return CLS_REG;
+}
+
+// Applies a same-binade run summarized by M to the value `head` (the value of
+// the run's leading direct element).  Returns false if the run's assumptions
+// do not hold (caller falls back).
+__device__ __forceinline__ bool seq_apply_run(double head, int e, const Mono& M, double* out) {
+  if (!(head > 0.0) || dexp(head) != e) return false;
+  const long long A = mono_apply(M, dsig(head));
+  if (A >= (1LL << 53) || A < (1LL << 52)) return false;
+  *out = dmake(A, e);
+  return true;
+}
+
+// Segmented-scan element: (has_head, mono since the last head).
+struct Seg {
+  int h;
+  Mono m;
+};
+__device__ __forceinline__ Seg seg_cat(const Seg& l, const Seg& r) {
+  Seg o;
+  o.h = l.h | r.h;
+  o.m = r.h ? r.m : mono_cat(l.m, r.m);
+  return o;
+}
+__device__ __forceinline__ Seg seg_shfl_up(const Seg& s, int d) {
+  Seg o;
+  o.h = __shfl_up_sync(0xffffffffu, s.h, d);
+  o.m.a0 = __shfl_up_sync(0xffffffffu, s.m.a0, d);
+  o.m.a1 = __shfl_up_sync(0xffffffffu, s.m.a1, d);
+  return o;
+}
+
+// Exclusive segmented block scan of one Seg per thread.  sh: >= 32 Segs.
+__device__ inline Seg block_seg_excl(Seg v, Seg* sh, Seg* total) {
+  const unsigned w = warp_id(), l = lane_id(), nw = (blockDim.x + 31) >> 5;
+  Seg inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    Seg o = seg_shfl_up(inc, d);
+    if ((int)l >= d) inc = seg_cat(o, inc);
+  }
+  if (l == 31) sh[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    Seg s = (l < nw) ? sh[l] : Seg{0, mono_id()};
+    Seg si = s;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      Seg o = seg_shfl_up(si, d);
+      if ((int)l >= d) si = seg_cat(o, si);
+    }
+    // exclusive = inclusive of previous lane
+    Seg ex = seg_shfl_up(si, 1);
+    if (l == 0) ex = Seg{0, mono_id()};
+    if (l < nw) sh[l] = ex;
+    if (l == nw - 1) sh[32] = si;
+  }
+  __syncthreads();
+  // exclusive prefix for this thread: warp prefix (sh[w]) then lanes before me
+  Seg lanes_ex = seg_shfl_up(inc, 1);
+  Seg res;
+  if (l == 0) res = sh[w];
+  else res = seg_cat(sh[w], lanes_ex);
+  if (total) *total = sh[32];
+  __syncthreads();
+  return res;
+}
+
+// --------------------------------------------------------------------------
+// Block-level exact sequential total of n >= 0 terms produced by get(i).
+// Deterministic; all threads return the same value.  `fail` set on self-check
+// failure in which case the sequential fallback result is returned.
+struct SeqSumSmem {
+  double dsh[33];
+  Seg ssh[33];
+  int ish[33];
+  int nd;
+  int bad;
+  double result;
+  // direct list
+  static constexpr int kCap = 512;
+  double dx[kCap];
+  Mono dm[kCap];
+  short de[kCap];
+  int di[kCap];
+  // per-thread boundary info
+  short last_e[1024];
+  Mono fin_m;
+  short fin_e;
+};
+
+template <typename Get>
+__device__ double block_exact_sum(const Get& get, long long n, SeqSumSmem& S, bool* fail) {
+  const int T = blockDim.x, t = threadIdx.x;
+  if (n <= 0) return 0.0;
+  const long long per = (n + T - 1) / T;
+  const long long b0 = min((long long)t * per, n), b1 = min(b0 + per, n);
+  // Pass A: approximate chunk sums -> exclusive prefix.
+  double cs = 0.0;
+  for (long long i = b0; i < b1; ++i) cs += get(i);
+  double tot;
+  double pre = block_excl_sum<double>(cs, S.dsh, &tot);
+  const double mg = seq_margin(n);
+  // Pass B: thread aggregate + direct count.
+  Seg agg{0, mono_id()};
+  int nd = 0;
+  short le = E_ZERO;
+  {
+    double P = pre;
+    for (long long i = b0; i < b1; ++i) {
+      const double x = get(i);
+      const double Pc = P + x;
+      int e = 0;
+      Mono m;
+      const int c = seq_classify(i == 0, P, Pc, x, mg, &e, &m);
+      if (c == CLS_REG) {
+        agg.m = mono_cat(agg.m, m);
+        le = (short)e;
+      } else {
+        agg.h = 1;
+        agg.m = mono_id();
+        if (c == CLS_DIRECT) ++nd;
+        le = (c == CLS_DIRECT) ? E_DIRECT : E_ZERO;
+      }
+      P = Pc;
+    }
+  }
+  if (t == 0) S.bad = 0;
+  S.last_e[t] = (b0 < b1) ? le : (short)0x7fff;  // 0x7fff: empty chunk
+  Seg carry = block_seg_excl(agg, S.ssh, nullptr);
+  int ntot;
+  int dpos = block_excl_sum<int>(nd, S.ish, &ntot);
+  if (ntot > SeqSumSmem::kCap) {
+    if (t == 0) S.bad = 1;
+  } else {
+    // Pass C: record each direct's preceding run summary.
+    double P = pre;
+    Mono M = carry.m;
+    // e of the element before my chunk: walk back over empty chunks.
+    short prev_e = E_ZERO;
+    for (int q = t - 1; q >= 0; --q) {
+      if (S.last_e[q] != (short)0x7fff) { prev_e = S.last_e[q]; break; }
+    }
+    for (long long i = b0; i < b1; ++i) {
+      const double x = get(i);
+      const double Pc = P + x;
+      int e = 0;
+      Mono m;
+      const int c = seq_classify(i == 0, P, Pc, x, mg, &e, &m);
+      if (c == CLS_REG) {
+        M = mono_cat(M, m);
+        prev_e = (short)e;
+      } else {
+        if (c == CLS_DIRECT) {
+          S.dx[dpos] = x;
+          S.dm[dpos] = M;
+          S.de[dpos] = prev_e;  // e of the element before (REG) or a sentinel
+          S.di[dpos] = (int)i;
+          ++dpos;
+        }
+        M = mono_id();
+        prev_e = (c == CLS_DIRECT) ? E_DIRECT : E_ZERO;
+      }
+      P = Pc;
+    }
+    if (b1 == n && b0 < b1) {
+      S.fin_m = M;
+      S.fin_e = prev_e;
+    }
+  }
+  __syncthreads();
+  if (t == 0) {
+    bool ok = !S.bad;
+    double acc = 0.0, head = 0.0;
+    if (ok) {
+      for (int q = 0; q < ntot && ok; ++q) {
+        if (S.de[q] >= -1100 && S.de[q] <= 1100) ok = seq_apply_run(head, S.de[q], S.dm[q], &acc);
+        acc = dadd(acc, S.dx[q]);
+        head = acc;
+      }
+      if (ok && S.fin_e >= -1100 && S.fin_e <= 1100) ok = seq_apply_run(head, S.fin_e, S.fin_m, &acc);
+    }
+    if (!ok) {  // sequential fallback: always the reference order
+      acc = 0.0;
+      for (long long i = 0; i < n; ++i) acc = dadd(acc, get(i));
+    }
+    S.result = acc;
+    S.bad = ok ? 0 : 1;
+  }
+  __syncthreads();
+  const double r = S.result;
+  if (fail) *fail = S.bad != 0;
+  __syncthreads();
+  return r;
+}
+
+}  // namespace ctdgpu
