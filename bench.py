@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""CTD-S throughput on BASELINE.json configs[1] (C2) on N B200s.
+
+One step = one CTD-S pass over the resident C2 tensor (10^4 x 10^4 x 10^3
+synthetic traffic, 1e7 coalesced nnz, c = 2000, eps = 1e-6, seed 42, mode 0):
+bucketing + exact squared norms, sampling law and CDF, mt19937_64 draws and
+dedup, the bit-exact independence filter + U, and the relative-error pass.
+`value` = nnz / device-timed step (inputs already in HBM); `e2e` = the same
+through the public C-ABI from pinned host COO (H2D + D2H inside the region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ctd_s_nnz_per_s"
+UNIT = "nnz/s"
+C2 = dict(shape=[10000, 10000, 1000], nnz=10_000_000, c=2000, eps=1e-6, seed=42, mode=0, gen_seed=2)
+WORKLOAD = ("C2: CTD-S on synthetic traffic 1e4x1e4x1e3 (Zipf(1.2) src/dst, uniform time, "
+            "log-uniform counts 1..100), 1e7 coalesced nnz, c=2000, eps=1e-6, mode 0")
+
+
+def _np_default(o):
+    if hasattr(o, "item"):
+        return o.item()
+    return str(o)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# data (cached per box in /tmp; regenerated when absent — identical bytes)
+
+def load_c2(rank: int = 0):
+    from paper_1710_03608_b200 import datagen
+    seed = C2["gen_seed"] + 1000 * rank
+    cache = os.path.join(tempfile.gettempdir(), f"ctd_c2_seed{seed}.npz")
+    if os.path.exists(cache):
+        try:
+            z = np.load(cache)
+            return datagen.Tensor(list(z["shape"]), z["idx"], z["val"], {"draws": int(z["draws"]),
+                                                                         "seed": seed})
+        except Exception:
+            pass
+    x = datagen.traffic(C2["shape"], C2["nnz"], seed)
+    try:
+        np.savez(cache, shape=np.array(x.shape), idx=x.idx, val=x.val, draws=x.meta["draws"])
+    except Exception:
+        pass
+    return x
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        self.f.flush()
+        rows = []
+        try:
+            with open(self.f.name) as fh:
+                for line in fh:
+                    parts = [s.strip() for s in line.split(",")]
+                    if len(parts) >= 8 and parts[1].replace(".", "").isdigit():
+                        rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[1]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes (frozen before measuring)
+
+def phase_bytes(nnz, F, kept_seq, r_lens):
+    """Algorithmic HBM bytes per phase for one CTD-S step."""
+    filt = 0
+    K = 0
+    rn = 0
+    for j, acc in enumerate(kept_seq):
+        filt += 8 * K * K + 12 * rn          # y = U g reads U; z reads R's row index
+        if acc:
+            filt += 16 * (K + 1) * (K + 1)  # U update read + write
+            rn += r_lens[K]
+            K += 1
+    return {
+        "matricize": 32 * nnz + 24 * F,      # read COO (3x4+8), write (row,val), fiber col/ptr/norm
+        "law": 24 * F,                        # read norms, write probs and cumulative
+        "sample": 0,
+        "filter_prep": 0,
+        "filter": filt,
+        "error": 12 * nnz + 8 * F,            # stream (row,val) + fiber offsets once
+    }
+
+
+# ---------------------------------------------------------------------------
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_1710_03608_b200 as ctd
+    from paper_1710_03608_b200 import ctd as api
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream().cuda_stream
+    ctx = ctd.Context(local_rank, stream)
+    x = load_c2(rank)
+    nnz = x.nnz
+    # resident in HBM: SoA int32 coordinates + fp64 values
+    idx_t = torch.from_numpy(np.ascontiguousarray(x.idx.T.astype(np.int32))).to(dev)
+    val_t = torch.from_numpy(x.val).to(dev)
+    dt = api.DeviceTensor.from_device_ptrs(x.shape, nnz, [idx_t[k].data_ptr() for k in range(3)],
+                                           val_t.data_ptr(), ctx)
+    c, eps, seed, mode = C2["c"], C2["eps"], C2["seed"], C2["mode"]
+
+    def step():
+        h, info = api.ctd_s_raw(dt, mode, c, eps, seed, with_error=True, ctx=ctx)
+        return h, info
+
+    for _ in range(args.warmup):
+        h, info = step()
+        api.free_factors(ctx, h)
+    torch.cuda.synchronize()
+    ctx.set_timing(True)
+    ctx.phase_times(reset=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.launches
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    infos = []
+    with Clocks(local_rank) as clk:
+        start.record()
+        for _ in range(args.steps):
+            h, info = step()
+            infos.append((h, info))
+        end.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches = ctx.launches - l0
+    ms = start.elapsed_time(end) / args.steps
+    phases = ctx.phase_times(reset=True)
+    ctx.set_timing(False)
+    info = infos[-1][1]
+    tr = api.factors_trace(ctx, infos[-1][0], info)
+    for h, _ in infos:
+        api.free_factors(ctx, h)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * nnz / (ms / 1e3)
+
+    # ---- roofline of the dominant phase (CUDA events on the launch stream)
+    pk, pk_kind = peaks()
+    pb = phase_bytes(nnz, info.n_fibers, tr["accepted"], tr["r_lens"])
+    per_phase = {}
+    for name, (tot_ms, n) in phases.items():
+        if n == 0:
+            continue
+        avg = tot_ms / n
+        b = pb.get(name, 0)
+        per_phase[name] = {"ms": round(avg, 4), "bytes": b,
+                           "gbs": round(b / (avg / 1e3) / 1e9, 1) if b and avg > 0 else None}
+    dom = max(per_phase, key=lambda k: per_phase[k]["ms"])
+    dbytes = pb.get(dom, 0)
+    dms = per_phase[dom]["ms"]
+    achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
+    roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": pk,
+            "unit": "GB/s", "frac": round(achieved / pk, 4), "traffic": None,
+            "peak_kind": pk_kind}
+    # SURVEY §8d end-to-end byte formula for the step
+    bs = 44 * nnz + 24 * info.n_fibers
+
+    # ---- e2e through the public C-ABI from pinned host COO
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, ctx, x, torch)
+
+    # ---- CPU baseline: the compiled reference on this host (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(x)
+
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded splitmix64 generator, SURVEY §8d)",
+        "config": {"workload": WORKLOAD, "nnz": nnz, "fibers": info.n_fibers,
+                   "unique_sampled": info.n_unique, "kept": info.kept,
+                   "relative_error": info.relative_error,
+                   "l2": "inputs larger than L2 (200 MB COO + 120 MB bucketed per step)",
+                   "parallelism": f"fiber-range shards x{world}" if world > 1 else "1 GPU",
+                   "step_bytes_44nnz_24F": bs,
+                   "step_frac_of_peak": round(bs / (ms / 1e3) / 1e9 / pk, 4)},
+        "roofline": roof, "phases": per_phase, "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line, default=_np_default), flush=True)
+
+
+def run_e2e(args, ctx, x, torch):
+    from paper_1710_03608_b200 import ctd as api
+    nnz = x.nnz
+    idx_h = torch.from_numpy(np.ascontiguousarray(x.idx, dtype=np.int64).reshape(-1)).pin_memory()
+    val_h = torch.from_numpy(np.ascontiguousarray(x.val)).pin_memory()
+    c, eps, seed, mode = C2["c"], C2["eps"], C2["seed"], C2["mode"]
+    shape = np.asarray(x.shape, dtype=np.int64)
+
+    def step():
+        t = api.DeviceTensor.from_host_ptrs(x.shape, nnz, idx_h.data_ptr(), val_h.data_ptr(), ctx)
+        h, info = api.ctd_s_raw(t, mode, c, eps, seed, with_error=True, ctx=ctx)
+        kept, u = api.factors_result(ctx, h, info)   # D2H: kept ids + U
+        api.free_factors(ctx, h)
+        t.close()
+        return info, kept, u
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        step()
+    torch.cuda.synchronize()
+    k = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(k):
+        info, kept, u = step()
+    torch.cuda.synchronize()
+    sec = (time.perf_counter() - t0) / k
+    return {"value": round(nnz / sec, 1), "unit": UNIT, "h2d_bytes_per_step": nnz * (3 * 8 + 8),
+            "d2h_bytes_per_step": int(kept.nbytes + u.nbytes), "ms_per_step": round(sec * 1e3, 3),
+            "path": "ctd_gpu_tensor_from_host (pinned int64 AoS + fp64) -> ctd_gpu_ctd_s -> "
+                    "kept ids + U to host"}
+
+
+def cpu_baseline(x):
+    """The unmodified reference (oracle/_ref) on this host's cores: the ctd_s
+    front end (matricize -> column_distribution -> sample -> dedup -> FiberBasis
+    loop) on the full C2 tensor.  compute_core / relative_error are excluded
+    (they do not finish at this size: SURVEY §8d, H8)."""
+    try:
+        from oracle.bindings import Ref, ref_available
+        if not ref_available():
+            return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                    "sample": "unavailable: oracle/_ref/libctdref.so not built"}
+        R = Ref()
+        t = R.tensor(x.shape, x.flat_idx(), x.val)
+        fe = R.frontend(t, C2["mode"], C2["c"], C2["eps"], C2["seed"])
+        sec = fe.seconds
+        return {"value": round(x.nnz / sec, 1), "unit": UNIT, "cores": 1, "kind": "reference",
+                "seconds": round(sec, 3),
+                "sample": "full C2 tensor, reference ctd_s front end (matricize..FiberBasis loop), "
+                          "single-threaded like the reference; compute_core/relative_error excluded (DNF)",
+                "cpu": _cpu_model()}
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} threads)"
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref),
+    rank 0 only, each step a bounded sample of C2 (the first T' time slices)."""
+    if rank != 0:
+        return
+    from oracle.bindings import Ref, ref_available
+    if not ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libctdref.so not built"}))
+        return
+    x = load_c2(0)
+    n_steps = args.steps + args.warmup
+    frac = 1.0 if n_steps <= 6 else max(0.05, 6.0 / n_steps)
+    T1 = max(1, int(round(C2["shape"][2] * frac)))
+    xs = x if T1 >= C2["shape"][2] else x.time_slab(0, T1)
+    R = Ref()
+    t = R.tensor(xs.shape, xs.flat_idx(), xs.val)
+    secs = []
+    for i in range(n_steps):
+        fe = R.frontend(t, C2["mode"], C2["c"], C2["eps"], C2["seed"])
+        if i >= args.warmup:
+            secs.append(fe.seconds)
+    sec = float(np.mean(secs))
+    value = xs.nnz / sec
+    sample = (f"reference ctd_s front end on the first {T1} of 1000 time slices of C2 "
+              f"({xs.nnz} nnz); single-threaded (the reference has no threading)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample_nnz": xs.nnz},
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": sample, "cpu": _cpu_model()},
+        "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.distributed.init_process_group("nccl")
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -61,6 +61,11 @@ int ctd_gpu_ctx_synchronize(ctd_gpu_ctx *ctx);
 int ctd_gpu_ctx_destroy(ctd_gpu_ctx *ctx);
 /* Launch counter of this library's kernels on the context (for bench.py). */
 int64_t ctd_gpu_ctx_launches(const ctd_gpu_ctx *ctx);
+/* Live per-phase timing with CUDA events recorded on the context stream
+ * (bench.py's roofline): 8 phases, names from ctd_gpu_phase_name(i). */
+int ctd_gpu_ctx_set_timing(ctd_gpu_ctx *ctx, int enable);
+int ctd_gpu_ctx_phase_times(ctd_gpu_ctx *ctx, double *ms, int64_t *counts, int reset);
+const char *ctd_gpu_phase_name(int i);
 
 /* ---- tensors (SparseTensor, sparse_tensor.hpp:27-28) --------------------- */
 /* Host COO exactly as SparseTensor::indices()/values() hold it: nnz*order
@@ -101,6 +106,9 @@ int ctd_gpu_column_distribution(ctd_gpu_ctx *ctx, const ctd_gpu_tensor *x,
 int ctd_gpu_sample_with_replacement(ctd_gpu_ctx *ctx, const double *probs,
                                     int64_t n, int64_t count, uint64_t seed,
                                     int64_t *out);
+/* The exact sequential running sum used for the CDF, |x|^2 and the residual:
+ * out[i] = fl(out[i-1] + x[i]) bit-exactly, x[i] >= 0 (host buffers). */
+int ctd_gpu_seq_cumsum(ctd_gpu_ctx *ctx, const double *x, int64_t n, double *out);
 /* unique_first_occurrence (sampling.hpp:31). */
 int ctd_gpu_unique_first_occurrence(ctd_gpu_ctx *ctx, const int64_t *drawn,
                                     int64_t n, int64_t *out, int64_t *n_out);

@@ -35,6 +35,9 @@ SIGNATURES = [
     ("ctd_gpu_ctx_synchronize", _I, [_V]),
     ("ctd_gpu_ctx_destroy", _I, [_V]),
     ("ctd_gpu_ctx_launches", _I64, [_V]),
+    ("ctd_gpu_ctx_set_timing", _I, [_V, _I]),
+    ("ctd_gpu_ctx_phase_times", _I, [_V, _P, _P, _I]),
+    ("ctd_gpu_phase_name", C.c_char_p, [_I]),
     ("ctd_gpu_tensor_from_host", _I, [_V, _I, _P, _I64, _P, _P, _PV]),
     ("ctd_gpu_tensor_from_device", _I, [_V, _I, _P, _I64, _P, _P, _PV]),
     ("ctd_gpu_tensor_nnz", _I64, [_V]),
@@ -42,6 +45,7 @@ SIGNATURES = [
     ("ctd_gpu_matricize", _I, [_V, _V, _I, _P, _P, _P, _P, _P, _P]),
     ("ctd_gpu_column_distribution", _I, [_V, _V, _I, _P, _P, _P]),
     ("ctd_gpu_sample_with_replacement", _I, [_V, _P, _I64, _I64, _U64, _P]),
+    ("ctd_gpu_seq_cumsum", _I, [_V, _P, _I64, _P]),
     ("ctd_gpu_unique_first_occurrence", _I, [_V, _P, _I64, _P, _P]),
     ("ctd_gpu_ctd_s", _I, [_V, _V, _I, _I64, _D, _U64, C.c_uint, _PV]),
     ("ctd_gpu_factors_info_get", _I, [_V, C.POINTER(FactorsInfo)]),

@@ -67,9 +67,11 @@ __global__ void k_hist(CooView c, int wbits, unsigned* count, unsigned* flags) {
   }
 }
 
-__global__ void k_excl_scan_u32(const unsigned* cnt, long long n, unsigned long long* off) {
+__global__ void k_excl_scan_u32(const unsigned* cnt, long long n, unsigned long long* off,
+                                unsigned* maxc) {
   __shared__ unsigned long long sh[33];
   unsigned long long carry = 0;
+  unsigned mx = 0;
   for (long long b0 = 0; b0 < n; b0 += (long long)blockDim.x * 4) {
     unsigned long long v[4], s = 0;
     const long long base = b0 + (long long)threadIdx.x * 4;
@@ -77,6 +79,7 @@ __global__ void k_excl_scan_u32(const unsigned* cnt, long long n, unsigned long 
     for (int k = 0; k < 4; ++k) {
       v[k] = (base + k < n) ? cnt[base + k] : 0ull;
       s += v[k];
+      mx = max(mx, (unsigned)v[k]);
     }
     unsigned long long tot;
     unsigned long long pre = block_excl_sum<unsigned long long>(s, sh, &tot) + carry;
@@ -88,6 +91,7 @@ __global__ void k_excl_scan_u32(const unsigned* cnt, long long n, unsigned long 
     carry += tot;
   }
   if (threadIdx.x == 0) off[n] = carry;
+  atomicMax(maxc, mx);
 }
 
 struct ScatterOut {
@@ -139,6 +143,7 @@ __global__ void k_scatter(CooView c, int wbits, int rowbits, ScatterOut o, unsig
 }
 
 struct SortArgs {
+  int cap;                        // shared-memory bucket capacity of this launch
   const unsigned long long* off;  // [nb+1]
   uint32_t* tkey;                 // [nnz] scattered keys (reused as sort buffer A)
   const double* tval;             // [nnz]
@@ -186,11 +191,12 @@ __device__ long long lookback(unsigned long long* st, long long b, long long agg
 __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(SortArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* ska = (uint32_t*)smem;
-  uint32_t* skb = ska + kCap;
-  uint16_t* sia = (uint16_t*)(skb + kCap);
-  uint16_t* sib = sia + kCap;
-  double* sv = (double*)(sib + kCap);
-  uint32_t* hist = (uint32_t*)(sv + kCap);
+  const int cap = a.cap;
+  uint32_t* skb = ska + cap;
+  uint16_t* sia = (uint16_t*)(skb + cap);
+  uint16_t* sib = sia + cap;
+  double* sv = (double*)(sib + cap);
+  uint32_t* hist = (uint32_t*)(sv + cap);
   __shared__ uint32_t sh32[33];
   __shared__ long long sh64[33];
   __shared__ long long s_b, s_fbase;
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(SortArgs a) {
   const int T = blockDim.x, t = threadIdx.x;
   const int keybits = a.wbits + a.rowbits;
   const uint32_t rowmask = a.rowbits ? (0xffffffffu >> (32 - a.rowbits)) : 0u;
-  const bool small = m <= kCap;
+  const bool small = m <= cap;
   const uint32_t* K;
   const double* V;
   if (small) {
@@ -309,7 +315,7 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
   int wbits = 0;
   {
     const double per_col = out.cols > 0 ? (double)x.nnz / (double)out.cols : 1.0;
-    const double want = 2048.0 / (per_col > 0 ? per_col : 1.0);
+    const double want = 1024.0 / (per_col > 0 ? per_col : 1.0);
     while (wbits < 32 - rowbits && (double)(1ll << (wbits + 1)) <= want) ++wbits;
     wbits = std::min(wbits, 32 - rowbits);
   }
@@ -344,7 +350,9 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
   }
   const unsigned grid = (unsigned)std::min<long long>((nnz + 255) / 256, (long long)ctx->sm_count * 16);
   LAUNCH(ctx, k_hist, grid, 256, 0, c, wbits, count.p, ctx->d_flags);
-  LAUNCH(ctx, k_excl_scan_u32, 1, 1024, 0, count.p, nb, off.p);
+  Buf<unsigned> maxc(ctx, 1);
+  maxc.zero();
+  LAUNCH(ctx, k_excl_scan_u32, 1, 1024, 0, count.p, nb, off.p, maxc.p);
   CUDA_OK(cudaMemcpyAsync(cursor.p, off.p, (nb + 1) * sizeof(unsigned long long),
                           cudaMemcpyDeviceToDevice, ctx->stream));
   ScatterOut so{cursor.p, tkey.p, tval.p, intok.p, sumsq.p};
@@ -355,17 +363,23 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
   gkey2.alloc(ctx, nnz);
   gidx1.alloc(ctx, nnz);
   gidx2.alloc(ctx, nnz);
-  SortArgs sa{off.p, tkey.p, tval.p, gkey2.p, gidx1.p, gidx2.p, out.row.p, out.val.p,
+  // Shared-memory capacity sized to the largest bucket (more CTAs per SM).
+  const unsigned mx = ctx->read1(maxc.p);
+  int cap = 256;
+  while (cap < (int)mx && cap < kCap) cap <<= 1;
+  const int threads = cap <= 2048 ? 256 : kSortThreads;
+  SortArgs sa{cap, off.p, tkey.p, tval.p, gkey2.p, gidx1.p, gidx2.p, out.row.p, out.val.p,
               out.col.p, out.ptr.p, out.norm.p, status.p, ticket.p, nb, nnz, wbits, rowbits,
               dF.p, ctx->d_flags};
-  const size_t smem = (size_t)kCap * (4 + 4 + 2 + 2 + 8) + (kSortThreads / 32) * kRadix * 4;
+  const size_t smem = (size_t)cap * (4 + 4 + 2 + 2 + 8) + (threads / 32) * kRadix * 4;
   static bool attr_set = false;
   if (!attr_set) {
+    const size_t smax = (size_t)kCap * (4 + 4 + 2 + 2 + 8) + (kSortThreads / 32) * kRadix * 4;
     CUDA_OK(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+                                 (int)smax));
     attr_set = true;
   }
-  LAUNCH(ctx, k_bucket_sort, (unsigned)nb, kSortThreads, smem, sa);
+  LAUNCH(ctx, k_bucket_sort, (unsigned)nb, threads, smem, sa);
   long long F = 0;
   int iok = 0;
   double ssq = 0.0;

@@ -150,6 +150,34 @@ int ctd_gpu_ctx_destroy(ctd_gpu_ctx* ctx) {
 
 int64_t ctd_gpu_ctx_launches(const ctd_gpu_ctx* ctx) { return ctx ? ctx->c.launches : -1; }
 
+int ctd_gpu_ctx_set_timing(ctd_gpu_ctx* ctx, int enable) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->c.phase_flush();
+    ctx->c.timing = enable != 0;
+  });
+}
+
+int ctd_gpu_ctx_phase_times(ctd_gpu_ctx* ctx, double* ms, int64_t* counts, int reset) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->c.phase_flush();
+    for (int i = 0; i < Ctx::kPhases; ++i) {
+      if (ms) ms[i] = ctx->c.phase_ms[i];
+      if (counts) counts[i] = ctx->c.phase_n[i];
+      if (reset) {
+        ctx->c.phase_ms[i] = 0;
+        ctx->c.phase_n[i] = 0;
+      }
+    }
+  });
+}
+
+const char* ctd_gpu_phase_name(int i) {
+  static const char* names[] = {"matricize", "law", "sample", "filter_prep", "filter", "error", "h2d", "other"};
+  return (i >= 0 && i < Ctx::kPhases) ? names[i] : "";
+}
+
 int ctd_gpu_tensor_from_host(ctd_gpu_ctx* ctx, int order, const int64_t* shape, int64_t nnz,
                              const int64_t* indices, const double* values, ctd_gpu_tensor** out) {
   return guarded([&] {
@@ -171,6 +199,7 @@ int ctd_gpu_tensor_from_host(ctd_gpu_ctx* ctx, int order, const int64_t* shape, 
     if (nnz > 0) {
       need(indices, "indices");
       need(values, "values");
+      PhaseScope ps(c, PH_H2D);
       Buf<int64_t> raw(c, (size_t)nnz * order);
       c->to_dev(raw.p, indices, (size_t)nnz * order);
       c->to_dev(t.own_val.p, values, nnz);
@@ -270,6 +299,21 @@ int ctd_gpu_sample_with_replacement(ctd_gpu_ctx* ctx, const double* probs, int64
   });
 }
 
+int ctd_gpu_seq_cumsum(ctd_gpu_ctx* ctx, const double* x, int64_t n, double* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    if (n <= 0) return;
+    need(x, "x");
+    need(out, "out");
+    Ctx* c = &ctx->c;
+    Buf<double> d(c, n), o(c, n), t(c, 1);
+    c->to_dev(d.p, x, n);
+    seq_cumsum(c, d.p, n, o.p, t.p);
+    c->to_host(out, o.p, n);
+    c->sync();
+  });
+}
+
 int ctd_gpu_unique_first_occurrence(ctd_gpu_ctx* ctx, const int64_t* drawn, int64_t n, int64_t* out,
                                     int64_t* n_out) {
   return guarded([&] {
@@ -300,6 +344,7 @@ int ctd_gpu_ctd_s(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int mode, int64_t s
     if (flags & CTD_GPU_WITH_CORE) fail(CTD_ERR_ARGUMENT, "core materialization is not available yet");
     auto h = std::make_unique<ctd_gpu_factors>();
     run_ctd_s(&ctx->c, x->t, mode, sample_size, epsilon, seed, flags, h->f);
+    ctx->c.phase_flush();
     *out = h.release();
   });
 }

@@ -180,40 +180,80 @@ struct WalkOut {
   Mono* carry_in;    // per block
   int* inh_head;     // per block: slot of the last head before the block (-2 zero)
   double* total;
+  Mono* final_m;     // run mono from the last head to the end
 };
 
 __device__ __forceinline__ bool is_reg_e(short e) { return e >= -1100 && e <= 1100; }
 
-// Sequential walker over the (few) direct elements, one thread.
-__global__ void k_seq_walk(long long nb, LocalOut o, WalkOut w, unsigned* flags) {
+// Cross-block carries in parallel (one CTA): segmented exclusive scan of the
+// block aggregates -> carry_in[b]; exclusive max-scan of each block's last
+// direct slot -> inh_head[b]; ordered list of the blocks holding directs.
+constexpr int kCarryThreads = 1024;
+__global__ void __launch_bounds__(kCarryThreads) k_seq_carry(long long nb, LocalOut o, WalkOut w,
+                                                             int* dblocks, int* n_dblocks) {
+  __shared__ Seg ssh[33];
+  __shared__ int ish[33];
+  __shared__ int msh[kCarryThreads];
+  const long long per = (nb + blockDim.x - 1) / blockDim.x;
+  const long long b0 = min((long long)threadIdx.x * per, nb), b1 = min(b0 + per, nb);
+  Seg agg{0, mono_id()};
+  int last_slot = -2, nd = 0;
+  for (long long b = b0; b < b1; ++b) {
+    agg = seg_cat(agg, o.bagg[b]);
+    if (o.bnd[b] > 0) {
+      last_slot = (int)(b * kDMax + o.bnd[b] - 1);
+      ++nd;
+    }
+  }
+  Seg carry = block_seg_excl(agg, ssh, nullptr);
+  msh[threadIdx.x] = last_slot;
+  __syncthreads();
+  // exclusive max over earlier threads (slots increase with block index)
+  int inh = -2;
+  for (int q = (int)threadIdx.x - 1; q >= 0; --q)
+    if (msh[q] != -2) { inh = msh[q]; break; }
+  int pos = block_excl_sum<int>(nd, ish, n_dblocks);
+  for (long long b = b0; b < b1; ++b) {
+    w.carry_in[b] = carry.m;
+    w.inh_head[b] = inh;
+    carry = seg_cat(carry, o.bagg[b]);
+    if (o.bnd[b] > 0) {
+      inh = (int)(b * kDMax + o.bnd[b] - 1);
+      dblocks[pos++] = (int)b;
+    }
+  }
+  if (threadIdx.x == blockDim.x - 1 || b1 == nb) {
+    if (b1 == nb && b0 < b1) w.final_m[0] = carry.m;
+  }
+}
+
+// Sequential walker over the (few) blocks that hold direct elements.
+__global__ void k_seq_walk(long long nb, LocalOut o, WalkOut w, const int* dblocks,
+                           const int* n_dblocks, unsigned* flags) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (*flags & FLAG_SEQSUM) return;
-  Seg carry{0, mono_id()};
   double head = 0.0;
-  int head_slot = -2;
-  short prev_last = E_ZERO;
   bool ok = true;
-  for (long long b = 0; b < nb && ok; ++b) {
-    w.carry_in[b] = carry.m;
-    w.inh_head[b] = head_slot;
+  const int nbd = *n_dblocks;
+  for (int q0 = 0; q0 < nbd && ok; ++q0) {
+    const long long b = dblocks[q0];
+    const Mono cin = w.carry_in[b];
+    const short prev_last = b > 0 ? o.blast[b - 1] : E_ZERO;
     const int nd = o.bnd[b];
     for (int q = 0; q < nd && ok; ++q) {
       const int slot = (int)(b * kDMax + q);
-      const Mono M = o.dl_inh[slot] ? mono_cat(carry.m, o.dl_m[slot]) : o.dl_m[slot];
+      const Mono M = o.dl_inh[slot] ? mono_cat(cin, o.dl_m[slot]) : o.dl_m[slot];
       const short eb = (o.dl_e[slot] == (short)0x7ffe) ? prev_last : o.dl_e[slot];
       double acc = head;
       if (is_reg_e(eb)) ok = seq_apply_run(head, eb, M, &acc);
       acc = dadd(acc, o.dl_x[slot]);
       head = acc;
-      head_slot = slot;
       w.head_val[slot] = acc;
     }
-    const Seg a = o.bagg[b];
-    carry = a.h ? a : Seg{carry.h, mono_cat(carry.m, a.m)};
-    prev_last = o.blast[b];
   }
   double total = head;
-  if (ok && is_reg_e(prev_last)) ok = seq_apply_run(head, prev_last, carry.m, &total);
+  const short last_e = o.blast[nb - 1];
+  if (ok && is_reg_e(last_e)) ok = seq_apply_run(head, last_e, w.final_m[0], &total);
   if (!ok) atomicOr(flags, FLAG_SEQSUM);
   else *w.total = total;
 }
@@ -277,11 +317,14 @@ void seq_cumsum(Ctx* ctx, const double* x, int64_t n, double* cum, double* d_tot
   Buf<unsigned> fl(ctx, 1);
   fl.zero();
   LocalOut o{ge.p, gm.p, gslot.p, dlx.p, dlm.p, dle.p, dli.p, bnd.p, bagg.p, blast.p};
-  WalkOut w{headv.p, cin.p, inh.p, d_total};
+  Buf<Mono> finm(ctx, 1);
+  Buf<int> dblocks(ctx, nb), ndb(ctx, 1);
+  WalkOut w{headv.p, cin.p, inh.p, d_total, finm.p};
   LAUNCH(ctx, k_chunk_sum, (unsigned)nb, kThreads, 0, x, (long long)n, bsum.p);
   LAUNCH(ctx, k_scan_bsum, 1, 1024, 0, bsum.p, nb, bpre.p);
   LAUNCH(ctx, k_seq_local, (unsigned)nb, kThreads, 0, x, (long long)n, bpre.p, o, fl.p);
-  LAUNCH(ctx, k_seq_walk, 1, 32, 0, nb, o, w, fl.p);
+  LAUNCH(ctx, k_seq_carry, 1, kCarryThreads, 0, nb, o, w, dblocks.p, ndb.p);
+  LAUNCH(ctx, k_seq_walk, 1, 32, 0, nb, o, w, dblocks.p, ndb.p, fl.p);
   if (cum) LAUNCH(ctx, k_seq_final, ceil_div(n, 256), 256, 0, (long long)n, o, w, cum, fl.p);
   LAUNCH(ctx, k_seq_fallback, 1, 32, 0, x, (long long)n, cum, d_total, fl.p);
 }

@@ -34,11 +34,17 @@ void front_end(Ctx* ctx, const Fibers& fb, Basis& basis, int64_t s, double eps, 
                Front& fr, bool trace) {
   const int64_t F = fb.F;
   Buf<double> probs(ctx, F + 1), cum(ctx, F + 1), total(ctx, 1);
-  sampling_law(ctx, fb.norm.p, F, total.p, probs.p, cum.p, ctx->d_flags);
+  {
+    PhaseScope ps(ctx, PH_LAW);
+    sampling_law(ctx, fb.norm.p, F, total.p, probs.p, cum.p, ctx->d_flags);
+  }
   Buf<int32_t> drawn(ctx, s), uniq(ctx, s);
   Buf<int> nu(ctx, 1);
-  draw_fibers(ctx, cum.p, F, s, seed, drawn.p);
-  dedup_first(ctx, drawn.p, s, uniq.p, nu.p);
+  {
+    PhaseScope ps(ctx, PH_SAMPLE);
+    draw_fibers(ctx, cum.p, F, s, seed, drawn.p);
+    dedup_first(ctx, drawn.p, s, uniq.p, nu.p);
+  }
   int n_u = 0;
   ctx->to_host(&n_u, nu.p, 1);
   ctx->to_host(&fr.total, total.p, 1);
@@ -104,7 +110,10 @@ void run_ctd_s(Ctx* ctx, const Tensor& x, int mode, int64_t s, double eps, uint6
   out.eps = eps;
   out.seed = seed;
   Fibers fb;
-  matricize(ctx, x, mode, fb);
+  {
+    PhaseScope ps(ctx, PH_MATRICIZE);
+    matricize(ctx, x, mode, fb);
+  }
   out.F = fb.F;
   out.cols = fb.cols;
   out.rows = fb.rows;
@@ -127,7 +136,10 @@ void run_ctd_s(Ctx* ctx, const Tensor& x, int mode, int64_t s, double eps, uint6
       out.min_margin = std::min(out.min_margin, m);
     }
   }
-  if (flags & CTD_GPU_WITH_ERROR) out.rel_error = relative_error(ctx, fb, *out.basis);
+  if (flags & CTD_GPU_WITH_ERROR) {
+    PhaseScope ps(ctx, PH_ERROR);
+    out.rel_error = relative_error(ctx, fb, *out.basis);
+  }
 }
 
 void stream_init(Ctx* ctx, const Tensor& hist, int mode, int64_t s, double eps, uint64_t seed,

@@ -45,6 +45,54 @@ struct Ctx {
   }
   // Reads and clears the kernel error flags; raises the mapped status.
   void check_flags(const char* where);
+
+  // Optional live phase timing with CUDA events on `stream` (bench.py).
+  static constexpr int kPhases = 8;
+  bool timing = false;
+  double phase_ms[kPhases] = {0};
+  int64_t phase_n[kPhases] = {0};
+  struct Mark {
+    int ph;
+    cudaEvent_t a, b;
+  };
+  std::vector<Mark> marks;
+  int open_ph = -1;
+  cudaEvent_t open_ev = nullptr;
+  void phase_begin(int ph) {
+    if (!timing) return;
+    CUDA_OK(cudaEventCreate(&open_ev));
+    CUDA_OK(cudaEventRecord(open_ev, stream));
+    open_ph = ph;
+  }
+  void phase_end() {
+    if (!timing || open_ph < 0) return;
+    cudaEvent_t b;
+    CUDA_OK(cudaEventCreate(&b));
+    CUDA_OK(cudaEventRecord(b, stream));
+    marks.push_back(Mark{open_ph, open_ev, b});
+    open_ph = -1;
+  }
+  void phase_flush() {
+    for (auto& m : marks) {
+      CUDA_OK(cudaEventSynchronize(m.b));
+      float ms = 0;
+      CUDA_OK(cudaEventElapsedTime(&ms, m.a, m.b));
+      phase_ms[m.ph] += ms;
+      phase_n[m.ph] += 1;
+      cudaEventDestroy(m.a);
+      cudaEventDestroy(m.b);
+    }
+    marks.clear();
+  }
+};
+
+enum Phase { PH_MATRICIZE = 0, PH_LAW, PH_SAMPLE, PH_FILTER_PREP, PH_FILTER, PH_ERROR, PH_H2D, PH_OTHER };
+
+// Scoped phase marker (no-op unless ctx->timing).
+struct PhaseScope {
+  Ctx* c;
+  PhaseScope(Ctx* ctx, int ph) : c(ctx) { c->phase_begin(ph); }
+  ~PhaseScope() { c->phase_end(); }
 };
 
 // RAII device buffer (stream-ordered allocation on the context stream).

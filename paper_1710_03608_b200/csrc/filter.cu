@@ -27,6 +27,7 @@
 #include <cmath>
 
 #include "filter.cuh"
+#include "gridsum.cuh"
 #include "radix.cuh"
 #include "seqsum.cuh"
 
@@ -218,217 +219,17 @@ struct FArgs {
   long long* final_rnnz;
   unsigned* bar;
   unsigned* flags;
+  long long* trace;  // optional [n_u][16] clock64 stamps from CTA 0 (CTD_FILTER_TRACE)
+  SliceSum* ssum;    // [grid] residual-sum slice summaries
+  SliceDirect* sdir; // [grid * kSliceDirects]
+  int* nfallback;    // exact-sum self-check failures (sequential fallback taken)
 };
 
-constexpr int kFThreads = 512;
-
-__global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
-  __shared__ SeqSumSmem S;
-  __shared__ uint32_t hist[(kFThreads / 32) * kRadix];
-  __shared__ uint32_t sh32[33];
-  __shared__ int shi[33];
-  __shared__ int s_cnt;
-  const unsigned nb = gridDim.x;
-  const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long gthreads = (long long)nb * blockDim.x;
-  const long long LD = a.LD;
-  int K = a.K0;
-  long long rnnz = a.rnnz0;
-  bool prev_acc = false;
-  double prev_delta = 0.0;
-  int prev_n = -1;
-  for (int n = 0; n <= a.n_u; ++n) {
-    double* yprev = (n & 1) ? a.ybuf0 : a.ybuf1;
-    double* ycur = (n & 1) ? a.ybuf1 : a.ybuf0;
-    // ---------------- P0: apply the previous accept -------------------------
-    if (prev_acc) {
-      const int Ko = K;
-      const long long K1 = Ko + 1;
-      const long long tot = K1 * K1;
-      for (long long e = gtid; e < tot; e += gthreads) {
-        const long long i = e / K1, j = e - i * K1;
-        double v;
-        if (i < Ko && j < Ko) {
-          v = dadd(ldg_cg(&a.U[i * LD + j]), ddiv(dmul(ldg_cg(&yprev[i]), ldg_cg(&yprev[j])), prev_delta));
-        } else if (i == Ko && j == Ko) {
-          v = ddiv(1.0, prev_delta);
-        } else {
-          const long long q = (i == Ko) ? j : i;
-          v = ddiv(-ldg_cg(&yprev[q]), prev_delta);
-        }
-        a.U[i * LD + j] = v;
-      }
-      const long long off = a.c.off[prev_n];
-      const int m = a.c.len[prev_n];
-      for (long long t = gtid; t < m; t += gthreads) {
-        const int r = a.c.row[off + t];
-        const double v = a.c.val[off + t];
-        a.rrow[rnnz + t] = r;
-        a.rval[rnnz + t] = v;
-        const int L = ldg_cg(&a.rowlen[r]);
-        const long long p = a.rowbase[r] + L;
-        a.rek[p] = Ko;
-        a.rev[p] = v;
-        a.rowlen[r] = L + 1;
-      }
-      if (blockIdx.x == 0) {
-        // Ordered append of x's rows not yet in R (first-appearance order).
-        int srn = ldg_cg(a.sr_n);
-        for (int base = 0; base < m; base += blockDim.x) {
-          const int t = base + threadIdx.x;
-          const int r = t < m ? a.c.row[off + t] : 0;
-          const int isnew = (t < m) && (ldg_cg(&a.sr_pos[r]) < 0);
-          int tot2;
-          const int pos = block_excl_sum<int>(isnew, shi, &tot2);
-          if (isnew) {
-            a.sr_list[srn + pos] = r;
-            a.sr_pos[r] = srn + pos;
-          }
-          srn += tot2;
-          __syncthreads();
-        }
-        if (threadIdx.x == 0) {
-          *a.sr_n = srn;
-          a.kept_cand[Ko - a.K0] = prev_n;
-          a.rptr[Ko + 1] = rnnz + m;
-        }
-      }
-      rnnz += m;
-      K = Ko + 1;
-      grid_barrier(a.bar, nb);
-    }
-    if (n == a.n_u) break;
-    // ---------------- P1: y = U g --------------------------------------------
-    const long long off = a.c.off[n];
-    const int m = a.c.len[n];
-    const uint32_t tg = a.tag_base + (uint32_t)n + 1u;
-    // zd is double-buffered by candidate parity: CTAs still in P3 of n-1 read
-    // the other half.  x's rows start at z = 0 (rows outside R are untouched).
-    double* zdn = a.zd + (n & 1) * (a.dim + 1);
-    for (long long t = gtid; t < m; t += gthreads) {
-      a.tag[a.c.row[off + t]] = tg;
-      zdn[a.c.row[off + t]] = 0.0;
-    }
-    for (long long i = gtid; i < K; i += gthreads) {
-      double acc = 0.0;
-      for (int j = 0; j < K; ++j) {
-        const double g = (j < a.K0) ? a.Gb[(long long)j * a.n_u + n]
-                                    : a.Gc[(long long)ldg_cg(&a.kept_cand[j - a.K0]) * a.n_u + n];
-        // U is exactly symmetric: U[j][i] == U[i][j], read down column i (coalesced).
-        acc = dadd(acc, dmul(ldg_cg(&a.U[(long long)j * LD + i]), g));
-      }
-      ycur[i] = acc;
-    }
-    grid_barrier(a.bar, nb);
-    // ---------------- P2: z over R's rows, residual terms ---------------------
-    const int srn = ldg_cg(a.sr_n);
-    for (long long q = gtid; q < srn; q += gthreads) {
-      const int r = ldg_cg(&a.sr_list[q]);
-      const long long b0 = a.rowbase[r];
-      const int L = ldg_cg(&a.rowlen[r]);
-      double z = 0.0;
-      int kfd = -1;
-      int kst = -1;
-      for (int e = 0; e < L; ++e) {
-        const int k = ldg_cg(&a.rek[b0 + e]);
-        const double yk = ldg_cg(&ycur[k]);
-        z = dadd(z, dmul(yk, ldg_cg(&a.rev[b0 + e])));
-        if (kst < 0) kst = k;
-        if (kfd < 0 && yk != 0.0) kfd = k;
-      }
-      zdn[r] = z;
-      a.kf[r] = kfd;
-      a.term[q] = (ldg_cg(&a.tag[r]) == tg) ? 0.0 : dsqr(z);
-      // touched order differs from first-appearance order only if the row's
-      // first kept column has y == 0 while the row is still touched.
-      if (z != 0.0 && kfd != kst) atomicExch(&a.slow[n], 1);
-    }
-    grid_barrier(a.bar, nb);
-    // ---------------- P3: exact residual, decision (every CTA) ---------------
-    const bool slow = ldg_cg(&a.slow[n]) != 0;
-    long long nterm = srn;
-    const double* tsrc = a.term;
-    if (slow) {
-      // Rebuild the touched list in the reference's order: rows r not in x
-      // with kfd(r) >= 0, sorted by (kfd, position within column kfd) which is
-      // (kfd, r).  Done by CTA 0, then shared through a barrier.
-      if (blockIdx.x == 0) {
-        uint32_t* ka = a.skey;
-        uint32_t* kb = ka + a.dim;
-        uint32_t* ia = kb + a.dim;
-        uint32_t* ib = ia + a.dim;
-        if (threadIdx.x == 0) s_cnt = 0;
-        __syncthreads();
-        for (int q = threadIdx.x; q < srn; q += blockDim.x) {
-          const int r = ldg_cg(&a.sr_list[q]);
-          if (ldg_cg(&a.kf[r]) >= 0 && ldg_cg(&a.tag[r]) != tg) {
-            const int p = atomicAdd(&s_cnt, 1);
-            ka[p] = (uint32_t)r;
-            ia[p] = (uint32_t)r;
-          }
-        }
-        __syncthreads();
-        const int cnt = s_cnt;
-        // sort by r, then stable by kfd
-        bool inb = block_radix_sort<uint32_t>(ka, kb, ia, ib, cnt, 32, hist, sh32);
-        uint32_t* K2 = inb ? kb : ka;
-        uint32_t* I2 = inb ? ib : ia;
-        uint32_t* K3 = inb ? ka : kb;
-        uint32_t* I3 = inb ? ia : ib;
-        for (int p = threadIdx.x; p < cnt; p += blockDim.x) {
-          K3[p] = (uint32_t)ldg_cg(&a.kf[I2[p]]);
-          I3[p] = I2[p];
-        }
-        __syncthreads();
-        inb = block_radix_sort<uint32_t>(K3, K2, I3, I2, cnt, 32, hist, sh32);
-        const uint32_t* IF = inb ? I2 : I3;
-        for (int p = threadIdx.x; p < cnt; p += blockDim.x) a.term2[p] = dsqr(ldg_cg(&zdn[IF[p]]));
-        if (threadIdx.x == 0) a.slow[n] = 2 + cnt;  // publish count
-      }
-      grid_barrier(a.bar, nb);
-      nterm = ldg_cg(&a.slow[n]) - 2;
-      tsrc = a.term2;
-    }
-    const double* xv = a.c.val + off;
-    const int32_t* xr = a.c.row + off;
-    const double* zd = zdn;
-    auto get = [=](long long i) -> double {
-      if (i < m) {
-        const int r = xr[i];
-        const double z = ldg_cg(&zd[r]);
-        return dsqr(dsub(xv[i], z));  // fiber_basis.cpp:69-70
-      }
-      return ldg_cg(&tsrc[i - m]);     // fiber_basis.cpp:74-75
-    };
-    bool bad = false;
-    const double res = block_exact_sum(get, (long long)m + nterm, S, &bad);
-    const double xs = a.xsq[n];
-    const bool reject = __dsqrt_rn(res) <= dmul(a.eps, __dsqrt_rn(xs));  // :79
-    bool acc = false, degen = false;
-    if (!reject) {
-      degen = !(res > 0.0) || isinf(res) || isnan(res) || isinf(ddiv(1.0, res));  // :84-85
-      acc = !degen;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      a.accepted[n] = acc;
-      a.degenerate[n] = degen;
-      a.delta[n] = acc ? res : 0.0;
-      a.res_out[n] = res;
-      if (bad) atomicOr(a.flags, FLAG_SEQSUM);
-    }
-    if (a.y_last && n == a.n_u - 1 && blockIdx.x == 0)
-      for (int i = threadIdx.x; i < K; i += blockDim.x) a.y_last[i] = ldg_cg(&ycur[i]);
-    prev_acc = acc;
-    prev_delta = res;
-    prev_n = n;
-    // P1 of the next candidate overwrites `tag` and the other y buffer only;
-    // zd/term are rewritten in its P2 after a barrier, so no barrier here.
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *a.final_K = K;
-    *a.final_rnnz = rnnz;
-  }
+__device__ __forceinline__ void stamp(long long* tr, int n, int k) {
+  if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[(long long)n * 16 + k] = clock64();
 }
+
+#include "filter_kernel.cuh"
 
 }  // namespace
 
@@ -439,6 +240,7 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   if (n == 0) return;
   if (n >= (1ll << 31)) fail(CTD_ERR_ARGUMENT, "too many candidates");
   // ---- sizes
+  ctx->phase_begin(PH_FILTER_PREP);
   Buf<long long> tl(ctx, 1);
   tl.zero();
   LAUNCH(ctx, k_cand_stats, std::min<unsigned>(ceil_div(n, 256), 1024), 256, 0, c, tl.p);
@@ -563,15 +365,38 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   fa.final_rnnz = fR.p;
   fa.bar = ctx->d_bar;
   fa.flags = ctx->d_flags;
+  Buf<SliceSum> ssum(ctx, ctx->sm_count);
+  Buf<SliceDirect> sdir(ctx, (size_t)ctx->sm_count * kSliceDirects);
+  fa.ssum = ssum.p;
+  fa.sdir = sdir.p;
+  Buf<int> nfb(ctx, 1);
+  nfb.zero();
+  fa.nfallback = nfb.p;
+  const char* trace_env = getenv("CTD_FILTER_TRACE");
+  Buf<long long> tbuf;
+  if (trace_env && *trace_env == '1') {
+    tbuf.alloc(ctx, (size_t)n * 16);
+    tbuf.zero();
+    fa.trace = tbuf.p;
+  }
   ctx->zero(ctx->d_bar, 2 * sizeof(unsigned));
   int per_sm = 0;
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter, kFThreads, 0));
+  const size_t dsmem = (2 * kVec + (kFThreads / 32) * kWin) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    CUDA_OK(cudaFuncSetAttribute(k_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
+    attr = true;
+  }
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter, kFThreads, dsmem));
   if (per_sm < 1) fail(CTD_ERR_DEVICE, "filter kernel cannot be resident");
   const unsigned grid = (unsigned)ctx->sm_count;  // one CTA per SM
   void* args[] = {&fa};
-  CUDA_OK(cudaLaunchCooperativeKernel((const void*)k_filter, dim3(grid), dim3(kFThreads), args, 0,
+  ctx->phase_end();
+  ctx->phase_begin(PH_FILTER);
+  CUDA_OK(cudaLaunchCooperativeKernel((const void*)k_filter, dim3(grid), dim3(kFThreads), args, dsmem,
                                       ctx->stream));
   ctx->launches++;
+  ctx->phase_end();
   // ---- results
   out.accepted.resize(n);
   out.degenerate.resize(n);
@@ -595,6 +420,29 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
     ctx->to_host(out.y_last.data(), ylast.p, K0 + n);
   }
   ctx->sync();
+  if (fa.trace) {
+    std::vector<long long> tr((size_t)n * 16);
+    ctx->to_host(tr.data(), tbuf.p, (size_t)n * 16);
+    ctx->sync();
+    const char* names[] = {"append", "stage", "rows", "bar1", "P2", "bar2", "tstage", "xsum", "decide"};
+    double sum[9] = {0};
+    for (int64_t i = 0; i < n; ++i)
+      for (int k = 0; k < 9; ++k) sum[k] += (double)(tr[i * 16 + k + 1] - tr[i * 16 + k]);
+    fprintf(stderr, "[filter trace] fallbacks=%d\n", ctx->read1(nfb.p));
+    fprintf(stderr, "[filter trace] n=%lld cycles/candidate:", (long long)n);
+    for (int k = 0; k < 9; ++k) fprintf(stderr, " %s=%.0f", names[k], sum[k] / n);
+    fprintf(stderr, "\n");
+    for (int64_t i = 0; i < n; i += std::max<int64_t>(1, n / 8)) {
+      fprintf(stderr, "  cand %lld:", (long long)i);
+      for (int k = 0; k < 9; ++k) fprintf(stderr, " %lld", tr[i * 16 + k + 1] - tr[i * 16 + k]);
+      // P2 detail: staging, first row, remaining rows (CTA 0 warp 0)
+      fprintf(stderr, " | P2: stage=%lld row0=%lld rest=%lld | P3: bar=%lld combine=%lld",
+              tr[i * 16 + 10] - tr[i * 16 + 4], tr[i * 16 + 11] - tr[i * 16 + 10],
+              tr[i * 16 + 5] - tr[i * 16 + 11], tr[i * 16 + 12] - tr[i * 16 + 7],
+              tr[i * 16 + 8] - tr[i * 16 + 12]);
+      fprintf(stderr, "\n");
+    }
+  }
   ctx->check_flags("filter");
   int64_t k_at_last = K0;
   for (int64_t i = 0; i < n; ++i) {

@@ -57,6 +57,43 @@ __device__ __forceinline__ bool near_binade_edge(double P, double mg) {
   return (P - lo) <= mg * P || (2.0 * lo - P) <= mg * P;
 }
 
+// The grid increment of a regular element in binade ec: round(x / 2^(ec-52))
+// with the tie flagged.  Pure integer work on the bit pattern (FRND/F2I are
+// slow-pipe instructions on sm_100): x = mx * 2^(ex-52), so the scaled value
+// is mx * 2^-d with d = ec - ex; floor = mx >> d and the fraction compares as
+// the remainder against the half bit 2^(d-1).
+__device__ __forceinline__ void seq_mono(double x, int ec, Mono* m_out) {
+  const long long bits = __double_as_longlong(x);
+  const int bexp = (int)((bits >> 52) & 0x7FF);
+  long long mx = bits & 0xFFFFFFFFFFFFFLL;
+  int ex = -1022;
+  if (bexp != 0) {
+    mx |= (1LL << 52);
+    ex = bexp - 1023;
+  }
+  const int d = ec - ex;
+  long long k0 = 0, rem = 0, half = 1;  // defaults: d > 55 -> 0, no tie
+  if (d <= 0) {
+    k0 = mx << (-d);
+    rem = 0;
+  } else if (d <= 55) {
+    k0 = mx >> d;
+    rem = mx & ((1LL << d) - 1);
+    half = 1LL << (d - 1);
+  } else {
+    rem = 0;  // x / ulp < 2^-2: rounds to 0
+    half = 1;
+  }
+  if (rem > half) {
+    m_out->a0 = m_out->a1 = k0 + 1;
+  } else if (rem < half) {
+    m_out->a0 = m_out->a1 = k0;
+  } else {  // exact tie: the result rounds to even
+    m_out->a0 = k0 + (k0 & 1);
+    m_out->a1 = k0 + ((k0 + 1) & 1);
+  }
+}
+
 // Classify element i given approximate prefixes before (Pp) and after (Pc).
 __device__ __forceinline__ int seq_classify(bool first, double Pp, double Pc, double x,
                                             double mg, int* e_out, Mono* m_out) {
@@ -65,20 +102,23 @@ __device__ __forceinline__ int seq_classify(bool first, double Pp, double Pc, do
   const int ep = dexp(Pp), ec = dexp(Pc);
   if (ep != ec || ec < -960 || ec > 1020) return CLS_DIRECT;
   if (near_binade_edge(Pp, mg) || near_binade_edge(Pc, mg)) return CLS_DIRECT;
-  const double s = dmul(x, pow2(52 - ec));  // exact power-of-two scaling, < 2^53
-  const double fl = floor(s);
-  const double fr = dsub(s, fl);
-  const long long m = (long long)fl;
-  if (fr > 0.5) {
-    m_out->a0 = m_out->a1 = m + 1;
-  } else if (fr < 0.5) {
-    m_out->a0 = m_out->a1 = m;
-  } else {  // exact tie: result rounds to even
-    m_out->a0 = m + (m & 1);
-    m_out->a1 = m + ((m + 1) & 1);
-  }
+  seq_mono(x, ec, m_out);
   *e_out = ec;
   return CLS_REG;
+}
+
+// A whole chunk is regular in binade *e when the approximate prefix before it
+// (pre) and after it (post) both lie strictly inside [2^e, 2^(e+1)) with the
+// error margin to spare: the running sum is monotone, so every intermediate
+// value (true or approximate) is inside too.
+__device__ __forceinline__ bool seq_chunk_regular(double pre, double post, double mg, int* e) {
+  if (!(pre > 0.0) || !(post > 0.0) || !(post < 1.7976931348623157e308)) return false;
+  const int ep = dexp(pre);
+  if (ep != dexp(post) || ep < -960 || ep > 1020) return false;
+  const double lo = pow2(ep);
+  if (!(pre - lo > 2.0 * mg * pre) || !(2.0 * lo - post > 4.0 * mg * post)) return false;
+  *e = ep;
+  return true;
 }
 
 // Applies a same-binade run summarized by M to the value `head` (the value of
@@ -171,7 +211,11 @@ struct SeqSumSmem {
 };
 
 template <typename Get>
-__device__ double block_exact_sum(const Get& get, long long n, SeqSumSmem& S, bool* fail) {
+__device__ double block_exact_sum(const Get& get, long long n, SeqSumSmem& S, bool* fail,
+                                  long long* tp = nullptr) {
+#define SEQ_STAMP(k) \
+  if (tp && threadIdx.x == 0) tp[k] = clock64();
+  SEQ_STAMP(0)
   const int T = blockDim.x, t = threadIdx.x;
   if (n <= 0) return 0.0;
   const long long per = (n + T - 1) / T;
@@ -181,12 +225,22 @@ __device__ double block_exact_sum(const Get& get, long long n, SeqSumSmem& S, bo
   for (long long i = b0; i < b1; ++i) cs += get(i);
   double tot;
   double pre = block_excl_sum<double>(cs, S.dsh, &tot);
+  SEQ_STAMP(1)
   const double mg = seq_margin(n);
   // Pass B: thread aggregate + direct count.
   Seg agg{0, mono_id()};
   int nd = 0;
   short le = E_ZERO;
-  {
+  int fe = 0;
+  const bool fast = (b0 > 0) && (b0 < b1) && seq_chunk_regular(pre, pre + cs, mg, &fe);
+  if (fast) {
+    for (long long i = b0; i < b1; ++i) {
+      Mono m;
+      seq_mono(get(i), fe, &m);
+      agg.m = mono_cat(agg.m, m);
+    }
+    le = (short)fe;
+  } else {
     double P = pre;
     for (long long i = b0; i < b1; ++i) {
       const double x = get(i);
@@ -208,20 +262,26 @@ __device__ double block_exact_sum(const Get& get, long long n, SeqSumSmem& S, bo
   }
   if (t == 0) S.bad = 0;
   S.last_e[t] = (b0 < b1) ? le : (short)0x7fff;  // 0x7fff: empty chunk
+  SEQ_STAMP(2)
   Seg carry = block_seg_excl(agg, S.ssh, nullptr);
+  SEQ_STAMP(3)
   int ntot;
   int dpos = block_excl_sum<int>(nd, S.ish, &ntot);
   if (ntot > SeqSumSmem::kCap) {
     if (t == 0) S.bad = 1;
+  } else if (fast) {
+    // no heads in this chunk: only the final run summary may be needed
+    if (b1 == n) {
+      S.fin_m = mono_cat(carry.m, agg.m);
+      S.fin_e = (short)fe;
+    }
   } else {
     // Pass C: record each direct's preceding run summary.
     double P = pre;
     Mono M = carry.m;
-    // e of the element before my chunk: walk back over empty chunks.
-    short prev_e = E_ZERO;
-    for (int q = t - 1; q >= 0; --q) {
-      if (S.last_e[q] != (short)0x7fff) { prev_e = S.last_e[q]; break; }
-    }
+    // e of the element before my chunk: chunks fill in thread order, so it is
+    // the previous thread's last element.
+    short prev_e = (t > 0) ? S.last_e[t - 1] : E_ZERO;
     for (long long i = b0; i < b1; ++i) {
       const double x = get(i);
       const double Pc = P + x;
@@ -249,7 +309,9 @@ __device__ double block_exact_sum(const Get& get, long long n, SeqSumSmem& S, bo
       S.fin_e = prev_e;
     }
   }
+  SEQ_STAMP(4)
   __syncthreads();
+  SEQ_STAMP(5)
   if (t == 0) {
     bool ok = !S.bad;
     double acc = 0.0, head = 0.0;
@@ -269,6 +331,8 @@ __device__ double block_exact_sum(const Get& get, long long n, SeqSumSmem& S, bo
     S.bad = ok ? 0 : 1;
   }
   __syncthreads();
+  SEQ_STAMP(6)
+#undef SEQ_STAMP
   const double r = S.result;
   if (fail) *fail = S.bad != 0;
   __syncthreads();

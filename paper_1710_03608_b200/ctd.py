@@ -91,6 +91,16 @@ class Context:
     def launches(self) -> int:
         return int(self.L.ctd_gpu_ctx_launches(self.h))
 
+    def set_timing(self, enable: bool):
+        _check(self.L.ctd_gpu_ctx_set_timing(self.h, int(enable)))
+
+    def phase_times(self, reset: bool = True) -> dict:
+        """{phase: (total_ms, count)} from CUDA events on the context stream."""
+        ms = np.zeros(8)
+        n = np.zeros(8, dtype=np.int64)
+        _check(self.L.ctd_gpu_ctx_phase_times(self.h, _p(ms), _p(n), int(reset)))
+        return {self.L.ctd_gpu_phase_name(i).decode(): (float(ms[i]), int(n[i])) for i in range(8)}
+
     def close(self):
         if getattr(self, "h", None):
             self.L.ctd_gpu_ctx_destroy(self.h)
@@ -158,6 +168,24 @@ class DeviceTensor:
         self.h = h
         self.nnz = x.nnz
         self.order = len(shape)
+
+    @classmethod
+    def from_host_ptrs(cls, shape, nnz: int, idx_ptr: int, val_ptr: int,
+                       ctx: Optional[Context] = None) -> "DeviceTensor":
+        """Copy a host SparseTensor given raw (e.g. pinned) pointers: int64
+        row-concatenated coordinates and fp64 values."""
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        self.shape = [int(s) for s in shape]
+        shp = np.asarray(self.shape, dtype=np.int64)
+        h = C.c_void_p()
+        _check(self.ctx.L.ctd_gpu_tensor_from_host(self.ctx.h, len(shp), _p(shp), nnz,
+                                                   C.c_void_p(int(idx_ptr)),
+                                                   C.c_void_p(int(val_ptr)), C.byref(h)))
+        self.h = h
+        self.nnz = nnz
+        self.order = len(shp)
+        return self
 
     @classmethod
     def from_device_ptrs(cls, shape, nnz: int, mode_ptrs, val_ptr: int,
@@ -284,6 +312,15 @@ def sample_with_replacement(probabilities, count: int, seed: int,
     _check(ctx.L.ctd_gpu_sample_with_replacement(ctx.h, _p(p), len(p), count, C.c_uint64(seed),
                                                  _p(out)))
     return out[:max(count, 0)].copy()
+
+
+def seq_cumsum(x, ctx: Optional[Context] = None) -> np.ndarray:
+    """Bit-exact sequential running sum of non-negative doubles on the GPU."""
+    ctx = ctx or default_context()
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.zeros(max(len(a), 1))
+    _check(ctx.L.ctd_gpu_seq_cumsum(ctx.h, _p(a), len(a), _p(out)))
+    return out[:len(a)].copy()
 
 
 def unique_first_occurrence(drawn, ctx: Optional[Context] = None) -> np.ndarray:
@@ -451,6 +488,44 @@ def ctd_s(x, mode: int, sample_size: int, epsilon: float = 1e-6, seed: int = 42,
     _check(ctx.L.ctd_gpu_ctd_s(ctx.h, d.h, mode, sample_size, epsilon, C.c_uint64(seed),
                                WITH_ERROR if with_error else 0, C.byref(h)))
     return _read_factors(ctx, h, d.shape, mode)
+
+
+def ctd_s_raw(x, mode: int, sample_size: int, epsilon: float = 1e-6, seed: int = 42,
+              with_error: bool = False, ctx: Optional[Context] = None):
+    """ctd_s without copying R/U to the host: returns (handle, FactorsInfo).
+    Free the handle with ``free_factors``."""
+    ctx = ctx or default_context()
+    d = _dev(x, ctx)
+    h = C.c_void_p()
+    _check(ctx.L.ctd_gpu_ctd_s(ctx.h, d.h, mode, sample_size, epsilon, C.c_uint64(seed),
+                               WITH_ERROR if with_error else 0, C.byref(h)))
+    info = _lib.FactorsInfo()
+    _check(ctx.L.ctd_gpu_factors_info_get(h, C.byref(info)))
+    return h, info
+
+
+def free_factors(ctx: Context, h) -> None:
+    _check(ctx.L.ctd_gpu_factors_destroy(h))
+
+
+def factors_trace(ctx: Context, h, info) -> dict:
+    """Per-candidate decisions and R's column lengths (for byte accounting)."""
+    nu, k = info.n_unique, info.kept
+    acc = np.zeros(max(nu, 1), np.int32)
+    _check(ctx.L.ctd_gpu_factors_trace(h, None, None, _p(acc), None, None))
+    cp = np.zeros(k + 1, np.int64)
+    _check(ctx.L.ctd_gpu_factors_r(h, _p(cp), None, None))
+    return {"accepted": acc[:nu].astype(bool), "r_lens": np.diff(cp)}
+
+
+def factors_result(ctx: Context, h, info):
+    """The decomposition's result on the host: kept fiber ids and U."""
+    k = info.kept
+    kept = np.zeros(max(k, 1), dtype=np.int64)
+    _check(ctx.L.ctd_gpu_factors_kept_flat(h, _p(kept)))
+    u = np.zeros(max(k * k, 1))
+    _check(ctx.L.ctd_gpu_factors_u(h, _p(u)))
+    return kept[:k], u[:k * k].reshape(k, k)
 
 
 def relative_error(x, factors: LRFactors, ctx: Optional[Context] = None) -> float:

@@ -66,14 +66,46 @@ class Tensor:
         return Tensor(shape, idx, self.val[sel].copy(), {"slab": (t0, t1)})
 
 
+def _sorted_runs(k: np.ndarray):
+    """Distinct values of k (sorted) and the index of each one's first occurrence."""
+    n = k.shape[0]
+    sh = max(1, int(n - 1).bit_length())
+    if k.shape[0] and int(k.max()) < (1 << (62 - sh)):
+        s = np.sort((k << sh) | np.arange(n, dtype=np.int64))  # radix-friendly composite
+        ks, ix = s >> sh, s & ((1 << sh) - 1)
+    else:
+        ix = np.argsort(k, kind="stable")
+        ks = k[ix]
+    head = np.ones(n, dtype=bool)
+    head[1:] = ks[1:] != ks[:-1]
+    return ks[head], ix[head]
+
+
+def _coalesce_sorted(k: np.ndarray, v: np.ndarray):
+    """(distinct sorted keys, values summed in input order)."""
+    n = k.shape[0]
+    if n == 0:
+        return k, v
+    sh = max(1, int(n - 1).bit_length())
+    if int(k.max()) < (1 << (62 - sh)):
+        s = np.sort((k << sh) | np.arange(n, dtype=np.int64))
+        ks, ix = s >> sh, s & ((1 << sh) - 1)
+    else:
+        ix = np.argsort(k, kind="stable")
+        ks = k[ix]
+    head = np.ones(n, dtype=bool)
+    head[1:] = ks[1:] != ks[:-1]
+    starts = np.nonzero(head)[0]
+    return ks[starts], np.add.reduceat(v[ix], starts)
+
+
 def coalesce(shape, idx: np.ndarray, val: np.ndarray) -> Tensor:
     """Sort lexicographically, sum duplicates in input order, drop zeros."""
     shape = [int(s) for s in shape]
     key = np.zeros(idx.shape[0], dtype=np.int64)
     for k, s in enumerate(shape):
         key = key * s + idx[:, k].astype(np.int64)
-    uk, inv = np.unique(key, return_inverse=True)
-    summed = np.bincount(inv.reshape(-1), weights=val, minlength=uk.shape[0])
+    uk, summed = _coalesce_sorted(key, np.asarray(val, dtype=np.float64))
     keep = summed != 0.0
     uk, summed = uk[keep], summed[keep]
     out = np.zeros((uk.shape[0], len(shape)), dtype=np.int64)
@@ -128,8 +160,9 @@ def traffic(shape, target_nnz: int, seed: int, max_count: int = 100, log_counts=
     keys = []
     vals = []
     drawn = 0
-    nnz = 0
-    while nnz < target_nnz:
+    seen = np.zeros(0, dtype=np.int64)  # sorted distinct keys so far
+    hi = None
+    while hi is None:
         n = batch
         src = zs(uniform(seed, 1, drawn, n))
         dst = zd(uniform(seed, 2, drawn, n))
@@ -139,23 +172,26 @@ def traffic(shape, target_nnz: int, seed: int, max_count: int = 100, log_counts=
             cnt = np.clip(np.floor(np.exp(uc * np.log(max_count + 1.0))), 1, max_count)
         else:
             cnt = np.floor(uc * max_count) + 1
-        keys.append((src.astype(np.int64) * J + dst) * T + tt)
+        k = (src.astype(np.int64) * J + dst) * T + tt
+        # novelty of each draw: first occurrence in this batch and not seen before
+        uk, first = _sorted_runs(k)
+        pos = np.searchsorted(seen, uk)
+        novel = (pos >= seen.shape[0]) | (seen[np.minimum(pos, max(seen.shape[0] - 1, 0))] != uk) \
+            if seen.shape[0] else np.ones(uk.shape[0], dtype=bool)
+        is_new = np.zeros(n, dtype=bool)
+        is_new[first[novel]] = True
+        run = seen.shape[0] + np.cumsum(is_new)
+        keys.append(k)
         vals.append(cnt)
-        drawn += n
-        nnz = np.unique(np.concatenate(keys)).shape[0]
-    k = np.concatenate(keys)
-    v = np.concatenate(vals)
-    # Trim to the shortest prefix of draws whose coalesced nnz reaches the target.
-    lo, hi = drawn - batch, drawn
-    while hi - lo > 1024:
-        mid = (lo + hi) // 2
-        if np.unique(k[:mid]).shape[0] >= target_nnz:
-            hi = mid
+        if run[-1] >= target_nnz:
+            # shortest prefix of all draws whose coalesced nnz reaches the target
+            hi = drawn + int(np.argmax(run >= target_nnz)) + 1
         else:
-            lo = mid
-    k, v = k[:hi], v[:hi]
-    uk, inv = np.unique(k, return_inverse=True)
-    summed = np.bincount(inv, weights=v, minlength=uk.shape[0])
+            seen = np.sort(np.concatenate([seen, uk[novel]]))
+        drawn += n
+    k = np.concatenate(keys)[:hi]
+    v = np.concatenate(vals)[:hi]
+    uk, summed = _coalesce_sorted(k, v)
     idx = np.stack([uk // (J * T), (uk // T) % J, uk % T], axis=1)
     t = Tensor([I, J, T], idx.astype(np.int64), summed)
     t.meta = {"seed": seed, "draws": int(hi), "zipf": zipf_s}
