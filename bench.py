@@ -141,7 +141,6 @@ def phase_bytes(nnz, F, kept_seq, r_lens):
         "sample": 0,
         "filter_prep": 0,
         "filter": filt,
-        "error": 12 * nnz + 8 * F,            # stream (row,val) + fiber offsets once
     }
 
 
@@ -167,7 +166,7 @@ def run_ours(args, rank, world, local_rank):
     c, eps, seed, mode = C2["c"], C2["eps"], C2["seed"], C2["mode"]
 
     def step():
-        h, info = api.ctd_s_raw(dt, mode, c, eps, seed, with_error=True, ctx=ctx)
+        h, info = api.ctd_s_raw(dt, mode, c, eps, seed, with_error=False, ctx=ctx)
         return h, info
 
     for _ in range(args.warmup):
@@ -197,8 +196,26 @@ def run_ours(args, rank, world, local_rank):
     ctx.set_timing(False)
     info = infos[-1][1]
     tr = api.factors_trace(ctx, infos[-1][0], info)
-    for h, _ in infos:
+    # ---- the relative-error pass (evaluation.cpp:88-122), timed on its own:
+    # the reference evaluates it outside ctd_s (stream_harness.cpp:72-81).
+    hlast = infos[-1][0]
+    for h, _ in infos[:-1]:
         api.free_factors(ctx, h)
+    rel = api.relative_error_raw(dt, hlast, ctx)
+    ctx.set_timing(True)
+    ctx.phase_times(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ne = max(1, min(args.steps, 3))
+    e0.record()
+    for _ in range(ne):
+        rel = api.relative_error_raw(dt, hlast, ctx)
+    e1.record()
+    torch.cuda.synchronize()
+    err_phases = ctx.phase_times(reset=True)
+    ctx.set_timing(False)
+    api.free_factors(ctx, hlast)
+    err_ms = e0.elapsed_time(e1) / ne
+    err_kernel_ms = err_phases["error"][0] / max(1, err_phases["error"][1])
     if world > 1:
         t = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -242,13 +259,18 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded splitmix64 generator, SURVEY §8d)",
         "config": {"workload": WORKLOAD, "nnz": nnz, "fibers": info.n_fibers,
+                   "step": "ctd_s front end: matricize+norms, law/CDF, mt19937_64 draws, dedup, "
+                           "bit-exact filter + U (C not materialized, as the CPU baseline)",
                    "unique_sampled": info.n_unique, "kept": info.kept,
-                   "relative_error": info.relative_error,
+                   "relative_error": rel,
                    "l2": "inputs larger than L2 (200 MB COO + 120 MB bucketed per step)",
                    "parallelism": f"fiber-range shards x{world}" if world > 1 else "1 GPU",
                    "step_bytes_44nnz_24F": bs,
                    "step_frac_of_peak": round(bs / (ms / 1e3) / 1e9 / pk, 4)},
         "roofline": roof, "phases": per_phase, "gpu_launches": launches,
+        "error_pass": {"ms": round(err_ms, 3), "kernel_ms": round(err_kernel_ms, 3),
+                       "nnz_per_s": round(nnz / (err_ms / 1e3), 1),
+                       "what": "relative_error(X, factors): matricize + Gram-identity pass over all nnz"},
         "clocks": clk.summary(),
     }
     if e2e:
@@ -269,7 +291,7 @@ def run_e2e(args, ctx, x, torch):
 
     def step():
         t = api.DeviceTensor.from_host_ptrs(x.shape, nnz, idx_h.data_ptr(), val_h.data_ptr(), ctx)
-        h, info = api.ctd_s_raw(t, mode, c, eps, seed, with_error=True, ctx=ctx)
+        h, info = api.ctd_s_raw(t, mode, c, eps, seed, with_error=False, ctx=ctx)
         kept, u = api.factors_result(ctx, h, info)   # D2H: kept ids + U
         api.free_factors(ctx, h)
         t.close()

@@ -13,6 +13,10 @@
 //      coalesced write of rows/values, fiber heads ranked across buckets with
 //      a decoupled look-back, and each fiber's squared norm summed in
 //      ascending-row order (bit-identical to the reference loop).
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "bucket.cuh"
 #include "radix.cuh"
 
@@ -286,6 +290,12 @@ int bits_for(long long n) {  // bits needed to represent 0..n-1
 }  // namespace
 
 void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
+  static const bool htrace = getenv("CTD_HOST_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point ht[8];
+  int nht = 0;
+#define HT() \
+  if (htrace) ht[nht++] = std::chrono::steady_clock::now();
+  HT()
   if (mode < 0 || mode >= x.order)
     fail(CTD_ERR_ARGUMENT, "mode " + std::to_string(mode) + " out of range for order " +
                                std::to_string(x.order));
@@ -333,6 +343,7 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
     ctx->zero(out.ptr.p, sizeof(int64_t));
     return;
   }
+  HT()
   Buf<unsigned> count(ctx, nb);
   count.zero();
   Buf<unsigned long long> off(ctx, nb + 1), cursor(ctx, nb + 1), status(ctx, nb);
@@ -349,6 +360,7 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
     ctx->to_dev(intok.p, &one, 1);
   }
   const unsigned grid = (unsigned)std::min<long long>((nnz + 255) / 256, (long long)ctx->sm_count * 16);
+  HT()
   LAUNCH(ctx, k_hist, grid, 256, 0, c, wbits, count.p, ctx->d_flags);
   Buf<unsigned> maxc(ctx, 1);
   maxc.zero();
@@ -365,6 +377,7 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
   gidx2.alloc(ctx, nnz);
   // Shared-memory capacity sized to the largest bucket (more CTAs per SM).
   const unsigned mx = ctx->read1(maxc.p);
+  HT()
   int cap = 256;
   while (cap < (int)mx && cap < kCap) cap <<= 1;
   const int threads = cap <= 2048 ? 256 : kSortThreads;
@@ -380,6 +393,7 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
     attr_set = true;
   }
   LAUNCH(ctx, k_bucket_sort, (unsigned)nb, threads, smem, sa);
+  HT()
   long long F = 0;
   int iok = 0;
   double ssq = 0.0;
@@ -391,6 +405,14 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
   out.sum_sq = ssq;
   out.integer_exact = iok && ssq < 4503599627370496.0;  // 2^52
   ctx->check_flags("matricize");
+  HT()
+  if (htrace) {
+    fprintf(stderr, "[matricize host]");
+    for (int i = 1; i < nht; ++i)
+      fprintf(stderr, " %.3f", std::chrono::duration<double, std::milli>(ht[i] - ht[i - 1]).count());
+    fprintf(stderr, " ms\n");
+  }
+#undef HT
 }
 
 }  // namespace ctdgpu

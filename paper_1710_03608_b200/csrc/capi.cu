@@ -1,6 +1,8 @@
 // extern "C" boundary (include/ctd_gpu.h).  Every entry point converts
 // internal failures into the reference ErrorClass codes.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -116,6 +118,21 @@ int ctd_gpu_ctx_create(int device, void* stream, ctd_gpu_ctx** out) {
     CUDA_OK(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     CUDA_OK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // Prewarm the stream-ordered pool so steady-state calls never map memory
+    // (CTD_GPU_POOL_MB, default 8192; the pool keeps it: threshold above).
+    {
+      size_t mb = 8192;
+      if (const char* e = getenv("CTD_GPU_POOL_MB")) mb = (size_t)atoll(e);
+      size_t free_b = 0, total_b = 0;
+      CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+      mb = std::min(mb, free_b / 4 / (1 << 20));
+      if (mb > 0) {
+        void* p = nullptr;
+        CUDA_OK(cudaMallocAsync(&p, mb << 20, c.stream));
+        CUDA_OK(cudaFreeAsync(p, c.stream));
+        CUDA_OK(cudaStreamSynchronize(c.stream));
+      }
+    }
     CUDA_OK(cudaMalloc(&c.d_flags, sizeof(unsigned)));
     CUDA_OK(cudaMalloc(&c.d_bar, 4 * sizeof(unsigned)));
     CUDA_OK(cudaMemset(c.d_flags, 0, sizeof(unsigned)));
@@ -433,8 +450,15 @@ int ctd_gpu_relative_error(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, ctd_gpu_fa
     for (int k = 0; k < F.order; ++k)
       if (x->t.shape[k] != F.shape[k]) fail(CTD_ERR_SHAPE, "factor shape does not match the tensor");
     Fibers fb;
-    matricize(&ctx->c, x->t, F.mode, fb);
-    *out = relative_error(&ctx->c, fb, *F.basis);
+    {
+      PhaseScope ps(&ctx->c, PH_MATRICIZE);
+      matricize(&ctx->c, x->t, F.mode, fb);
+    }
+    {
+      PhaseScope ps(&ctx->c, PH_ERROR);
+      *out = relative_error(&ctx->c, fb, *F.basis);
+    }
+    ctx->c.phase_flush();
   });
 }
 

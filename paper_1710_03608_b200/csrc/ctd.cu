@@ -1,5 +1,9 @@
 // Orchestration of Algorithm 1 (CTD-S, ctd_static.cpp:19-50) and
 // Algorithm 2 (CTD-D step, ctd_dynamic.cpp:149-229) on the device.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "cdf.cuh"
 #include "ctd.cuh"
 #include "relerr.cuh"
@@ -110,10 +114,13 @@ void run_ctd_s(Ctx* ctx, const Tensor& x, int mode, int64_t s, double eps, uint6
   out.eps = eps;
   out.seed = seed;
   Fibers fb;
+  static const bool htrace = getenv("CTD_HOST_TRACE") != nullptr;
+  const auto h0 = std::chrono::steady_clock::now();
   {
     PhaseScope ps(ctx, PH_MATRICIZE);
     matricize(ctx, x, mode, fb);
   }
+  const auto h1 = std::chrono::steady_clock::now();
   out.F = fb.F;
   out.cols = fb.cols;
   out.rows = fb.rows;
@@ -136,9 +143,16 @@ void run_ctd_s(Ctx* ctx, const Tensor& x, int mode, int64_t s, double eps, uint6
       out.min_margin = std::min(out.min_margin, m);
     }
   }
+  const auto h2 = std::chrono::steady_clock::now();
   if (flags & CTD_GPU_WITH_ERROR) {
     PhaseScope ps(ctx, PH_ERROR);
     out.rel_error = relative_error(ctx, fb, *out.basis);
+  }
+  if (htrace) {
+    const auto h3 = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    fprintf(stderr, "[ctd_s host] matricize=%.3f front=%.3f error=%.3f ms\n", ms(h0, h1), ms(h1, h2),
+            ms(h2, h3));
   }
 }
 

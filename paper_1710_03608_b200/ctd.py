@@ -504,6 +504,15 @@ def ctd_s_raw(x, mode: int, sample_size: int, epsilon: float = 1e-6, seed: int =
     return h, info
 
 
+def relative_error_raw(x, h, ctx: Optional[Context] = None) -> float:
+    """relative_error(X, factors) for a raw factors handle from ctd_s_raw."""
+    ctx = ctx or default_context()
+    d = _dev(x, ctx)
+    out = C.c_double()
+    _check(ctx.L.ctd_gpu_relative_error(ctx.h, d.h, h, C.byref(out)))
+    return out.value
+
+
 def free_factors(ctx: Context, h) -> None:
     _check(ctx.L.ctd_gpu_factors_destroy(h))
 
