@@ -97,7 +97,10 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
   const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long gthreads = (long long)nb * blockDim.x;
   const int lane = threadIdx.x & 31;
-  const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // Rows are dealt round-robin over SMs first (warp-major), so a few hundred
+  // dependent chains spread over all SMs instead of saturating the FP64 pipes
+  // of the first few.
+  const long long gwarp = (long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
   const long long gwarps = (long long)nb * (blockDim.x >> 5);
   const long long LD = a.LD;
   const int nu = a.n_u;
@@ -144,8 +147,10 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         a.rev[p] = v;
         a.rowlen[r] = L + 1;
       }
-      if (blockIdx.x == 0) {
+      if (blockIdx.x == nb - 1) {
         // Ordered append of x's rows not yet in R (first-appearance order).
+        // The last CTA does it: U rows are dealt from CTA 0 upward, so it
+        // usually owns none and this overlaps the y chains.
         int srn = ldg_cg(a.sr_n);
         for (int base = 0; base < pm; base += blockDim.x) {
           const int t = base + threadIdx.x;
@@ -198,29 +203,62 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
           // Windows of kWin elements: 8 loads in flight per lane, all U
           // updates and products computed lane-parallel into the warp's
           // window, then lane 0 runs the add chain over the window.
-          for (int j0 = c0; j0 < c1; j0 += kWin) {
-            double u[kWin / 32];
+          double u[kWin / 32];
 #pragma unroll
-            for (int s = 0; s < kWin / 32; ++s) {
-              const int j = j0 + 32 * s + lane;
-              u[s] = (j < c1 && j < Ko && i < Ko) ? ldg_cg(&urow[j]) : 0.0;
+          for (int s = 0; s < kWin / 32; ++s) {
+            const int j = c0 + 32 * s + lane;
+            u[s] = (j < c1 && j < Ko && i < Ko) ? ldg_cg(&urow[j]) : 0.0;
+          }
+          for (int j0 = c0; j0 < c1; j0 += kWin) {
+            double unv[kWin / 32];
+            if (upd) {
+              // U_new[i][j] = fl(U + fl(fl(y_i y_j)/d)): branch-free exact
+              // divisions (overlapping), certified; a lane whose check fails
+              // redoes its window with __ddiv_rn.
+              bool wok = true;
+#pragma unroll
+              for (int s = 0; s < kWin / 32; ++s) {
+                const int j = j0 + 32 * s + lane;
+                const double num = (i < Ko && j < Ko) ? dmul(yi, vB[j - c0])
+                                 : (i == Ko && j == Ko) ? 1.0
+                                 : (i == Ko) ? -vB[j - c0] : -yi;
+                bool ok;
+                const double qd = ddiv_try(num, prev_delta, &ok);
+                wok &= ok | (j >= c1);
+                unv[s] = (i < Ko && j < Ko) ? dadd(u[s], qd) : qd;
+              }
+              if (__any_sync(0xffffffffu, !wok) && !wok) {
+#pragma unroll
+                for (int s = 0; s < kWin / 32; ++s) {
+                  const int j = j0 + 32 * s + lane;
+                  if (j >= c1) continue;
+                  if (i < Ko && j < Ko) unv[s] = dadd(u[s], ddiv(dmul(yi, vB[j - c0]), prev_delta));
+                  else if (i == Ko && j == Ko) unv[s] = ddiv(1.0, prev_delta);
+                  else if (i == Ko) unv[s] = ddiv(-vB[j - c0], prev_delta);
+                  else unv[s] = ddiv(-yi, prev_delta);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int s = 0; s < kWin / 32; ++s) unv[s] = u[s];
             }
 #pragma unroll
             for (int s = 0; s < kWin / 32; ++s) {
               const int j = j0 + 32 * s + lane;
               double p = 0.0;
               if (j < c1) {
-                double un = u[s];
-                if (upd) {
-                  if (i < Ko && j < Ko) un = dadd(u[s], ddiv(dmul(yi, vB[j - c0]), prev_delta));
-                  else if (i == Ko && j == Ko) un = ddiv(1.0, prev_delta);
-                  else if (i == Ko) un = ddiv(-vB[j - c0], prev_delta);
-                  else un = ddiv(-yi, prev_delta);
-                  urow[j] = un;
-                }
-                if (!last) p = dmul(un, vA[j - c0]);
+                if (upd) urow[j] = unv[s];
+                if (!last) p = dmul(unv[s], vA[j - c0]);
               }
               wwin[32 * s + lane] = p;
+            }
+            const int jn = j0 + kWin;  // next window's U loads overlap this chain
+            if (jn < c1) {
+#pragma unroll
+              for (int s = 0; s < kWin / 32; ++s) {
+                const int j = jn + 32 * s + lane;
+                u[s] = (j < c1 && j < Ko && i < Ko) ? ldg_cg(&urow[j]) : 0.0;
+              }
             }
             if (!last) acc = window_chain(wwin, lane, min(kWin, c1 - j0), acc);
           }
@@ -243,7 +281,76 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     };
     if (y_fits) stage_y(0, K);
     stamp(a.trace, n, 10);
-    for (long long rb = 0; rb < srn; rb += gwarps) {
+    if (y_fits) {
+      // Warp w owns rows q = w + k*gwarps.  Metadata (row id, base, length,
+      // tag) of 32 of them is fetched at once, one row per lane, so the rows
+      // themselves only wait on their entry windows.
+      for (long long k0 = 0; gwarp + k0 * gwarps < srn; k0 += 32) {
+        const long long qk = gwarp + (k0 + lane) * gwarps;
+        int rk = 0, Lk = 0;
+        long long bk = 0;
+        uint32_t tk = 0;
+        if (qk < srn) rk = ldg_cg(&a.sr_list[qk]);
+        if (qk < srn) {
+          bk = a.rowbase[rk];
+          Lk = ldg_cg(&a.rowlen[rk]);
+          tk = ldg_cg(&a.tag[rk]);
+        }
+        for (int kq = 0; kq < 32; ++kq) {
+          const long long q = gwarp + (k0 + kq) * gwarps;
+          if (q >= srn) break;
+          const int r = __shfl_sync(0xffffffffu, rk, kq);
+          const long long b0 = __shfl_sync(0xffffffffu, bk, kq);
+          const int L = __shfl_sync(0xffffffffu, Lk, kq);
+          const bool inx = __shfl_sync(0xffffffffu, tk, kq) == tg;
+          double z = 0.0;
+          int kfd = -1;
+          const int kst = L > 0 ? __shfl_sync(0xffffffffu, ldg_cg(&a.rek[b0 + (lane & 0)]), 0) : -1;
+          // software pipeline: the next window's entries are in flight while
+          // the current window's chain runs
+          int kk[kWin / 32];
+          double vv[kWin / 32];
+#pragma unroll
+          for (int s = 0; s < kWin / 32; ++s) {
+            const int t = 32 * s + lane;
+            kk[s] = t < L ? ldg_cg(&a.rek[b0 + t]) : 0;
+            vv[s] = t < L ? ldg_cg(&a.rev[b0 + t]) : 0.0;
+          }
+          for (int e = 0; e < L; e += kWin) {
+            unsigned nzm[kWin / 32];
+#pragma unroll
+            for (int s = 0; s < kWin / 32; ++s) {
+              const int t = e + 32 * s + lane;
+              const double yk = t < L ? vA[kk[s]] : 0.0;
+              wwin[32 * s + lane] = dmul(yk, vv[s]);
+              nzm[s] = __ballot_sync(0xffffffffu, t < L && yk != 0.0);
+            }
+            if (kfd < 0) {
+#pragma unroll
+              for (int s = kWin / 32 - 1; s >= 0; --s)
+                if (nzm[s]) kfd = __shfl_sync(0xffffffffu, kk[s], __ffs(nzm[s]) - 1);
+            }
+            const int en = e + kWin;
+            if (en < L) {
+#pragma unroll
+              for (int s = 0; s < kWin / 32; ++s) {
+                const int t = en + 32 * s + lane;
+                kk[s] = t < L ? ldg_cg(&a.rek[b0 + t]) : 0;
+                vv[s] = t < L ? ldg_cg(&a.rev[b0 + t]) : 0.0;
+              }
+            }
+            z = window_chain(wwin, lane, min(kWin, L - e), z);
+          }
+          if (lane == 0) {
+            zdn[r] = z;
+            a.kf[r] = kfd;
+            a.term[q] = inx ? 0.0 : dsqr(z);
+            if (z != 0.0 && kfd != kst) atomicExch(&a.slow[n], 1);
+          }
+        }
+      }
+    }
+    for (long long rb = 0; !y_fits && rb < srn; rb += gwarps) {
       const long long q = rb + gwarp;
       int r = 0, L = 0, e = 0, kfd = -1, kst = -1;
       long long b0 = 0;

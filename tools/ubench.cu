@@ -2,6 +2,7 @@
 //   dependent DADD latency, LDS->DADD chain, grid-barrier round trip.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/ubench tools/ubench.cu
 #include <cstdio>
+#include <vector>
 #include <cuda_runtime.h>
 
 __global__ void k_dadd(double* out, long long* cyc, int n) {
@@ -140,6 +141,186 @@ __global__ void __launch_bounds__(512) k_scans(long long* cyc) {
   }
 }
 
+// window_chain as in the filter: lanes write 256 products, lane 0 chains.
+constexpr int kWinB = 256;
+__device__ __forceinline__ double window_chain_b(const double* wwin, int lane, int cnt, double acc) {
+  __syncwarp();
+  if (lane == 0) {
+    const double2* w2 = reinterpret_cast<const double2*>(wwin);
+    for (int b = 0; b < cnt; b += 32) {
+      double v[32];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const double2 t = w2[(b >> 1) + q];
+        v[2 * q] = t.x;
+        v[2 * q + 1] = t.y;
+      }
+      const int mm = min(32, cnt - b);
+      if (mm == 32) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc = __dadd_rn(acc, v[q]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (q < mm) acc = __dadd_rn(acc, v[q]);
+      }
+    }
+  }
+  __syncwarp();
+  return acc;
+}
+
+__global__ void k_wchain(const double* x, int reps, long long* cyc, double* out) {
+  extern __shared__ __align__(16) double wsm[];
+  double* wwin = wsm + (threadIdx.x >> 5) * kWinB;
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll
+    for (int s = 0; s < kWinB / 32; ++s) wwin[32 * s + lane] = x[(32 * s + lane + r) & 1023] * 1.0000001;
+    acc = window_chain_b(wwin, lane, kWinB, acc);
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+// The filter's P1 row loop for one row (fused U update + products + chain).
+__global__ void k_p1row(double* U, const double* g, const double* yv, int K, double delta, int upd,
+                        long long* cyc, double* out) {
+  extern __shared__ __align__(16) double sm[];
+  double* vA = sm;
+  double* vB = sm + 4096;
+  double* wwin = sm + 8192 + (threadIdx.x >> 5) * kWinB;
+  const int lane = threadIdx.x & 31;
+  for (int j = threadIdx.x; j < K; j += blockDim.x) {
+    vA[j] = g[j];
+    vB[j] = yv[j];
+  }
+  __syncthreads();
+  const int i = threadIdx.x >> 5;  // row per warp
+  double* urow = U + (long long)i * K;
+  const double yi = yv[i];
+  const int Ko = K;
+  long long t0 = clock64();
+  double acc = 0.0;
+  double u[kWinB / 32];
+#pragma unroll
+  for (int s = 0; s < kWinB / 32; ++s) {
+    const int j = 32 * s + lane;
+    u[s] = j < K ? __ldcg(&urow[j]) : 0.0;
+  }
+  for (int j0 = 0; j0 < K; j0 += kWinB) {
+    if (upd == 3) {
+      double unv[kWinB / 32];
+      bool wok = true;
+#pragma unroll
+      for (int s = 0; s < kWinB / 32; ++s) {
+        const int j = j0 + 32 * s + lane;
+        bool ok;
+        const double qd = ctdgpu::ddiv_try(__dmul_rn(yi, vB[j]), delta, &ok);
+        wok &= ok;
+        unv[s] = __dadd_rn(u[s], qd);
+      }
+      if (__any_sync(0xffffffffu, !wok) && !wok) {
+#pragma unroll
+        for (int s = 0; s < kWinB / 32; ++s) {
+          const int j = j0 + 32 * s + lane;
+          unv[s] = __dadd_rn(u[s], __ddiv_rn(__dmul_rn(yi, vB[j]), delta));
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < kWinB / 32; ++s) {
+        const int j = j0 + 32 * s + lane;
+        double p = 0.0;
+        if (j < K) {
+          urow[j] = unv[s];
+          p = __dmul_rn(unv[s], vA[j]);
+        }
+        wwin[32 * s + lane] = p;
+      }
+    } else
+#pragma unroll
+    for (int s = 0; s < kWinB / 32; ++s) {
+      const int j = j0 + 32 * s + lane;
+      double p = 0.0;
+      if (j < K) {
+        double un = u[s];
+        if (upd) {
+          if (i < Ko && j < Ko)
+            un = __dadd_rn(u[s], upd == 2 ? __ddiv_rn(__dmul_rn(yi, vB[j]), delta)
+                                          : ctdgpu::ddiv_exact(__dmul_rn(yi, vB[j]), delta));
+          urow[j] = un;
+        }
+        p = __dmul_rn(un, vA[j]);
+      }
+      wwin[32 * s + lane] = p;
+    }
+    const int jn = j0 + kWinB;
+    if (jn < K) {
+#pragma unroll
+      for (int s = 0; s < kWinB / 32; ++s) {
+        const int j = jn + 32 * s + lane;
+        u[s] = j < K ? __ldcg(&urow[j]) : 0.0;
+      }
+    }
+    acc = window_chain_b(wwin, lane, min(kWinB, K - j0), acc);
+  }
+  long long t1 = clock64();
+  if (lane == 0) {
+    out[i] = acc;
+    if (i == 0) cyc[0] = t1 - t0;
+  }
+}
+
+// ddiv_exact vs __ddiv_rn on pseudo-random operands of several kinds.
+__global__ void k_divcheck(unsigned long long seed, long long n, unsigned long long* bad, double* ex) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  unsigned long long nb = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    unsigned long long s = seed ^ (i * 0x9E3779B97F4A7C15ull);
+    auto nx = [&]() {
+      s ^= s << 13; s ^= s >> 7; s ^= s << 17;
+      return s;
+    };
+    const int kind = (int)(i & 7);
+    double a, b;
+    if (kind < 3) {  // random mantissas, moderate exponents, random signs
+      a = __longlong_as_double((long long)((nx() & 0x800FFFFFFFFFFFFFull) | ((unsigned long long)(1023 + (int)(nx() % 200) - 100) << 52)));
+      b = __longlong_as_double((long long)((nx() & 0x800FFFFFFFFFFFFFull) | ((unsigned long long)(1023 + (int)(nx() % 200) - 100) << 52)));
+    } else if (kind < 5) {  // products of small integers / integers: many exact & tie cases
+      a = (double)(long long)(nx() % 2000001) - 1000000.0;
+      b = (double)(long long)(nx() % 1999) + 1.0;
+      a = a * (double)(1ll << (nx() % 40));
+    } else if (kind == 5) {  // y_i*y_j / delta shapes from the filter
+      const double y1 = ((double)(nx() >> 11) * 0x1.0p-53 - 0.5) * 1e-3, y2 = ((double)(nx() >> 11) * 0x1.0p-53 - 0.5) * 1e-2;
+      a = __dmul_rn(y1, y2);
+      b = (double)(nx() >> 11) * 0x1.0p-53 * 1e-4 + 1e-12;
+    } else if (kind == 6) {  // quotients near powers of two
+      b = (double)(nx() % 1000 + 1);
+      a = b * (double)(1ll << (nx() % 30));
+      a = __longlong_as_double(__double_as_longlong(a) + (long long)(nx() % 5) - 2);
+    } else {  // extreme exponents (fallback paths)
+      a = __longlong_as_double((long long)(nx() & 0xFFFFFFFFFFFFFFFull));
+      b = __longlong_as_double((long long)(nx() & 0xFFFFFFFFFFFFFFFull));
+      if (b == 0.0) b = 1.0;
+    }
+    const double q1 = ctdgpu::ddiv_exact(a, b), q2 = __ddiv_rn(a, b);
+    bool ok;
+    const double q3 = ctdgpu::ddiv_try(a, b, &ok);
+    if (!ok) atomicAdd(bad + 1, 1ull);
+    if ((__double_as_longlong(q1) != __double_as_longlong(q2) && !(q1 != q1 && q2 != q2)) ||
+        (ok && __double_as_longlong(q3) != __double_as_longlong(q2))) {
+      ++nb;
+      ex[0] = a;
+      ex[1] = b;
+    }
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+
 int main() {
   double* d;
   long long* c;
@@ -167,6 +348,67 @@ int main() {
     cudaDeviceSynchronize();
     cudaMemcpy(&cyc, c, 8, cudaMemcpyDeviceToHost);
     printf("grid barrier (%d CTAs): %.0f cycles\n", g, (double)cyc / it);
+  }
+  {
+    double* xx;
+    double* oo;
+    cudaMalloc(&xx, 1024 * 8);
+    cudaMalloc(&oo, 148 * 512 * 8);
+    cudaMemset(xx, 0, 1024 * 8);
+    cudaFuncSetAttribute(k_wchain, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * kWinB * 8);
+    for (int warps : {1, 4, 16}) {
+      k_wchain<<<1, 32 * warps, warps * kWinB * 8>>>(xx, 64, c, oo);
+      cudaDeviceSynchronize();
+      long long st;
+      cudaMemcpy(&st, c, 8, cudaMemcpyDeviceToHost);
+      printf("window_chain: %d warps/SM: %.2f cycles/element\n", warps, (double)st / (64.0 * kWinB));
+    }
+  }
+  {
+    const int K = 1024;
+    double *U, *g, *yv, *o;
+    cudaMalloc(&U, (size_t)16 * K * 8);
+    cudaMalloc(&g, K * 8);
+    cudaMalloc(&yv, K * 8);
+    cudaMalloc(&o, 64 * 8);
+    {
+      std::vector<double> h((size_t)16 * K);
+      unsigned long long s = 99;
+      for (auto& v : h) {
+        s ^= s << 13; s ^= s >> 7; s ^= s << 17;
+        v = (double)(s >> 11) * 0x1.0p-53 - 0.5;
+      }
+      cudaMemcpy(U, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+      cudaMemcpy(g, h.data() + 7, K * 8, cudaMemcpyHostToDevice);
+      cudaMemcpy(yv, h.data() + 5000, K * 8, cudaMemcpyHostToDevice);
+    }
+    const int smem = (8192 + 16 * kWinB) * 8;
+    cudaFuncSetAttribute(k_p1row, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int upd : {0, 1, 2, 3})
+      for (int warps : {1, 4, 16}) {
+        k_p1row<<<1, 32 * warps, smem>>>(U, g, yv, K, 0.37, upd, c, o);
+        cudaDeviceSynchronize();
+        long long st;
+        cudaMemcpy(&st, c, 8, cudaMemcpyDeviceToHost);
+        printf("P1 row (upd=%d, %d warps/SM): %.2f cycles/element\n", upd, warps, (double)st / K);
+      }
+  }
+  {
+    unsigned long long* nbad;
+    double* ex;
+    cudaMalloc(&nbad, 16);
+    cudaMalloc(&ex, 16);
+    cudaMemset(nbad, 0, 16);
+    const long long N = 1ll << 30;
+    k_divcheck<<<148 * 8, 256>>>(12345, N, nbad, ex);
+    cudaDeviceSynchronize();
+    unsigned long long hb2[2];
+    double hex[2];
+    cudaMemcpy(hb2, nbad, 16, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hex, ex, 16, cudaMemcpyDeviceToHost);
+    const unsigned long long hb = hb2[0];
+    printf("ddiv_exact/ddiv_try vs __ddiv_rn: %llu mismatches of %lld, try not-ok %llu (last a=%.17g b=%.17g)\n",
+           hb, N, hb2[1], hb ? hex[0] : 0.0, hb ? hex[1] : 0.0);
   }
   {
     k_elem<<<1, 1>>>(d, c, d + 4);
