@@ -77,7 +77,9 @@ __global__ void k_count_rows(Cands c, int32_t* cnt) {
 
 __global__ void k_row_caps(const int32_t* rowlen, const int32_t* cnt, long long dim, long long* cap) {
   const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < dim) cap[r] = (long long)rowlen[r] + cnt[r];
+  // multiples of 4 entries: every row segment is 16-byte aligned for the
+  // filter's bulk (TMA) copies, which may read up to 3 entries past the end
+  if (r < dim) cap[r] = ((long long)rowlen[r] + cnt[r] + 3) & ~3ll;
 }
 
 __global__ void k_excl_scan_ll(const long long* in, long long n, long long* out) {
@@ -248,7 +250,7 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   const int64_t K0 = B.K;
   // ---- capacities: U, R columns, R entries
   if (B.LD < K0 + n) {
-    const int64_t nld = std::max<int64_t>(K0 + n, B.LD * 2);
+    const int64_t nld = (std::max<int64_t>(K0 + n, B.LD * 2) + 1) & ~int64_t(1);  // even: 16-byte rows
     Buf<double> nu(ctx, (size_t)nld * nld);
     if (K0 > 0)
       LAUNCH(ctx, k_copy_u, ceil_div(K0 * K0, 256), 256, 0, B.U.p, (long long)B.LD, nu.p,
@@ -284,7 +286,7 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
     Buf<int64_t> cap(ctx, dim + 1), nbase(ctx, dim + 1);
     LAUNCH(ctx, k_row_caps, ceil_div(dim, 256), 256, 0, B.rowlen.p, cnt.p, dim, (long long*)cap.p);
     LAUNCH(ctx, k_excl_scan_ll, 1, 1024, 0, (const long long*)cap.p, dim, (long long*)nbase.p);
-    const int64_t ncap = B.rnnz + total_len + 1;
+    const int64_t ncap = B.rnnz + total_len + 3 * dim + 4;
     Buf<int32_t> nk(ctx, ncap);
     Buf<double> nv(ctx, ncap);
     if (B.rnnz)
@@ -381,7 +383,7 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   }
   ctx->zero(ctx->d_bar, 2 * sizeof(unsigned));
   int per_sm = 0;
-  const size_t dsmem = (2 * kVec + (kFThreads / 32) * kWin) * sizeof(double);
+  const size_t dsmem = kFilterSmem;
   static bool attr = false;
   if (!attr) {
     CUDA_OK(cudaFuncSetAttribute(k_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
@@ -440,6 +442,8 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
               tr[i * 16 + 10] - tr[i * 16 + 4], tr[i * 16 + 11] - tr[i * 16 + 10],
               tr[i * 16 + 5] - tr[i * 16 + 11], tr[i * 16 + 12] - tr[i * 16 + 7],
               tr[i * 16 + 8] - tr[i * 16 + 12]);
+      fprintf(stderr, " | P1 cons-wait=%lld cons-chain=%lld prod-mbar=%lld prod-issue=%lld", tr[i * 16 + 13],
+              tr[i * 16 + 11], tr[i * 16 + 14], tr[i * 16 + 15]);
       fprintf(stderr, "\n");
     }
   }

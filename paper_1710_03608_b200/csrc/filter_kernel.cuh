@@ -18,7 +18,7 @@
 // because every CTA derives the same decision.
 
 constexpr int kFThreads = 512;
-constexpr int kVec = 8192;  // doubles per staged vector (two buffers)
+constexpr int kVec = 4096;  // doubles per staged vector (two buffers)
 
 // acc <- (((acc + p_0) + p_1) + ... + p_{cnt-1}) where lane q holds p_q.
 // Lanes stage their products in the warp's shared slot; lane 0 runs the
@@ -77,6 +77,70 @@ __device__ __forceinline__ double window_chain(const double* wwin, int lane, int
     }
   }
   __syncwarp();
+  return acc;
+}
+
+// Producer/consumer ring (P1, P2 when the staged vector fits): warps
+// 0..kProdWarps-1 compute the terms of up to 32 chains (one chain per row
+// this CTA owns) for kRingW consecutive steps into ring slot q&1; the chain
+// warp (the last warp) runs all 32 sequential add chains at once, one per
+// lane.  Slots are handed over with named barriers: "full" 1+b, "empty"
+// 1+kRingSlots+b.  (Measured with tools/ubench_ring.cu: fewer/smaller slots
+// couple the chain to the producers' latency.)
+constexpr int kRingW = 96;                 // steps per ring chunk
+constexpr int kRingS = 33;                 // padded lane stride (doubles)
+constexpr int kRingSlots = 3;
+constexpr int kRingDoubles = kRingSlots * kRingW * kRingS;
+// (Keeping producers off the chain warp's SM sub-partition measured slower:
+// the producers, not issue-slot sharing, bound the ring.)
+constexpr int kChainWarp = kFThreads / 32 - 1;
+constexpr int kProdWarps = kFThreads / 32 - 1;
+constexpr int kProdThreads = kProdWarps * 32;
+constexpr int kRingThreads = kProdThreads + 32;   // named-barrier participants
+__device__ __forceinline__ bool is_producer(int warp) { return warp < kProdWarps; }
+__device__ __forceinline__ int producer_index(int warp, int lane) { return warp * 32 + lane; }
+// Producer thread p owns step t = p % kRingW of every chunk and the rows
+// r = p / kRingW + kRowPh * k (k < kRowSlots) of the 32-row group.
+constexpr int kRowPh = kProdThreads / kRingW;
+constexpr int kRowSlots = (32 + kRowPh - 1) / kRowPh;
+static_assert(kRowPh * kRingW == kProdThreads && kRingW % 32 == 0, "ring mapping");
+constexpr int kMeta = kFThreads;           // P2 rows per ring session (one group per warp)
+constexpr int kWinArea = (kFThreads / 32) * kWin > kRingDoubles ? (kFThreads / 32) * kWin : kRingDoubles;
+
+constexpr size_t kFilterSmem = (size_t)(2 * kVec + kWinArea) * 8;
+
+__device__ __forceinline__ void nbar_sync(int id, int cnt) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int cnt) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+
+// acc <- (((acc + s_0) + s_1) + ... + s_{cnt-1}), s_t = rb[t * kRingS + lane]:
+// 32 independent chains, one per lane, loads 16 steps ahead.
+__device__ __forceinline__ double lane_chain(const double* rb, int lane, int cnt, double acc) {
+  const double* p = rb + lane;
+  if (cnt == kRingW) {
+    double v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = p[q * kRingS];
+#pragma unroll
+    for (int h = 0; h < kRingW / 16; ++h) {
+      double w[16];
+      if (h + 1 < kRingW / 16) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) w[q] = p[((h + 1) * 16 + q) * kRingS];
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc = dadd(acc, v[q]);
+      if (h + 1 < kRingW / 16) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = w[q];
+      }
+    }
+  } else {
+    for (int t = 0; t < cnt; ++t) acc = dadd(acc, p[t * kRingS]);
+  }
   return acc;
 }
 
@@ -190,7 +254,117 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
       };
       if (one_chunk) stage(0, Kn);
       if (!last) stamp(a.trace, n, 2);
-      for (long long rb = 0; rb < Kn; rb += gwarps) {
+      // U_new[i][j] (fiber_basis.cpp:97-105): fl(U + fl(fl(y_i y_j)/d)), the
+      // new column/row -y/d and the corner 1/d.  The division uses the
+      // divisor's correctly rounded reciprocal (few FP64 instructions: the
+      // chain warp shares the SM's FP64 pipe), certified; __ddiv_rn when the
+      // check fails.
+      const double rdelta = upd ? __drcp_rn(prev_delta) : 0.0;
+      auto unew = [&](long long i, int j, double uo) -> double {
+        const double num = (i < Ko && j < Ko) ? dmul(vB[i], vB[j])
+                         : (i == Ko && j == Ko) ? 1.0
+                         : (i == Ko) ? -vB[j] : -vB[i];
+        bool ok;
+        double qd = ddiv_rcp(num, prev_delta, rdelta, &ok);
+        if (!ok) qd = ddiv(num, prev_delta);
+        return (i < Ko && j < Ko) ? dadd(uo, qd) : qd;
+      };
+      // This CTA owns rows i = blockIdx.x + nb * r (r < Rs); groups of 32.
+      const int Rs = ((int)blockIdx.x < Kn) ? (Kn - 1 - (int)blockIdx.x) / (int)nb + 1 : 0;
+      const int nch = (Kn + kRingW - 1) / kRingW;
+      const int Q = ((Rs + 31) / 32) * nch;
+      const int warp = threadIdx.x >> 5;
+      double* ring = dyn + 2 * kVec;
+      if (one_chunk && last) {
+        for (long long e = threadIdx.x; e < (long long)Rs * Kn; e += blockDim.x) {
+          const int r = (int)(e / Kn), j = (int)(e - (long long)r * Kn);
+          const long long i = blockIdx.x + (long long)nb * r;
+          double* up = a.U + i * LD + j;
+          *up = unew(i, j, (i < Ko && j < Ko) ? ldg_cg(up) : 0.0);
+        }
+      } else if (one_chunk && is_producer(warp)) {
+        // producers: U_new and the products U_new[i][j] g_j of 32 rows x
+        // kRingW steps; the next chunk's U loads are in flight meanwhile.
+        // (Bulk/TMA staging of the U segments measured slower: it inflates
+        // the chain warp's latency, tools/ubench_ring.cu.)
+        const int pi = producer_index(warp, lane);
+        const int t = pi % kRingW, rq = pi / kRingW;
+        double uv[kRowSlots];
+        auto load = [&](int q) {
+          const int g = q / nch, j = (q - g * nch) * kRingW + t;
+          const int nr = min(32, Rs - 32 * g);
+#pragma unroll
+          for (int k = 0; k < kRowSlots; ++k) {
+            const int r = rq + kRowPh * k;
+            const long long i = blockIdx.x + (long long)nb * (32 * g + r);
+            uv[k] = 0.0;
+            if (r < nr && j < Ko && i < Ko) uv[k] = ldg_cg(&a.U[i * LD + j]);
+          }
+        };
+        if (Q > 0) load(0);
+        for (int q = 0; q < Q; ++q) {
+          const int g = q / nch, j = (q - g * nch) * kRingW + t;
+          const int nr = min(32, Rs - 32 * g);
+          const int b = q % kRingSlots;
+          double* rb = ring + b * (kRingW * kRingS) + t * kRingS;
+          if (q >= kRingSlots) nbar_sync(1 + kRingSlots + b, kRingThreads);
+          const bool jin = j < Kn;
+          const double gj = jin ? vA[j] : 0.0;
+          const double yj = (jin && j < Ko) ? vB[j] : 0.0;
+#pragma unroll
+          for (int k = 0; k < kRowSlots; ++k) {
+            const int r = rq + kRowPh * k;
+            if (r < nr) {
+              double p = 0.0;
+              if (jin) {
+                const long long i = blockIdx.x + (long long)nb * (32 * g + r);
+                double un = uv[k];
+                if (upd) {
+                  // fiber_basis.cpp:97-105 (see unew)
+                  const double num = (i < Ko && j < Ko) ? dmul(vB[i], yj)
+                                   : (i == Ko && j == Ko) ? 1.0
+                                   : (i == Ko) ? -yj : -vB[i];
+                  bool ok;
+                  double qd = ddiv_rcp(num, prev_delta, rdelta, &ok);
+                  if (!ok) qd = ddiv(num, prev_delta);
+                  un = (i < Ko && j < Ko) ? dadd(un, qd) : qd;
+                  a.U[i * LD + j] = un;
+                }
+                p = dmul(un, gj);
+              }
+              rb[r] = p;
+            }
+          }
+          nbar_arrive(1 + b, kRingThreads);
+          if (q + 1 < Q) load(q + 1);
+        }
+      } else if (one_chunk && warp == kChainWarp) {
+        // chain warp: y_i = sum_j fl(U_new[i][j] g_j) in j order (dense_matrix.cpp:42-47)
+        double acc = 0.0;
+        long long tw = 0, tcc = 0;
+        for (int q = 0; q < Q; ++q) {
+          const int g = q / nch, ch = q - g * nch;
+          const int cnt = min(kRingW, Kn - ch * kRingW);
+          const int b = q % kRingSlots;
+          const long long tw0 = clock64();
+          nbar_sync(1 + b, kRingThreads);
+          tw += clock64() - tw0;
+          const long long tc0 = clock64();
+          acc = lane_chain(ring + b * (kRingW * kRingS), lane, cnt, acc);
+          tcc += clock64() - tc0;
+          if (q + kRingSlots < Q) nbar_arrive(1 + kRingSlots + b, kRingThreads);
+          if (ch == nch - 1) {
+            const int r = 32 * g + lane;
+            if (r < Rs) ycur[blockIdx.x + (long long)nb * r] = acc;
+            acc = 0.0;
+          }
+        }
+        if (a.trace && blockIdx.x == 0 && lane == 0) {
+          a.trace[(long long)n * 16 + 13] = tw;
+          a.trace[(long long)n * 16 + 11] = tcc;
+        }
+      }
+      for (long long rb = 0; !one_chunk && rb < Kn; rb += gwarps) {
         const long long i = rb + gwarp;
         const bool active = i < Kn;
         const double yi = (upd && active && i < Ko) ? ldg_cg(&yprev[i]) : 0.0;
@@ -282,70 +456,127 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     if (y_fits) stage_y(0, K);
     stamp(a.trace, n, 10);
     if (y_fits) {
-      // Warp w owns rows q = w + k*gwarps.  Metadata (row id, base, length,
-      // tag) of 32 of them is fetched at once, one row per lane, so the rows
-      // themselves only wait on their entry windows.
-      for (long long k0 = 0; gwarp + k0 * gwarps < srn; k0 += 32) {
-        const long long qk = gwarp + (k0 + lane) * gwarps;
-        int rk = 0, Lk = 0;
-        long long bk = 0;
-        uint32_t tk = 0;
-        if (qk < srn) rk = ldg_cg(&a.sr_list[qk]);
-        if (qk < srn) {
-          bk = a.rowbase[rk];
-          Lk = ldg_cg(&a.rowlen[rk]);
-          tk = ldg_cg(&a.tag[rk]);
-        }
-        for (int kq = 0; kq < 32; ++kq) {
-          const long long q = gwarp + (k0 + kq) * gwarps;
-          if (q >= srn) break;
-          const int r = __shfl_sync(0xffffffffu, rk, kq);
-          const long long b0 = __shfl_sync(0xffffffffu, bk, kq);
-          const int L = __shfl_sync(0xffffffffu, Lk, kq);
-          const bool inx = __shfl_sync(0xffffffffu, tk, kq) == tg;
-          double z = 0.0;
-          int kfd = -1;
-          const int kst = L > 0 ? __shfl_sync(0xffffffffu, ldg_cg(&a.rek[b0 + (lane & 0)]), 0) : -1;
-          // software pipeline: the next window's entries are in flight while
-          // the current window's chain runs
-          int kk[kWin / 32];
-          double vv[kWin / 32];
-#pragma unroll
-          for (int s = 0; s < kWin / 32; ++s) {
-            const int t = 32 * s + lane;
-            kk[s] = t < L ? ldg_cg(&a.rek[b0 + t]) : 0;
-            vv[s] = t < L ? ldg_cg(&a.rev[b0 + t]) : 0.0;
+      // Ring sessions of up to kMeta rows of R owned by this CTA (positions
+      // q = blockIdx.x + nb * r of the first-appearance list); warp w stages
+      // the metadata of group w (32 rows) in the free vB area.
+      int* s_row = reinterpret_cast<int*>(vB);
+      int* s_len = s_row + kMeta;
+      int* s_tf = s_len + kMeta;
+      int* s_inx = s_tf + kMeta;
+      int* s_gch = s_inx + kMeta;  // [32] chunks per group
+      long long* s_base = reinterpret_cast<long long*>(s_gch + 32);
+      double* ring = dyn + 2 * kVec;
+      const int warp = threadIdx.x >> 5;
+      const int Rs2 = ((int)blockIdx.x < srn) ? (srn - 1 - (int)blockIdx.x) / (int)nb + 1 : 0;
+      for (int sb0 = 0; sb0 < Rs2; sb0 += kMeta) {
+        const int ns = min(kMeta, Rs2 - sb0);
+        __syncthreads();
+        {
+          const int r = threadIdx.x;
+          int L = 0;
+          if (r < ns) {
+            const long long q = blockIdx.x + (long long)nb * (sb0 + r);
+            const int row = ldg_cg(&a.sr_list[q]);
+            L = ldg_cg(&a.rowlen[row]);
+            s_row[r] = row;
+            s_base[r] = a.rowbase[row];
+            s_len[r] = L;
+            s_inx[r] = ldg_cg(&a.tag[row]) == tg;
+            s_tf[r] = 0x7fffffff;
           }
-          for (int e = 0; e < L; e += kWin) {
-            unsigned nzm[kWin / 32];
+          const int mx = __reduce_max_sync(0xffffffffu, L);
+          if (lane == 0) s_gch[warp] = max(1, (mx + kRingW - 1) / kRingW);
+        }
+        __syncthreads();
+        const int ngr = (ns + 31) / 32;
+        int Q = 0;
+        for (int g = 0; g < ngr; ++g) Q += s_gch[g];
+        if (is_producer(warp)) {
+          // the next chunk's entries (k, value) are in flight meanwhile;
+          // thread: step t of each chunk, rows rq + kRowPh * k of the group
+          const int pi = producer_index(warp, lane);
+        const int t = pi % kRingW, rq = pi / kRingW;
+          int kv[kRowSlots];
+          double vv[kRowSlots];
+          unsigned okm = 0;    // rows with an entry at this step (prefetched chunk)
+          unsigned found = 0;  // rows whose first y != 0 entry is known (warp-uniform)
+          auto load = [&](int g, int ch) {
+            const int nr = min(32, ns - 32 * g);
+            const int te = ch * kRingW + t;
+            okm = 0;
 #pragma unroll
-            for (int s = 0; s < kWin / 32; ++s) {
-              const int t = e + 32 * s + lane;
-              const double yk = t < L ? vA[kk[s]] : 0.0;
-              wwin[32 * s + lane] = dmul(yk, vv[s]);
-              nzm[s] = __ballot_sync(0xffffffffu, t < L && yk != 0.0);
+            for (int k = 0; k < kRowSlots; ++k) {
+              const int r = rq + kRowPh * k;
+              const bool ok = r < nr && te < s_len[32 * g + min(r, 31)];
+              const long long idx = ok ? s_base[32 * g + r] + te : 0;
+              kv[k] = ok ? ldg_cg(&a.rek[idx]) : 0;
+              vv[k] = ok ? ldg_cg(&a.rev[idx]) : 0.0;
+              okm |= (unsigned)ok << k;
             }
-            if (kfd < 0) {
+          };
+          int g = 0, ch = 0;
+          if (Q > 0) load(0, 0);
+          for (int q = 0; q < Q; ++q) {
+            const int nr = min(32, ns - 32 * g);
+            const int b = q % kRingSlots;
+            double* rb = ring + b * (kRingW * kRingS) + t * kRingS;
+            const int te = ch * kRingW + t;
+            if (q >= kRingSlots) nbar_sync(1 + kRingSlots + b, kRingThreads);
 #pragma unroll
-              for (int s = kWin / 32 - 1; s >= 0; --s)
-                if (nzm[s]) kfd = __shfl_sync(0xffffffffu, kk[s], __ffs(nzm[s]) - 1);
-            }
-            const int en = e + kWin;
-            if (en < L) {
-#pragma unroll
-              for (int s = 0; s < kWin / 32; ++s) {
-                const int t = en + 32 * s + lane;
-                kk[s] = t < L ? ldg_cg(&a.rek[b0 + t]) : 0;
-                vv[s] = t < L ? ldg_cg(&a.rev[b0 + t]) : 0.0;
+            for (int k = 0; k < kRowSlots; ++k) {
+              const int r = rq + kRowPh * k;
+              if (r < nr) {  // warp-uniform: a warp covers 32 steps of one row
+                const bool ok = (okm >> k) & 1;
+                const double yk = ok ? vA[kv[k]] : 0.0;
+                rb[r] = dmul(yk, vv[k]);
+                if (!((found >> k) & 1)) {
+                  // first kept column of the row with y != 0 (the touch order)
+                  const unsigned nz = __ballot_sync(0xffffffffu, ok && yk != 0.0);
+                  if (nz) {
+                    if (lane == __ffs(nz) - 1) atomicMin(&s_tf[32 * g + r], te);
+                    found |= 1u << k;
+                  }
+                }
               }
             }
-            z = window_chain(wwin, lane, min(kWin, L - e), z);
+            nbar_arrive(1 + b, kRingThreads);
+            if (++ch == s_gch[g]) {
+              ch = 0;
+              ++g;
+              found = 0;
+            }
+            if (q + 1 < Q) load(g, ch);
           }
-          if (lane == 0) {
-            zdn[r] = z;
-            a.kf[r] = kfd;
-            a.term[q] = inx ? 0.0 : dsqr(z);
-            if (z != 0.0 && kfd != kst) atomicExch(&a.slow[n], 1);
+        } else if (warp == kChainWarp) {
+          // chain warp: z_r = sum_k fl(y_k R[r,k]) in ascending k (fiber_basis.cpp:56-65)
+          double z = 0.0;
+          int g = 0, ch = 0;
+          for (int q = 0; q < Q; ++q) {
+            const int b = q % kRingSlots;
+            nbar_sync(1 + b, kRingThreads);
+            // steps past a row's length hold +-0.0, which leave z unchanged
+            z = lane_chain(ring + b * (kRingW * kRingS), lane, kRingW, z);
+            if (q + kRingSlots < Q) nbar_arrive(1 + kRingSlots + b, kRingThreads);
+            if (++ch == s_gch[g]) {
+              const int r = 32 * g + lane;
+              if (r < ns) {
+                const int row = s_row[r];
+                const int L = s_len[r];
+                const long long b0 = s_base[r];
+                const int tf = s_tf[r];
+                const int kfd = tf < L ? ldg_cg(&a.rek[b0 + tf]) : -1;
+                const int kst = L > 0 ? ldg_cg(&a.rek[b0]) : -1;
+                zdn[row] = z;
+                a.kf[row] = kfd;
+                a.term[blockIdx.x + (long long)nb * (sb0 + r)] = s_inx[r] ? 0.0 : dsqr(z);
+                // touched order differs from first-appearance order only if
+                // the row's first kept column has y == 0 while it is touched
+                if (z != 0.0 && kfd != kst) atomicExch(&a.slow[n], 1);
+              }
+              z = 0.0;
+              ch = 0;
+              ++g;
+            }
           }
         }
       }

@@ -311,6 +311,10 @@ __global__ void k_divcheck(unsigned long long seed, long long n, unsigned long l
     bool ok;
     const double q3 = ctdgpu::ddiv_try(a, b, &ok);
     if (!ok) atomicAdd(bad + 1, 1ull);
+    bool ok4;
+    const double q4 = ctdgpu::ddiv_rcp(a, b, __drcp_rn(b), &ok4);
+    if (!ok4) atomicAdd(bad + 2, 1ull);
+    if (ok4 && __double_as_longlong(q4) != __double_as_longlong(q2)) atomicAdd(bad + 3, 1ull);
     if ((__double_as_longlong(q1) != __double_as_longlong(q2) && !(q1 != q1 && q2 != q2)) ||
         (ok && __double_as_longlong(q3) != __double_as_longlong(q2))) {
       ++nb;
@@ -319,6 +323,27 @@ __global__ void k_divcheck(unsigned long long seed, long long n, unsigned long l
     }
   }
   if (nb) atomicAdd(bad, nb);
+}
+
+// FP64 issue throughput: every thread runs 8 independent chains.
+__global__ void k_fp64tp(double* out, long long* cyc, int n, int kind) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = out[k] + threadIdx.x;
+  const double m = 1.0000001, c = 1e-9;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = kind == 0 ? __fma_rn(a[k], m, c) : kind == 1 ? __dadd_rn(a[k], c) : __dmul_rn(a[k], m);
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  out[16 + blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) cyc[0] = t1 - t0;
 }
 
 int main() {
@@ -338,6 +363,21 @@ int main() {
   k_dmul_dadd<<<1, 1>>>(d, c, n);
   cudaMemcpy(&cyc, c, 8, cudaMemcpyDeviceToHost);
   printf("dependent DADD(DMUL): %.2f cycles\n", (double)cyc / n);
+  {
+    double* fo;
+    cudaMalloc(&fo, (16 + 148 * 1024) * 8);
+    cudaMemset(fo, 0, (16 + 148 * 1024) * 8);
+    const char* kn[] = {"DFMA", "DADD", "DMUL"};
+    for (int kind = 0; kind < 3; ++kind)
+      for (int thr : {32, 128, 512, 1024}) {
+        const int n = 4096;
+        k_fp64tp<<<148, thr>>>(fo, c, n, kind);
+        cudaDeviceSynchronize();
+        long long st;
+        cudaMemcpy(&st, c, 8, cudaMemcpyDeviceToHost);
+        printf("%s throughput, %4d threads/SM: %.2f lane-ops/cycle/SM\n", kn[kind], thr, (double)thr * n * 8 / st);
+      }
+  }
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   for (int g : {1, 16, 74, sms}) {
@@ -396,19 +436,20 @@ int main() {
   {
     unsigned long long* nbad;
     double* ex;
-    cudaMalloc(&nbad, 16);
+    cudaMalloc(&nbad, 32);
     cudaMalloc(&ex, 16);
-    cudaMemset(nbad, 0, 16);
+    cudaMemset(nbad, 0, 32);
     const long long N = 1ll << 30;
     k_divcheck<<<148 * 8, 256>>>(12345, N, nbad, ex);
     cudaDeviceSynchronize();
-    unsigned long long hb2[2];
+    unsigned long long hb2[4];
     double hex[2];
-    cudaMemcpy(hb2, nbad, 16, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hb2, nbad, 32, cudaMemcpyDeviceToHost);
     cudaMemcpy(hex, ex, 16, cudaMemcpyDeviceToHost);
     const unsigned long long hb = hb2[0];
     printf("ddiv_exact/ddiv_try vs __ddiv_rn: %llu mismatches of %lld, try not-ok %llu (last a=%.17g b=%.17g)\n",
            hb, N, hb2[1], hb ? hex[0] : 0.0, hb ? hex[1] : 0.0);
+    printf("ddiv_rcp vs __ddiv_rn: %llu mismatches among certified, not-ok %llu of %lld\n", hb2[3], hb2[2], N);
   }
   {
     k_elem<<<1, 1>>>(d, c, d + 4);
