@@ -221,14 +221,17 @@ struct FArgs {
   long long* final_rnnz;
   unsigned* bar;
   unsigned* flags;
-  long long* trace;  // optional [n_u][16] clock64 stamps from CTA 0 (CTD_FILTER_TRACE)
+  long long* trace;  // optional [n_u][kTraceW] clock64 stamps from CTA 0 (CTD_FILTER_TRACE)
   SliceSum* ssum;    // [grid] residual-sum slice summaries
   SliceDirect* sdir; // [grid * kSliceDirects]
   int* nfallback;    // exact-sum self-check failures (sequential fallback taken)
+  SliceLoc* sloc;    // [grid] published approximate slice sums (epoch-flagged)
+  unsigned* sflag;   // [grid] slice-summary epoch flags
 };
 
+constexpr int kTraceW = 32;  // clock64 slots per candidate
 __device__ __forceinline__ void stamp(long long* tr, int n, int k) {
-  if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[(long long)n * 16 + k] = clock64();
+  if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[(long long)n * kTraceW + k] = clock64();
 }
 
 #include "filter_kernel.cuh"
@@ -371,13 +374,20 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   Buf<SliceDirect> sdir(ctx, (size_t)ctx->sm_count * kSliceDirects);
   fa.ssum = ssum.p;
   fa.sdir = sdir.p;
+  Buf<SliceLoc> sloc(ctx, ctx->sm_count);
+  sloc.zero();
+  Buf<unsigned> sflag(ctx, (size_t)ctx->sm_count * kFlagStride);
+  sflag.zero();
+  fa.sloc = sloc.p;
+  fa.sflag = sflag.p;
   Buf<int> nfb(ctx, 1);
   nfb.zero();
   fa.nfallback = nfb.p;
   const char* trace_env = getenv("CTD_FILTER_TRACE");
   Buf<long long> tbuf;
   if (trace_env && *trace_env == '1') {
-    tbuf.alloc(ctx, (size_t)n * 16);
+    tbuf.alloc(ctx, (size_t)n * kTraceW);
+    tbuf.zero();
     tbuf.zero();
     fa.trace = tbuf.p;
   }
@@ -423,27 +433,32 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   }
   ctx->sync();
   if (fa.trace) {
-    std::vector<long long> tr((size_t)n * 16);
-    ctx->to_host(tr.data(), tbuf.p, (size_t)n * 16);
+    std::vector<long long> tr((size_t)n * kTraceW);
+    ctx->to_host(tr.data(), tbuf.p, (size_t)n * kTraceW);
     ctx->sync();
     const char* names[] = {"append", "stage", "rows", "bar1", "P2", "bar2", "tstage", "xsum", "decide"};
     double sum[9] = {0};
     for (int64_t i = 0; i < n; ++i)
-      for (int k = 0; k < 9; ++k) sum[k] += (double)(tr[i * 16 + k + 1] - tr[i * 16 + k]);
+      for (int k = 0; k < 9; ++k) sum[k] += (double)(tr[i * kTraceW + k + 1] - tr[i * kTraceW + k]);
     fprintf(stderr, "[filter trace] fallbacks=%d\n", ctx->read1(nfb.p));
     fprintf(stderr, "[filter trace] n=%lld cycles/candidate:", (long long)n);
     for (int k = 0; k < 9; ++k) fprintf(stderr, " %s=%.0f", names[k], sum[k] / n);
     fprintf(stderr, "\n");
     for (int64_t i = 0; i < n; i += std::max<int64_t>(1, n / 8)) {
       fprintf(stderr, "  cand %lld:", (long long)i);
-      for (int k = 0; k < 9; ++k) fprintf(stderr, " %lld", tr[i * 16 + k + 1] - tr[i * 16 + k]);
+      for (int k = 0; k < 9; ++k) fprintf(stderr, " %lld", tr[i * kTraceW + k + 1] - tr[i * kTraceW + k]);
       // P2 detail: staging, first row, remaining rows (CTA 0 warp 0)
       fprintf(stderr, " | P2: stage=%lld row0=%lld rest=%lld | P3: bar=%lld combine=%lld",
-              tr[i * 16 + 10] - tr[i * 16 + 4], tr[i * 16 + 11] - tr[i * 16 + 10],
-              tr[i * 16 + 5] - tr[i * 16 + 11], tr[i * 16 + 12] - tr[i * 16 + 7],
-              tr[i * 16 + 8] - tr[i * 16 + 12]);
-      fprintf(stderr, " | P1 cons-wait=%lld cons-chain=%lld prod-mbar=%lld prod-issue=%lld", tr[i * 16 + 13],
-              tr[i * 16 + 11], tr[i * 16 + 14], tr[i * 16 + 15]);
+              tr[i * kTraceW + 10] - tr[i * kTraceW + 4], tr[i * kTraceW + 11] - tr[i * kTraceW + 10],
+              tr[i * kTraceW + 5] - tr[i * kTraceW + 11], tr[i * kTraceW + 12] - tr[i * kTraceW + 7],
+              tr[i * kTraceW + 8] - tr[i * kTraceW + 12]);
+      fprintf(stderr, " | P1 cons-wait=%lld cons-chain=%lld", tr[i * kTraceW + 13], tr[i * kTraceW + 11]);
+      // warp_grid_sum stages (CTA 0 lane 0), slots 16..26
+      fprintf(stderr, " | P3:");
+      for (int k = 17; k <= 24; ++k)
+        if (tr[i * kTraceW + k] && tr[i * kTraceW + k - 1]) fprintf(stderr, " %lld", tr[i * kTraceW + k] - tr[i * kTraceW + k - 1]);
+      fprintf(stderr, " directs=%lld | P1 prod wait=%lld compute=%lld", tr[i * kTraceW + 25], tr[i * kTraceW + 27],
+              tr[i * kTraceW + 28]);
       fprintf(stderr, "\n");
     }
   }

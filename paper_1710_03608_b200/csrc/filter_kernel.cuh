@@ -144,12 +144,55 @@ __device__ __forceinline__ double lane_chain(const double* rb, int lane, int cnt
   return acc;
 }
 
+// The residual terms of try_append_fiber in the reference's summation order
+// (fiber_basis.cpp:66-77): x's rows ascending ((x_i - z_i)^2, :69-70), then
+// R's rows in first-touch order (z_r^2, :74-75).
+struct ResidualTerms {
+  const double* xv;
+  const int32_t* xr;
+  const double* zd;
+  long long m;
+  const double* tsrc;
+  __device__ double operator()(long long i) const {
+    if (i < m) return dsqr(dsub(xv[i], __ldcg(&zd[xr[i]])));
+    return __ldcg(&tsrc[i - m]);
+  }
+  // terms b0, b0+1, ... (< b1) into out[], every load of a level issued together
+  template <int N>
+  __device__ void batch(long long b0, long long b1, double (&out)[N]) const {
+    int r[N];
+    double v[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const long long i = b0 + k;
+      r[k] = 0;
+      v[k] = 0.0;
+      if (i < b1) {
+        if (i < m) {
+          r[k] = xr[i];
+          v[k] = xv[i];
+        } else {
+          v[k] = __ldcg(&tsrc[i - m]);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const long long i = b0 + k;
+      out[k] = v[k];
+      if (i < b1 && i < m) out[k] = dsqr(dsub(v[k], __ldcg(&zd[r[k]])));
+    }
+  }
+};
+
 __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
-  __shared__ SeqSumSmem S;
   __shared__ uint32_t hist[(kFThreads / 32) * kRadix];
   __shared__ uint32_t sh32[33];
   __shared__ int shi[33];
   __shared__ int s_cnt;
+  __shared__ WarpSumSmem WS;
+  __shared__ double s_res;
+  __shared__ int s_bad;
   // Per-warp product windows: lanes compute kWin products in parallel, lane 0
   // replays the sequential add chain from shared memory (128-bit loads).
   extern __shared__ __align__(16) double dyn[];  // 2*kVec + (warps)*kWin doubles
@@ -266,7 +309,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
                          : (i == Ko) ? -vB[j] : -vB[i];
         bool ok;
         double qd = ddiv_rcp(num, prev_delta, rdelta, &ok);
-        if (!ok) qd = ddiv(num, prev_delta);
+        if (!ok) qd = ddiv_slow(num, prev_delta);
         return (i < Ko && j < Ko) ? dadd(uo, qd) : qd;
       };
       // This CTA owns rows i = blockIdx.x + nb * r (r < Rs); groups of 32.
@@ -326,7 +369,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
                                    : (i == Ko) ? -yj : -vB[i];
                   bool ok;
                   double qd = ddiv_rcp(num, prev_delta, rdelta, &ok);
-                  if (!ok) qd = ddiv(num, prev_delta);
+                  if (!ok) qd = ddiv_slow(num, prev_delta);
                   un = (i < Ko && j < Ko) ? dadd(un, qd) : qd;
                   a.U[i * LD + j] = un;
                 }
@@ -360,8 +403,8 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
           }
         }
         if (a.trace && blockIdx.x == 0 && lane == 0) {
-          a.trace[(long long)n * 16 + 13] = tw;
-          a.trace[(long long)n * 16 + 11] = tcc;
+          a.trace[(long long)n * kTraceW + 13] = tw;
+          a.trace[(long long)n * kTraceW + 11] = tcc;
         }
       }
       for (long long rb = 0; !one_chunk && rb < Kn; rb += gwarps) {
@@ -704,16 +747,24 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     bool bad = false;
     // Terms in the reference's summation order (fiber_basis.cpp:66-77): x's
     // rows ascending, then R's rows in first-touch order.
-    const double* zd = zdn;
-    auto get = [=](long long i) -> double {
-      if (i < m) return dsqr(dsub(xv[i], ldg_cg(&zd[xr[i]])));  // fiber_basis.cpp:69-70
-      return ldg_cg(&tsrc[i - m]);                              // fiber_basis.cpp:74-75
-    };
-    slice_summarize(get, nt, a.ssum, a.sdir, S);
+    const ResidualTerms get{xv, xr, zdn, (long long)m, tsrc};
+    // exact sequential residual: warp 0 of every CTA (warp_grid_sum); the
+    // other warps wait at the CTA barrier
     stamp(a.trace, n, 7);
-    grid_barrier(a.bar, nb);
     stamp(a.trace, n, 12);
-    const double res = slice_combine(get, nt, a.ssum, a.sdir, S, dyn, &bad);
+    if ((threadIdx.x >> 5) == 0) {
+      SliceDirect* sd = reinterpret_cast<SliceDirect*>(dyn);
+      const double r = warp_grid_sum(get, nt, tg, a.sloc, a.ssum, a.sdir, a.sflag, WS, sd,
+                                     reinterpret_cast<int*>(sd + kMaxDirectsTotal), &bad,
+                                     a.trace ? a.trace + (long long)n * kTraceW + 16 : nullptr);
+      if (lane == 0) {
+        s_res = r;
+        s_bad = bad;
+      }
+    }
+    __syncthreads();
+    const double res = s_res;
+    bad = s_bad != 0;
     stamp(a.trace, n, 8);
     const double xs = a.xsq[n];
     const bool reject = __dsqrt_rn(res) <= dmul(a.eps, __dsqrt_rn(xs));  // :79

@@ -261,4 +261,355 @@ __device__ double slice_combine(const Get& get, long long nt, const SliceSum* ps
   return r;
 }
 
+// ---------------------------------------------------------------------------
+// Single-warp-per-CTA variant used by the filter: the same slice algorithm,
+// but every scan is a warp shuffle scan (no CTA barriers), the approximate
+// prefix before a slice comes from the earlier slices' published local sums
+// (each CTA publishes its own, so nothing chains), and the slice summaries are
+// published with per-slice epoch flags that the combiners wait on instead of
+// a grid barrier.  Called by warp 0 of every CTA; all CTAs are co-resident.
+// One 128-byte line per slice for the published sums and flags, so the
+// pollers of different slices never share an L2 line.
+struct SliceLoc {
+  double s;
+  unsigned epoch;
+  unsigned pad[29];
+};
+static_assert(sizeof(SliceLoc) == 128, "one line per slice");
+constexpr int kFlagStride = 32;  // unsigned per slice flag (128 bytes)
+
+// Polls with a short back-off so that many waiting warps do not saturate the
+// L2 slice holding the flag.
+__device__ __forceinline__ void wait_epoch(const unsigned* f, unsigned epoch);
+constexpr int kMaxSlices = 256;
+constexpr int kWarpCache = 4;  // terms cached in registers per lane
+
+struct WarpSumSmem {
+  SliceSum ss[kMaxSlices];
+  Mono cin[kMaxSlices];
+  int doff[kMaxSlices];
+  int nd[kMaxSlices];
+  short sprev[kMaxSlices];
+  Mono finm;
+  short prev_last;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void wait_epoch(const unsigned* f, unsigned epoch) {
+  while (ld_relaxed_u32(f) != epoch) __nanosleep(64);
+  fence_acq_rel_gpu();
+}
+
+__device__ __forceinline__ Seg warp_seg_excl(Seg v, Seg* total) {
+  const int l = threadIdx.x & 31;
+  Seg inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const Seg o = seg_shfl_up(inc, d);
+    if (l >= d) inc = seg_cat(o, inc);
+  }
+  Seg ex = seg_shfl_up(inc, 1);
+  if (l == 0) ex = Seg{0, mono_id()};
+  if (total) {
+    total->h = __shfl_sync(0xffffffffu, inc.h, 31);
+    total->m.a0 = __shfl_sync(0xffffffffu, inc.m.a0, 31);
+    total->m.a1 = __shfl_sync(0xffffffffu, inc.m.a1, 31);
+  }
+  return ex;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_excl(T v, T* total) {
+  const T inc = warp_incl_sum(v);
+  if (total) *total = __shfl_sync(0xffffffffu, inc, 31);
+  return inc - v;
+}
+
+template <typename Get>
+__device__ double warp_grid_sum(const Get& get, long long nt, unsigned epoch, SliceLoc* loc, SliceSum* ps,
+                                SliceDirect* pd, unsigned* sflag, WarpSumSmem& W, SliceDirect* sdir,
+                                int* sslice, bool* fail, long long* tp = nullptr) {
+  const unsigned FULL = 0xffffffffu;
+#define WGS_STAMP(k) \
+  if (tp && blockIdx.x == 0 && (threadIdx.x & 31) == 0) tp[k] = clock64();
+  WGS_STAMP(0)
+  const int lane = threadIdx.x & 31;
+  const int nbk = gridDim.x, b = blockIdx.x;
+  constexpr int kR = kMaxSlices / 32;
+  // ---- A: summarize slice b (one per CTA)
+  const long long per_slice = (nt + nbk - 1) / nbk;
+  const long long s0 = min((long long)b * per_slice, nt), s1 = min(s0 + per_slice, nt);
+  const long long n = s1 - s0;
+  const long long per = (n + 31) / 32;
+  const long long b0 = s0 + min((long long)lane * per, n), b1 = s0 + min((long long)(lane + 1) * per, n);
+  double xv[kWarpCache];
+  get.batch(b0, b1, xv);
+  double cs = 0.0;
+#pragma unroll
+  for (int k = 0; k < kWarpCache; ++k) cs += xv[k];
+  for (long long i = b0 + kWarpCache; i < b1; ++i) cs += get(i);
+  WGS_STAMP(1)
+  double T;
+  const double ex = warp_excl<double>(cs, &T);
+  if (lane == 0) {
+    __stcg(&loc[b].s, T);
+    st_release_u32(&loc[b].epoch, epoch);
+  }
+  // earlier slices' sums (approximate prefix; any order): polls together
+  for (;;) {
+    bool ready = true;
+#pragma unroll
+    for (int k = 0; k < kR; ++k) {
+      const int c = lane + 32 * k;
+      if (c < b) ready &= ld_relaxed_u32(&loc[c].epoch) == epoch;
+    }
+    if (__all_sync(FULL, ready)) break;
+  }
+  fence_acq_rel_gpu();  // relaxed polls + fence: acquire for the loads below
+  double p0 = 0.0;
+#pragma unroll
+  for (int k = 0; k < kR; ++k) {
+    const int c = lane + 32 * k;
+    if (c < b) p0 += __ldcg(&loc[c].s);
+  }
+  const double pre = warp_sum(p0) + ex;  // approximate prefix before my chunk
+  WGS_STAMP(2)
+  const double mg = seq_margin(nt);
+  // classify the cached terms independently (their approximate prefixes
+  // first: one add chain), so the branchy per-term work overlaps
+  const int nc = (int)min((long long)kWarpCache, b1 - b0);
+  double Pv[kWarpCache + 1];
+  Pv[0] = pre;
+#pragma unroll
+  for (int k = 0; k < kWarpCache; ++k) Pv[k + 1] = Pv[k] + xv[k];
+  int cls[kWarpCache], ee[kWarpCache];
+  Mono mm[kWarpCache];
+#pragma unroll
+  for (int k = 0; k < kWarpCache; ++k) {
+    ee[k] = 0;
+    mm[k] = mono_id();
+    cls[k] = CLS_ZERO;
+    if (k < nc) cls[k] = seq_classify(b0 + k == 0, Pv[k], Pv[k + 1], xv[k], mg, &ee[k], &mm[k]);
+  }
+  Seg agg{0, mono_id()};
+  int nd = 0;
+  short le = (short)0x7fff;
+#pragma unroll
+  for (int k = 0; k < kWarpCache; ++k) {
+    if (k < nc) {
+      if (cls[k] == CLS_REG) {
+        agg.m = mono_cat(agg.m, mm[k]);
+        le = (short)ee[k];
+      } else {
+        agg.h = 1;
+        agg.m = mono_id();
+        if (cls[k] == CLS_DIRECT) ++nd;
+        le = (cls[k] == CLS_DIRECT) ? E_DIRECT : E_ZERO;
+      }
+    }
+  }
+  // terms beyond the register cache (large slices): sequential
+  double P = Pv[kWarpCache];
+  for (long long i = b0 + kWarpCache; i < b1; ++i) {
+    const double x = get(i);
+    const double Pc = P + x;
+    int e = 0;
+    Mono m;
+    const int c = seq_classify(i == 0, P, Pc, x, mg, &e, &m);
+    if (c == CLS_REG) {
+      agg.m = mono_cat(agg.m, m);
+      le = (short)e;
+    } else {
+      agg.h = 1;
+      agg.m = mono_id();
+      if (c == CLS_DIRECT) ++nd;
+      le = (c == CLS_DIRECT) ? E_DIRECT : E_ZERO;
+    }
+    P = Pc;
+  }
+  const short le_chunk = (b0 < b1) ? le : (short)0x7fff;
+  Seg tot;
+  const Seg carry = warp_seg_excl(agg, &tot);
+  int ntot;
+  int dpos = warp_excl<int>(nd, &ntot);
+  const bool over = ntot > kSliceDirects;
+  // e of the element before my chunk: the previous lane's last (chunks fill
+  // lanes in order), else the previous slice (resolved in the combine)
+  const short prev_lane_e = (short)__shfl_up_sync(FULL, (int)le_chunk, 1);
+  if (!over && nd > 0) {
+    short prev_e = (lane > 0) ? prev_lane_e : (short)0x7ffe;
+    Mono M = carry.m;
+    int inh = carry.h ? 0 : 1;
+    auto step = [&](int c, int e, const Mono& m, double x) {
+      if (c == CLS_REG) {
+        M = mono_cat(M, m);
+        prev_e = (short)e;
+      } else {
+        if (c == CLS_DIRECT) {
+          SliceDirect d;
+          d.x = x;
+          d.m = M;
+          d.inh = inh;
+          d.e = prev_e;
+          pd[(long long)b * kSliceDirects + dpos] = d;
+          ++dpos;
+        }
+        M = mono_id();
+        inh = 0;
+        prev_e = (c == CLS_DIRECT) ? E_DIRECT : E_ZERO;
+      }
+    };
+#pragma unroll
+    for (int k = 0; k < kWarpCache; ++k)
+      if (k < nc) step(cls[k], ee[k], mm[k], xv[k]);
+    double P2 = Pv[kWarpCache];
+    for (long long i = b0 + kWarpCache; i < b1; ++i) {
+      const double x = get(i);
+      const double Pc = P2 + x;
+      int e = 0;
+      Mono m;
+      const int c = seq_classify(i == 0, P2, Pc, x, mg, &e, &m);
+      step(c, e, m, x);
+      P2 = Pc;
+    }
+  }
+  WGS_STAMP(3)
+  const long long tlast = n > 0 ? (n - 1) / per : 0;
+  if (lane == tlast) {
+    SliceSum s;
+    s.agg = tot;
+    s.nd = over ? -1 : ntot;
+    s.last_e = (n > 0) ? le : (short)0x7fff;
+    ps[b] = s;
+  }
+  __syncwarp();  // orders the other lanes' summary/direct writes before lane 0's release
+  if (lane == 0) st_release_u32(&sflag[b * kFlagStride], epoch);
+#ifdef CTD_WGS_GT
+  if (lane == 0) { unsigned long long g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); CTD_WGS_GT[b] = g; }
+#endif
+  // ---- B: combine all slices (redundantly in every CTA).  Staged in shared
+  // memory, then lane l folds the contiguous slices [l*per2, (l+1)*per2).
+  for (;;) {
+    bool ready = true;
+#pragma unroll
+    for (int k = 0; k < kR; ++k) {
+      const int c = lane + 32 * k;
+      if (c < nbk) ready &= ld_relaxed_u32(&sflag[c * kFlagStride]) == epoch;
+    }
+    if (__all_sync(FULL, ready)) break;
+  }
+  fence_acq_rel_gpu();
+#pragma unroll
+  for (int k = 0; k < kR; ++k) {
+    const int c = lane + 32 * k;
+    if (c < nbk) W.ss[c] = ldcg_struct(ps + c);
+  }
+  __syncwarp();
+#ifdef CTD_WGS_GT
+  if (lane == 0) { unsigned long long g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); CTD_WGS_GT[256 + b] = g; }
+#endif
+  WGS_STAMP(4)
+  const int per2 = (nbk + 31) / 32;
+  const int c0 = min(lane * per2, nbk), c1 = min(c0 + per2, nbk);
+  Seg lt{0, mono_id()};
+  int ndl = 0, any_over = 0;
+  int lne = 0x7fff;  // my last non-empty slice's last_e
+  for (int c = c0; c < c1; ++c) {
+    const SliceSum sv = W.ss[c];
+    lt = seg_cat(lt, sv.agg);
+    ndl += sv.nd < 0 ? 0 : sv.nd;
+    any_over |= sv.nd < 0;
+    if (sv.last_e != (short)0x7fff) lne = sv.last_e;
+  }
+  Seg lc = warp_seg_excl(lt, nullptr);
+  int total_d;
+  int off = warp_excl<int>(ndl, &total_d);
+  int pl = lne;  // nearest non-empty slice before mine: "right unless empty"
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(FULL, pl, d);
+    if (lane >= d && pl == 0x7fff) pl = o;
+  }
+  int prev = __shfl_up_sync(FULL, pl, 1);
+  if (lane == 0 || prev == 0x7fff) prev = E_ZERO;
+  const int last_all = __shfl_sync(FULL, pl, 31);
+  const bool over_all = __any_sync(FULL, any_over) || total_d > kMaxDirectsTotal;
+  for (int c = c0; c < c1; ++c) {
+    const SliceSum sv = W.ss[c];
+    W.cin[c] = lc.m;
+    W.doff[c] = off;
+    const int ndc = sv.nd < 0 ? 0 : sv.nd;
+    W.nd[c] = ndc;
+    W.sprev[c] = (short)prev;
+    if (c == nbk - 1) W.finm = seg_cat(Seg{0, lc.m}, sv.agg).m;
+    lc = seg_cat(lc, sv.agg);
+    off += ndc;
+    if (sv.last_e != (short)0x7fff) prev = sv.last_e;
+  }
+  __syncwarp();
+  WGS_STAMP(5)
+  // directs in order, each with its run monoid and binade resolved (parallel)
+  if (!over_all) {
+    for (int idx = lane; idx < total_d; idx += 32) {
+      int lo = 0, hi = nbk - 1;  // last slice with doff <= idx and nd > 0
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (W.doff[mid] <= idx) lo = mid;
+        else hi = mid - 1;
+      }
+      while (W.nd[lo] == 0 || W.doff[lo] + W.nd[lo] <= idx) ++lo;
+      SliceDirect d = ldcg_struct(pd + (long long)lo * kSliceDirects + (idx - W.doff[lo]));
+      if (d.inh) d.m = mono_cat(W.cin[lo], d.m);
+      if (d.e == (short)0x7ffe) d.e = W.sprev[lo];  // "previous slice"
+      sdir[idx] = d;
+    }
+  }
+  __syncwarp();
+  WGS_STAMP(6)
+  double acc = 0.0;
+  int bad = 0;
+  if (lane == 0) {
+    bool ok = !over_all;
+    double head = 0.0;
+    if (ok) {
+      for (int idx = 0; idx < total_d && ok; ++idx) {
+        const SliceDirect d = sdir[idx];
+        acc = head;
+        if (d.e >= -1100 && d.e <= 1100) ok = seq_apply_run(head, d.e, d.m, &acc);
+        acc = dadd(acc, d.x);
+        head = acc;
+      }
+      acc = head;
+      const short pl2 = (short)last_all;
+      if (ok && pl2 >= -1100 && pl2 <= 1100) ok = seq_apply_run(head, pl2, W.finm, &acc);
+    }
+    if (!ok) {  // sequential fallback: always the reference order
+      acc = 0.0;
+      for (long long i = 0; i < nt; ++i) acc = dadd(acc, get(i));
+    }
+    bad = ok ? 0 : 1;
+  }
+  WGS_STAMP(7)
+  if (tp && blockIdx.x == 0 && lane == 0) tp[9] = total_d;
+#undef WGS_STAMP
+  acc = __shfl_sync(FULL, acc, 0);
+  bad = __shfl_sync(FULL, bad, 0);
+  if (fail) *fail = bad != 0;
+  (void)sslice;
+  return acc;
+}
+
 }  // namespace ctdgpu

@@ -320,6 +320,90 @@ void run_ring2(double* U, long long LD, int rows, int K, long long* c, double* o
   }
 }
 
+// Ring v3: producers stage U segments with cp.async.cg (16 B) DEPTH chunks
+// ahead into a shared-memory stage ring, then compute from shared memory.
+template <int W, int NS, int DEPTH>
+__global__ void __launch_bounds__(kT, 1) k_ring3(double* U, long long LD, int rows, int Q2, long long* cyc, double* out) {
+  extern __shared__ __align__(16) double sm[];
+  double* ring = sm;                   // [NS][W][kS]
+  double* stage = sm + NS * W * kS;    // [DEPTH+1][32][W]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long row0 = blockIdx.x;
+  const double rcp17 = __drcp_rn(1.7);
+  __syncthreads();
+  long long t0 = clock64();
+  if (warp < 15) {
+    const int pi = threadIdx.x;
+    // copy units: rows x (W/2) 16-byte pieces
+    auto issue = [&](int q) {
+      double* st = stage + (q % (DEPTH + 1)) * 32 * W;
+      const int units = rows * (W / 2);
+      for (int u = pi; u < units; u += 480) {
+        const int r = u / (W / 2), c = (u % (W / 2)) * 2;
+        const double* src = U + (row0 + 148 * r) * LD + q * W + c;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(st + r * W + c)), "l"(src) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int q = 0; q < DEPTH && q < Q2; ++q) issue(q);
+    constexpr int kP2 = (32 * W + 479) / 480;
+    for (int q = 0; q < Q2; ++q) {
+      const int sl = q % NS;
+      double* rb = ring + sl * W * kS;
+      if (q + DEPTH < Q2) issue(q + DEPTH);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH) : "memory");
+      nsync(9, 480);  // everyone's copies for chunk q landed
+      const double* st = stage + (q % (DEPTH + 1)) * 32 * W;
+      if (q >= NS) nsync(1 + NS + sl, kT);
+#pragma unroll
+      for (int s = 0; s < kP2; ++s) {
+        const int e = pi + s * 480, r = e / W, t = e % W;
+        if (e < 32 * W && r < rows) {
+          bool ok;
+          const double uv = st[r * W + t];
+          double u = ctdgpu::dadd(uv, ctdgpu::ddiv_rcp(ctdgpu::dmul(uv, 0.37), 1.7, rcp17, &ok));
+          rb[t * kS + r] = ctdgpu::dmul(u, 1.0000001);
+        }
+      }
+      narv(1 + sl, kT);
+      nsync(10, 480);  // stage slot free before it is refilled
+    }
+  } else {
+    double acc = 0.0;
+    for (int q = 0; q < Q2; ++q) {
+      const int sl = q % NS;
+      nsync(1 + sl, kT);
+      const double* p = ring + sl * W * kS + lane;
+#pragma unroll
+      for (int k0 = 0; k0 < W; k0 += 16) {
+        double v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = p[(k0 + k) * kS];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc = ctdgpu::dadd(acc, v[k]);
+      }
+      if (q + NS < Q2) narv(1 + NS + sl, kT);
+    }
+    out[blockIdx.x * 32 + lane] = acc;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) cyc[0] = clock64() - t0;
+}
+
+template <int W, int NS, int DEPTH>
+void run_ring3(double* U, long long LD, int rows, int K, long long* c, double* o) {
+  const int smem = (NS * W * kS + (DEPTH + 1) * 32 * W) * 8;
+  cudaFuncSetAttribute(k_ring3<W, NS, DEPTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaMemset(c, 0, 24);
+  k_ring3<W, NS, DEPTH><<<148, kT, smem>>>(U, LD, rows, K / W, c, o);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h;
+  cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  printf("ring3 (cp.async) W=%d slots=%d depth=%d: %.1f cycles/step %s\n", W, NS, DEPTH, (double)h / K,
+         e ? cudaGetErrorString(e) : "");
+}
+
 int main() {
   const int K = 1280, rows = 9;
   const long long LD = 1280;
@@ -351,6 +435,9 @@ int main() {
   }
   run_ring2<64, 3>(U, LD, rows, K, c, o);
   run_ring2<128, 2>(U, LD, rows, K, c, o);
+  run_ring3<64, 3, 2>(U, LD, rows, K, c, o);
+  run_ring3<64, 3, 4>(U, LD, rows, K, c, o);
+  run_ring3<128, 2, 2>(U, LD, rows, K, c, o);
   for (int first : {0})
   for (int pair : {2})
   for (int avoid : {0})
