@@ -146,6 +146,27 @@ def phase_bytes(nnz, F, kept_seq, r_lens):
 
 # ---------------------------------------------------------------------------
 
+# phase -> its dominant kernel in the committed ncu captures (profiles/)
+PHASE_KERNEL = {"filter": "k_filter", "matricize": "k_bucket_sort", "law": "k_seq_local",
+                "error": "k_cd"}
+
+
+def ncu_traffic(phase):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the phase's
+    kernel from the latest committed `ncu --set full` capture (profiles/r*_kernels.json),
+    or None when that kernel was not captured."""
+    import glob
+    kern = PHASE_KERNEL.get(phase)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_kernels.json")))
+    if not kern or not files:
+        return None
+    rows = [d for d in json.load(open(files[-1])) if d.get("kernel") == kern
+            and d.get("dram_read") is not None and d.get("dram_write") is not None]
+    if not rows:
+        return None
+    return int(sum(d["dram_read"] + d["dram_write"] for d in rows) / len(rows))
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -238,7 +259,7 @@ def run_ours(args, rank, world, local_rank):
     dms = per_phase[dom]["ms"]
     achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
     roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": pk,
-            "unit": "GB/s", "frac": round(achieved / pk, 4), "traffic": None,
+            "unit": "GB/s", "frac": round(achieved / pk, 4), "traffic": ncu_traffic(dom),
             "peak_kind": pk_kind}
     # SURVEY §8d end-to-end byte formula for the step
     bs = 44 * nnz + 24 * info.n_fibers
