@@ -70,6 +70,115 @@ def load_c2(rank: int = 0):
     return x
 
 
+C3 = dict(n=5000, steps=100, slices=10, d=500, eps=1e-6, seed=42, mode=0, hist_steps=50, gen_seed=3)
+
+
+def load_c3():
+    from paper_1710_03608_b200 import datagen
+    seed = C3["gen_seed"]
+    cache = os.path.join(tempfile.gettempdir(), f"ctd_c3_seed{seed}.npz")
+    if os.path.exists(cache):
+        try:
+            z = np.load(cache)
+            return datagen.Tensor(list(z["shape"]), z["idx"], z["val"], {"seed": seed})
+        except Exception:
+            pass
+    x = datagen.c3_stream(seed=seed, n_steps=C3["steps"], slices_per_step=C3["slices"], n=C3["n"])
+    try:
+        np.savez(cache, shape=np.array(x.shape), idx=x.idx, val=x.val)
+    except Exception:
+        pass
+    return x
+
+
+def time_slices(x, t0, t1):
+    """Per-slice slabs [I1, I2, 1] for t0 <= t < t1 (sorted, coalesced), host arrays."""
+    tm = x.order - 1
+    order = np.argsort(x.idx[:, tm], kind="stable")  # keeps (src, dst) order within a slice
+    ts = x.idx[order, tm]
+    bounds = np.searchsorted(ts, np.arange(t0, t1 + 1))
+    out = []
+    for k in range(t1 - t0):
+        sel = order[bounds[k]:bounds[k + 1]]
+        idx = x.idx[sel].copy()
+        idx[:, tm] = 0
+        out.append((idx, x.val[sel].copy()))
+    return out
+
+
+def run_ctd_d(args, ctx, torch):
+    """C3 (BASELINE configs[2]): CTD-D per-step latency.  init_stream on the first
+    hist_steps x 10 slices, then one ctd_d_step per incoming slice (time extent 1,
+    d = 500 samples, seed ^ t), each timed alone like stream_harness.cpp:90-92 (step
+    only; slabs already resident on the device).  Scope: the step's front end
+    (slab bucketing + norms, law/CDF, draws, dedup, bit-exact filter against R(t),
+    kept-id append); the Eq. 13 core blocks are not maintained (SURVEY §8f #2)."""
+    from paper_1710_03608_b200 import ctd as api
+    x = load_c3()
+    H = C3["hist_steps"] * C3["slices"]
+    T = C3["steps"] * C3["slices"]
+    hist = x.time_slab(0, H)
+    slabs_h = time_slices(x, H, T)
+    shape1 = [C3["n"], C3["n"], 1]
+    dev = [api.DeviceTensor(api.SparseTensor(shape1, i, v), ctx) if v.shape[0] else None for i, v in slabs_h]
+    ht = api.DeviceTensor(api.SparseTensor.from_datagen(hist), ctx)
+    t0 = time.perf_counter()
+    st = api.init_stream(ht, C3["mode"], C3["d"], C3["eps"], C3["seed"], ctx=ctx)
+    torch.cuda.synchronize()
+    init_s = time.perf_counter() - t0
+    lat = []
+    nnz_steps = 0
+    for k, dt in enumerate(dev):
+        if dt is None:
+            continue
+        t0 = time.perf_counter()
+        api.ctd_d_step(st, dt, C3["d"])
+        torch.cuda.synchronize()
+        lat.append(time.perf_counter() - t0)
+        nnz_steps += dt.nnz
+    kept = st.factors()
+    lat_ms = np.array(lat) * 1e3
+    for d in dev:
+        if d is not None:
+            d.close()
+    ht.close()
+    return {"workload": "C3: CTD-D on 5000x5000 src x dst, 10 slices/step x 100 steps, Zipf(1.2), "
+                        "counts 1..50, planted 50x50x10 block (+100) at step 60; d=500, eps=1e-6",
+            "history_slices": H, "streamed_slices": len(lat), "history_nnz": hist.nnz,
+            "init_stream_ms": round(init_s * 1e3, 2),
+            "step_ms_p50": round(float(np.percentile(lat_ms, 50)), 3),
+            "step_ms_p99": round(float(np.percentile(lat_ms, 99)), 3),
+            "step_ms_mean": round(float(lat_ms.mean()), 3),
+            "slices_per_s": round(len(lat) / (lat_ms.sum() / 1e3), 1),
+            "nnz_per_s": round(nnz_steps / (lat_ms.sum() / 1e3), 1),
+            "kept_final": len(kept.kept_flat) if hasattr(kept, "kept_flat") else None,
+            "scope": "step front end (bucketing, law, seed^t draws, dedup, bit-exact filter vs R(t), "
+                     "kept-id append); Eq. 13 core blocks not maintained (SURVEY 8f #2)"}
+
+
+def ctd_d_reference_sample():
+    """The reference ctd_d_step (oracle/_ref, which also updates the Eq. 13 core) on C3:
+    init_stream on the first 10 slices, then 5 timed steps (a bounded sample)."""
+    try:
+        from oracle.bindings import Ref, ref_available
+        if not ref_available():
+            return None
+        x = load_c3()
+        R = Ref()
+        h = x.time_slab(0, 10)
+        st = R.stream(R.tensor(h.shape, h.flat_idx(), h.val), C3["mode"], C3["d"], C3["eps"], C3["seed"])
+        secs = []
+        for i, (idx, val) in enumerate(time_slices(x, 10, 15)):
+            from paper_1710_03608_b200 import datagen
+            sl = datagen.Tensor([C3["n"], C3["n"], 1], idx, val)
+            secs.append(st.step(R.tensor(sl.shape, sl.flat_idx(), sl.val), C3["d"]))
+        return {"step_ms_mean": round(float(np.mean(secs)) * 1e3, 2), "cores": 1, "kind": "reference",
+                "sample": "reference ctd_d_step (includes its Eq. 13 core update) at t = 10..14 "
+                          "after init_stream on 10 slices; single-threaded"}
+    except Exception as e:  # pragma: no cover
+        return {"sample": f"failed: {e}"}
+
+
 # ---------------------------------------------------------------------------
 # clocks during the timed region
 
@@ -274,6 +383,12 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(x)
 
+    ctdd = None
+    if rank == 0 and world == 1 and not args.no_ctdd:
+        ctdd = run_ctd_d(args, ctx, torch)
+        if not args.no_cpu:
+            ctdd["cpu_reference"] = ctd_d_reference_sample()
+
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
@@ -298,6 +413,8 @@ def run_ours(args, rank, world, local_rank):
         line["e2e"] = e2e
     if cpu:
         line["cpu_baseline"] = cpu
+    if ctdd is not None:
+        line["ctd_d"] = ctdd
     if rank == 0:
         print(json.dumps(line, default=_np_default), flush=True)
 
@@ -412,6 +529,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ctdd", action="store_true", help="skip the C3 CTD-D per-step latency run")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
