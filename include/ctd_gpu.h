@@ -176,6 +176,54 @@ int ctd_gpu_basis_try_append(ctd_gpu_basis *b, int64_t dim, int64_t nnz,
                              double *y);
 int ctd_gpu_basis_u(const ctd_gpu_basis *b, double *u);
 
+/* ---- sharded CTD-S building blocks (multi-GPU) ---------------
+ * Each rank matricizes its own fiber range (ctd_gpu_matricize), the fibers'
+ * global column ids and exact squared norms are all-gathered, every rank
+ * draws the same sample, candidates are all-gathered from their owners, the
+ * filter runs replicated, and the error partials are all-reduced.
+ * (The reference entry points these compose: column_distribution +
+ * sample_with_replacement + unique_first_occurrence, sampling.cpp:21-78;
+ * FiberBasis::try_append_fiber, fiber_basis.cpp:43-109; relative_error,
+ * evaluation.cpp:88-122.) */
+/* Law, draws and dedup over the nonempty fibers given by host arrays
+ * (fiber_col strictly ascending global column ids, sq_norms their exact
+ * squared norms): bit-exact with column_distribution /
+ * sample_with_replacement / unique_first_occurrence over all N_alpha columns
+ * (the absent columns have probability exactly 0).  unique[sample_size]
+ * receives the unique drawn column ids in first-occurrence order. */
+int ctd_gpu_sample_fibers(ctd_gpu_ctx *ctx, int64_t n_fibers, const int64_t *fiber_col,
+                          const double *sq_norms, int64_t sample_size, uint64_t seed,
+                          double *total_sq_norm, int64_t *unique, int64_t *n_unique);
+/* try_append_fiber for n candidates in order (host CSC: cand_ptr[n+1], rows
+ * ascending per candidate, values without zeros); per-candidate outcomes. */
+int ctd_gpu_basis_append_batch(ctd_gpu_basis *b, int64_t n, const int64_t *cand_ptr,
+                               const int64_t *rows, const double *vals, double epsilon,
+                               int32_t *accepted, int32_t *degenerate, double *delta);
+/* R of the basis as CSC (size()+1, r_nnz, r_nnz), acceptance order. */
+int64_t ctd_gpu_basis_r_nnz(const ctd_gpu_basis *b);
+int ctd_gpu_basis_r(const ctd_gpu_basis *b, int64_t *col_ptr, int64_t *rows, double *vals);
+/* A shard of X bucketed once and kept resident: its fibers' global column
+ * ids and exact squared norms (for the all-gather), owner-side gathers of
+ * candidate fibers, and the error partials over its fibers. */
+typedef struct ctd_gpu_shard ctd_gpu_shard;
+int ctd_gpu_shard_create(ctd_gpu_ctx *ctx, const ctd_gpu_tensor *x, int mode,
+                         ctd_gpu_shard **out);
+int64_t ctd_gpu_shard_n_fibers(const ctd_gpu_shard *s);
+int ctd_gpu_shard_fibers(const ctd_gpu_shard *s, int64_t *fiber_col, double *sq_norms);
+/* cand_ptr[n+1] always; rows/vals (cand_ptr[n] entries) when non-NULL.
+ * Every cols[k] must be a fiber of this shard (ArgumentError otherwise). */
+int ctd_gpu_shard_gather(const ctd_gpu_shard *s, int64_t n, const int64_t *cols,
+                         int64_t *cand_ptr, int64_t *rows, double *vals);
+int ctd_gpu_shard_error_partials(const ctd_gpu_shard *s, const ctd_gpu_basis *b,
+                                 double *x_sq, double *cross);
+int ctd_gpu_shard_destroy(ctd_gpu_shard *s);
+/* relative_error's two sums over the fibers of x (one shard):
+ * x_sq = |X_p|^2 and cross = sum_j x_j^T (R U R^T) x_j; after summing the
+ * shards, rel = (x_sq - cross) / x_sq. */
+int ctd_gpu_basis_error_partials(ctd_gpu_ctx *ctx, const ctd_gpu_basis *b,
+                                 const ctd_gpu_tensor *x, int mode, double *x_sq,
+                                 double *cross);
+
 /* ---- CTD-D (ctd_dynamic.hpp:42-58) -------------------------------------- */
 int ctd_gpu_stream_init(ctd_gpu_ctx *ctx, const ctd_gpu_tensor *historical,
                         int mode, int64_t sample_size, double epsilon,

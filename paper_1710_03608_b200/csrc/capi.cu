@@ -30,6 +30,11 @@ struct ctd_gpu_basis {
 struct ctd_gpu_stream {
   Stream s;
 };
+struct ctd_gpu_shard {
+  Ctx* ctx;
+  Fibers fb;                       // the shard's bucketed fibers, resident in HBM
+  std::vector<int64_t> col, ptr;   // host copies for owner lookups
+};
 
 namespace {
 
@@ -526,6 +531,236 @@ int ctd_gpu_basis_try_append(ctd_gpu_basis* b, int64_t dim, int64_t nnz, const i
     if (delta) *delta = bo.delta[0];
     if (y) std::memcpy(y, bo.y_last.data(), (size_t)k_before * sizeof(double));
   });
+}
+
+// ---- sharded CTD-S building blocks ----------------------------
+
+int ctd_gpu_sample_fibers(ctd_gpu_ctx* ctx, int64_t n_fibers, const int64_t* fiber_col, const double* sq_norms,
+                          int64_t sample_size, uint64_t seed, double* total_sq_norm, int64_t* unique,
+                          int64_t* n_unique) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(unique, "unique");
+    need(n_unique, "n_unique");
+    if (sample_size < 1) fail(CTD_ERR_ARGUMENT, "sample size must be at least 1");  // sampling.cpp:36
+    if (n_fibers < 0) fail(CTD_ERR_ARGUMENT, "negative fiber count");
+    if (n_fibers == 0) fail(CTD_ERR_EMPTY_INPUT, "column distribution of an all-zero matrix");  // :22-23
+    need(fiber_col, "fiber_col");
+    need(sq_norms, "sq_norms");
+    for (int64_t i = 1; i < n_fibers; ++i)
+      if (fiber_col[i] <= fiber_col[i - 1]) fail(CTD_ERR_ARGUMENT, "fiber columns must be strictly ascending");
+    Ctx* c = &ctx->c;
+    const int64_t F = n_fibers;
+    Buf<double> norm(c, F + 1), probs(c, F + 1), cum(c, F + 1), total(c, 1);
+    c->to_dev(norm.p, sq_norms, F);
+    {
+      PhaseScope ps(c, PH_LAW);
+      sampling_law(c, norm.p, F, total.p, probs.p, cum.p, c->d_flags);
+    }
+    Buf<int32_t> drawn(c, sample_size), uniq(c, sample_size);
+    Buf<int> nu(c, 1);
+    {
+      PhaseScope ps(c, PH_SAMPLE);
+      draw_fibers(c, cum.p, F, sample_size, seed, drawn.p);
+      dedup_first(c, drawn.p, sample_size, uniq.p, nu.p);
+    }
+    int n_u = 0;
+    c->to_host(&n_u, nu.p, 1);
+    if (total_sq_norm) c->to_host(total_sq_norm, total.p, 1);
+    c->sync();
+    c->check_flags("sampling");
+    std::vector<int32_t> u32(n_u > 0 ? n_u : 1);
+    if (n_u) c->to_host(u32.data(), uniq.p, n_u);
+    c->sync();
+    for (int i = 0; i < n_u; ++i) unique[i] = fiber_col[u32[i]];
+    *n_unique = n_u;
+    c->phase_flush();
+  });
+}
+
+int ctd_gpu_basis_append_batch(ctd_gpu_basis* b, int64_t n, const int64_t* cand_ptr, const int64_t* rows,
+                               const double* vals, double epsilon, int32_t* accepted, int32_t* degenerate,
+                               double* delta) {
+  return guarded([&] {
+    need(b, "basis");
+    if (n < 0) fail(CTD_ERR_ARGUMENT, "negative candidate count");
+    if (n == 0) return;
+    need(cand_ptr, "cand_ptr");
+    Basis& B = *b->b;
+    Ctx* c = b->ctx;
+    if (cand_ptr[0] != 0) fail(CTD_ERR_ARGUMENT, "cand_ptr[0] must be 0");
+    const int64_t nnz = cand_ptr[n];
+    std::vector<int32_t> r32(nnz > 0 ? nnz : 1), len(n);
+    std::vector<int64_t> off(n);
+    for (int64_t k = 0; k < n; ++k) {
+      if (cand_ptr[k + 1] < cand_ptr[k]) fail(CTD_ERR_ARGUMENT, "cand_ptr must be non-decreasing");
+      if (cand_ptr[k + 1] - cand_ptr[k] >= (int64_t(1) << 31)) fail(CTD_ERR_ARGUMENT, "candidate too long");
+      off[k] = cand_ptr[k];
+      len[k] = (int32_t)(cand_ptr[k + 1] - cand_ptr[k]);
+      for (int64_t i = cand_ptr[k]; i < cand_ptr[k + 1]; ++i) {
+        if (rows[i] < 0 || rows[i] >= B.dim) fail(CTD_ERR_SHAPE, "fiber index out of range");  // :45
+        if (i > cand_ptr[k] && rows[i] <= rows[i - 1]) fail(CTD_ERR_ARGUMENT, "fiber rows must ascend");
+        r32[i] = (int32_t)rows[i];
+      }
+    }
+    Buf<int32_t> drow(c, nnz + 1), dlen(c, n);
+    Buf<double> dval(c, nnz + 1);
+    Buf<int64_t> doff(c, n);
+    if (nnz) {
+      c->to_dev(drow.p, r32.data(), nnz);
+      c->to_dev(dval.p, vals, nnz);
+    }
+    c->to_dev(doff.p, off.data(), n);
+    c->to_dev(dlen.p, len.data(), n);
+    Cands cd;
+    cd.n = n;
+    cd.off = doff.p;
+    cd.len = dlen.p;
+    cd.row = drow.p;
+    cd.val = dval.p;
+    BatchOut bo;
+    {
+      PhaseScope ps(c, PH_FILTER);
+      filter_batch(B, cd, epsilon, bo, false);
+    }
+    for (int64_t k = 0; k < n; ++k) {
+      if (accepted) accepted[k] = bo.accepted[k];
+      if (degenerate) degenerate[k] = bo.degenerate[k];
+      if (delta) delta[k] = bo.delta[k];
+    }
+    c->phase_flush();
+  });
+}
+
+int64_t ctd_gpu_basis_r_nnz(const ctd_gpu_basis* b) { return b ? b->b->rnnz : -1; }
+
+int ctd_gpu_basis_r(const ctd_gpu_basis* b, int64_t* col_ptr, int64_t* rows, double* vals) {
+  return guarded([&] {
+    need(b, "basis");
+    need(col_ptr, "col_ptr");
+    basis_r(*b->b, col_ptr, rows, vals);
+  });
+}
+
+int ctd_gpu_basis_error_partials(ctd_gpu_ctx* ctx, const ctd_gpu_basis* b, const ctd_gpu_tensor* x, int mode,
+                                 double* x_sq, double* cross) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(b, "basis");
+    need(x, "x");
+    need(x_sq, "x_sq");
+    need(cross, "cross");
+    if (mode < 0 || mode >= x->t.order) fail(CTD_ERR_ARGUMENT, "mode out of range");
+    if (x->t.shape[mode] != b->b->dim) fail(CTD_ERR_SHAPE, "fiber length does not match basis");
+    Fibers fb;
+    {
+      PhaseScope ps(&ctx->c, PH_MATRICIZE);
+      matricize(&ctx->c, x->t, mode, fb);
+    }
+    {
+      PhaseScope ps(&ctx->c, PH_ERROR);
+      error_partials(&ctx->c, fb, *b->b, x_sq, cross);
+    }
+    ctx->c.phase_flush();
+  });
+}
+
+namespace {
+// copies candidate k's entries [src[k], src[k]+len[k]) to [dst[k], ...)
+__global__ void k_gather_fibers(const int64_t* src, const int64_t* dst, const int64_t* len, const int32_t* row,
+                                const double* val, int64_t* orow, double* oval) {
+  const int k = blockIdx.x;
+  const int64_t s = src[k], d = dst[k], n = len[k];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    orow[d + i] = row[s + i];
+    oval[d + i] = val[s + i];
+  }
+}
+}  // namespace
+
+int ctd_gpu_shard_create(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int mode, ctd_gpu_shard** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(x, "x");
+    need(out, "out");
+    if (mode < 0 || mode >= x->t.order) fail(CTD_ERR_ARGUMENT, "mode out of range");
+    auto h = std::make_unique<ctd_gpu_shard>();
+    h->ctx = &ctx->c;
+    {
+      PhaseScope ps(&ctx->c, PH_MATRICIZE);
+      matricize(&ctx->c, x->t, mode, h->fb);
+    }
+    const int64_t F = h->fb.F;
+    h->col.resize(F);
+    h->ptr.resize(F + 1);
+    if (F) ctx->c.to_host(h->col.data(), h->fb.col.p, F);
+    ctx->c.to_host(h->ptr.data(), h->fb.ptr.p, F + 1);
+    ctx->c.sync();
+    ctx->c.phase_flush();
+    *out = h.release();
+  });
+}
+
+int64_t ctd_gpu_shard_n_fibers(const ctd_gpu_shard* s) { return s ? s->fb.F : -1; }
+
+int ctd_gpu_shard_fibers(const ctd_gpu_shard* s, int64_t* fiber_col, double* sq_norms) {
+  return guarded([&] {
+    need(s, "shard");
+    const int64_t F = s->fb.F;
+    if (fiber_col && F) std::memcpy(fiber_col, s->col.data(), F * sizeof(int64_t));
+    if (sq_norms && F) {
+      s->ctx->to_host(sq_norms, s->fb.norm.p, F);
+      s->ctx->sync();
+    }
+  });
+}
+
+int ctd_gpu_shard_gather(const ctd_gpu_shard* s, int64_t n, const int64_t* cols, int64_t* cand_ptr,
+                         int64_t* rows, double* vals) {
+  return guarded([&] {
+    need(s, "shard");
+    need(cand_ptr, "cand_ptr");
+    if (n < 0) fail(CTD_ERR_ARGUMENT, "negative count");
+    std::vector<int64_t> src(n), len(n);
+    cand_ptr[0] = 0;
+    for (int64_t k = 0; k < n; ++k) {
+      const auto it = std::lower_bound(s->col.begin(), s->col.end(), cols[k]);
+      if (it == s->col.end() || *it != cols[k]) fail(CTD_ERR_ARGUMENT, "fiber not held by this shard");
+      const int64_t f = it - s->col.begin();
+      src[k] = s->ptr[f];
+      len[k] = s->ptr[f + 1] - s->ptr[f];
+      cand_ptr[k + 1] = cand_ptr[k] + len[k];
+    }
+    if (!rows || !vals || n == 0 || cand_ptr[n] == 0) return;
+    Ctx* c = s->ctx;
+    const int64_t tot = cand_ptr[n];
+    Buf<int64_t> dsrc(c, n), ddst(c, n), dlen(c, n), orow(c, tot);
+    Buf<double> oval(c, tot);
+    c->to_dev(dsrc.p, src.data(), n);
+    c->to_dev(ddst.p, cand_ptr, n);
+    c->to_dev(dlen.p, len.data(), n);
+    LAUNCH(c, k_gather_fibers, (unsigned)n, 128, 0, dsrc.p, ddst.p, dlen.p, s->fb.row.p, s->fb.val.p, orow.p,
+           oval.p);
+    c->to_host(rows, orow.p, tot);
+    c->to_host(vals, oval.p, tot);
+    c->sync();
+  });
+}
+
+int ctd_gpu_shard_error_partials(const ctd_gpu_shard* s, const ctd_gpu_basis* b, double* x_sq, double* cross) {
+  return guarded([&] {
+    need(s, "shard");
+    need(b, "basis");
+    need(x_sq, "x_sq");
+    need(cross, "cross");
+    if (s->fb.rows != b->b->dim) fail(CTD_ERR_SHAPE, "fiber length does not match basis");
+    PhaseScope ps(s->ctx, PH_ERROR);
+    error_partials(s->ctx, s->fb, *b->b, x_sq, cross);
+  });
+}
+
+int ctd_gpu_shard_destroy(ctd_gpu_shard* s) {
+  return guarded([&] { delete s; });
 }
 
 int ctd_gpu_basis_u(const ctd_gpu_basis* b, double* u) {

@@ -93,6 +93,14 @@ __global__ void k_reduce(const double* p, long long n, double* out) {
 }  // namespace
 
 double relative_error(Ctx* ctx, const Fibers& fb, const Basis& B) {
+  double hx = 0.0, hcd = 0.0;
+  error_partials(ctx, fb, B, &hx, &hcd);
+  if (hx == 0.0) fail(CTD_ERR_METRIC, "relative error undefined for a zero tensor");
+  if (B.K == 0) return 1.0;
+  return (hx - hcd) / hx;
+}
+
+void error_partials(Ctx* ctx, const Fibers& fb, const Basis& B, double* x_sq, double* cross) {
   const long long K = B.K, dim = B.dim;
   // |X|^2
   const unsigned sgrid = (unsigned)ctx->sm_count * 4;
@@ -100,9 +108,9 @@ double relative_error(Ctx* ctx, const Fibers& fb, const Basis& B) {
   LAUNCH(ctx, k_sumsq, sgrid, 256, 0, fb.val.p, (long long)fb.nnz, sp.p);
   LAUNCH(ctx, k_reduce, 1, 1024, 0, sp.p, (long long)sgrid, xsq.p);
   if (K == 0) {
-    const double x = ctx->read1(xsq.p);
-    if (x == 0.0) fail(CTD_ERR_METRIC, "relative error undefined for a zero tensor");
-    return 1.0;
+    *x_sq = ctx->read1(xsq.p);
+    *cross = 0.0;
+    return;
   }
   Buf<double> Rd(ctx, (size_t)dim * K), Q(ctx, (size_t)dim * K);
   Rd.zero();
@@ -114,12 +122,9 @@ double relative_error(Ctx* ctx, const Fibers& fb, const Basis& B) {
   Buf<double> cp(ctx, nwarps);
   LAUNCH(ctx, k_cd, cgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, Rd.p, Q.p, K, cp.p);
   LAUNCH(ctx, k_reduce, 1, 1024, 0, cp.p, nwarps, cd.p);
-  double hx = 0, hcd = 0;
-  ctx->to_host(&hx, xsq.p, 1);
-  ctx->to_host(&hcd, cd.p, 1);
+  ctx->to_host(x_sq, xsq.p, 1);
+  ctx->to_host(cross, cd.p, 1);
   ctx->sync();
-  if (hx == 0.0) fail(CTD_ERR_METRIC, "relative error undefined for a zero tensor");
-  return (hx - hcd) / hx;
 }
 
 }  // namespace ctdgpu

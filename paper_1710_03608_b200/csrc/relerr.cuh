@@ -8,4 +8,9 @@ namespace ctdgpu {
 // factors (R, U) with C = R^T X implied.
 double relative_error(Ctx* ctx, const Fibers& fb, const Basis& B);
 
+// The two sums relative_error combines, over the fibers of fb (one shard of
+// X in the sharded path): |X|^2 and sum_j x_j^T (R U R^T) x_j, so
+// rel = (|X|^2 - cross) / |X|^2 after summing the shards' partials.
+void error_partials(Ctx* ctx, const Fibers& fb, const Basis& B, double* x_sq, double* cross);
+
 }  // namespace ctdgpu

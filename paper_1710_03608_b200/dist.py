@@ -1,0 +1,333 @@
+"""Sharded CTD-S across ranks: one process per GPU, nonzeros
+partitioned by contiguous fiber-id range.
+
+Per rank (reference functions in parentheses):
+  1. bucket the local shard and compute its fibers' exact squared norms
+     (matricize + column_sq_norms, tensor_ops.cpp:118-135,194-202);
+  2. all-gather the fibers' global column ids and norms; because the shards are
+     contiguous ascending fiber ranges the concatenation is the global fiber
+     list in column order, so every rank computes the identical bit-exact law,
+     draws and dedup (column_distribution / sample_with_replacement /
+     unique_first_occurrence, sampling.cpp:21-78);
+  3. the owner of each unique candidate contributes its fiber; an all-gather
+     assembles every candidate in draw order on every rank;
+  4. the filter and U recurrence run replicated (deterministic: identical
+     decisions and bits on every rank, FiberBasis::try_append_fiber,
+     fiber_basis.cpp:43-109);
+  5. the relative error's two sums are computed on each shard and all-reduced
+     (relative_error, evaluation.cpp:88-122; the scalar is only checked to
+     1e-9, so the reduction order does not matter).
+
+Collectives go through torch.distributed (NCCL over NVLink on GPUs, gloo on
+CPU tests).  The per-rank compute is a `kernels` object: `GpuKernels` (the
+C-ABI library, the only product implementation) by default.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import ctd as api
+
+
+# ---------------------------------------------------------------------------
+# fiber ids and range partitions
+
+def fiber_strides(shape, mode):
+    """fiber_strides (tensor_ops.cpp:106-116): the non-mode extents, first fastest."""
+    strides = []
+    s = 1
+    for k, n in enumerate(shape):
+        if k == mode:
+            strides.append(0)
+        else:
+            strides.append(s)
+            s *= int(n)
+    return np.asarray(strides, dtype=np.int64), s
+
+
+def fiber_ids(shape, mode, idx: np.ndarray) -> np.ndarray:
+    st, _ = fiber_strides(shape, mode)
+    return (np.asarray(idx, dtype=np.int64) * st[None, :]).sum(axis=1)
+
+
+def fiber_range_bounds(shape, mode, idx: np.ndarray, world: int) -> np.ndarray:
+    """Contiguous fiber-id ranges [b[r], b[r+1]) balanced by nnz (world+1 bounds)."""
+    _, n_cols = fiber_strides(shape, mode)
+    j = np.sort(fiber_ids(shape, mode, idx))
+    b = [0]
+    for r in range(1, world):
+        q = j[min(len(j) - 1, (len(j) * r) // world)] if len(j) else 0
+        b.append(max(b[-1], int(q)))
+    b.append(n_cols)
+    return np.asarray(b, dtype=np.int64)
+
+
+def shard(x_shape, idx: np.ndarray, val: np.ndarray, mode: int, bounds: np.ndarray, rank: int):
+    """The entries of the global tensor whose fiber id lies in rank's range
+    (still in the global index space, so fiber ids stay global)."""
+    j = fiber_ids(x_shape, mode, idx)
+    sel = (j >= bounds[rank]) & (j < bounds[rank + 1])
+    return idx[sel], val[sel]
+
+
+# ---------------------------------------------------------------------------
+# collectives (torch.distributed)
+
+class Comm:
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        backend = dist.get_backend(group)
+        self.device = (torch.device("cuda", torch.cuda.current_device())
+                       if backend == "nccl" else torch.device("cpu"))
+
+    def _t(self, a: np.ndarray):
+        return self.torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
+
+    def allgather(self, a: np.ndarray) -> list:
+        """Variable-length all-gather of a 1-D array; returns every rank's array."""
+        n = self._t(np.array([a.shape[0]], dtype=np.int64))
+        ns = [self.torch.zeros_like(n) for _ in range(self.world)]
+        self.dist.all_gather(ns, n, group=self.group)
+        ns = [int(t.item()) for t in ns]
+        m = max(ns) if ns else 0
+        buf = np.zeros(max(m, 1), dtype=a.dtype)
+        buf[:a.shape[0]] = a
+        t = self._t(buf)
+        outs = [self.torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(outs, t, group=self.group)
+        return [o.cpu().numpy()[:k] for o, k in zip(outs, ns)]
+
+    def allreduce_sum(self, a: np.ndarray) -> np.ndarray:
+        t = self._t(a)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return t.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# per-rank kernels (the C-ABI library)
+
+@dataclass
+class LocalFibers:
+    """Compressed CSC of the local shard's nonempty fibers (global column ids)."""
+    col: np.ndarray
+    ptr: np.ndarray
+    row: np.ndarray
+    val: np.ndarray
+    norm: np.ndarray
+
+
+class GpuKernels:
+    """Per-rank compute through libctd_gpu (no CPU fallback)."""
+
+    def __init__(self, ctx: Optional[api.Context] = None):
+        self.ctx = ctx or api.default_context()
+        self.L = self.ctx.L
+
+    def shard(self, x, mode):
+        """Bucket this rank's entries once (x: DeviceTensor, or (shape, idx, val) host
+        arrays in the global index space); the fibers stay resident in HBM."""
+        if not isinstance(x, api.DeviceTensor):
+            shape, idx, val = x
+            x = api.DeviceTensor(api.SparseTensor(list(shape), idx, val), self.ctx)
+        return _GpuShard(self, x, mode)
+
+    def sample_fibers(self, col, norm, s, seed):
+        col = np.ascontiguousarray(col, dtype=np.int64)
+        norm = np.ascontiguousarray(norm, dtype=np.float64)
+        out = np.zeros(s, dtype=np.int64)
+        nu = C.c_int64()
+        tot = C.c_double()
+        api._check(self.L.ctd_gpu_sample_fibers(self.ctx.h, col.shape[0], api._p(col), api._p(norm), s,
+                                                C.c_uint64(seed), C.byref(tot), api._p(out), C.byref(nu)))
+        return tot.value, out[:nu.value].copy()
+
+    def basis(self, dim):
+        return _GpuBasis(self, dim)
+
+
+class _GpuShard:
+    def __init__(self, k: GpuKernels, x: "api.DeviceTensor", mode: int):
+        self.k, self.x = k, x
+        h = C.c_void_p()
+        api._check(k.L.ctd_gpu_shard_create(k.ctx.h, x.h, mode, C.byref(h)))
+        self.h = h
+        F = int(k.L.ctd_gpu_shard_n_fibers(h))
+        self.col = np.zeros(max(F, 1), np.int64)
+        self.norm = np.zeros(max(F, 1))
+        api._check(k.L.ctd_gpu_shard_fibers(h, api._p(self.col), api._p(self.norm)))
+        self.col, self.norm = self.col[:F], self.norm[:F]
+
+    def gather(self, cols):
+        cols = np.ascontiguousarray(cols, np.int64)
+        n = cols.shape[0]
+        ptr = np.zeros(n + 1, np.int64)
+        api._check(self.k.L.ctd_gpu_shard_gather(self.h, n, api._p(cols), api._p(ptr), None, None))
+        rows = np.zeros(max(int(ptr[-1]), 1), np.int64)
+        vals = np.zeros(max(int(ptr[-1]), 1))
+        api._check(self.k.L.ctd_gpu_shard_gather(self.h, n, api._p(cols), api._p(ptr), api._p(rows), api._p(vals)))
+        return ptr, rows[:ptr[-1]], vals[:ptr[-1]]
+
+    def error_partials(self, basis):
+        xs, cr = C.c_double(), C.c_double()
+        api._check(self.k.L.ctd_gpu_shard_error_partials(self.h, basis.h, C.byref(xs), C.byref(cr)))
+        return xs.value, cr.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.k.L.ctd_gpu_shard_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _GpuBasis:
+    def __init__(self, k: GpuKernels, dim: int):
+        self.k, self.dim = k, dim
+        h = C.c_void_p()
+        api._check(k.L.ctd_gpu_basis_create(k.ctx.h, dim, C.byref(h)))
+        self.h = h
+
+    def append_batch(self, ptr, rows, vals, eps):
+        n = ptr.shape[0] - 1
+        acc = np.zeros(max(n, 1), np.int32)
+        deg = np.zeros(max(n, 1), np.int32)
+        dl = np.zeros(max(n, 1))
+        ptr = np.ascontiguousarray(ptr, np.int64)
+        rows = np.ascontiguousarray(rows, np.int64)
+        vals = np.ascontiguousarray(vals, np.float64)
+        api._check(self.k.L.ctd_gpu_basis_append_batch(self.h, n, api._p(ptr), api._p(rows), api._p(vals), eps,
+                                                       api._p(acc), api._p(deg), api._p(dl)))
+        return acc[:n], deg[:n], dl[:n]
+
+    def size(self):
+        return int(self.k.L.ctd_gpu_basis_size(self.h))
+
+    def u(self):
+        K = self.size()
+        u = np.zeros(K * K)
+        if K:
+            api._check(self.k.L.ctd_gpu_basis_u(self.h, api._p(u)))
+        return u.reshape(K, K)
+
+    def r(self):
+        K = self.size()
+        nnz = int(self.k.L.ctd_gpu_basis_r_nnz(self.h))
+        cp = np.zeros(K + 1, np.int64)
+        rows = np.zeros(max(nnz, 1), np.int64)
+        vals = np.zeros(max(nnz, 1))
+        api._check(self.k.L.ctd_gpu_basis_r(self.h, api._p(cp), api._p(rows), api._p(vals)))
+        return cp, rows[:nnz], vals[:nnz]
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.k.L.ctd_gpu_basis_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# the sharded front end
+
+@dataclass
+class ShardedResult:
+    kept_flat: np.ndarray
+    U: np.ndarray
+    R_col_ptr: np.ndarray
+    R_row: np.ndarray
+    R_val: np.ndarray
+    unique: np.ndarray
+    accepted: np.ndarray
+    degenerate: np.ndarray
+    delta: np.ndarray
+    total_sq_norm: float
+    relative_error: Optional[float] = None
+    n_fibers: int = 0
+    stats: dict = field(default_factory=dict)
+
+
+def ctd_s_sharded(shape, local, mode: int, sample_size: int, epsilon: float = 1e-6, seed: int = 42,
+                  comm: Optional[Comm] = None, kernels=None, with_error: bool = False) -> ShardedResult:
+    """CTD-S front end over fiber-range shards; every rank returns the same
+    (replicated) kept ids, U and R.  `local` is this rank's part of X in the
+    GLOBAL index space (see `shard`): a DeviceTensor or (idx, val) host arrays.
+    Mirrors ctd_s (ctd_static.cpp:19-50) without compute_core."""
+    comm = comm or Comm()
+    k = kernels or GpuKernels()
+    if sample_size < 1:
+        raise api.ArgumentError("sample size must be at least 1")
+    if not (epsilon > 0.0):
+        raise api.ArgumentError("epsilon must be positive")
+    # 1. local bucketing + exact norms (resident)
+    sh = k.shard(local if isinstance(local, api.DeviceTensor) else (shape, local[0], local[1]), mode)
+    # 2. global fiber list (ranks own ascending ranges) -> replicated law/draws/dedup
+    gcol = np.concatenate(comm.allgather(sh.col.astype(np.int64)))
+    gnorm = np.concatenate(comm.allgather(sh.norm.astype(np.float64)))
+    if gcol.shape[0] > 1 and not np.all(gcol[1:] > gcol[:-1]):
+        raise api.ArgumentError("shards must hold disjoint ascending fiber ranges in rank order")
+    total, unique = k.sample_fibers(gcol, gnorm, sample_size, seed)
+    # 3. candidate payloads from their owners, assembled in draw order
+    pos = np.searchsorted(sh.col, unique)
+    ok = pos < sh.col.shape[0]
+    mine = np.zeros(unique.shape[0], bool)
+    mine[ok] = sh.col[pos[ok]] == unique[ok]
+    which = np.nonzero(mine)[0].astype(np.int64)
+    lptr, lrows, lvals = sh.gather(unique[which])
+    g_which = comm.allgather(which)
+    g_lens = comm.allgather(np.diff(lptr).astype(np.int64))
+    g_rows = comm.allgather(lrows.astype(np.int64))
+    g_vals = comm.allgather(lvals.astype(np.float64))
+    n_u = unique.shape[0]
+    owner = np.full(n_u, -1, np.int64)
+    cand_len = np.zeros(n_u, np.int64)
+    for r, (w, ln) in enumerate(zip(g_which, g_lens)):
+        owner[w] = r
+        cand_len[w] = ln
+    if n_u and owner.min() < 0:
+        raise api.CtdError("a drawn fiber has no owner (shards do not cover the fiber space)")
+    cptr = np.concatenate([[0], np.cumsum(cand_len)]).astype(np.int64)
+    crow = np.zeros(int(cptr[-1]), np.int64)
+    cval = np.zeros(int(cptr[-1]))
+    for w, ln, rr, vv in zip(g_which, g_lens, g_rows, g_vals):
+        if w.size == 0:
+            continue
+        src = np.concatenate([[0], np.cumsum(ln)])
+        # scatter each owned candidate's entries to its slot in draw order
+        dst_idx = np.concatenate([np.arange(cptr[c], cptr[c + 1]) for c in w])
+        crow[dst_idx] = rr[:src[-1]]
+        cval[dst_idx] = vv[:src[-1]]
+    # 4. replicated filter + U recurrence
+    dim = int(shape[mode])
+    B = k.basis(dim)
+    acc, deg, dl = B.append_batch(cptr, crow, cval, epsilon)
+    kept = unique[np.nonzero(acc)[0]]
+    U = B.u()
+    rp, rr, rv = B.r()
+    res = ShardedResult(kept, U, rp, rr, rv, unique, acc, deg, dl, float(total), None, int(gcol.shape[0]),
+                        {"local_fibers": int(sh.col.shape[0]), "candidate_nnz": int(cptr[-1])})
+    # 5. error partials, all-reduced
+    if with_error:
+        xs, cr = sh.error_partials(B)
+        s = comm.allreduce_sum(np.array([xs, cr], dtype=np.float64))
+        if s[0] == 0.0:
+            raise api.MetricError("relative error undefined for a zero tensor")
+        res.relative_error = 1.0 if U.shape[0] == 0 else float((s[0] - s[1]) / s[0])
+    B.close()
+    sh.close()
+    return res

@@ -1,0 +1,104 @@
+"""Test-only per-rank kernels for paper_1710_03608_b200.dist built on the CPU
+oracle (oracle/ctd_oracle.c via oracle.bindings.Port), so the sharded host
+logic and its collectives can run in gloo world_size>1 tests without a GPU.
+Never used by the product path (GpuKernels is the only product backend).
+"""
+import numpy as np
+
+from paper_1710_03608_b200.dist import LocalFibers
+
+
+class OracleKernels:
+    def __init__(self, port):
+        self.P = port
+
+    def shard(self, x, mode):
+        shape, idx, val = x
+        return _OracleShard(self.P, shape, idx, val, mode)
+
+    def sample_fibers(self, col, norm, s, seed):
+        # column_distribution (sampling.cpp:21-31): sequential total, p = n / T
+        total = 0.0
+        for v in norm:
+            total += float(v)
+        probs = np.asarray(norm, dtype=np.float64) / total
+        drawn = self.P.sample_with_replacement(probs, s, seed)
+        uniq = self.P.unique_first_occurrence(drawn)
+        return total, np.asarray(col, dtype=np.int64)[uniq]
+
+    def basis(self, dim):
+        return _OracleBasis(self.P.basis(dim))
+
+
+class _OracleShard:
+    def __init__(self, P, shape, idx, val, mode):
+        m = P.matricize(shape, np.asarray(idx).reshape(-1), val, mode)
+        counts = np.diff(m.col_ptr)
+        cols = np.nonzero(counts > 0)[0].astype(np.int64)
+        sel = np.concatenate([np.arange(m.col_ptr[c], m.col_ptr[c + 1]) for c in cols]) if cols.size else \
+            np.zeros(0, np.int64)
+        self.lf = LocalFibers(cols, np.concatenate([[0], np.cumsum(counts[cols])]).astype(np.int64),
+                              m.row[sel].astype(np.int64), m.val[sel], P.column_sq_norms(m)[cols])
+        self.col, self.norm = self.lf.col, self.lf.norm
+
+    def gather(self, cols):
+        lf = self.lf
+        f = np.searchsorted(lf.col, cols)
+        ptr = np.concatenate([[0], np.cumsum(lf.ptr[f + 1] - lf.ptr[f])]).astype(np.int64)
+        rows = np.concatenate([lf.row[lf.ptr[a]:lf.ptr[a + 1]] for a in f]) if f.size else np.zeros(0, np.int64)
+        vals = np.concatenate([lf.val[lf.ptr[a]:lf.ptr[a + 1]] for a in f]) if f.size else np.zeros(0)
+        return ptr, rows, vals
+
+    def error_partials(self, basis):
+        lf = self.lf
+        xs = float(np.sum(lf.val * lf.val))
+        K = basis.size()
+        if K == 0:
+            return xs, 0.0
+        cp, rr, rv = basis.r()
+        Rd = np.zeros((basis.b.dim, K))
+        for k in range(K):
+            Rd[rr[cp[k]:cp[k + 1]], k] = rv[cp[k]:cp[k + 1]]
+        U = basis.u()
+        cross = 0.0
+        for f in range(lf.col.shape[0]):
+            g = Rd[lf.row[lf.ptr[f]:lf.ptr[f + 1]]].T @ lf.val[lf.ptr[f]:lf.ptr[f + 1]]
+            cross += float(g @ (U @ g))
+        return xs, cross
+
+    def close(self):
+        pass
+
+
+class _OracleBasis:
+    def __init__(self, b):
+        self.b = b
+        self.cols = []
+
+    def append_batch(self, ptr, rows, vals, eps):
+        n = ptr.shape[0] - 1
+        acc = np.zeros(n, np.int32)
+        deg = np.zeros(n, np.int32)
+        dl = np.zeros(n)
+        for k in range(n):
+            r, v = rows[ptr[k]:ptr[k + 1]], vals[ptr[k]:ptr[k + 1]]
+            a, d, delta, _ = self.b.try_append(r, v, eps)
+            acc[k], deg[k], dl[k] = a, d, delta
+            if a:
+                self.cols.append((r.copy(), v.copy()))
+        return acc, deg, dl
+
+    def size(self):
+        return self.b.size()
+
+    def u(self):
+        return self.b.U()
+
+    def r(self):
+        cp = np.concatenate([[0], np.cumsum([c[0].shape[0] for c in self.cols])]).astype(np.int64)
+        rows = np.concatenate([c[0] for c in self.cols]) if self.cols else np.zeros(0, np.int64)
+        vals = np.concatenate([c[1] for c in self.cols]) if self.cols else np.zeros(0)
+        return cp, rows, vals
+
+    def close(self):
+        pass

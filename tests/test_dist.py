@@ -1,0 +1,132 @@
+"""Sharded CTD-S (paper_1710_03608_b200.dist) with world_size 2.
+
+CPU: two gloo ranks run the sharded host logic (fiber-range shards, all-gather
+of fiber norms and candidate payloads, replicated filter, all-reduced error
+partials) with oracle-backed per-rank kernels; the replicated result must equal
+the single-process oracle bit for bit (kept ids, decisions, U) and the error
+within 1e-9.  GPU: the same with the C-ABI kernels (two ranks on one device,
+host-side gloo collectives) against the single-process GPU ctd_s.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_1710_03608_b200 import datagen, dist
+
+CASES = {
+    "c1": lambda: datagen.c1(),
+    "cp": lambda: datagen.low_rank([30, 25, 12], 3, 0.3, 11) if hasattr(datagen, "low_rank") else datagen.c1(),
+    "traffic": lambda: datagen.traffic([80, 80, 30], 6000, 5),
+}
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, case, mode, s, backend, out):
+    import torch.distributed as tdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x = CASES[case]()
+        bounds = dist.fiber_range_bounds(x.shape, mode, x.idx, world)
+        il, vl = dist.shard(x.shape, x.idx, x.val, mode, bounds, rank)
+        if backend == "oracle":
+            from oracle.bindings import Port
+            from dist_oracle_kernels import OracleKernels
+            k = OracleKernels(Port())
+        else:
+            k = dist.GpuKernels()
+        r = dist.ctd_s_sharded(x.shape, (il, vl), mode, s, 1e-6, 42, comm=dist.Comm(), kernels=k,
+                               with_error=True)
+        np.savez(os.path.join(out, f"r{rank}.npz"), kept=r.kept_flat, U=r.U, acc=r.accepted, deg=r.degenerate,
+                 delta=r.delta, unique=r.unique, rel=r.relative_error, total=r.total_sq_norm,
+                 cp=r.R_col_ptr, rr=r.R_row, rv=r.R_val)
+    finally:
+        tdist.destroy_process_group()
+
+
+def _run(case, mode, s, backend, tmp_path, world=2):
+    import torch.multiprocessing as mp
+    mp.spawn(_worker, args=(world, _free_port(), case, mode, s, backend, str(tmp_path)), nprocs=world, join=True)
+    return [dict(np.load(tmp_path / f"r{r}.npz")) for r in range(world)]
+
+
+def test_fiber_ids_match_matricize_order(port):
+    x = datagen.c1()
+    for mode in range(3):
+        m = port.matricize(x.shape, x.idx.reshape(-1), x.val, mode)
+        j = dist.fiber_ids(x.shape, mode, x.idx)
+        cols = np.nonzero(np.diff(m.col_ptr) > 0)[0]
+        assert np.array_equal(np.unique(j), cols)
+
+
+def test_bounds_partition_everything():
+    x = datagen.traffic([80, 80, 30], 6000, 5)
+    for world in (1, 2, 3, 8):
+        b = dist.fiber_range_bounds(x.shape, 0, x.idx, world)
+        assert b[0] == 0 and b[-1] == 80 * 30 and np.all(np.diff(b) >= 0)
+        n = sum(dist.shard(x.shape, x.idx, x.val, 0, b, r)[1].shape[0] for r in range(world))
+        assert n == x.nnz
+
+
+@pytest.mark.parametrize("case,mode,s", [("c1", 0, 200), ("c1", 2, 150), ("traffic", 0, 300), ("cp", 1, 120)])
+def test_sharded_equals_single_process_oracle(case, mode, s, port, tmp_path):
+    res = _run(case, mode, s, "oracle", tmp_path)
+    x = CASES[case]()
+    fe = port.frontend(x.shape, x.idx.reshape(-1), x.val, mode, s, 1e-6, 42)
+    for r in res:  # every rank holds the same replicated result
+        assert np.array_equal(r["unique"], fe.unique)
+        assert np.array_equal(r["acc"], fe.accepted)
+        assert np.array_equal(r["deg"], fe.degenerate)
+        assert np.array_equal(r["delta"].view(np.int64), fe.delta.view(np.int64))
+        assert np.array_equal(r["kept"], fe.kept_flat)
+        assert np.array_equal(r["U"].view(np.int64), fe.U.view(np.int64))
+        assert np.array_equal(r["cp"], fe.R.col_ptr) and np.array_equal(r["rr"], fe.R.row)
+        assert r["total"] == fe.total
+    # the error partials combine to the single-process value of the same formula
+    # (|X|^2 - sum_j x_j^T R U R^T x_j) / |X|^2 ...
+    want = _gram_identity_error(port, x, mode, fe.R, fe.U)
+    for r in res:
+        assert abs(float(r["rel"]) - want) <= 1e-9 * max(1.0, abs(want))
+    # ... which is the reference's relative_error when U is well conditioned
+    fe2, core, rel = port.ctd_s_error(x.shape, x.idx.reshape(-1), x.val, mode, s, 1e-6, 42)
+    if 0.0 <= rel <= 1.0:
+        assert abs(want - rel) <= 1e-9 * max(1.0, abs(rel))
+
+
+def _gram_identity_error(port, x, mode, R, U):
+    m = port.matricize(x.shape, x.idx.reshape(-1), x.val, mode)
+    K = U.shape[0]
+    Rd = np.zeros((m.rows, K))
+    for k in range(K):
+        Rd[R.row[R.col_ptr[k]:R.col_ptr[k + 1]], k] = R.val[R.col_ptr[k]:R.col_ptr[k + 1]]
+    xs = float(np.sum(m.val * m.val))
+    cross = 0.0
+    for c in range(m.cols):
+        a, b = m.col_ptr[c], m.col_ptr[c + 1]
+        if b > a:
+            g = Rd[m.row[a:b]].T @ m.val[a:b]
+            cross += float(g @ (U @ g))
+    return 1.0 if K == 0 else (xs - cross) / xs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,mode,s", [("c1", 0, 200), ("traffic", 0, 300)])
+def test_sharded_gpu_two_ranks_equal_single_gpu(case, mode, s, tmp_path):
+    from paper_1710_03608_b200 import ctd
+    res = _run(case, mode, s, "gpu", tmp_path)
+    x = CASES[case]()
+    f = ctd.ctd_s(ctd.SparseTensor.from_datagen(x), mode, s, 1e-6, 42, with_error=True)
+    for r in res:
+        assert np.array_equal(r["kept"], f.kept_flat)
+        assert np.array_equal(r["U"].view(np.int64), f.U.view(np.int64))
+        assert abs(float(r["rel"]) - f.relative_error) <= 1e-9 * max(1.0, abs(f.relative_error))
