@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
   bool prev_acc = false;
   double prev_delta = 0.0;
   int prev_n = -1;
+  bool pre = false;  // candidate n's setup (tags, z half, g and y staging) done during P3 of n-1
   for (int n = 0; n <= nu; ++n) {
     const bool last = (n == nu);
     if (!last) stamp(a.trace, n, 0);
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
       tg = a.tag_base + (uint32_t)n + 1u;
       // x's rows: tag them, start z at 0 (rows outside R stay untouched).
       // zd is double-buffered by parity: CTAs still in P3 of n-1 read the other half.
-      for (long long t = gtid; t < m; t += gthreads) {
+      for (long long t = gtid; !pre && t < m; t += gthreads) {
         a.tag[a.c.row[off + t]] = tg;
         zdn[a.c.row[off + t]] = 0.0;
       }
@@ -295,7 +296,16 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         }
         __syncthreads();
       };
-      if (one_chunk) stage(0, Kn);
+      if (one_chunk && pre) {
+        // g (j < Ko) and y_{n-1} were staged during P3 of n-1; add x_{n-1}'s column
+        if (upd && threadIdx.x == 0) {
+          vA[Ko] = a.Gc[(long long)prev_n * nu + n];
+          vB[Ko] = 0.0;
+        }
+        __syncthreads();
+      } else if (one_chunk) {
+        stage(0, Kn);
+      }
       if (!last) stamp(a.trace, n, 2);
       // U_new[i][j] (fiber_basis.cpp:97-105): fl(U + fl(fl(y_i y_j)/d)), the
       // new column/row -y/d and the corner 1/d.  The division uses the
@@ -752,8 +762,13 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     // other warps wait at the CTA barrier
     stamp(a.trace, n, 7);
     stamp(a.trace, n, 12);
+    // the other warps set up candidate n+1 meanwhile (independent of n's
+    // decision): tag its rows, zero its z half, stage g_{n+1} over the current
+    // K columns and y_n.  Not when the slow touch-order path is active (it
+    // reads the tags of n) or the vectors do not fit one staging chunk.
+    const bool prestage = !slow && n + 1 < nu && K + 1 <= kVec;
     if ((threadIdx.x >> 5) == 0) {
-      SliceDirect* sd = reinterpret_cast<SliceDirect*>(dyn);
+      SliceDirect* sd = reinterpret_cast<SliceDirect*>(dyn + 2 * kVec);  // ring area, idle in P3
       const double r = warp_grid_sum(get, nt, tg, a.sloc, a.ssum, a.sdir, a.sflag, WS, sd,
                                      reinterpret_cast<int*>(sd + kMaxDirectsTotal), &bad,
                                      a.trace ? a.trace + (long long)n * kTraceW + 16 : nullptr);
@@ -761,8 +776,26 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         s_res = r;
         s_bad = bad;
       }
+    } else if (prestage) {
+      const int n1 = n + 1;
+      const long long tw = (long long)nb * (blockDim.x - 32);
+      const long long off1 = a.c.off[n1];
+      const int m1 = a.c.len[n1];
+      const uint32_t tg1 = a.tag_base + (uint32_t)n1 + 1u;
+      double* zd1 = a.zd + (n1 & 1) * (a.dim + 1);
+      for (long long t = (long long)blockIdx.x * (blockDim.x - 32) + threadIdx.x - 32; t < m1; t += tw) {
+        const int r = a.c.row[off1 + t];
+        a.tag[r] = tg1;
+        zd1[r] = 0.0;
+      }
+      for (int j = threadIdx.x - 32; j < K; j += blockDim.x - 32) {
+        vA[j] = (j < a.K0) ? a.Gb[(long long)j * nu + n1]
+                           : a.Gc[(long long)ldg_cg(&a.kept_cand[j - a.K0]) * nu + n1];
+        vB[j] = ldg_cg(&ycur[j]);
+      }
     }
     __syncthreads();
+    pre = prestage;
     const double res = s_res;
     bad = s_bad != 0;
     stamp(a.trace, n, 8);
