@@ -553,17 +553,29 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
           double vv[kRowSlots];
           unsigned okm = 0;    // rows with an entry at this step (prefetched chunk)
           unsigned found = 0;  // rows whose first y != 0 entry is known (warp-uniform)
+          // per row slot of the group being loaded: its length (base read only when needed)
+          int slen[kRowSlots];
+          int lg = -1;
           auto load = [&](int g, int ch) {
             const int nr = min(32, ns - 32 * g);
+            if (g != lg) {
+              lg = g;
+#pragma unroll
+              for (int k = 0; k < kRowSlots; ++k)
+                slen[k] = (rq + kRowPh * k < nr) ? s_len[32 * g + min(rq + kRowPh * k, 31)] : 0;
+            }
             const int te = ch * kRingW + t;
             okm = 0;
 #pragma unroll
             for (int k = 0; k < kRowSlots; ++k) {
-              const int r = rq + kRowPh * k;
-              const bool ok = r < nr && te < s_len[32 * g + min(r, 31)];
-              const long long idx = ok ? s_base[32 * g + r] + te : 0;
-              kv[k] = ok ? ldg_cg(&a.rek[idx]) : 0;
-              vv[k] = ok ? ldg_cg(&a.rev[idx]) : 0.0;
+              const bool ok = te < slen[k];
+              kv[k] = 0;
+              vv[k] = 0.0;
+              if (ok) {
+                const long long idx = s_base[32 * g + rq + kRowPh * k] + te;
+                kv[k] = ldg_cg(&a.rek[idx]);
+                vv[k] = ldg_cg(&a.rev[idx]);
+              }
               okm |= (unsigned)ok << k;
             }
           };
