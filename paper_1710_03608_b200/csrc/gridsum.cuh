@@ -402,7 +402,7 @@ __device__ double warp_grid_sum(const Get& get, long long nt, unsigned epoch, Sl
     ee[k] = 0;
     mm[k] = mono_id();
     cls[k] = CLS_ZERO;
-    if (k < nc) cls[k] = seq_classify(b0 + k == 0, Pv[k], Pv[k + 1], xv[k], mg, &ee[k], &mm[k]);
+    if (k < nc) cls[k] = seq_classify_bf(b0 + k == 0, Pv[k], Pv[k + 1], xv[k], mg, &ee[k], &mm[k]);
   }
   Seg agg{0, mono_id()};
   int nd = 0;

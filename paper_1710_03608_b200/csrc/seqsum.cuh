@@ -107,6 +107,41 @@ __device__ __forceinline__ int seq_classify(bool first, double Pp, double Pc, do
   return CLS_REG;
 }
 
+// Branch-free seq_mono / seq_classify (same results): straight-line selects so
+// the classifications of several terms interleave (block_exact_sum_ilp).
+__device__ __forceinline__ Mono seq_mono_bf(double x, int ec) {
+  const long long bits = __double_as_longlong(x);
+  const int bexp = (int)((bits >> 52) & 0x7FF);
+  const long long mx = (bits & 0xFFFFFFFFFFFFFLL) | (bexp != 0 ? (1LL << 52) : 0LL);
+  const int ex = bexp != 0 ? bexp - 1023 : -1022;
+  const int d = ec - ex;
+  const int dl = min(max(-d, 0), 62);     // left shift when d <= 0
+  const int dr = min(max(d, 1), 55);      // right shift when 0 < d <= 55
+  const bool mid = (d > 0) & (d <= 55);
+  const long long k0 = (d <= 0) ? (mx << dl) : (mid ? (mx >> dr) : 0LL);
+  const long long rem = mid ? (mx & ((1LL << dr) - 1)) : 0LL;
+  const long long half = mid ? (1LL << (dr - 1)) : 1LL;
+  const bool tie = rem == half;
+  const long long up = rem > half ? 1LL : 0LL;
+  Mono m;
+  m.a0 = tie ? k0 + (k0 & 1) : k0 + up;
+  m.a1 = tie ? k0 + ((k0 + 1) & 1) : k0 + up;
+  return m;
+}
+
+__device__ __forceinline__ int seq_classify_bf(bool first, double Pp, double Pc, double x, double mg, int* e_out,
+                                               Mono* m_out) {
+  const int ep = dexp(Pp), ec = dexp(Pc);
+  bool direct = first | !(Pp > 0.0) | !(Pc > 0.0) | !(x < 1.7976931348623157e308) | (ep != ec) | (ec < -960) |
+                (ec > 1020);
+  const double lo = pow2(min(max(ec, -1020), 1020));
+  direct |= ((Pp - lo) <= mg * Pp) | ((2.0 * lo - Pp) <= mg * Pp) | ((Pc - lo) <= mg * Pc) |
+            ((2.0 * lo - Pc) <= mg * Pc);
+  *m_out = seq_mono_bf(x, min(max(ec, -1022), 1023));
+  *e_out = ec;
+  return (Pc == 0.0) ? CLS_ZERO : (direct ? CLS_DIRECT : CLS_REG);
+}
+
 // A whole chunk is regular in binade *e when the approximate prefix before it
 // (pre) and after it (post) both lie strictly inside [2^e, 2^(e+1)) with the
 // error margin to spare: the running sum is monotone, so every intermediate
@@ -333,6 +368,238 @@ __device__ double block_exact_sum(const Get& get, long long n, SeqSumSmem& S, bo
   __syncthreads();
   SEQ_STAMP(6)
 #undef SEQ_STAMP
+  const double r = S.result;
+  if (fail) *fail = S.bad != 0;
+  __syncthreads();
+  return r;
+}
+
+// --------------------------------------------------------------------------
+// block_exact_sum with the per-thread work restructured for instruction-level
+// parallelism: each thread's chunk (cached in registers, kCache terms) is
+// classified kGroup terms at a time with their approximate prefixes computed
+// first.  Evaluated for the filter's residual (every CTA summing all terms
+// redundantly, no cross-CTA exchange) and measured slower than the
+// distributed warp_grid_sum (gridsum.cuh): the slowest chunk still costs ~1k
+// cycles per term (tools/ubench_p3.cu keeps the comparison).  `get` provides
+// operator()(i), batch(b0, b1, out[N]) and strided(i0, step, n, out[N]).
+template <int kCache, int kGroup, typename Get, typename Overlap>
+__device__ double block_exact_sum_ilp(const Get& get, long long n, SeqSumSmem& S, bool* fail,
+                                      const Overlap& overlap, double* tbuf = nullptr, long long* tp = nullptr) {
+#define BES_STAMP(k) \
+  if (tp && threadIdx.x == 0) tp[k] = clock64();
+  BES_STAMP(0)
+  const int T = blockDim.x, t = threadIdx.x;
+  if (n <= 0) {
+    if (t >= 32) overlap();
+    __syncthreads();
+    if (fail) *fail = false;
+    return 0.0;
+  }
+  const long long per = (n + T - 1) / T;
+  const long long b0 = min((long long)t * per, n), b1 = min(b0 + per, n);
+  double xv[kCache];
+  if (tbuf && per <= kCache) {
+    // coalesced: lane l loads the warp's elements l, l+32, ... then the warp
+    // transposes them through shared memory into contiguous per-thread chunks
+    // (row stride kCache+1: conflict-free)
+    const int w = t >> 5, l = t & 31;
+    double* wb = tbuf + w * 32 * (kCache + 1);
+    const long long wb0 = min((long long)w * 32 * per, n);
+    double lv[kCache];
+    get.strided(wb0 + l, 32, n, lv);
+    const unsigned p = (unsigned)per, inv = 65536u / p + 1u;  // e / p for e < 32 kCache
+#pragma unroll
+    for (int k = 0; k < kCache; ++k) {
+      if (k < (int)p) {
+        const unsigned e = (unsigned)(k * 32 + l), row = (e * inv) >> 16, col = e - row * p;
+        wb[row * (kCache + 1) + col] = lv[k];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kCache; ++k) xv[k] = (b0 + k < b1) ? wb[l * (kCache + 1) + k] : 0.0;
+  } else {
+    get.batch(b0, b1, xv);
+  }
+  double cs = 0.0;
+#pragma unroll
+  for (int k = 0; k < kCache; ++k) cs += xv[k];
+  for (long long i = b0 + kCache; i < b1; ++i) cs += get(i);
+  BES_STAMP(1)
+  const double pre = block_excl_sum<double>(cs, S.dsh, nullptr);
+  BES_STAMP(2)
+  const double mg = seq_margin(n);
+  const int nc = (int)min((long long)kCache, b1 - b0);
+  // classify cached terms group by group; `step` folds one classified term
+  Seg agg{0, mono_id()};
+  int nd = 0;
+  short le = E_ZERO;
+  auto fold = [&](int c, int e, const Mono& m) {
+    if (c == CLS_REG) {
+      agg.m = mono_cat(agg.m, m);
+      le = (short)e;
+    } else {
+      agg.h = 1;
+      agg.m = mono_id();
+      if (c == CLS_DIRECT) ++nd;
+      le = (c == CLS_DIRECT) ? E_DIRECT : E_ZERO;
+    }
+  };
+  int fe = 0;
+  const bool fast = (b0 > 0) && (b0 < b1) && seq_chunk_regular(pre, pre + cs, mg, &fe);
+  double P = pre;
+  if (fast) {
+#pragma unroll
+    for (int k = 0; k < kCache; ++k)
+      if (k < nc) {
+        Mono m;
+        seq_mono(xv[k], fe, &m);
+        agg.m = mono_cat(agg.m, m);
+      }
+    for (long long i = b0 + kCache; i < b1; ++i) {
+      Mono m;
+      seq_mono(get(i), fe, &m);
+      agg.m = mono_cat(agg.m, m);
+    }
+    le = (short)fe;
+  } else {
+#pragma unroll
+    for (int k0 = 0; k0 < kCache; k0 += kGroup) {
+      if (k0 < nc) {
+        double Pv[kGroup + 1];
+        Pv[0] = P;
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k) Pv[k + 1] = Pv[k] + ((k0 + k < nc) ? xv[k0 + k] : 0.0);
+        int cl[kGroup], ee[kGroup];
+        Mono mm[kGroup];
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k) {
+          ee[k] = 0;
+          mm[k] = mono_id();
+          cl[k] = (k0 + k < nc) ? seq_classify_bf(b0 + k0 + k == 0, Pv[k], Pv[k + 1], xv[k0 + k], mg, &ee[k], &mm[k])
+                                : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k)
+          if (cl[k] >= 0) fold(cl[k], ee[k], mm[k]);
+        P = Pv[kGroup];
+      }
+    }
+    for (long long i = b0 + kCache; i < b1; ++i) {
+      const double x = get(i);
+      const double Pc = P + x;
+      int e = 0;
+      Mono m;
+      fold(seq_classify(i == 0, P, Pc, x, mg, &e, &m), e, m);
+      P = Pc;
+    }
+  }
+  if (t == 0) S.bad = 0;
+  S.last_e[t] = (b0 < b1) ? le : (short)0x7fff;
+  BES_STAMP(3)
+  const Seg carry = block_seg_excl(agg, S.ssh, nullptr);
+  BES_STAMP(4)
+  int ntot;
+  int dpos = block_excl_sum<int>(nd, S.ish, &ntot);
+  BES_STAMP(5)
+  if (ntot > SeqSumSmem::kCap) {
+    if (t == 0) S.bad = 1;
+  } else if (fast) {
+    if (b1 == n) {
+      S.fin_m = mono_cat(carry.m, agg.m);
+      S.fin_e = (short)fe;
+    }
+  } else {
+    // record each direct with the run monoid before it (re-classify, grouped)
+    Mono M = carry.m;
+    short prev_e = (t > 0) ? S.last_e[t - 1] : E_ZERO;
+    auto step = [&](long long i, int c, int e, const Mono& m, double x) {
+      if (c == CLS_REG) {
+        M = mono_cat(M, m);
+        prev_e = (short)e;
+      } else {
+        if (c == CLS_DIRECT) {
+          S.dx[dpos] = x;
+          S.dm[dpos] = M;
+          S.de[dpos] = prev_e;
+          S.di[dpos] = (int)i;
+          ++dpos;
+        }
+        M = mono_id();
+        prev_e = (c == CLS_DIRECT) ? E_DIRECT : E_ZERO;
+      }
+    };
+    if (nd > 0) {
+      double P2 = pre;
+#pragma unroll
+      for (int k0 = 0; k0 < kCache; k0 += kGroup) {
+        if (k0 < nc) {
+          double Pv[kGroup + 1];
+          Pv[0] = P2;
+#pragma unroll
+          for (int k = 0; k < kGroup; ++k) Pv[k + 1] = Pv[k] + ((k0 + k < nc) ? xv[k0 + k] : 0.0);
+          int cl[kGroup], ee[kGroup];
+          Mono mm[kGroup];
+#pragma unroll
+          for (int k = 0; k < kGroup; ++k) {
+            ee[k] = 0;
+            mm[k] = mono_id();
+            cl[k] = (k0 + k < nc)
+                        ? seq_classify_bf(b0 + k0 + k == 0, Pv[k], Pv[k + 1], xv[k0 + k], mg, &ee[k], &mm[k])
+                        : -1;
+          }
+#pragma unroll
+          for (int k = 0; k < kGroup; ++k)
+            if (cl[k] >= 0) step(b0 + k0 + k, cl[k], ee[k], mm[k], xv[k0 + k]);
+          P2 = Pv[kGroup];
+        }
+      }
+      for (long long i = b0 + kCache; i < b1; ++i) {
+        const double x = get(i);
+        const double Pc = P2 + x;
+        int e = 0;
+        Mono m;
+        step(i, seq_classify(i == 0, P2, Pc, x, mg, &e, &m), e, m, x);
+        P2 = Pc;
+      }
+    } else {
+      // no directs here: only the run through my chunk matters
+      M = agg.h ? agg.m : mono_cat(M, agg.m);
+      if (b0 < b1) prev_e = le;
+    }
+    if (b1 == n && b0 < b1) {
+      S.fin_m = M;
+      S.fin_e = prev_e;
+    }
+  }
+  BES_STAMP(6)
+  __syncthreads();
+  BES_STAMP(7)
+  if (t == 0) {
+    bool ok = !S.bad;
+    double acc = 0.0, head = 0.0;
+    if (ok) {
+      for (int q = 0; q < ntot && ok; ++q) {
+        if (S.de[q] >= -1100 && S.de[q] <= 1100) ok = seq_apply_run(head, S.de[q], S.dm[q], &acc);
+        acc = dadd(acc, S.dx[q]);
+        head = acc;
+      }
+      if (ok && S.fin_e >= -1100 && S.fin_e <= 1100) ok = seq_apply_run(head, S.fin_e, S.fin_m, &acc);
+    }
+    if (!ok) {  // sequential fallback: always the reference order
+      acc = 0.0;
+      for (long long i = 0; i < n; ++i) acc = dadd(acc, get(i));
+    }
+    S.result = acc;
+    S.bad = ok ? 0 : 1;
+    BES_STAMP(8)
+  } else if (t >= 32) {
+    overlap();  // independent work while thread 0 walks the directs
+  }
+  __syncthreads();
+  BES_STAMP(9)
+#undef BES_STAMP
   const double r = S.result;
   if (fail) *fail = S.bad != 0;
   __syncthreads();

@@ -15,6 +15,11 @@ struct Terms {
   const double* t;
   __device__ double operator()(long long i) const { return __ldcg(&t[i]); }
   template <int N>
+  __device__ void strided(long long i0, long long step, long long n, double (&out)[N]) const {
+#pragma unroll
+    for (int k = 0; k < N; ++k) out[k] = (i0 + k * step < n) ? __ldcg(&t[i0 + k * step]) : 0.0;
+  }
+  template <int N>
   __device__ void batch(long long b0, long long b1, double (&out)[N]) const {
 #pragma unroll
     for (int k = 0; k < N; ++k) out[k] = (b0 + k < b1) ? __ldcg(&t[b0 + k]) : 0.0;
@@ -83,6 +88,42 @@ __global__ void k_pieces(const double* t, long long* cyc, double* out) {
   out[lane] = v.m.a0 + iv + agg.a0 + P;
 }
 
+template <int KC, int KG>
+__global__ void __launch_bounds__(512, 1) k_block(const double* t, long long nt, long long* cyc, double* out) {
+  __shared__ SeqSumSmem S;
+  extern __shared__ __align__(16) double tb[];
+  bool bad = false;
+  __syncthreads();
+  long long t0 = clock64();
+  double v = 0;
+  for (int r = 0; r < 4; ++r) v = block_exact_sum_ilp<KC, KG>(Terms{t}, nt, S, &bad, [] {}, tb, blockIdx.x == 0 ? cyc + 8 : nullptr);
+  long long t1 = clock64();
+  if (threadIdx.x == 0) {
+    cyc[0] = (t1 - t0) / 4;
+    out[0] = v;
+    out[1] = bad;
+  }
+}
+
+template <int KC, int KG>
+void run_block(const double* t, long long nt, double ref, long long* c, double* o) {
+  const int sm = 16 * 32 * (KC + 1) * 8;
+  cudaFuncSetAttribute(k_block<KC, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  k_block<KC, KG><<<148, 512, sm>>>(t, nt, c, o);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h;
+  double ho[2];
+  cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(ho, o, 16, cudaMemcpyDeviceToHost);
+  printf("block_exact_sum_ilp<%d,%d> n=%lld: %lld cycles exact=%d bad=%g %s\n", KC, KG, nt, h, ho[0] == ref, ho[1],
+         e ? cudaGetErrorString(e) : "");
+  long long st[10];
+  cudaMemcpy(st, c + 8, 80, cudaMemcpyDeviceToHost);
+  printf("   stages:");
+  for (int k = 1; k < 10; ++k) printf(" %lld", st[k] - st[k - 1]);
+  printf("\n");
+}
+
 int main() {
   const long long nt = 10000;
   std::vector<double> h(nt);
@@ -110,7 +151,16 @@ int main() {
     printf("warp_seg_excl: %.0f cycles, warp_excl<int>: %.0f cycles, classify: %.0f cycles/element\n", hc[0] / 100.0,
            hc[1] / 100.0, hc[2] / 100.0);
   }
-  for (int grid : {1, 32, 148}) {
+  {
+    long long* c;
+    cudaMalloc(&c, 256);
+    run_block<24, 4>(t, nt, ref, c, o);
+    run_block<24, 2>(t, nt, ref, c, o);
+    run_block<12, 4>(t, nt, ref, c, o);
+    run_block<8, 4>(t, nt, ref, c, o);
+    run_block<24, 1>(t, nt, ref, c, o);
+  }
+  for (int grid : {148}) {
     SliceLoc* loc;
     SliceSum* ps;
     SliceDirect* pd;
