@@ -779,28 +779,30 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     // K columns and y_n.  Not when the slow touch-order path is active (it
     // reads the tags of n) or the vectors do not fit one staging chunk.
     const bool prestage = !slow && n + 1 < nu && K + 1 <= kVec;
-    if ((threadIdx.x >> 5) == 0) {
+    const int ncw = (int)(nb + 31) / 32;  // combine warps of warp_grid_sum
+    if ((int)(threadIdx.x >> 5) < ncw) {
       SliceDirect* sd = reinterpret_cast<SliceDirect*>(dyn + 2 * kVec);  // ring area, idle in P3
       const double r = warp_grid_sum(get, nt, tg, a.sloc, a.ssum, a.sdir, a.sflag, WS, sd,
                                      reinterpret_cast<int*>(sd + kMaxDirectsTotal), &bad,
                                      a.trace ? a.trace + (long long)n * kTraceW + 16 : nullptr);
-      if (lane == 0) {
+      if (threadIdx.x == 0) {
         s_res = r;
         s_bad = bad;
       }
     } else if (prestage) {
       const int n1 = n + 1;
-      const long long tw = (long long)nb * (blockDim.x - 32);
+      const int pw = blockDim.x - 32 * ncw;  // prestage threads per CTA
+      const long long tw = (long long)nb * pw;
       const long long off1 = a.c.off[n1];
       const int m1 = a.c.len[n1];
       const uint32_t tg1 = a.tag_base + (uint32_t)n1 + 1u;
       double* zd1 = a.zd + (n1 & 1) * (a.dim + 1);
-      for (long long t = (long long)blockIdx.x * (blockDim.x - 32) + threadIdx.x - 32; t < m1; t += tw) {
+      for (long long t = (long long)blockIdx.x * pw + threadIdx.x - 32 * ncw; t < m1; t += tw) {
         const int r = a.c.row[off1 + t];
         a.tag[r] = tg1;
         zd1[r] = 0.0;
       }
-      for (int j = threadIdx.x - 32; j < K; j += blockDim.x - 32) {
+      for (int j = threadIdx.x - 32 * ncw; j < K; j += pw) {
         vA[j] = (j < a.K0) ? a.Gb[(long long)j * nu + n1]
                            : a.Gc[(long long)ldg_cg(&a.kept_cand[j - a.K0]) * nu + n1];
         vB[j] = ldg_cg(&ycur[j]);

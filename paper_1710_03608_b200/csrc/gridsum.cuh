@@ -284,7 +284,12 @@ __device__ __forceinline__ void wait_epoch(const unsigned* f, unsigned epoch);
 constexpr int kMaxSlices = 256;
 constexpr int kWarpCache = 4;  // terms cached in registers per lane
 
+constexpr int kCombineBar = 8;  // named barrier of the combine warps
 struct WarpSumSmem {
+  Seg rt_seg[kMaxSlices / 32];   // per-round (32 slices) totals of the combine
+  int rt_nd[kMaxSlices / 32];
+  int rt_last[kMaxSlices / 32];
+  int rt_over[kMaxSlices / 32];
   SliceSum ss[kMaxSlices];
   Mono cin[kMaxSlices];
   int doff[kMaxSlices];
@@ -347,9 +352,11 @@ __device__ double warp_grid_sum(const Get& get, long long nt, unsigned epoch, Sl
   if (tp && blockIdx.x == 0 && (threadIdx.x & 31) == 0) tp[k] = clock64();
   WGS_STAMP(0)
   const int lane = threadIdx.x & 31;
+  const int cw = threadIdx.x >> 5;  // combine warp (warps 0..ceil(nbk/32)-1 call this)
   const int nbk = gridDim.x, b = blockIdx.x;
   constexpr int kR = kMaxSlices / 32;
-  // ---- A: summarize slice b (one per CTA)
+  if (cw == 0) {
+  // ---- A: summarize slice b (one per CTA), warp 0
   const long long per_slice = (nt + nbk - 1) / nbk;
   const long long s0 = min((long long)b * per_slice, nt), s1 = min(s0 + per_slice, nt);
   const long long n = s1 - s0;
@@ -500,66 +507,81 @@ __device__ double warp_grid_sum(const Get& get, long long nt, unsigned epoch, Sl
 #ifdef CTD_WGS_GT
   if (lane == 0) { unsigned long long g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); CTD_WGS_GT[b] = g; }
 #endif
-  // ---- B: combine all slices (redundantly in every CTA).  Staged in shared
-  // memory, then lane l folds the contiguous slices [l*per2, (l+1)*per2).
-  for (;;) {
-    bool ready = true;
+  }  // warp 0: part A
+  // ---- B: combine all slices (redundantly in every CTA).  Combine warp w
+  // takes slices 32w..32w+31 (one warp scan each); the rounds' totals are
+  // exchanged through shared memory and each warp applies its carry.
+  const int R = (nbk + 31) / 32;
+  const int c = 32 * cw + lane;
+  SliceSum sv;
+  sv.agg = Seg{0, mono_id()};
+  sv.nd = 0;
+  sv.last_e = (short)0x7fff;
+  if (cw == 0) {
+    // warp 0 alone polls every slice's flag (no polling traffic from the
+    // other combine warps), then releases them
+    for (;;) {
+      bool ready = true;
 #pragma unroll
-    for (int k = 0; k < kR; ++k) {
-      const int c = lane + 32 * k;
-      if (c < nbk) ready &= ld_relaxed_u32(&sflag[c * kFlagStride]) == epoch;
+      for (int k = 0; k < kR; ++k) {
+        const int cc = lane + 32 * k;
+        if (cc < nbk) ready &= ld_relaxed_u32(&sflag[cc * kFlagStride]) == epoch;
+      }
+      if (__all_sync(FULL, ready)) break;
     }
-    if (__all_sync(FULL, ready)) break;
+    fence_acq_rel_gpu();
   }
-  fence_acq_rel_gpu();
-#pragma unroll
-  for (int k = 0; k < kR; ++k) {
-    const int c = lane + 32 * k;
-    if (c < nbk) W.ss[c] = ldcg_struct(ps + c);
-  }
-  __syncwarp();
+  asm volatile("bar.sync %0, %1;" ::"r"(kCombineBar), "r"(R * 32) : "memory");
+  if (c < nbk) sv = ldcg_struct(ps + c);
 #ifdef CTD_WGS_GT
-  if (lane == 0) { unsigned long long g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); CTD_WGS_GT[256 + b] = g; }
+  if (lane == 0 && cw == 0) { unsigned long long g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); CTD_WGS_GT[256 + b] = g; }
 #endif
   WGS_STAMP(4)
-  const int per2 = (nbk + 31) / 32;
-  const int c0 = min(lane * per2, nbk), c1 = min(c0 + per2, nbk);
-  Seg lt{0, mono_id()};
-  int ndl = 0, any_over = 0;
-  int lne = 0x7fff;  // my last non-empty slice's last_e
-  for (int c = c0; c < c1; ++c) {
-    const SliceSum sv = W.ss[c];
-    lt = seg_cat(lt, sv.agg);
-    ndl += sv.nd < 0 ? 0 : sv.nd;
-    any_over |= sv.nd < 0;
-    if (sv.last_e != (short)0x7fff) lne = sv.last_e;
-  }
-  Seg lc = warp_seg_excl(lt, nullptr);
-  int total_d;
-  int off = warp_excl<int>(ndl, &total_d);
-  int pl = lne;  // nearest non-empty slice before mine: "right unless empty"
+  Seg rtot;
+  const Seg ex = warp_seg_excl(sv.agg, &rtot);
+  const int ndv = sv.nd < 0 ? 0 : sv.nd;
+  int rnd;
+  const int offl = warp_excl<int>(ndv, &rnd);
+  int pl = sv.last_e;  // nearest non-empty slice before mine within the round
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const int o = __shfl_up_sync(FULL, pl, d);
     if (lane >= d && pl == 0x7fff) pl = o;
   }
-  int prev = __shfl_up_sync(FULL, pl, 1);
-  if (lane == 0 || prev == 0x7fff) prev = E_ZERO;
-  const int last_all = __shfl_sync(FULL, pl, 31);
-  const bool over_all = __any_sync(FULL, any_over) || total_d > kMaxDirectsTotal;
-  for (int c = c0; c < c1; ++c) {
-    const SliceSum sv = W.ss[c];
-    W.cin[c] = lc.m;
-    W.doff[c] = off;
-    const int ndc = sv.nd < 0 ? 0 : sv.nd;
-    W.nd[c] = ndc;
-    W.sprev[c] = (short)prev;
-    if (c == nbk - 1) W.finm = seg_cat(Seg{0, lc.m}, sv.agg).m;
-    lc = seg_cat(lc, sv.agg);
-    off += ndc;
-    if (sv.last_e != (short)0x7fff) prev = sv.last_e;
+  int prevl = __shfl_up_sync(FULL, pl, 1);
+  if (lane == 0) prevl = 0x7fff;
+  const int rlast = __shfl_sync(FULL, pl, 31);
+  const int rover = __any_sync(FULL, sv.nd < 0) ? 1 : 0;
+  if (lane == 0) {
+    W.rt_seg[cw] = rtot;
+    W.rt_nd[cw] = rnd;
+    W.rt_last[cw] = rlast;
+    W.rt_over[cw] = rover;
   }
-  __syncwarp();
+  asm volatile("bar.sync %0, %1;" ::"r"(kCombineBar), "r"(R * 32) : "memory");
+  Seg car{0, mono_id()};
+  int doff0 = 0, last0 = 0x7fff, total_d = 0, last_all = 0x7fff, any_over = 0;
+  for (int r = 0; r < R; ++r) {
+    if (r < cw) {
+      car = seg_cat(car, W.rt_seg[r]);
+      doff0 += W.rt_nd[r];
+      if (W.rt_last[r] != 0x7fff) last0 = W.rt_last[r];
+    }
+    total_d += W.rt_nd[r];
+    any_over |= W.rt_over[r];
+    if (W.rt_last[r] != 0x7fff) last_all = W.rt_last[r];
+  }
+  const bool over_all = any_over || total_d > kMaxDirectsTotal;
+  if (c < nbk) {
+    const Seg cin = seg_cat(car, ex);
+    W.cin[c] = cin.m;
+    W.doff[c] = doff0 + offl;
+    W.nd[c] = ndv;
+    W.sprev[c] = (short)(prevl != 0x7fff ? prevl : (last0 != 0x7fff ? last0 : E_ZERO));
+    if (c == nbk - 1) W.finm = seg_cat(Seg{0, cin.m}, sv.agg).m;
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(kCombineBar), "r"(R * 32) : "memory");
+  if (cw != 0) return 0.0;  // warp 0 finishes
   WGS_STAMP(5)
   // directs in order, each with its run monoid and binade resolved (parallel)
   if (!over_all) {
