@@ -579,27 +579,21 @@ __device__ double warp_grid_sum(const Get& get, long long nt, unsigned epoch, Sl
     W.nd[c] = ndv;
     W.sprev[c] = (short)(prevl != 0x7fff ? prevl : (last0 != 0x7fff ? last0 : E_ZERO));
     if (c == nbk - 1) W.finm = seg_cat(Seg{0, cin.m}, sv.agg).m;
+    // this slice's directs into the ordered list, each with its run monoid
+    // and preceding binade resolved against the carry
+    if (!over_all) {
+      const short pe = (short)(prevl != 0x7fff ? prevl : (last0 != 0x7fff ? last0 : E_ZERO));
+      for (int k = 0; k < ndv; ++k) {
+        SliceDirect d = ldcg_struct(pd + (long long)c * kSliceDirects + k);
+        if (d.inh) d.m = mono_cat(cin.m, d.m);
+        if (d.e == (short)0x7ffe) d.e = pe;  // "previous slice"
+        sdir[doff0 + offl + k] = d;
+      }
+    }
   }
   asm volatile("bar.sync %0, %1;" ::"r"(kCombineBar), "r"(R * 32) : "memory");
   if (cw != 0) return 0.0;  // warp 0 finishes
   WGS_STAMP(5)
-  // directs in order, each with its run monoid and binade resolved (parallel)
-  if (!over_all) {
-    for (int idx = lane; idx < total_d; idx += 32) {
-      int lo = 0, hi = nbk - 1;  // last slice with doff <= idx and nd > 0
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (W.doff[mid] <= idx) lo = mid;
-        else hi = mid - 1;
-      }
-      while (W.nd[lo] == 0 || W.doff[lo] + W.nd[lo] <= idx) ++lo;
-      SliceDirect d = ldcg_struct(pd + (long long)lo * kSliceDirects + (idx - W.doff[lo]));
-      if (d.inh) d.m = mono_cat(W.cin[lo], d.m);
-      if (d.e == (short)0x7ffe) d.e = W.sprev[lo];  // "previous slice"
-      sdir[idx] = d;
-    }
-  }
-  __syncwarp();
   WGS_STAMP(6)
   double acc = 0.0;
   int bad = 0;
@@ -607,12 +601,14 @@ __device__ double warp_grid_sum(const Get& get, long long nt, unsigned epoch, Sl
     bool ok = !over_all;
     double head = 0.0;
     if (ok) {
-      for (int idx = 0; idx < total_d && ok; ++idx) {
+      // only head -> run -> add is on the dependent path; the run checks are
+      // accumulated into `ok` (seq_apply_run's conditions, evaluated lazily)
+      for (int idx = 0; idx < total_d; ++idx) {
         const SliceDirect d = sdir[idx];
-        acc = head;
-        if (d.e >= -1100 && d.e <= 1100) ok = seq_apply_run(head, d.e, d.m, &acc);
-        acc = dadd(acc, d.x);
-        head = acc;
+        const bool run = (d.e >= -1100) & (d.e <= 1100);
+        const long long A = mono_apply(d.m, dsig(head));
+        ok &= !run | ((head > 0.0) & (dexp(head) == d.e) & (A < (1LL << 53)) & (A >= (1LL << 52)));
+        head = dadd(run ? dmake(A, d.e) : head, d.x);
       }
       acc = head;
       const short pl2 = (short)last_all;
