@@ -363,7 +363,6 @@ int ctd_gpu_ctd_s(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int mode, int64_t s
     need(ctx, "ctx");
     need(x, "x");
     need(out, "out");
-    if (flags & CTD_GPU_WITH_CORE) fail(CTD_ERR_ARGUMENT, "core materialization is not available yet");
     auto h = std::make_unique<ctd_gpu_factors>();
     run_ctd_s(&ctx->c, x->t, mode, sample_size, epsilon, seed, flags, h->f);
     ctx->c.phase_flush();
@@ -380,7 +379,7 @@ int ctd_gpu_factors_info_get(const ctd_gpu_factors* f, ctd_gpu_factors_info* inf
     info->kept = (int64_t)F.kept_flat.size();
     info->r_rows = F.rows;
     info->r_nnz = F.basis ? F.basis->rnnz : 0;
-    info->c_nnz = 0;
+    info->c_nnz = F.has_core ? F.core.nnz : 0;
     info->n_drawn = (int64_t)F.drawn.size();
     info->n_unique = (int64_t)F.unique.size();
     info->n_fibers = F.F;
@@ -420,10 +419,24 @@ int ctd_gpu_factors_u(const ctd_gpu_factors* f, double* u) {
   });
 }
 
-int ctd_gpu_factors_core(const ctd_gpu_factors* f, int64_t*, int64_t*, int64_t*, int64_t*, double*) {
+int ctd_gpu_factors_core(const ctd_gpu_factors* f, int64_t* c_cols, int64_t* col_id, int64_t* col_ptr,
+                         int64_t* rows, double* vals) {
   return guarded([&] {
     need(f, "factors");
-    fail(CTD_ERR_ARGUMENT, "core materialization is not available yet");
+    const Factors& F = f->f;
+    if (!F.has_core) fail(CTD_ERR_ARGUMENT, "factors were computed without CTD_GPU_WITH_CORE");
+    const Core& c = F.core;
+    if (c_cols) *c_cols = c.cols;
+    if (col_id && c.cols) std::memcpy(col_id, c.col_id.data(), c.cols * sizeof(int64_t));
+    if (col_ptr) std::memcpy(col_ptr, c.ptr.data(), (c.cols + 1) * sizeof(int64_t));
+    if (c.nnz && (rows || vals)) {
+      Ctx* cx = F.ctx;
+      if (vals) cx->to_host(vals, c.val.p, c.nnz);
+      std::vector<int32_t> r32(rows ? c.nnz : 0);
+      if (rows) cx->to_host(r32.data(), c.row.p, c.nnz);
+      cx->sync();
+      for (int64_t i = 0; rows && i < c.nnz; ++i) rows[i] = r32[i];
+    }
   });
 }
 
@@ -472,8 +485,17 @@ int ctd_gpu_memory_usage(const ctd_gpu_tensor* x, const ctd_gpu_factors* f, doub
     need(x, "x");
     need(f, "factors");
     need(out, "out");
-    if (x->t.nnz == 0) fail(CTD_ERR_METRIC, "memory usage undefined for an empty tensor");
-    fail(CTD_ERR_ARGUMENT, "memory_usage needs nnz(C): core materialization is not available yet");
+    if (x->t.nnz == 0) fail(CTD_ERR_METRIC, "memory usage undefined for an empty tensor");  // evaluation.cpp:125-126
+    const Factors& F = f->f;
+    if (!F.has_core) fail(CTD_ERR_ARGUMENT, "memory_usage needs nnz(C): compute the factors with CTD_GPU_WITH_CORE");
+    // (nnz(C) + nnz(U) + nnz(R)) / nnz(X), nnz(U) = exact nonzeros (dense_matrix.cpp:24-29)
+    const int64_t K = F.basis ? F.basis->K : 0;
+    std::vector<double> u((size_t)K * K);
+    if (K) basis_u(*F.basis, u.data());
+    int64_t u_nnz = 0;
+    for (double v : u) u_nnz += (v != 0.0);
+    const int64_t r_nnz = F.basis ? F.basis->rnnz : 0;
+    *out = (double)(F.core.nnz + u_nnz + r_nnz) / (double)x->t.nnz;
   });
 }
 

@@ -148,6 +148,11 @@ void run_ctd_s(Ctx* ctx, const Tensor& x, int mode, int64_t s, double eps, uint6
     PhaseScope ps(ctx, PH_ERROR);
     out.rel_error = relative_error(ctx, fb, *out.basis);
   }
+  if (flags & CTD_GPU_WITH_CORE) {  // factors.C = compute_core(x, R, mode) (ctd_static.cpp:47)
+    PhaseScope ps(ctx, PH_OTHER);
+    compute_core(ctx, fb, *out.basis, out.core);
+    out.has_core = true;
+  }
   if (htrace) {
     const auto h3 = std::chrono::steady_clock::now();
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };

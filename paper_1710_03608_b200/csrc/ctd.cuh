@@ -1,4 +1,5 @@
 #pragma once
+#include "core.cuh"
 #include <cmath>
 #include <memory>
 #include <vector>
@@ -25,6 +26,8 @@ struct Factors {
   double min_margin = INFINITY;
   bool integer_exact = false;
   bool slow_path = false;
+  bool has_core = false;  // CTD_GPU_WITH_CORE: C_(mode) = R^T X_(mode)
+  Core core;
 };
 
 // Algorithm 1 (ctd_static.cpp:19-50) minus compute_core; with

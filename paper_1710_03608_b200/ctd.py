@@ -56,6 +56,7 @@ _ERRORS = {1: ArgumentError, 2: ShapeError, 3: EmptyInputError, 5: MetricError,
 
 WITH_ERROR = 0x1
 WITH_CORE = 0x2
+WITH_CORE = 0x2
 
 
 def _check(st: int):
@@ -427,6 +428,12 @@ class LRFactors:
     min_margin: float = float("inf")
     info: Optional[_lib.FactorsInfo] = None
     handle: object = None
+    # C_(mode) = R^T X_(mode) (compute_core) when requested: CSC over the columns
+    # that keep an entry (C_col: their column ids), rows = kept-fiber index
+    C_col: Optional[np.ndarray] = None
+    C_ptr: Optional[np.ndarray] = None
+    C_row: Optional[np.ndarray] = None
+    C_val: Optional[np.ndarray] = None
 
     @property
     def kept_fibers(self):
@@ -464,6 +471,16 @@ def _read_factors(ctx: Context, h, shape, mode, trace=True) -> LRFactors:
                   u[:k * k].reshape(k, k), cp, rr[:info.r_nnz].copy(), rv[:info.r_nnz].copy(),
                   total_sq_norm=info.total_sq_norm, relative_error=info.relative_error,
                   min_margin=info.min_margin, info=info, handle=_FactorsHandle(ctx, h))
+    if info.c_nnz or (with_core_flag(h, ctx)):
+        cc = C.c_int64()
+        _check(L.ctd_gpu_factors_core(h, C.byref(cc), None, None, None, None))
+        nc, nz = cc.value, info.c_nnz
+        f.C_col = np.zeros(max(nc, 1), np.int64)
+        f.C_ptr = np.zeros(nc + 1, np.int64)
+        f.C_row = np.zeros(max(nz, 1), np.int64)
+        f.C_val = np.zeros(max(nz, 1))
+        _check(L.ctd_gpu_factors_core(h, C.byref(cc), _p(f.C_col), _p(f.C_ptr), _p(f.C_row), _p(f.C_val)))
+        f.C_col, f.C_row, f.C_val = f.C_col[:nc], f.C_row[:nz], f.C_val[:nz]
     if trace and info.n_drawn:
         nd, nu = info.n_drawn, info.n_unique
         f.drawn = np.zeros(nd, np.int64)
@@ -478,16 +495,34 @@ def _read_factors(ctx: Context, h, shape, mode, trace=True) -> LRFactors:
     return f
 
 
+def with_core_flag(h, ctx) -> bool:
+    """Whether the factors carry C (a zero-entry core still has columns info)."""
+    cc = C.c_int64()
+    return ctx.L.ctd_gpu_factors_core(h, C.byref(cc), None, None, None, None) == 0
+
+
 def ctd_s(x, mode: int, sample_size: int, epsilon: float = 1e-6, seed: int = 42,
-          with_error: bool = False, ctx: Optional[Context] = None) -> LRFactors:
-    """Algorithm 1 (ctd_static.hpp:22-24).  C (compute_core) is not materialized;
+          with_error: bool = False, with_core: bool = False, ctx: Optional[Context] = None) -> LRFactors:
+    """Algorithm 1 (ctd_static.hpp:22-24).  ``with_core`` materializes
+    C = X x_mode R^T (compute_core, ctd_static.cpp:12-17) as its matricization;
     ``with_error`` runs the relative-error pass (evaluation.cpp:88-122)."""
     ctx = ctx or default_context()
     d = _dev(x, ctx)
     h = C.c_void_p()
-    _check(ctx.L.ctd_gpu_ctd_s(ctx.h, d.h, mode, sample_size, epsilon, C.c_uint64(seed),
-                               WITH_ERROR if with_error else 0, C.byref(h)))
+    flags = (WITH_ERROR if with_error else 0) | (WITH_CORE if with_core else 0)
+    _check(ctx.L.ctd_gpu_ctd_s(ctx.h, d.h, mode, sample_size, epsilon, C.c_uint64(seed), flags,
+                               C.byref(h)))
     return _read_factors(ctx, h, d.shape, mode)
+
+
+def memory_usage(x, f: LRFactors, ctx: Optional[Context] = None) -> float:
+    """memory_usage (evaluation.cpp:124-129): (nnz(C) + nnz(U) + nnz(R)) / nnz(X);
+    the factors must carry C (``ctd_s(..., with_core=True)``)."""
+    ctx = ctx or default_context()
+    d = _dev(x, ctx)
+    out = C.c_double()
+    _check(ctx.L.ctd_gpu_memory_usage(d.h, f.handle.h, C.byref(out)))
+    return out.value
 
 
 def ctd_s_raw(x, mode: int, sample_size: int, epsilon: float = 1e-6, seed: int = 42,

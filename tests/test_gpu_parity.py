@@ -137,6 +137,33 @@ def test_relative_error(ctx, ref, name):
     assert abs(f.relative_error - e) <= 1e-9 * max(1.0, abs(e)), (f.relative_error, e)
 
 
+@pytest.mark.parametrize("name,mode", [("c1", 0), ("c1", 2), ("rand_fp", 1), ("rand_int", 0), ("lowrank", 0),
+                                       ("traffic", 0), ("order4", 3)])
+def test_core_bitexact(ctx, port, name, mode):
+    """compute_core (ctd_static.cpp:12-17): C_(mode) = R^T X_(mode) entry for entry,
+    including the 1e-14 drop rule, against the oracle's multiply_columns."""
+    x = CASES[name]()
+    f = ctd.ctd_s(_st(x), mode, 150, 1e-6, 42, with_core=True, ctx=ctx)
+    xm = port.matricize(x.shape, x.idx.reshape(-1), x.val, mode)
+    o = port.frontend(x.shape, x.idx.reshape(-1), x.val, mode, 150, 1e-6, 42)
+    c = port.core_matricized(xm, o.R)
+    nonempty = np.nonzero(np.diff(c.col_ptr) > 0)[0]
+    assert np.array_equal(f.C_col, nonempty)
+    assert np.array_equal(f.C_ptr, np.concatenate([[0], np.cumsum(np.diff(c.col_ptr)[nonempty])]))
+    assert np.array_equal(f.C_row, c.row)
+    assert np.array_equal(f.C_val.view(np.int64), c.val.view(np.int64))
+
+
+@pytest.mark.parametrize("name", ["c1", "rand_fp", "lowrank"])
+def test_memory_usage(ctx, ref, name):
+    x = CASES[name]()
+    st = _st(x)
+    f = ctd.ctd_s(st, 0, 200, 1e-6, 42, with_core=True, ctx=ctx)
+    r = ref.ctd_s(ref.tensor(x.shape, x.flat_idx(), x.val), 0, 200, 1e-6, 42)
+    assert int(f.info.c_nnz) == r.extra["c_nnz"]
+    assert ctd.memory_usage(st, f, ctx=ctx) == r.extra["memory_usage"]
+
+
 def test_stream_vs_port(ctx, port):
     x = g.c3_stream(seed=5, n_steps=3, slices_per_step=3, draws_per_slice=3000, n=400,
                     planted_step=2, block=20)
