@@ -799,9 +799,8 @@ int ctd_gpu_stream_init(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* historical, int 
     need(ctx, "ctx");
     need(historical, "historical");
     need(out, "out");
-    (void)flags;
     auto h = std::make_unique<ctd_gpu_stream>();
-    stream_init(&ctx->c, historical->t, mode, sample_size, epsilon, seed, h->s);
+    stream_init(&ctx->c, historical->t, mode, sample_size, epsilon, seed, flags, h->s);
     *out = h.release();
   });
 }
@@ -854,6 +853,25 @@ int ctd_gpu_stream_factors(ctd_gpu_stream* s, ctd_gpu_factors** out) {
       CUDA_OK(cudaMemcpyAsync(nb->rval.p, B.rval.p, B.rnnz * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     }
     F.basis = std::move(nb);
+    if (S.with_core) {  // StreamState::factors folds the core (:114-127); kept matricized here
+      const DevCore& dc = S.core;
+      Core& cc = F.core;
+      cc.rows = B.K;
+      cc.cols = dc.cols;
+      cc.nnz = dc.nnz;
+      cc.col_id.resize(dc.cols);
+      cc.ptr.resize(dc.cols + 1);
+      if (dc.cols) c->to_host(cc.col_id.data(), dc.col.p, dc.cols);
+      c->to_host(cc.ptr.data(), dc.ptr.p, dc.cols + 1);
+      cc.row.alloc(c, dc.nnz + 1);
+      cc.val.alloc(c, dc.nnz + 1);
+      if (dc.nnz) {
+        CUDA_OK(cudaMemcpyAsync(cc.row.p, dc.row.p, dc.nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
+        CUDA_OK(cudaMemcpyAsync(cc.val.p, dc.val.p, dc.nnz * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      }
+      c->sync();
+      F.has_core = true;
+    }
     *out = h.release();
   });
 }

@@ -30,6 +30,7 @@ __global__ void k_gather_cols(const int32_t* fib, long long n, const int64_t* fc
 // Front end shared by CTD-S and the CTD-D step: law, draws, dedup, filter.
 struct Front {
   std::vector<int64_t> drawn, unique;
+  std::vector<int32_t> unique_fib;  // fiber index (into the Fibers) of each unique candidate
   BatchOut bo;
   double total = 0.0;
 };
@@ -73,7 +74,9 @@ void front_end(Ctx* ctx, const Fibers& fb, Basis& basis, int64_t s, double eps, 
     ctx->sync();
   }
   fr.unique.resize(n_u);
+  fr.unique_fib.resize(n_u);
   if (n_u > 0) {
+    ctx->to_host(fr.unique_fib.data(), uniq.p, n_u);
     LAUNCH(ctx, k_gather_cols, ceil_div(n_u, 256), 256, 0, uniq.p, (long long)n_u, fb.col.p, cols.p);
     ctx->to_host(fr.unique.data(), cols.p, n_u);
     ctx->sync();
@@ -162,12 +165,14 @@ void run_ctd_s(Ctx* ctx, const Tensor& x, int mode, int64_t s, double eps, uint6
 }
 
 void stream_init(Ctx* ctx, const Tensor& hist, int mode, int64_t s, double eps, uint64_t seed,
-                 Stream& out) {
+                 unsigned flags, Stream& out) {
   // ctd_dynamic.cpp:133-136
   if (hist.order < 2) fail(CTD_ERR_ARGUMENT, "a stream needs at least one non-time mode");
   if (mode < 0 || mode >= hist.order - 1) fail(CTD_ERR_ARGUMENT, "mode must precede the time mode");
   Factors f;
-  run_ctd_s(ctx, hist, mode, s, eps, seed, 0, f);
+  out.with_core = (flags & CTD_GPU_WITH_CORE) != 0;
+  run_ctd_s(ctx, hist, mode, s, eps, seed, out.with_core ? CTD_GPU_WITH_CORE : 0, f);
+  if (out.with_core) core_from_static(ctx, f.core, out.core);  // matricize(f.C, mode) (:141)
   out.ctx = ctx;
   out.order = hist.order;
   out.mode = mode;
@@ -190,9 +195,20 @@ void stream_step(Stream& st, const Tensor& slab, int64_t d) {
   if (slab.nnz > 0) {  // :173-188
     Fibers fb;
     matricize(ctx, slab, st.mode, fb);
+    // snapshot U^(t) for the core update (:165-167)
+    const int64_t Kold = st.basis->K;
+    Buf<double> uold(ctx, st.with_core ? (size_t)Kold * Kold + 1 : 1);
+    if (st.with_core && Kold)
+      CUDA_OK(cudaMemcpy2DAsync(uold.p, Kold * sizeof(double), st.basis->U.p, st.basis->LD * sizeof(double),
+                                Kold * sizeof(double), Kold, cudaMemcpyDeviceToDevice, ctx->stream));
     Front fr;
     front_end(ctx, fb, *st.basis, d, st.eps, st.seed ^ (uint64_t)st.t, fr, false);
-    for (int32_t k : fr.bo.kept_cand) st.kept_flat.push_back(fr.unique[k] + st.t * fb.cols);
+    std::vector<int32_t> appended;
+    for (int32_t k : fr.bo.kept_cand) {
+      st.kept_flat.push_back(fr.unique[k] + st.t * fb.cols);
+      appended.push_back(fr.unique_fib[k]);
+    }
+    if (st.with_core) core_step(ctx, st.core, fb, *st.basis, Kold, uold.p, appended, st.t * fb.cols);
   }
   st.t += 1;  // :227
 }

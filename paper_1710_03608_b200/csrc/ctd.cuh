@@ -1,5 +1,6 @@
 #pragma once
 #include "core.cuh"
+#include "stream_core.cuh"
 #include <cmath>
 #include <memory>
 #include <vector>
@@ -52,10 +53,12 @@ struct Stream {
   uint64_t seed = 0;
   std::unique_ptr<Basis> basis;
   std::vector<int64_t> kept_flat;
+  bool with_core = false;  // CTD_GPU_WITH_CORE: maintain the Eq. 13 core
+  DevCore core;
 };
 
 void stream_init(Ctx* ctx, const Tensor& hist, int mode, int64_t s, double eps, uint64_t seed,
-                 Stream& out);
+                 unsigned flags, Stream& out);
 void stream_step(Stream& st, const Tensor& slab, int64_t d);
 
 }  // namespace ctdgpu

@@ -610,12 +610,14 @@ class StreamState:
 
 
 def init_stream(historical, mode: int, sample_size: int, epsilon: float = 1e-6,
-                seed: int = 42, ctx: Optional[Context] = None) -> StreamState:
+                seed: int = 42, with_core: bool = False, ctx: Optional[Context] = None) -> StreamState:
+    """init_stream (ctd_dynamic.cpp:129-147).  ``with_core`` maintains the core
+    C(t) through every step (Eq. 13 blocks); ``factors()`` then carries it."""
     ctx = ctx or default_context()
     d = _dev(historical, ctx)
     h = C.c_void_p()
-    _check(ctx.L.ctd_gpu_stream_init(ctx.h, d.h, mode, sample_size, epsilon, C.c_uint64(seed), 0,
-                                     C.byref(h)))
+    _check(ctx.L.ctd_gpu_stream_init(ctx.h, d.h, mode, sample_size, epsilon, C.c_uint64(seed),
+                                     WITH_CORE if with_core else 0, C.byref(h)))
     return StreamState(ctx, h, mode, d.shape[:-1])
 
 

@@ -180,6 +180,40 @@ def test_stream_vs_port(ctx, port):
     assert st.t == ps.t
 
 
+def _dense_cols(ncols, C_col, C_ptr):
+    cp = np.zeros(ncols + 1, np.int64)
+    cnt = np.zeros(ncols, np.int64)
+    cnt[C_col] = np.diff(C_ptr)
+    cp[1:] = np.cumsum(cnt)
+    return cp
+
+
+@pytest.mark.parametrize("seed,d", [(5, 60), (6, 25)])
+def test_stream_core_vs_port(ctx, port, seed, d):
+    """CTD-D with the core maintained (Eq. 13: top-right R^T dX, chain-product
+    bottom-left, bottom-right dR^T dX, assemble_blocks) bit for bit."""
+    x = g.c3_stream(seed=seed, n_steps=3, slices_per_step=3, draws_per_slice=2500, n=300,
+                    planted_step=2, block=20)
+    hist = x.time_slab(0, 3)
+    st = ctd.init_stream(_st(hist), 0, 120, 1e-6, 7, with_core=True, ctx=ctx)
+    ps = port.stream(hist.shape, hist.flat_idx(), hist.val, 0, 120, 1e-6, 7)
+    grew = 0
+    for t in range(3, x.shape[2]):
+        slab = x.time_slab(t, t + 1)
+        k0 = len(ps.kept_flat())
+        ctd.ctd_d_step(st, _st(slab), d)
+        ps.step(slab.shape, slab.flat_idx(), slab.val, d)
+        grew += len(ps.kept_flat()) > k0
+        f = st.factors()
+        c = ps.core()
+        assert np.array_equal(f.kept_flat, ps.kept_flat()), t
+        assert c.cols == x.shape[1] * (t + 1)
+        assert np.array_equal(_dense_cols(c.cols, f.C_col, f.C_ptr), c.col_ptr), t
+        assert np.array_equal(f.C_row, c.row), t
+        assert np.array_equal(f.C_val.view(np.int64), c.val.view(np.int64)), t
+    assert grew >= 2  # the chain-product (bottom-left) block was exercised
+
+
 def test_errors(ctx):
     x = g.c1()
     t = _st(x)
