@@ -274,14 +274,31 @@ def ctd_s_sharded(shape, local, mode: int, sample_size: int, epsilon: float = 1e
         raise api.ArgumentError("sample size must be at least 1")
     if not (epsilon > 0.0):
         raise api.ArgumentError("epsilon must be positive")
+    import os
+    import time
+    trace = os.environ.get("CTD_DIST_TRACE") == "1"
+    tm = [time.perf_counter()]
+
+    def mark():
+        if trace:
+            try:
+                import torch
+                torch.cuda.synchronize()
+            except Exception:
+                pass
+            tm.append(time.perf_counter())
+
     # 1. local bucketing + exact norms (resident)
     sh = k.shard(local if isinstance(local, api.DeviceTensor) else (shape, local[0], local[1]), mode)
+    mark()
     # 2. global fiber list (ranks own ascending ranges) -> replicated law/draws/dedup
     gcol = np.concatenate(comm.allgather(sh.col.astype(np.int64)))
     gnorm = np.concatenate(comm.allgather(sh.norm.astype(np.float64)))
     if gcol.shape[0] > 1 and not np.all(gcol[1:] > gcol[:-1]):
         raise api.ArgumentError("shards must hold disjoint ascending fiber ranges in rank order")
+    mark()
     total, unique = k.sample_fibers(gcol, gnorm, sample_size, seed)
+    mark()
     # 3. candidate payloads from their owners, assembled in draw order
     pos = np.searchsorted(sh.col, unique)
     ok = pos < sh.col.shape[0]
@@ -307,11 +324,13 @@ def ctd_s_sharded(shape, local, mode: int, sample_size: int, epsilon: float = 1e
     for w, ln, rr, vv in zip(g_which, g_lens, g_rows, g_vals):
         if w.size == 0:
             continue
-        src = np.concatenate([[0], np.cumsum(ln)])
         # scatter each owned candidate's entries to its slot in draw order
-        dst_idx = np.concatenate([np.arange(cptr[c], cptr[c + 1]) for c in w])
-        crow[dst_idx] = rr[:src[-1]]
-        cval[dst_idx] = vv[:src[-1]]
+        n_e = int(ln.sum())
+        src0 = np.concatenate([[0], np.cumsum(ln)[:-1]])
+        dst_idx = np.repeat(cptr[w] - src0, ln) + np.arange(n_e)
+        crow[dst_idx] = rr[:n_e]
+        cval[dst_idx] = vv[:n_e]
+    mark()
     # 4. replicated filter + U recurrence
     dim = int(shape[mode])
     B = k.basis(dim)
@@ -319,6 +338,11 @@ def ctd_s_sharded(shape, local, mode: int, sample_size: int, epsilon: float = 1e
     kept = unique[np.nonzero(acc)[0]]
     U = B.u()
     rp, rr, rv = B.r()
+    mark()
+    if trace:
+        names = ["shard", "allgather fibers", "law+draws", "candidates", "filter+U/R"]
+        print("[dist trace] rank %d: " % comm.rank + " ".join(
+            f"{n}={1e3 * (b - a):.1f}ms" for n, a, b in zip(names, tm[:-1], tm[1:])), flush=True)
     res = ShardedResult(kept, U, rp, rr, rv, unique, acc, deg, dl, float(total), None, int(gcol.shape[0]),
                         {"local_fibers": int(sh.col.shape[0]), "candidate_nnz": int(cptr[-1])})
     # 5. error partials, all-reduced
