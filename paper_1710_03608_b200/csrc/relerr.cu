@@ -44,9 +44,12 @@ __global__ void k_cd(const int64_t* fptr, long long F, const int32_t* row, const
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
   double part = 0.0;
-  for (long long f = warp; f < F; f += nwarps) {
-    const long long b = fptr[f], e = fptr[f + 1];
-    for (long long c0 = 0; c0 < K; c0 += 32 * kCW) {
+  // column chunk outermost: the grid sweeps all fibers against one 128-column
+  // tile of Rd and Q at a time, so the tile (dim x 128 x 16 B) stays in L2 and
+  // the heavy rows' tiles in L1, instead of every fiber walking all of K
+  for (long long c0 = 0; c0 < K; c0 += 32 * kCW) {
+    for (long long f = warp; f < F; f += nwarps) {
+      const long long b = fptr[f], e = fptr[f + 1];
       double ac[kCW], ad[kCW];
 #pragma unroll
       for (int u = 0; u < kCW; ++u) ac[u] = ad[u] = 0.0;
