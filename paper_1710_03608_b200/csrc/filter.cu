@@ -225,6 +225,8 @@ struct FArgs {
   SliceSum* ssum;    // [grid] residual-sum slice summaries
   SliceDirect* sdir; // [grid * kSliceDirects]
   int* nfallback;    // exact-sum self-check failures (sequential fallback taken)
+  double* gscr;      // [grid][LD+1] per-CTA g staging when K exceeds shared memory
+  int kvec;          // largest K whose g / y vectors are staged in shared memory
   SliceLoc* sloc;    // [grid] published approximate slice sums (epoch-flagged)
   unsigned* sflag;   // [grid] slice-summary epoch flags
 };
@@ -374,6 +376,12 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   Buf<SliceDirect> sdir(ctx, (size_t)ctx->sm_count * kSliceDirects);
   fa.ssum = ssum.p;
   fa.sdir = sdir.p;
+  Buf<double> gscr(ctx, (size_t)ctx->sm_count * (B.LD + 1));
+  fa.gscr = gscr.p;
+  // CTD_FILTER_KVEC (tests) lowers the shared-memory staging limit to exercise
+  // the global-operand path at small K
+  static const int kvec_env = getenv("CTD_FILTER_KVEC") ? atoi(getenv("CTD_FILTER_KVEC")) : 0;
+  fa.kvec = (kvec_env > 0 && kvec_env < kVec) ? kvec_env : kVec;
   Buf<SliceLoc> sloc(ctx, ctx->sm_count);
   sloc.zero();
   Buf<unsigned> sflag(ctx, (size_t)ctx->sm_count * kFlagStride);

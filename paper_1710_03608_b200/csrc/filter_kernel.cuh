@@ -20,65 +20,7 @@
 constexpr int kFThreads = 512;
 constexpr int kVec = 4096;  // doubles per staged vector (two buffers)
 
-// acc <- (((acc + p_0) + p_1) + ... + p_{cnt-1}) where lane q holds p_q.
-// Lanes stage their products in the warp's shared slot; lane 0 runs the
-// dependent chain (the result is meaningful on lane 0 only).
-__device__ __forceinline__ double warp_chain(double* wbuf, int lane, double p, int cnt, double acc) {
-  wbuf[lane] = p;
-  __syncwarp();
-  if (lane == 0) {
-    // all loads issued before the dependent chain starts
-    const double2* w2 = reinterpret_cast<const double2*>(wbuf);
-    double v[32];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const double2 t = w2[q];
-      v[2 * q] = t.x;
-      v[2 * q + 1] = t.y;
-    }
-    if (cnt == 32) {
-#pragma unroll
-      for (int q = 0; q < 32; ++q) acc = dadd(acc, v[q]);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 32; ++q)
-        if (q < cnt) acc = dadd(acc, v[q]);
-    }
-  }
-  __syncwarp();
-  return acc;
-}
-
-constexpr int kWin = 256;  // products per warp window
-
-// acc <- (((acc + w_0) + w_1) + ... + w_{cnt-1}) over the warp's window (lanes
-// wrote it); lane 0 runs the chain, batches of 16 128-bit loads ahead of it.
-__device__ __forceinline__ double window_chain(const double* wwin, int lane, int cnt, double acc) {
-  __syncwarp();
-  if (lane == 0) {
-    const double2* w2 = reinterpret_cast<const double2*>(wwin);
-    for (int b = 0; b < cnt; b += 32) {
-      double v[32];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const double2 t = w2[(b >> 1) + q];
-        v[2 * q] = t.x;
-        v[2 * q + 1] = t.y;
-      }
-      const int mm = min(32, cnt - b);
-      if (mm == 32) {
-#pragma unroll
-        for (int q = 0; q < 32; ++q) acc = dadd(acc, v[q]);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 32; ++q)
-          if (q < mm) acc = dadd(acc, v[q]);
-      }
-    }
-  }
-  __syncwarp();
-  return acc;
-}
+constexpr int kWin = 256;  // per-warp window doubles (sizes the shared window area)
 
 // Producer/consumer ring (P1, P2 when the staged vector fits): warps
 // 0..kProdWarps-1 compute the terms of up to 32 chains (one chain per row
@@ -198,17 +140,10 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
   extern __shared__ __align__(16) double dyn[];  // 2*kVec + (warps)*kWin doubles
   double* vA = dyn;
   double* vB = dyn + kVec;
-  double* wwin = dyn + 2 * kVec + (threadIdx.x >> 5) * kWin;
-  double* wbuf = wwin;
   const unsigned nb = gridDim.x;
   const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long gthreads = (long long)nb * blockDim.x;
   const int lane = threadIdx.x & 31;
-  // Rows are dealt round-robin over SMs first (warp-major), so a few hundred
-  // dependent chains spread over all SMs instead of saturating the FP64 pipes
-  // of the first few.
-  const long long gwarp = (long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
-  const long long gwarps = (long long)nb * (blockDim.x >> 5);
   const long long LD = a.LD;
   const int nu = a.n_u;
   int K = a.K0;
@@ -282,28 +217,34 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     }
     if (!last) stamp(a.trace, n, 1);
     if (upd || !last) {
-      // Stage g (and y_{n-1}) in shared memory: once when it fits (rows then
-      // proceed without CTA synchronization), else per chunk of kVec.
-      const bool one_chunk = Kn <= kVec;
+      // g (and y_{n-1}) in shared memory when they fit (sm); otherwise g in
+      // this CTA's global scratch row and y read from the global y buffer
+      // (both L2-resident; the producers prefetch them with U).
+      const bool sm = Kn <= a.kvec;
+      double* gsc = a.gscr + (long long)blockIdx.x * (LD + 1);
       auto stage = [&](int c0, int c1) {
         __syncthreads();
         for (int j = c0 + threadIdx.x; j < c1; j += blockDim.x) {
-          if (!last)
-            vA[j - c0] = (j < a.K0) ? a.Gb[(long long)j * nu + n]
-                       : (j < Ko)   ? a.Gc[(long long)ldg_cg(&a.kept_cand[j - a.K0]) * nu + n]
-                                    : a.Gc[(long long)prev_n * nu + n];  // j == Ko: x_{n-1}
-          if (upd) vB[j - c0] = (j < Ko) ? ldg_cg(&yprev[j]) : 0.0;
+          if (!last) {
+            const double gj = (j < a.K0) ? a.Gb[(long long)j * nu + n]
+                            : (j < Ko)   ? a.Gc[(long long)ldg_cg(&a.kept_cand[j - a.K0]) * nu + n]
+                                         : a.Gc[(long long)prev_n * nu + n];  // j == Ko: x_{n-1}
+            if (sm) vA[j - c0] = gj;
+            else gsc[j] = gj;
+          }
+          if (upd && sm) vB[j - c0] = (j < Ko) ? ldg_cg(&yprev[j]) : 0.0;
         }
         __syncthreads();
       };
-      if (one_chunk && pre) {
+      auto yval = [&](long long i) -> double { return sm ? vB[i] : ldg_cg(&yprev[i]); };
+      if (sm && pre) {
         // g (j < Ko) and y_{n-1} were staged during P3 of n-1; add x_{n-1}'s column
         if (upd && threadIdx.x == 0) {
           vA[Ko] = a.Gc[(long long)prev_n * nu + n];
           vB[Ko] = 0.0;
         }
         __syncthreads();
-      } else if (one_chunk) {
+      } else {
         stage(0, Kn);
       }
       if (!last) stamp(a.trace, n, 2);
@@ -314,9 +255,10 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
       // check fails.
       const double rdelta = upd ? __drcp_rn(prev_delta) : 0.0;
       auto unew = [&](long long i, int j, double uo) -> double {
-        const double num = (i < Ko && j < Ko) ? dmul(vB[i], vB[j])
+        const double yi = i < Ko ? yval(i) : 0.0, yj = j < Ko ? yval(j) : 0.0;
+        const double num = (i < Ko && j < Ko) ? dmul(yi, yj)
                          : (i == Ko && j == Ko) ? 1.0
-                         : (i == Ko) ? -vB[j] : -vB[i];
+                         : (i == Ko) ? -yj : -yi;
         bool ok;
         double qd = ddiv_rcp(num, prev_delta, rdelta, &ok);
         if (!ok) qd = ddiv_slow(num, prev_delta);
@@ -328,14 +270,14 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
       const int Q = ((Rs + 31) / 32) * nch;
       const int warp = threadIdx.x >> 5;
       double* ring = dyn + 2 * kVec;
-      if (one_chunk && last) {
+      if (last) {
         for (long long e = threadIdx.x; e < (long long)Rs * Kn; e += blockDim.x) {
           const int r = (int)(e / Kn), j = (int)(e - (long long)r * Kn);
           const long long i = blockIdx.x + (long long)nb * r;
           double* up = a.U + i * LD + j;
           *up = unew(i, j, (i < Ko && j < Ko) ? ldg_cg(up) : 0.0);
         }
-      } else if (one_chunk && is_producer(warp)) {
+      } else if (is_producer(warp)) {
         // producers: U_new and the products U_new[i][j] g_j of 32 rows x
         // kRingW steps; the next chunk's U loads are in flight meanwhile.
         // (Bulk/TMA staging of the U segments measured slower: it inflates
@@ -343,6 +285,9 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         const int pi = producer_index(warp, lane);
         const int t = pi % kRingW, rq = pi / kRingW;
         double uv[kRowSlots];
+        double gn = 0.0, yn = 0.0;  // g_j, y_j of the prefetched chunk (global-operand mode)
+        double ryi[kRowSlots];
+        int ygrp = -1;
         auto load = [&](int q) {
           const int g = q / nch, j = (q - g * nch) * kRingW + t;
           const int nr = min(32, Rs - 32 * g);
@@ -353,6 +298,10 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
             uv[k] = 0.0;
             if (r < nr && j < Ko && i < Ko) uv[k] = ldg_cg(&a.U[i * LD + j]);
           }
+          if (!sm) {
+            gn = j < Kn ? ldg_cg(&gsc[j]) : 0.0;
+            yn = (upd && j < Ko) ? ldg_cg(&yprev[j]) : 0.0;
+          }
         };
         if (Q > 0) load(0);
         for (int q = 0; q < Q; ++q) {
@@ -362,8 +311,16 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
           double* rb = ring + b * (kRingW * kRingS) + t * kRingS;
           if (q >= kRingSlots) nbar_sync(1 + kRingSlots + b, kRingThreads);
           const bool jin = j < Kn;
-          const double gj = jin ? vA[j] : 0.0;
-          const double yj = (jin && j < Ko) ? vB[j] : 0.0;
+          const double gj = sm ? (jin ? vA[j] : 0.0) : gn;
+          const double yj = sm ? ((jin && j < Ko) ? vB[j] : 0.0) : yn;
+          if (upd && !sm && g != ygrp) {  // y_i of this group's rows (global-operand mode)
+            ygrp = g;
+#pragma unroll
+            for (int k = 0; k < kRowSlots; ++k) {
+              const long long i = blockIdx.x + (long long)nb * (32 * g + min(rq + kRowPh * k, 31));
+              ryi[k] = i < Ko ? ldg_cg(&yprev[i]) : 0.0;
+            }
+          }
 #pragma unroll
           for (int k = 0; k < kRowSlots; ++k) {
             const int r = rq + kRowPh * k;
@@ -374,9 +331,10 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
                 double un = uv[k];
                 if (upd) {
                   // fiber_basis.cpp:97-105 (see unew)
-                  const double num = (i < Ko && j < Ko) ? dmul(vB[i], yj)
+                  const double yi = i < Ko ? (sm ? vB[i] : ryi[k]) : 0.0;
+                  const double num = (i < Ko && j < Ko) ? dmul(yi, yj)
                                    : (i == Ko && j == Ko) ? 1.0
-                                   : (i == Ko) ? -yj : -vB[i];
+                                   : (i == Ko) ? -yj : -yi;
                   bool ok;
                   double qd = ddiv_rcp(num, prev_delta, rdelta, &ok);
                   if (!ok) qd = ddiv_slow(num, prev_delta);
@@ -391,7 +349,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
           nbar_arrive(1 + b, kRingThreads);
           if (q + 1 < Q) load(q + 1);
         }
-      } else if (one_chunk && warp == kChainWarp) {
+      } else if (warp == kChainWarp) {
         // chain warp: y_i = sum_j fl(U_new[i][j] g_j) in j order (dense_matrix.cpp:42-47)
         double acc = 0.0;
         long long tw = 0, tcc = 0;
@@ -417,81 +375,6 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
           a.trace[(long long)n * kTraceW + 11] = tcc;
         }
       }
-      for (long long rb = 0; !one_chunk && rb < Kn; rb += gwarps) {
-        const long long i = rb + gwarp;
-        const bool active = i < Kn;
-        const double yi = (upd && active && i < Ko) ? ldg_cg(&yprev[i]) : 0.0;
-        double* urow = a.U + (active ? i : 0) * LD;
-        double acc = 0.0;
-        for (int c0 = 0; c0 < Kn; c0 += kVec) {
-          const int c1 = min(Kn, c0 + kVec);
-          if (!one_chunk) stage(c0, c1);
-          if (!active) continue;
-          // Windows of kWin elements: 8 loads in flight per lane, all U
-          // updates and products computed lane-parallel into the warp's
-          // window, then lane 0 runs the add chain over the window.
-          double u[kWin / 32];
-#pragma unroll
-          for (int s = 0; s < kWin / 32; ++s) {
-            const int j = c0 + 32 * s + lane;
-            u[s] = (j < c1 && j < Ko && i < Ko) ? ldg_cg(&urow[j]) : 0.0;
-          }
-          for (int j0 = c0; j0 < c1; j0 += kWin) {
-            double unv[kWin / 32];
-            if (upd) {
-              // U_new[i][j] = fl(U + fl(fl(y_i y_j)/d)): branch-free exact
-              // divisions (overlapping), certified; a lane whose check fails
-              // redoes its window with __ddiv_rn.
-              bool wok = true;
-#pragma unroll
-              for (int s = 0; s < kWin / 32; ++s) {
-                const int j = j0 + 32 * s + lane;
-                const double num = (i < Ko && j < Ko) ? dmul(yi, vB[j - c0])
-                                 : (i == Ko && j == Ko) ? 1.0
-                                 : (i == Ko) ? -vB[j - c0] : -yi;
-                bool ok;
-                const double qd = ddiv_try(num, prev_delta, &ok);
-                wok &= ok | (j >= c1);
-                unv[s] = (i < Ko && j < Ko) ? dadd(u[s], qd) : qd;
-              }
-              if (__any_sync(0xffffffffu, !wok) && !wok) {
-#pragma unroll
-                for (int s = 0; s < kWin / 32; ++s) {
-                  const int j = j0 + 32 * s + lane;
-                  if (j >= c1) continue;
-                  if (i < Ko && j < Ko) unv[s] = dadd(u[s], ddiv(dmul(yi, vB[j - c0]), prev_delta));
-                  else if (i == Ko && j == Ko) unv[s] = ddiv(1.0, prev_delta);
-                  else if (i == Ko) unv[s] = ddiv(-vB[j - c0], prev_delta);
-                  else unv[s] = ddiv(-yi, prev_delta);
-                }
-              }
-            } else {
-#pragma unroll
-              for (int s = 0; s < kWin / 32; ++s) unv[s] = u[s];
-            }
-#pragma unroll
-            for (int s = 0; s < kWin / 32; ++s) {
-              const int j = j0 + 32 * s + lane;
-              double p = 0.0;
-              if (j < c1) {
-                if (upd) urow[j] = unv[s];
-                if (!last) p = dmul(unv[s], vA[j - c0]);
-              }
-              wwin[32 * s + lane] = p;
-            }
-            const int jn = j0 + kWin;  // next window's U loads overlap this chain
-            if (jn < c1) {
-#pragma unroll
-              for (int s = 0; s < kWin / 32; ++s) {
-                const int j = jn + 32 * s + lane;
-                u[s] = (j < c1 && j < Ko && i < Ko) ? ldg_cg(&urow[j]) : 0.0;
-              }
-            }
-            if (!last) acc = window_chain(wwin, lane, min(kWin, c1 - j0), acc);
-          }
-        }
-        if (!last && active && lane == 0) ycur[i] = acc;
-      }
     }
     K = Kn;
     if (last) break;
@@ -500,7 +383,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     stamp(a.trace, n, 4);
     // ---------------- P2: z over R's rows, residual terms ---------------------
     const int srn = ldg_cg(a.sr_n);
-    const bool y_fits = K <= kVec;
+    const bool y_fits = K <= a.kvec;
     auto stage_y = [&](int c0, int c1) {
       __syncthreads();
       for (int j = c0 + threadIdx.x; j < c1; j += blockDim.x) vA[j - c0] = ldg_cg(&ycur[j]);
@@ -508,7 +391,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     };
     if (y_fits) stage_y(0, K);
     stamp(a.trace, n, 10);
-    if (y_fits) {
+    {
       // Ring sessions of up to kMeta rows of R owned by this CTA (positions
       // q = blockIdx.x + nb * r of the first-appearance list); warp w stages
       // the metadata of group w (32 rows) in the free vB area.
@@ -592,7 +475,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
               const int r = rq + kRowPh * k;
               if (r < nr) {  // warp-uniform: a warp covers 32 steps of one row
                 const bool ok = (okm >> k) & 1;
-                const double yk = ok ? vA[kv[k]] : 0.0;
+                const double yk = ok ? (y_fits ? vA[kv[k]] : ldg_cg(&ycur[kv[k]])) : 0.0;
                 rb[r] = dmul(yk, vv[k]);
                 if (!((found >> k) & 1)) {
                   // first kept column of the row with y != 0 (the touch order)
@@ -644,71 +527,6 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
             }
           }
         }
-      }
-    }
-    for (long long rb = 0; !y_fits && rb < srn; rb += gwarps) {
-      const long long q = rb + gwarp;
-      int r = 0, L = 0, e = 0, kfd = -1, kst = -1;
-      long long b0 = 0;
-      double z = 0.0;
-      if (q < srn) {
-        r = ldg_cg(&a.sr_list[q]);
-        b0 = a.rowbase[r];
-        L = ldg_cg(&a.rowlen[r]);
-      }
-      for (int c0 = 0; c0 < K; c0 += kVec) {
-        const int c1 = min(K, c0 + kVec);
-        if (!y_fits) stage_y(c0, c1);
-        if (q >= srn) continue;
-        if (K <= kVec) {
-          // whole row in one chunk: windows of kWin entries, all loads first
-          for (; e < L; e += kWin) {
-            int kk[kWin / 32];
-            double vv[kWin / 32];
-#pragma unroll
-            for (int s = 0; s < kWin / 32; ++s) {
-              const int t = e + 32 * s + lane;
-              kk[s] = t < L ? ldg_cg(&a.rek[b0 + t]) : 0;
-              vv[s] = t < L ? ldg_cg(&a.rev[b0 + t]) : 0.0;
-            }
-#pragma unroll
-            for (int s = 0; s < kWin / 32; ++s) {
-              const int t = e + 32 * s + lane;
-              const double yk = t < L ? vA[kk[s]] : 0.0;
-              wwin[32 * s + lane] = dmul(yk, vv[s]);
-              if (kst < 0) kst = __shfl_sync(0xffffffffu, kk[s], 0);
-              const unsigned nz = __ballot_sync(0xffffffffu, t < L && yk != 0.0);
-              if (kfd < 0 && nz) kfd = __shfl_sync(0xffffffffu, kk[s], __ffs(nz) - 1);
-            }
-            z = window_chain(wwin, lane, min(kWin, L - e), z);
-          }
-        } else {
-          while (e < L) {
-            const int t = e + lane;
-            const int k = (t < L) ? ldg_cg(&a.rek[b0 + t]) : 0x7fffffff;
-            const bool in = k < c1;  // entries sorted by k: `in` is a lane prefix
-            const unsigned inmask = __ballot_sync(0xffffffffu, in);
-            if (!inmask) break;
-            const double yk = in ? vA[k - c0] : 0.0;
-            const double p = in ? dmul(yk, ldg_cg(&a.rev[b0 + t])) : 0.0;
-            if (kst < 0) kst = __shfl_sync(0xffffffffu, k, 0);
-            const unsigned nzmask = __ballot_sync(0xffffffffu, in && yk != 0.0);
-            if (kfd < 0 && nzmask) kfd = __shfl_sync(0xffffffffu, k, __ffs(nzmask) - 1);
-            const int cnt = __popc(inmask);
-            z = warp_chain(wbuf, lane, p, cnt, z);
-            e += cnt;
-            if (cnt < 32) break;
-          }
-        }
-      }
-      if (rb == 0) stamp(a.trace, n, 11);
-      if (q < srn && lane == 0) {
-        zdn[r] = z;
-        a.kf[r] = kfd;
-        a.term[q] = (ldg_cg(&a.tag[r]) == tg) ? 0.0 : dsqr(z);
-        // touched order differs from first-appearance order only if the row's
-        // first kept column has y == 0 while the row is still touched.
-        if (z != 0.0 && kfd != kst) atomicExch(&a.slow[n], 1);
       }
     }
     stamp(a.trace, n, 5);
@@ -778,7 +596,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     // decision): tag its rows, zero its z half, stage g_{n+1} over the current
     // K columns and y_n.  Not when the slow touch-order path is active (it
     // reads the tags of n) or the vectors do not fit one staging chunk.
-    const bool prestage = !slow && n + 1 < nu && K + 1 <= kVec;
+    const bool prestage = !slow && n + 1 < nu && K + 1 <= a.kvec;
     const int ncw = (int)(nb + 31) / 32;  // combine warps of warp_grid_sum
     if ((int)(threadIdx.x >> 5) < ncw) {
       SliceDirect* sd = reinterpret_cast<SliceDirect*>(dyn + 2 * kVec);  // ring area, idle in P3

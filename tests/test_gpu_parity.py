@@ -228,3 +228,36 @@ def test_errors(ctx):
     bad = ctd.SparseTensor([3, 3, 3], np.array([[0, 0, 5]], np.int64), np.array([1.0]))
     with pytest.raises(ctd.ShapeError):
         ctd.ctd_s(bad, 0, 5, ctx=ctx)
+
+
+_KVEC_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_1710_03608_b200 as ctd
+from paper_1710_03608_b200 import datagen as g
+from oracle.bindings import Port
+port = Port()
+cases = [g.c1(), g.traffic([500, 500, 20], 20000, 11), g.low_rank([40, 12, 10], 3, 0.7, 9)]
+assert ctd.ctd_s(ctd.SparseTensor.from_datagen(cases[0]), 0, 300, 1e-6, 42).kept_count() > 64
+for x in cases:
+    f = ctd.ctd_s(ctd.SparseTensor.from_datagen(x), 0, 300, 1e-6, 42)
+    o = port.frontend(x.shape, x.idx.reshape(-1), x.val, 0, 300, 1e-6, 42)
+    assert np.array_equal(f.kept_flat, o.kept_flat)
+    assert np.array_equal(f.accepted, o.accepted)
+    assert np.array_equal(f.delta.view(np.int64), o.delta.view(np.int64))
+    assert np.array_equal(f.U.view(np.int64), o.U.view(np.int64))
+print("OK")
+"""
+
+
+def test_filter_global_operand_path():
+    """K beyond the shared-memory staging limit: g and y come from global
+    memory (CTD_FILTER_KVEC lowers the limit to 64 in a fresh process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CTD_FILTER_KVEC="64")
+    r = subprocess.run([sys.executable, "-c", _KVEC_SCRIPT.format(root=root)], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
