@@ -1,0 +1,148 @@
+"""The compiled C++ drop-in (paper_1710_03608_b200/shim): the reference's own
+library relinked with `ld --wrap` so ctd::ctd_s / ctd::init_stream /
+ctd::ctd_d_step run on the B200 through libctd_gpu.so.  The reference's own
+driver code (oracle/ref_driver.cpp, through the `Ref` binding) is called on
+both builds: the unmodified CPU library and the drop-in; everything the
+caller sees (kept fibers, R, U, the folded core C, relative_error and
+memory_usage computed by the reference's own evaluation code on the returned
+factors, the stream's matricized core) must be identical."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from paper_1710_03608_b200 import datagen as g
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DROPIN = os.path.join(ROOT, "paper_1710_03608_b200", "shim", "libctd_dropin.so")
+WRAPPED = ("_ZN3ctd5ctd_sERKNS_12SparseTensorEildm",
+           "_ZN3ctd11init_streamERKNS_12SparseTensorEildmbb",
+           "_ZN3ctd10ctd_d_stepENS_11StreamStateERKNS_12SparseTensorEl")
+
+needs_dropin = pytest.mark.skipif(not os.path.exists(DROPIN),
+                                  reason="drop-in not built (make -C paper_1710_03608_b200/shim)")
+
+
+@needs_dropin
+def test_dropin_exports_wrappers():
+    """Loads on a GPU-less host; the wrapped entry points and the reference
+    driver's symbols are present."""
+    lib = C.CDLL(DROPIN)
+    for s in WRAPPED:
+        assert hasattr(lib, "__wrap_" + s), s
+    for s in ("ref_ctd_s", "ref_init_stream", "ref_stream_step", "ref_relative_error"):
+        assert hasattr(lib, s), s
+
+
+def _fold_c(R, h):
+    L = R.L
+    n = int(L.ref_factors_c_nnz(h))
+    order = int(L.ref_factors_c_order(h))
+    shape = np.zeros(order, np.int64)
+    L.ref_factors_c_shape(h, shape.ctypes.data)
+    idx = np.zeros(n * order, np.int64)
+    val = np.zeros(n)
+    L.ref_factors_c(h, idx.ctypes.data, val.ctypes.data)
+    return shape, idx, val
+
+
+def _ctd_s_full(R, x, mode, s, eps, seed):
+    t = R.tensor(x.shape, x.flat_idx(), x.val)
+    h = C.c_void_p()
+    R._chk(R.L.ref_ctd_s(t.h, mode, s, eps, C.c_uint64(seed), C.byref(h)), "ctd_s")
+    try:
+        fe = R._factors(h, False)
+        shape, idx, val = _fold_c(R, h)
+        e, m = C.c_double(), C.c_double()
+        R._chk(R.L.ref_relative_error(t.h, h, C.byref(e)), "relative_error")
+        R._chk(R.L.ref_memory_usage(t.h, h, C.byref(m)), "memory_usage")
+        return fe, shape, idx, val, e.value, m.value
+    finally:
+        R.L.ref_factors_free(h)
+
+
+CASES = {
+    "c1": (lambda: g.c1(), 0, 200),
+    "rand_fp_m1": (lambda: g.random_sparse([30, 40, 50], 0.05, 7), 1, 300),
+    "traffic": (lambda: g.traffic([500, 500, 20], 20000, 11), 0, 400),
+    "order4": (lambda: g.random_sparse([8, 9, 10, 11], 0.05, 12), 2, 150),
+}
+
+
+@pytest.fixture(scope="module")
+def dropin():
+    from oracle.bindings import Ref
+    return Ref(DROPIN)
+
+
+@pytest.mark.gpu
+@needs_dropin
+@pytest.mark.parametrize("name", list(CASES))
+def test_dropin_ctd_s(ref, dropin, name):
+    make, mode, s = CASES[name]
+    x = make()
+    a = _ctd_s_full(ref, x, mode, s, 1e-6, 42)
+    b = _ctd_s_full(dropin, x, mode, s, 1e-6, 42)
+    fa, fb = a[0], b[0]
+    assert np.array_equal(fa.kept_flat, fb.kept_flat)
+    assert np.array_equal(fa.U.view(np.int64), fb.U.view(np.int64))
+    assert np.array_equal(fa.R.col_ptr, fb.R.col_ptr)
+    assert np.array_equal(fa.R.row, fb.R.row)
+    assert np.array_equal(fa.R.val.view(np.int64), fb.R.val.view(np.int64))
+    assert np.array_equal(a[1], b[1])  # folded core shape
+    assert np.array_equal(a[2], b[2])  # core coordinates (reference fold order)
+    assert np.array_equal(a[3].view(np.int64), b[3].view(np.int64))  # core values, bit for bit
+    # the reference's own evaluation on identical factors: identical results
+    assert a[4] == b[4] or abs(a[4] - b[4]) <= 1e-9 * max(1.0, abs(a[4]))
+    assert a[5] == b[5]
+
+
+@pytest.mark.gpu
+@needs_dropin
+def test_dropin_errors(ref, dropin):
+    from oracle.bindings import OracleError
+    x = g.c1()
+    for mode, s, eps in ((3, 10, 1e-6), (0, 0, 1e-6), (0, 10, 0.0)):
+        codes = []
+        for R in (ref, dropin):
+            t = R.tensor(x.shape, x.flat_idx(), x.val)
+            h = C.c_void_p()
+            with pytest.raises(OracleError) as ei:
+                R._chk(R.L.ref_ctd_s(t.h, mode, s, eps, C.c_uint64(42), C.byref(h)), "ctd_s")
+            codes.append(ei.value.code)
+        assert codes[0] == codes[1], (mode, s, eps, codes)
+
+
+@pytest.mark.gpu
+@needs_dropin
+@pytest.mark.parametrize("keep_history", [False, True])
+def test_dropin_stream(ref, dropin, keep_history):
+    x = g.c3_stream(seed=5, n_steps=3, slices_per_step=3, draws_per_slice=2500, n=300,
+                    planted_step=2, block=20)
+    hist = x.time_slab(0, 3)
+    sa = ref.stream(ref.tensor(hist.shape, hist.flat_idx(), hist.val), 0, 120, 1e-6, 7,
+                    keep_history=keep_history)
+    sb = dropin.stream(dropin.tensor(hist.shape, hist.flat_idx(), hist.val), 0, 120, 1e-6, 7,
+                       keep_history=keep_history)
+    grew = 0
+    for t in range(3, x.shape[2]):
+        slab = x.time_slab(t, t + 1)
+        k0 = len(sa.factors().kept_flat)
+        sa.step(ref.tensor(slab.shape, slab.flat_idx(), slab.val), 40)
+        sb.step(dropin.tensor(slab.shape, slab.flat_idx(), slab.val), 40)
+        fa, fb = sa.factors(), sb.factors()
+        grew += len(fa.kept_flat) > k0
+        assert sa.t == sb.t == t + 1
+        assert np.array_equal(fa.kept_flat, fb.kept_flat), t
+        assert np.array_equal(fa.U.view(np.int64), fb.U.view(np.int64)), t
+        assert np.array_equal(fa.R.row, fb.R.row) and np.array_equal(fa.R.val, fb.R.val), t
+        ca, cb = sa.core(), sb.core()
+        assert (ca.rows, ca.cols) == (cb.rows, cb.cols), t
+        assert np.array_equal(ca.col_ptr, cb.col_ptr), t
+        assert np.array_equal(ca.row, cb.row), t
+        assert np.array_equal(ca.val.view(np.int64), cb.val.view(np.int64)), t
+        if keep_history:  # core_drift reads the retained history (concatenated by the shim)
+            da, db = sa.core_drift(), sb.core_drift()
+            assert da == db or abs(da - db) <= 1e-9 * max(1.0, abs(da)), t
+    assert grew >= 1
