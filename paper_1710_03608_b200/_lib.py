@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libctd_gpu.so")
+# CTD_GPU_LIB: an alternative build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("CTD_GPU_LIB") or os.path.join(HERE, "libctd_gpu.so")
 
 _lib = None
 

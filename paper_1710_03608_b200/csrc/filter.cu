@@ -465,8 +465,9 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
       fprintf(stderr, " | P3:");
       for (int k = 17; k <= 24; ++k)
         if (tr[i * kTraceW + k] && tr[i * kTraceW + k - 1]) fprintf(stderr, " %lld", tr[i * kTraceW + k] - tr[i * kTraceW + k - 1]);
-      fprintf(stderr, " directs=%lld | P1 prod wait=%lld compute=%lld", tr[i * kTraceW + 25], tr[i * kTraceW + 27],
-              tr[i * kTraceW + 28]);
+      fprintf(stderr, " directs=%lld | P1 prod wait=%lld compute=%lld probe=%lld", tr[i * kTraceW + 25],
+              tr[i * kTraceW + 28], tr[i * kTraceW + 29], tr[i * kTraceW + 27]);
+      fprintf(stderr, " | uncertified div=%lld", tr[i * kTraceW + 30]);
       fprintf(stderr, "\n");
     }
   }

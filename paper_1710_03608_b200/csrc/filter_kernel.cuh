@@ -17,6 +17,8 @@
 // Two grid barriers per candidate (P1|P2, P2|P3); P3 needs none after it
 // because every CTA derives the same decision.
 
+#include <type_traits>
+
 constexpr int kFThreads = 512;
 constexpr int kVec = 4096;  // doubles per staged vector (two buffers)
 
@@ -29,18 +31,32 @@ constexpr int kWin = 256;  // per-warp window doubles (sizes the shared window a
 // lane.  Slots are handed over with named barriers: "full" 1+b, "empty"
 // 1+kRingSlots+b.  (Measured with tools/ubench_ring.cu: fewer/smaller slots
 // couple the chain to the producers' latency.)
-constexpr int kRingW = 96;                 // steps per ring chunk
+#ifndef CTD_RING_W
+#define CTD_RING_W 96
+#endif
+#ifndef CTD_RING_SLOTS
+#define CTD_RING_SLOTS 3
+#endif
+constexpr int kRingW = CTD_RING_W;         // steps per ring chunk
 constexpr int kRingS = 33;                 // padded lane stride (doubles)
-constexpr int kRingSlots = 3;
+constexpr int kRingSlots = CTD_RING_SLOTS;
 constexpr int kRingDoubles = kRingSlots * kRingW * kRingS;
 // (Keeping producers off the chain warp's SM sub-partition measured slower:
 // the producers, not issue-slot sharing, bound the ring.)
 constexpr int kChainWarp = kFThreads / 32 - 1;
+#ifdef CTD_RING_AVOID_SMSP
+// producers only on the three SM sub-partitions the chain warp does not use
+// (warp w runs on sub-partition w % 4)
+constexpr int kProdWarps = (kFThreads / 32) / 4 * 3;
+__device__ __forceinline__ bool is_producer(int warp) { return (warp & 3) != (kChainWarp & 3); }
+__device__ __forceinline__ int producer_index(int warp, int lane) { return (warp - (warp >> 2)) * 32 + lane; }
+#else
 constexpr int kProdWarps = kFThreads / 32 - 1;
-constexpr int kProdThreads = kProdWarps * 32;
-constexpr int kRingThreads = kProdThreads + 32;   // named-barrier participants
 __device__ __forceinline__ bool is_producer(int warp) { return warp < kProdWarps; }
 __device__ __forceinline__ int producer_index(int warp, int lane) { return warp * 32 + lane; }
+#endif
+constexpr int kProdThreads = kProdWarps * 32;
+constexpr int kRingThreads = kProdThreads + 32;   // named-barrier participants
 // Producer thread p owns step t = p % kRingW of every chunk and the rows
 // r = p / kRingW + kRowPh * k (k < kRowSlots) of the 32-row group.
 constexpr int kRowPh = kProdThreads / kRingW;
@@ -63,22 +79,23 @@ __device__ __forceinline__ void nbar_arrive(int id, int cnt) {
 __device__ __forceinline__ double lane_chain(const double* rb, int lane, int cnt, double acc) {
   const double* p = rb + lane;
   if (cnt == kRingW) {
+    // The batch h+1 loads are issued in iteration h of a loop that is NOT
+    // unrolled, so they stay 16 adds (~130 cycles) ahead of their use: fully
+    // unrolled, ptxas re-interleaves them ~4 adds ahead, which the ring's
+    // shared-memory traffic then exposes on every add.
     double v[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) v[q] = p[q * kRingS];
-#pragma unroll
+#pragma unroll 1
     for (int h = 0; h < kRingW / 16; ++h) {
       double w[16];
-      if (h + 1 < kRingW / 16) {
+      const double* pn = p + (h + 1 < kRingW / 16 ? h + 1 : h) * 16 * kRingS;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) w[q] = p[((h + 1) * 16 + q) * kRingS];
-      }
+      for (int q = 0; q < 16; ++q) w[q] = pn[q * kRingS];
 #pragma unroll
       for (int q = 0; q < 16; ++q) acc = dadd(acc, v[q]);
-      if (h + 1 < kRingW / 16) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = w[q];
-      }
+      for (int q = 0; q < 16; ++q) v[q] = w[q];
     }
   } else {
     for (int t = 0; t < cnt; ++t) acc = dadd(acc, p[t * kRingS]);
@@ -280,79 +297,121 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
       } else if (is_producer(warp)) {
         // producers: U_new and the products U_new[i][j] g_j of 32 rows x
         // kRingW steps; the next chunk's U loads are in flight meanwhile.
+        // The producers are issue-bound, so the row slots this thread owns
+        // in a group (NA <= kRowSlots, warp-uniform) are a compile-time
+        // count: no predicated-off work for absent rows.
         // (Bulk/TMA staging of the U segments measured slower: it inflates
         // the chain warp's latency, tools/ubench_ring.cu.)
         const int pi = producer_index(warp, lane);
-        const int t = pi % kRingW, rq = pi / kRingW;
-        double uv[kRowSlots];
-        double gn = 0.0, yn = 0.0;  // g_j, y_j of the prefetched chunk (global-operand mode)
-        double ryi[kRowSlots];
-        int ygrp = -1;
-        auto load = [&](int q) {
-          const int g = q / nch, j = (q - g * nch) * kRingW + t;
-          const int nr = min(32, Rs - 32 * g);
+        const int t = pi % kRingW, rq = pi / kRingW;  // rq is warp-uniform
+        double* ring_t = ring + t * kRingS;
+        const bool ptr = a.trace && blockIdx.x == 0 && pi == 0;
+        long long pwt = 0, pct = 0;
+        int q = 0;
+        auto group = [&](int g, auto na_c) {
+          constexpr int NA = decltype(na_c)::value;
+          double* up[NA];
+          double yi[NA];
+          unsigned inew = 0;
 #pragma unroll
-          for (int k = 0; k < kRowSlots; ++k) {
-            const int r = rq + kRowPh * k;
-            const long long i = blockIdx.x + (long long)nb * (32 * g + r);
-            uv[k] = 0.0;
-            if (r < nr && j < Ko && i < Ko) uv[k] = ldg_cg(&a.U[i * LD + j]);
+          for (int k = 0; k < NA; ++k) {
+            const long long i = blockIdx.x + (long long)nb * (32 * g + rq + kRowPh * k);
+            up[k] = a.U + i * LD;
+            yi[k] = (upd && i < Ko) ? yval(i) : 0.0;
+            inew |= (unsigned)(i == Ko) << k;
           }
-          if (!sm) {
-            gn = j < Kn ? ldg_cg(&gsc[j]) : 0.0;
-            yn = (upd && j < Ko) ? ldg_cg(&yprev[j]) : 0.0;
+          double uv[NA];
+          double gn = 0.0, yn = 0.0;  // g_j, y_j of the prefetched chunk (global-operand mode)
+          auto load = [&](int j) {
+#pragma unroll
+            for (int k = 0; k < NA; ++k) uv[k] = (j < Ko && !((inew >> k) & 1)) ? ldg_cg(up[k] + j) : 0.0;
+            if (!sm) {
+              gn = j < Kn ? ldg_cg(&gsc[j]) : 0.0;
+              yn = (upd && j < Ko) ? ldg_cg(&yprev[j]) : 0.0;
+            }
+          };
+          load(t);
+          for (int j0 = 0; j0 < Kn; j0 += kRingW, ++q) {
+            const int j = j0 + t;
+            const int b = q % kRingSlots;
+            double* rb = ring_t + b * (kRingW * kRingS);
+            const long long pt0 = ptr ? clock64() : 0;
+            if (q >= kRingSlots) nbar_sync(1 + kRingSlots + b, kRingThreads);
+            const long long pt1 = ptr ? clock64() : 0;
+            const bool jin = j < Kn;
+            const double gj = sm ? (jin ? vA[j] : 0.0) : gn;
+            double un[NA];
+#pragma unroll
+            for (int k = 0; k < NA; ++k) un[k] = uv[k];
+            if (upd) {
+              // fiber_basis.cpp:97-105: fl(U + fl(fl(y_i y_j)/d)); the new
+              // row/column -y/d; the corner 1/d
+              const double yj = sm ? ((j < Ko) ? vB[j] : 0.0) : yn;
+              const bool jnew = j == Ko;
+              unsigned bad = 0;
+#pragma unroll
+              for (int k = 0; k < NA; ++k) {
+                const bool in = (inew >> k) & 1;
+                const double num = in ? (jnew ? 1.0 : -yj) : (jnew ? -yi[k] : dmul(yi[k], yj));
+                bool ok;
+                const double qd = ddiv_rcp(num, prev_delta, rdelta, &ok);
+                bad |= (unsigned)!ok << k;
+                un[k] = (in || jnew) ? qd : dadd(uv[k], qd);
+              }
+              if (bad) {  // rare: quotients the fast path could not certify
+#pragma unroll
+                for (int k = 0; k < NA; ++k)
+                  if ((bad >> k) & 1) {
+                    const bool in = (inew >> k) & 1;
+                    const double num = in ? (jnew ? 1.0 : -yj) : (jnew ? -yi[k] : dmul(yi[k], yj));
+                    const double qd = ddiv_slow(num, prev_delta);
+                    un[k] = (in || jnew) ? qd : dadd(uv[k], qd);
+                  }
+              }
+              if (jin) {
+#pragma unroll
+                for (int k = 0; k < NA; ++k) up[k][j] = un[k];
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < NA; ++k) rb[rq + kRowPh * k] = dmul(un[k], gj);
+            nbar_arrive(1 + b, kRingThreads);
+            if (ptr) {
+              pwt += pt1 - pt0;
+              pct += clock64() - pt1;
+            }
+            if (j0 + kRingW < Kn) load(j + kRingW);
           }
         };
-        if (Q > 0) load(0);
-        for (int q = 0; q < Q; ++q) {
-          const int g = q / nch, j = (q - g * nch) * kRingW + t;
+        for (int g = 0; g < (Rs + 31) / 32; ++g) {
           const int nr = min(32, Rs - 32 * g);
-          const int b = q % kRingSlots;
-          double* rb = ring + b * (kRingW * kRingS) + t * kRingS;
-          if (q >= kRingSlots) nbar_sync(1 + kRingSlots + b, kRingThreads);
-          const bool jin = j < Kn;
-          const double gj = sm ? (jin ? vA[j] : 0.0) : gn;
-          const double yj = sm ? ((jin && j < Ko) ? vB[j] : 0.0) : yn;
-          if (upd && !sm && g != ygrp) {  // y_i of this group's rows (global-operand mode)
-            ygrp = g;
-#pragma unroll
-            for (int k = 0; k < kRowSlots; ++k) {
-              const long long i = blockIdx.x + (long long)nb * (32 * g + min(rq + kRowPh * k, 31));
-              ryi[k] = i < Ko ? ldg_cg(&yprev[i]) : 0.0;
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < kRowSlots; ++k) {
-            const int r = rq + kRowPh * k;
-            if (r < nr) {
-              double p = 0.0;
-              if (jin) {
-                const long long i = blockIdx.x + (long long)nb * (32 * g + r);
-                double un = uv[k];
-                if (upd) {
-                  // fiber_basis.cpp:97-105 (see unew)
-                  const double yi = i < Ko ? (sm ? vB[i] : ryi[k]) : 0.0;
-                  const double num = (i < Ko && j < Ko) ? dmul(yi, yj)
-                                   : (i == Ko && j == Ko) ? 1.0
-                                   : (i == Ko) ? -yj : -yi;
-                  bool ok;
-                  double qd = ddiv_rcp(num, prev_delta, rdelta, &ok);
-                  if (!ok) qd = ddiv_slow(num, prev_delta);
-                  un = (i < Ko && j < Ko) ? dadd(un, qd) : qd;
-                  a.U[i * LD + j] = un;
-                }
-                p = dmul(un, gj);
+          const int nact = nr > rq ? (nr - rq + kRowPh - 1) / kRowPh : 0;  // row slots of this thread
+          switch (nact) {
+            case 0: {  // no rows: hand the slots over
+              for (int j0 = 0; j0 < Kn; j0 += kRingW, ++q) {
+                const int b = q % kRingSlots;
+                if (q >= kRingSlots) nbar_sync(1 + kRingSlots + b, kRingThreads);
+                nbar_arrive(1 + b, kRingThreads);
               }
-              rb[r] = p;
+              break;
             }
+            case 1: group(g, std::integral_constant<int, 1>{}); break;
+            case 2: group(g, std::integral_constant<int, 2>{}); break;
+            case 3: group(g, std::integral_constant<int, 3>{}); break;
+            case 4: group(g, std::integral_constant<int, 4>{}); break;
+            case 5: group(g, std::integral_constant<int, 5>{}); break;
+            case 6: group(g, std::integral_constant<int, 6>{}); break;
+            default: group(g, std::integral_constant<int, kRowSlots>{}); break;
           }
-          nbar_arrive(1 + b, kRingThreads);
-          if (q + 1 < Q) load(q + 1);
+        }
+        if (ptr) {
+          a.trace[(long long)n * kTraceW + 28] = pwt;
+          a.trace[(long long)n * kTraceW + 29] = pct;
         }
       } else if (warp == kChainWarp) {
         // chain warp: y_i = sum_j fl(U_new[i][j] g_j) in j order (dense_matrix.cpp:42-47)
         double acc = 0.0;
-        long long tw = 0, tcc = 0;
+        long long tw = 0, tcc = 0, tprobe = 0;
         for (int q = 0; q < Q; ++q) {
           const int g = q / nch, ch = q - g * nch;
           const int cnt = min(kRingW, Kn - ch * kRingW);
@@ -360,8 +419,24 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
           const long long tw0 = clock64();
           nbar_sync(1 + b, kRingThreads);
           tw += clock64() - tw0;
+#ifdef CTD_EXP_DADD_PROBE
+          {
+            // in-situ latency probe: 96 dependent register DADDs
+            const long long tp0 = clock64();
+            double d = (double)lane;
+#pragma unroll 1
+            for (int s = 0; s < 6; ++s) {
+#pragma unroll
+              for (int u = 0; u < 16; ++u) d = dadd(d, 1e-300);
+            }
+            tprobe += clock64() - tp0;
+            if (d == 12345.0) ring[lane] = d;
+          }
+#endif
           const long long tc0 = clock64();
+#ifndef CTD_EXP_NOCHAIN
           acc = lane_chain(ring + b * (kRingW * kRingS), lane, cnt, acc);
+#endif
           tcc += clock64() - tc0;
           if (q + kRingSlots < Q) nbar_arrive(1 + kRingSlots + b, kRingThreads);
           if (ch == nch - 1) {
@@ -373,6 +448,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         if (a.trace && blockIdx.x == 0 && lane == 0) {
           a.trace[(long long)n * kTraceW + 13] = tw;
           a.trace[(long long)n * kTraceW + 11] = tcc;
+          a.trace[(long long)n * kTraceW + 27] = tprobe;
         }
       }
     }
@@ -393,14 +469,18 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     stamp(a.trace, n, 10);
     {
       // Ring sessions of up to kMeta rows of R owned by this CTA (positions
-      // q = blockIdx.x + nb * r of the first-appearance list); warp w stages
-      // the metadata of group w (32 rows) in the free vB area.
+      // q = blockIdx.x + nb * r of the first-appearance list).  The rows of a
+      // session are ranked by length (longest first) so the 32-row groups are
+      // homogeneous: a group's chain runs for its longest row.
       int* s_row = reinterpret_cast<int*>(vB);
       int* s_len = s_row + kMeta;
       int* s_tf = s_len + kMeta;
       int* s_inx = s_tf + kMeta;
-      int* s_gch = s_inx + kMeta;  // [32] chunks per group
-      long long* s_base = reinterpret_cast<long long*>(s_gch + 32);
+      int* s_pos = s_inx + kMeta;  // original session position of ranked row
+      int* s_gch = s_pos + kMeta;  // [32] chunks per group
+      int* s_gmx = s_gch + 32;     // [32] longest row per group
+      long long* s_base = reinterpret_cast<long long*>(s_gmx + 32);
+      int* s_key = reinterpret_cast<int*>(s_base + kMeta);  // lengths by position (ranking)
       double* ring = dyn + 2 * kVec;
       const int warp = threadIdx.x >> 5;
       const int Rs2 = ((int)blockIdx.x < srn) ? (srn - 1 - (int)blockIdx.x) / (int)nb + 1 : 0;
@@ -409,19 +489,34 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         __syncthreads();
         {
           const int r = threadIdx.x;
-          int L = 0;
+          int row = 0, L = 0;
           if (r < ns) {
             const long long q = blockIdx.x + (long long)nb * (sb0 + r);
-            const int row = ldg_cg(&a.sr_list[q]);
+            row = ldg_cg(&a.sr_list[q]);
             L = ldg_cg(&a.rowlen[row]);
-            s_row[r] = row;
-            s_base[r] = a.rowbase[row];
-            s_len[r] = L;
-            s_inx[r] = ldg_cg(&a.tag[row]) == tg;
-            s_tf[r] = 0x7fffffff;
+            s_key[r] = L;
           }
-          const int mx = __reduce_max_sync(0xffffffffu, L);
-          if (lane == 0) s_gch[warp] = max(1, (mx + kRingW - 1) / kRingW);
+          __syncthreads();
+          if (r < ns) {
+            int rank = 0;
+            for (int u = 0; u < ns; ++u) {
+              const int Lu = s_key[u];
+              rank += (Lu > L) | ((Lu == L) & (u < r));
+            }
+            s_row[rank] = row;
+            s_base[rank] = a.rowbase[row];
+            s_len[rank] = L;
+            s_inx[rank] = ldg_cg(&a.tag[row]) == tg;
+            s_tf[rank] = 0x7fffffff;
+            s_pos[rank] = r;
+          }
+          __syncthreads();
+          const int Lr = r < ns ? s_len[r] : 0;
+          const int mx = __reduce_max_sync(0xffffffffu, Lr);
+          if (lane == 0) {
+            s_gch[warp] = max(1, (mx + kRingW - 1) / kRingW);
+            s_gmx[warp] = mx;
+          }
         }
         __syncthreads();
         const int ngr = (ns + 31) / 32;
@@ -430,50 +525,44 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         if (is_producer(warp)) {
           // the next chunk's entries (k, value) are in flight meanwhile;
           // thread: step t of each chunk, rows rq + kRowPh * k of the group
+          // (NA active row slots, compile-time as in P1)
           const int pi = producer_index(warp, lane);
-        const int t = pi % kRingW, rq = pi / kRingW;
-          int kv[kRowSlots];
-          double vv[kRowSlots];
-          unsigned okm = 0;    // rows with an entry at this step (prefetched chunk)
-          unsigned found = 0;  // rows whose first y != 0 entry is known (warp-uniform)
-          // per row slot of the group being loaded: its length (base read only when needed)
-          int slen[kRowSlots];
-          int lg = -1;
-          auto load = [&](int g, int ch) {
-            const int nr = min(32, ns - 32 * g);
-            if (g != lg) {
-              lg = g;
+          const int t = pi % kRingW, rq = pi / kRingW;
+          double* ring_t = ring + t * kRingS;
+          int q = 0;
+          auto group = [&](int g, auto na_c) {
+            constexpr int NA = decltype(na_c)::value;
+            const int nchk = s_gch[g];
+            int slen[NA];
+            long long sbase[NA];
 #pragma unroll
-              for (int k = 0; k < kRowSlots; ++k)
-                slen[k] = (rq + kRowPh * k < nr) ? s_len[32 * g + min(rq + kRowPh * k, 31)] : 0;
+            for (int k = 0; k < NA; ++k) {
+              slen[k] = s_len[32 * g + rq + kRowPh * k];
+              sbase[k] = s_base[32 * g + rq + kRowPh * k];
             }
-            const int te = ch * kRingW + t;
-            okm = 0;
+            int kv[NA];
+            double vv[NA];
+            unsigned okm = 0;    // rows with an entry at this step (prefetched chunk)
+            unsigned found = 0;  // rows whose first y != 0 entry is known (warp-uniform)
+            auto load = [&](int te) {
+              okm = 0;
 #pragma unroll
-            for (int k = 0; k < kRowSlots; ++k) {
-              const bool ok = te < slen[k];
-              kv[k] = 0;
-              vv[k] = 0.0;
-              if (ok) {
-                const long long idx = s_base[32 * g + rq + kRowPh * k] + te;
-                kv[k] = ldg_cg(&a.rek[idx]);
-                vv[k] = ldg_cg(&a.rev[idx]);
+              for (int k = 0; k < NA; ++k) {
+                const bool ok = te < slen[k];
+                kv[k] = ok ? ldg_cg(&a.rek[sbase[k] + te]) : 0;
+                vv[k] = ok ? ldg_cg(&a.rev[sbase[k] + te]) : 0.0;
+                okm |= (unsigned)ok << k;
               }
-              okm |= (unsigned)ok << k;
-            }
-          };
-          int g = 0, ch = 0;
-          if (Q > 0) load(0, 0);
-          for (int q = 0; q < Q; ++q) {
-            const int nr = min(32, ns - 32 * g);
-            const int b = q % kRingSlots;
-            double* rb = ring + b * (kRingW * kRingS) + t * kRingS;
-            const int te = ch * kRingW + t;
-            if (q >= kRingSlots) nbar_sync(1 + kRingSlots + b, kRingThreads);
+            };
+            load(t);
+            for (int ch = 0; ch < nchk; ++ch, ++q) {
+              const int b = q % kRingSlots;
+              double* rb = ring_t + b * (kRingW * kRingS);
+              const int te = ch * kRingW + t;
+              if (q >= kRingSlots) nbar_sync(1 + kRingSlots + b, kRingThreads);
 #pragma unroll
-            for (int k = 0; k < kRowSlots; ++k) {
-              const int r = rq + kRowPh * k;
-              if (r < nr) {  // warp-uniform: a warp covers 32 steps of one row
+              for (int k = 0; k < NA; ++k) {
+                const int r = rq + kRowPh * k;
                 const bool ok = (okm >> k) & 1;
                 const double yk = ok ? (y_fits ? vA[kv[k]] : ldg_cg(&ycur[kv[k]])) : 0.0;
                 rb[r] = dmul(yk, vv[k]);
@@ -486,44 +575,58 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
                   }
                 }
               }
+              nbar_arrive(1 + b, kRingThreads);
+              if (ch + 1 < nchk) load(te + kRingW);
             }
-            nbar_arrive(1 + b, kRingThreads);
-            if (++ch == s_gch[g]) {
-              ch = 0;
-              ++g;
-              found = 0;
+          };
+          for (int g = 0; g < ngr; ++g) {
+            const int nr = min(32, ns - 32 * g);
+            const int nact = nr > rq ? (nr - rq + kRowPh - 1) / kRowPh : 0;
+            switch (nact) {
+              case 0: {
+                for (int ch = 0; ch < s_gch[g]; ++ch, ++q) {
+                  const int b = q % kRingSlots;
+                  if (q >= kRingSlots) nbar_sync(1 + kRingSlots + b, kRingThreads);
+                  nbar_arrive(1 + b, kRingThreads);
+                }
+                break;
+              }
+              case 1: group(g, std::integral_constant<int, 1>{}); break;
+              case 2: group(g, std::integral_constant<int, 2>{}); break;
+              case 3: group(g, std::integral_constant<int, 3>{}); break;
+              case 4: group(g, std::integral_constant<int, 4>{}); break;
+              case 5: group(g, std::integral_constant<int, 5>{}); break;
+              case 6: group(g, std::integral_constant<int, 6>{}); break;
+              default: group(g, std::integral_constant<int, kRowSlots>{}); break;
             }
-            if (q + 1 < Q) load(g, ch);
           }
         } else if (warp == kChainWarp) {
           // chain warp: z_r = sum_k fl(y_k R[r,k]) in ascending k (fiber_basis.cpp:56-65)
-          double z = 0.0;
-          int g = 0, ch = 0;
-          for (int q = 0; q < Q; ++q) {
-            const int b = q % kRingSlots;
-            nbar_sync(1 + b, kRingThreads);
-            // steps past a row's length hold +-0.0, which leave z unchanged
-            z = lane_chain(ring + b * (kRingW * kRingS), lane, kRingW, z);
-            if (q + kRingSlots < Q) nbar_arrive(1 + kRingSlots + b, kRingThreads);
-            if (++ch == s_gch[g]) {
-              const int r = 32 * g + lane;
-              if (r < ns) {
-                const int row = s_row[r];
-                const int L = s_len[r];
-                const long long b0 = s_base[r];
-                const int tf = s_tf[r];
-                const int kfd = tf < L ? ldg_cg(&a.rek[b0 + tf]) : -1;
-                const int kst = L > 0 ? ldg_cg(&a.rek[b0]) : -1;
-                zdn[row] = z;
-                a.kf[row] = kfd;
-                a.term[blockIdx.x + (long long)nb * (sb0 + r)] = s_inx[r] ? 0.0 : dsqr(z);
-                // touched order differs from first-appearance order only if
-                // the row's first kept column has y == 0 while it is touched
-                if (z != 0.0 && kfd != kst) atomicExch(&a.slow[n], 1);
-              }
-              z = 0.0;
-              ch = 0;
-              ++g;
+          int q = 0;
+          for (int g = 0; g < ngr; ++g) {
+            const int nchk = s_gch[g], mx = s_gmx[g];
+            double z = 0.0;
+            for (int ch = 0; ch < nchk; ++ch, ++q) {
+              const int b = q % kRingSlots;
+              nbar_sync(1 + b, kRingThreads);
+              // steps past a row's length hold +-0.0, which leave z unchanged
+              z = lane_chain(ring + b * (kRingW * kRingS), lane, min(kRingW, mx - ch * kRingW), z);
+              if (q + kRingSlots < Q) nbar_arrive(1 + kRingSlots + b, kRingThreads);
+            }
+            const int r = 32 * g + lane;
+            if (r < ns) {
+              const int row = s_row[r];
+              const int L = s_len[r];
+              const long long b0 = s_base[r];
+              const int tf = s_tf[r];
+              const int kfd = tf < L ? ldg_cg(&a.rek[b0 + tf]) : -1;
+              const int kst = L > 0 ? ldg_cg(&a.rek[b0]) : -1;
+              zdn[row] = z;
+              a.kf[row] = kfd;
+              a.term[blockIdx.x + (long long)nb * (sb0 + s_pos[r])] = s_inx[r] ? 0.0 : dsqr(z);
+              // touched order differs from first-appearance order only if
+              // the row's first kept column has y == 0 while it is touched
+              if (z != 0.0 && kfd != kst) atomicExch(&a.slow[n], 1);
             }
           }
         }
