@@ -409,7 +409,11 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   }
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter, kFThreads, dsmem));
   if (per_sm < 1) fail(CTD_ERR_DEVICE, "filter kernel cannot be resident");
-  const unsigned grid = (unsigned)ctx->sm_count;  // one CTA per SM
+  unsigned grid = (unsigned)ctx->sm_count;  // one CTA per SM
+  if (const char* ge = getenv("CTD_FILTER_GRID")) {  // experiment hook: fewer CTAs
+    const int gv = atoi(ge);
+    if (gv > 0 && gv < (int)grid) grid = (unsigned)gv;
+  }
   void* args[] = {&fa};
   ctx->phase_end();
   ctx->phase_begin(PH_FILTER);
