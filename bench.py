@@ -505,7 +505,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roof, "phases": per_phase, "gpu_launches": launches,
         "error_pass": {"ms": round(err_ms, 3), "kernel_ms": round(err_kernel_ms, 3),
                        "nnz_per_s": round(nnz / (err_ms / 1e3), 1),
-                       "what": "relative_error(X, factors): matricize + Gram-identity pass over all nnz"},
+                       "what": "relative_error(X, factors): matricize + one pass over all nnz against the orthonormal panel W = R T (U = T T^T)"},
         "clocks": clk.summary(),
     }
     if e2e:

@@ -229,6 +229,8 @@ struct FArgs {
   int kvec;          // largest K whose g / y vectors are staged in shared memory
   SliceLoc* sloc;    // [grid] published approximate slice sums (epoch-flagged)
   unsigned* sflag;   // [grid] slice-summary epoch flags
+  double* W;         // optional [dim][Wld] orthonormal panel R T (error pass), column k written at accept k
+  long long Wld;
 };
 
 constexpr int kTraceW = 32;  // clock64 slots per candidate
@@ -255,6 +257,8 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   const int64_t K0 = B.K;
   // ---- capacities: U, R columns, R entries
   if (B.LD < K0 + n) {
+    B.Wok = false;  // the panel follows U's capacity; rebuilt only from an empty basis
+    B.W = Buf<double>();
     const int64_t nld = (std::max<int64_t>(K0 + n, B.LD * 2) + 1) & ~int64_t(1);  // even: 16-byte rows
     Buf<double> nu(ctx, (size_t)nld * nld);
     if (K0 > 0)
@@ -335,6 +339,17 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   fa.K0 = (int)K0;
   fa.dim = B.dim;
   fa.LD = B.LD;
+  // the orthonormal panel for the error pass (relerr.cu): started with an
+  // empty basis, kept while U's capacity holds
+  if (K0 == 0 && (double)B.dim * (double)B.LD * 8.0 <= kWPanelBytes) {
+    B.W.alloc(ctx, (size_t)B.dim * B.LD);
+    B.W.zero();
+    B.Wok = true;
+  }
+  if (B.Wok) {
+    fa.W = B.W.p;
+    fa.Wld = B.LD;
+  }
   fa.c = c;
   fa.xsq = xsq.p;
   fa.Gc = Gc.p;

@@ -9,6 +9,8 @@ namespace ctdgpu {
 // visits them), the first-appearance order of R's rows (the reference's
 // `touched` order when every y_k != 0), and U = (R^T R)^-1 dense, leading
 // dimension LD.  U is kept exactly symmetric, as the reference's is.
+constexpr double kWPanelBytes = 8.0e9;  // largest W panel kept on the device
+
 struct Basis {
   Ctx* ctx = nullptr;
   int64_t dim = 0;
@@ -32,6 +34,10 @@ struct Basis {
   uint32_t tag_base = 0;
   Buf<double> zd;        // [dim]
   Buf<int32_t> kf;       // [dim] dynamic first k (slow path)
+  // W = R T with U = T T^T: the orthonormal panel [dim][LD] (row-major) the
+  // error pass gathers; Wok when it holds all K columns
+  Buf<double> W;
+  bool Wok = false;
 
   Basis(Ctx* c, int64_t d);
   // Copy R's host CSC and U (resume ctor, fiber_basis.cpp:13-19).

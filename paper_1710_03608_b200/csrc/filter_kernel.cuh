@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
   double prev_delta = 0.0;
   int prev_n = -1;
   bool pre = false;  // candidate n's setup (tags, z half, g and y staging) done during P3 of n-1
+  int last_srn = 0;  // rows of R when candidate n-1 was tested
   for (int n = 0; n <= nu; ++n) {
     const bool last = (n == nu);
     if (!last) stamp(a.trace, n, 0);
@@ -231,6 +232,18 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         }
       }
       rnnz += pm;
+      if (a.W) {
+        // Orthonormal panel W = R T, U = T T^T (T's new column is (-y, 1)/sqrt(d)
+        // by the bordering of fiber_basis.cpp:92-106), so W's new column is
+        // the residual (x - R y)/sqrt(d) of the accepted candidate: -z/sqrt(d)
+        // on R's rows now, x's own rows after the barrier (x - z).
+        const double sc = ddiv(1.0, __dsqrt_rn(prev_delta));
+        const double* zp = a.zd + (prev_n & 1) * (a.dim + 1);
+        for (long long q = gtid; q < last_srn; q += gthreads) {
+          const int r = ldg_cg(&a.sr_list[q]);
+          a.W[(long long)r * a.Wld + Ko] = -ldg_cg(&zp[r]) * sc;
+        }
+      }
     }
     if (!last) stamp(a.trace, n, 1);
     if (upd || !last) {
@@ -453,12 +466,32 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
       }
     }
     K = Kn;
-    if (last) break;
+    auto w_xrows = [&]() {  // W's new column on the accepted fiber's rows (after the R-row writes)
+      if (a.W && upd) {
+        const double sc = ddiv(1.0, __dsqrt_rn(prev_delta));
+        const double* zp = a.zd + (prev_n & 1) * (a.dim + 1);
+        const long long poff = a.c.off[prev_n];
+        const int pm = a.c.len[prev_n];
+        for (long long t = gtid; t < pm; t += gthreads) {
+          const int r = a.c.row[poff + t];
+          a.W[(long long)r * a.Wld + Ko] = (a.c.val[poff + t] - ldg_cg(&zp[r])) * sc;
+        }
+      }
+    };
+    if (last) {
+      if (a.W && upd) {
+        grid_barrier(a.bar, nb);
+        w_xrows();
+      }
+      break;
+    }
     stamp(a.trace, n, 3);
     grid_barrier(a.bar, nb);
     stamp(a.trace, n, 4);
+    w_xrows();
     // ---------------- P2: z over R's rows, residual terms ---------------------
     const int srn = ldg_cg(a.sr_n);
+    last_srn = srn;
     const bool y_fits = K <= a.kvec;
     auto stage_y = [&](int c0, int c1) {
       __syncthreads();

@@ -11,6 +11,8 @@
 // so it uses FMA and a deterministic (fixed-order) reduction.
 #include "relerr.cuh"
 
+#include <cstdlib>
+
 namespace ctdgpu {
 
 namespace {
@@ -75,6 +77,37 @@ __global__ void k_cd(const int64_t* fptr, long long F, const int32_t* row, const
   if (lane == 0) partial[warp] = part;
 }
 
+// sum_j |W^T x_j|^2 with W = R T orthonormal-by-construction (U = T T^T):
+// the same column-chunked sweep as k_cd with one panel instead of two.
+__global__ void k_cdw(const int64_t* fptr, long long F, const int32_t* row, const double* val, const double* W,
+                      long long LD, long long K, double* partial) {
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  double part = 0.0;
+  for (long long c0 = 0; c0 < K; c0 += 32 * kCW) {
+    for (long long f = warp; f < F; f += nwarps) {
+      const long long b = fptr[f], e = fptr[f + 1];
+      double ac[kCW];
+#pragma unroll
+      for (int u = 0; u < kCW; ++u) ac[u] = 0.0;
+      for (long long t = b; t < e; ++t) {
+        const double v = val[t];
+        const double* ww = W + (long long)row[t] * LD;
+#pragma unroll
+        for (int u = 0; u < kCW; ++u) {
+          const long long c = c0 + lane + 32 * u;
+          if (c < K) ac[u] = __fma_rn(v, ww[c], ac[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kCW; ++u) part = __fma_rn(ac[u], ac[u], part);
+    }
+  }
+  part = warp_sum(part);
+  if (lane == 0) partial[warp] = part;
+}
+
 __global__ void k_sumsq(const double* v, long long n, double* partial) {
   __shared__ double sh[33];
   double s = 0.0;
@@ -115,14 +148,24 @@ void error_partials(Ctx* ctx, const Fibers& fb, const Basis& B, double* x_sq, do
     *cross = 0.0;
     return;
   }
+  const unsigned cgrid = (unsigned)ctx->sm_count * 8;
+  const long long nwarps = (long long)cgrid * 256 / 32;
+  Buf<double> cp(ctx, nwarps);
+  if (B.Wok && !getenv("CTD_RELERR_TWO_PANELS")) {
+    // one orthonormal panel, maintained by the filter
+    LAUNCH(ctx, k_cdw, cgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, B.W.p, (long long)B.LD, K,
+           cp.p);
+    LAUNCH(ctx, k_reduce, 1, 1024, 0, cp.p, nwarps, cd.p);
+    ctx->to_host(x_sq, xsq.p, 1);
+    ctx->to_host(cross, cd.p, 1);
+    ctx->sync();
+    return;
+  }
   Buf<double> Rd(ctx, (size_t)dim * K), Q(ctx, (size_t)dim * K);
   Rd.zero();
   LAUNCH(ctx, k_dense_r, (unsigned)K, 128, 0, B.rptr.p, B.rrow.p, B.rval.p, K, Rd.p);
   LAUNCH(ctx, k_ru, ceil_div(dim * K, 256), 256, 0, B.rowbase.p, B.rowlen.p, B.rek.p, B.rev.p, B.U.p,
          (long long)B.LD, dim, K, Q.p);
-  const unsigned cgrid = (unsigned)ctx->sm_count * 8;
-  const long long nwarps = (long long)cgrid * 256 / 32;
-  Buf<double> cp(ctx, nwarps);
   LAUNCH(ctx, k_cd, cgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, Rd.p, Q.p, K, cp.p);
   LAUNCH(ctx, k_reduce, 1, 1024, 0, cp.p, nwarps, cd.p);
   ctx->to_host(x_sq, xsq.p, 1);
