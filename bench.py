@@ -427,9 +427,16 @@ def run_ours(args, rank, world, local_rank):
     tr = api.factors_trace(ctx, infos[-1][0], info)
     # ---- the relative-error pass (evaluation.cpp:88-122), timed on its own:
     # the reference evaluates it outside ctd_s (stream_harness.cpp:72-81).
-    hlast = infos[-1][0]
-    for h, _ in infos[:-1]:
+    for h, _ in infos:
         api.free_factors(ctx, h)
+    # the factors for the error pass keep the orthonormal panel W (built by the
+    # filter on request, CTD_GPU_KEEP_PANEL: ~2% of the front end, not in the
+    # timed steps above, which match the reference's ctd_s)
+    torch.cuda.synchronize()
+    p0 = time.perf_counter()
+    hlast, _ = api.ctd_s_raw(dt, mode, c, eps, seed, with_error=False, ctx=ctx, keep_panel=True)
+    torch.cuda.synchronize()
+    panel_front_ms = (time.perf_counter() - p0) * 1e3
     rel = api.relative_error_raw(dt, hlast, ctx)
     ctx.set_timing(True)
     ctx.phase_times(reset=True)
@@ -505,7 +512,9 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roof, "phases": per_phase, "gpu_launches": launches,
         "error_pass": {"ms": round(err_ms, 3), "kernel_ms": round(err_kernel_ms, 3),
                        "nnz_per_s": round(nnz / (err_ms / 1e3), 1),
-                       "what": "relative_error(X, factors): matricize + one pass over all nnz against the orthonormal panel W = R T (U = T T^T)"},
+                       "what": "relative_error(X, factors): matricize + one pass over all nnz against the orthonormal panel W = R T (U = T T^T)",
+                       "panel": "W kept by the filter on request (CTD_GPU_KEEP_PANEL)",
+                       "front_end_with_panel_ms": round(panel_front_ms, 3)},
         "clocks": clk.summary(),
     }
     if e2e:

@@ -42,6 +42,8 @@ enum ctd_gpu_status {
 /* ctd_s flags */
 #define CTD_GPU_WITH_ERROR 0x1u /* also run the relative-error pass (evaluation.cpp:88-122) */
 #define CTD_GPU_WITH_CORE 0x2u  /* also materialize C = X x_mode R^T (ctd_static.cpp:12-17) */
+#define CTD_GPU_KEEP_PANEL 0x4u /* keep the orthonormal panel W = R T for a later ctd_gpu_relative_error
+                                   (implied by CTD_GPU_WITH_ERROR; ~2% of the filter's time) */
 
 typedef struct ctd_gpu_ctx ctd_gpu_ctx;         /* device, stream, scratch pool */
 typedef struct ctd_gpu_tensor ctd_gpu_tensor;   /* SparseTensor (sparse_tensor.hpp:17-60) resident in HBM */

@@ -142,6 +142,7 @@ int ctd_gpu_ctx_create(int device, void* stream, ctd_gpu_ctx** out) {
     CUDA_OK(cudaMalloc(&c.d_bar, 4 * sizeof(unsigned)));
     CUDA_OK(cudaMemset(c.d_flags, 0, sizeof(unsigned)));
     CUDA_OK(cudaMemset(c.d_bar, 0, 4 * sizeof(unsigned)));
+    ctx_register(&h->c, true);
     *out = h.release();
   });
 }
@@ -164,6 +165,7 @@ int ctd_gpu_ctx_destroy(ctd_gpu_ctx* ctx) {
   return guarded([&] {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->c.stream);
+    ctx_register(&ctx->c, false);
     cudaFree(ctx->c.d_flags);
     cudaFree(ctx->c.d_bar);
     delete ctx;
@@ -507,6 +509,7 @@ int ctd_gpu_basis_create(ctd_gpu_ctx* ctx, int64_t dim, ctd_gpu_basis** out) {
     auto h = std::make_unique<ctd_gpu_basis>();
     h->ctx = &ctx->c;
     h->b = std::make_unique<Basis>(&ctx->c, dim);
+    h->b->want_panel = true;  // error partials over shards use the orthonormal panel (relerr.cu)
     *out = h.release();
   });
 }

@@ -129,6 +129,7 @@ void run_ctd_s(Ctx* ctx, const Tensor& x, int mode, int64_t s, double eps, uint6
   out.rows = fb.rows;
   out.integer_exact = fb.integer_exact;
   out.basis = std::make_unique<Basis>(ctx, fb.rows);
+  out.basis->want_panel = (flags & (CTD_GPU_WITH_ERROR | CTD_GPU_KEEP_PANEL)) != 0;
   Front fr;
   front_end(ctx, fb, *out.basis, s, eps, seed, fr, true);
   out.total = fr.total;

@@ -1,11 +1,35 @@
 // Context, device buffers and tensor handles.
 #pragma once
 
+#include <mutex>
+#include <set>
 #include <vector>
 
 #include "common.cuh"
 
 namespace ctdgpu {
+
+struct Ctx;
+// Contexts alive in this process.  A buffer owned by an object the caller
+// destroys after its context (e.g. at interpreter shutdown) is then left to
+// process teardown instead of being freed through a dead stream.
+inline std::mutex& ctx_registry_mutex() {
+  static std::mutex m;
+  return m;
+}
+inline std::set<const Ctx*>& ctx_registry() {
+  static std::set<const Ctx*> s;
+  return s;
+}
+inline void ctx_register(const Ctx* c, bool live) {
+  std::lock_guard<std::mutex> lk(ctx_registry_mutex());
+  if (live) ctx_registry().insert(c);
+  else ctx_registry().erase(c);
+}
+inline bool ctx_alive(const Ctx* c) {
+  std::lock_guard<std::mutex> lk(ctx_registry_mutex());
+  return ctx_registry().count(c) != 0;
+}
 
 struct Ctx {
   int device = 0;
@@ -112,7 +136,7 @@ struct Buf {
   }
   ~Buf() { reset(); }
   void reset() {
-    if (p && c) c->release(p);
+    if (p && c && ctx_alive(c)) c->release(p);
     p = nullptr;
     n = 0;
   }

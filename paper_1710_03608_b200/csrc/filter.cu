@@ -341,10 +341,12 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   fa.LD = B.LD;
   // the orthonormal panel for the error pass (relerr.cu): started with an
   // empty basis, kept while U's capacity holds
-  if (K0 == 0 && (double)B.dim * (double)B.LD * 8.0 <= kWPanelBytes) {
+  static const bool no_w = getenv("CTD_NO_WPANEL") != nullptr;  // the two-panel error pass only
+  if (K0 == 0 && B.want_panel && !no_w && (double)B.dim * (double)B.LD * 8.0 <= kWPanelBytes) {
     B.W.alloc(ctx, (size_t)B.dim * B.LD);
     B.W.zero();
     B.Wok = true;
+    B.Wscale.clear();
   }
   if (B.Wok) {
     fa.W = B.W.p;
@@ -498,6 +500,15 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
     if (i < n - 1 && out.accepted[i]) ++k_at_last;
   }
   if (want_y) out.y_last.resize(k_at_last);
+  if (B.Wok) {
+    // W's columns hold the accepted candidates' residuals x - z; the error
+    // pass weighs column k by 1/delta_k (W = R T, T's column (-y, 1)/sqrt(delta))
+    B.Wscale.resize(K0);
+    for (int64_t i = 0; i < n; ++i)
+      if (out.accepted[i]) B.Wscale.push_back(1.0 / out.delta[i]);
+    B.Wsc.alloc(ctx, B.Wscale.size() + 1);
+    if (!B.Wscale.empty()) ctx->to_dev(B.Wsc.p, B.Wscale.data(), B.Wscale.size());
+  }
   B.K = newK;
   B.rnnz = newR;
   B.srn = srn;

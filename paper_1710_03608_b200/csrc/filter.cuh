@@ -1,4 +1,5 @@
 #pragma once
+#include <vector>
 #include "ctx.cuh"
 
 namespace ctdgpu {
@@ -37,7 +38,10 @@ struct Basis {
   // W = R T with U = T T^T: the orthonormal panel [dim][LD] (row-major) the
   // error pass gathers; Wok when it holds all K columns
   Buf<double> W;
+  bool want_panel = false;  // maintain W (callers that will evaluate the error)
   bool Wok = false;
+  std::vector<double> Wscale;  // 1/delta of each kept column (host)
+  Buf<double> Wsc;             // the same on the device
 
   Basis(Ctx* c, int64_t d);
   // Copy R's host CSC and U (resume ctor, fiber_basis.cpp:13-19).

@@ -112,8 +112,15 @@ struct ResidualTerms {
   const double* zd;
   long long m;
   const double* tsrc;
+  double* wcol = nullptr;  // optional: the W panel's column for this candidate (x rows get x - z)
+  long long wld = 0;
   __device__ double operator()(long long i) const {
-    if (i < m) return dsqr(dsub(xv[i], __ldcg(&zd[xr[i]])));
+    if (i < m) {
+      const int r = xr[i];
+      const double d = dsub(xv[i], __ldcg(&zd[r]));
+      if (wcol) wcol[(long long)r * wld] = d;
+      return dsqr(d);
+    }
     return __ldcg(&tsrc[i - m]);
   }
   // terms b0, b0+1, ... (< b1) into out[], every load of a level issued together
@@ -135,11 +142,21 @@ struct ResidualTerms {
         }
       }
     }
+    double d[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       const long long i = b0 + k;
       out[k] = v[k];
-      if (i < b1 && i < m) out[k] = dsqr(dsub(v[k], __ldcg(&zd[r[k]])));
+      d[k] = 0.0;
+      if (i < b1 && i < m) {
+        d[k] = dsub(v[k], __ldcg(&zd[r[k]]));
+        out[k] = dsqr(d[k]);
+      }
+    }
+    if (wcol) {  // stores after every load of the batch (they may alias)
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+        if (b0 + k < b1 && b0 + k < m) wcol[(long long)r[k] * wld] = d[k];
     }
   }
 };
@@ -169,7 +186,6 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
   double prev_delta = 0.0;
   int prev_n = -1;
   bool pre = false;  // candidate n's setup (tags, z half, g and y staging) done during P3 of n-1
-  int last_srn = 0;  // rows of R when candidate n-1 was tested
   for (int n = 0; n <= nu; ++n) {
     const bool last = (n == nu);
     if (!last) stamp(a.trace, n, 0);
@@ -194,6 +210,13 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
       }
     }
     // ---------------- P1: append previous accept; fused U update + y --------
+    if (a.W && !upd && prev_n >= 0) {
+      // n-1 was not kept: its x rows outside R hold x - z in W's column K,
+      // which candidate n reuses (R's rows and n's own rows are rewritten)
+      const long long poff = a.c.off[prev_n];
+      const int pm = a.c.len[prev_n];
+      for (long long t = gtid; t < pm; t += gthreads) a.W[(long long)a.c.row[poff + t] * a.Wld + K] = 0.0;
+    }
     if (upd) {
       const long long poff = a.c.off[prev_n];
       const int pm = a.c.len[prev_n];
@@ -232,18 +255,6 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         }
       }
       rnnz += pm;
-      if (a.W) {
-        // Orthonormal panel W = R T, U = T T^T (T's new column is (-y, 1)/sqrt(d)
-        // by the bordering of fiber_basis.cpp:92-106), so W's new column is
-        // the residual (x - R y)/sqrt(d) of the accepted candidate: -z/sqrt(d)
-        // on R's rows now, x's own rows after the barrier (x - z).
-        const double sc = ddiv(1.0, __dsqrt_rn(prev_delta));
-        const double* zp = a.zd + (prev_n & 1) * (a.dim + 1);
-        for (long long q = gtid; q < last_srn; q += gthreads) {
-          const int r = ldg_cg(&a.sr_list[q]);
-          a.W[(long long)r * a.Wld + Ko] = -ldg_cg(&zp[r]) * sc;
-        }
-      }
     }
     if (!last) stamp(a.trace, n, 1);
     if (upd || !last) {
@@ -466,32 +477,12 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
       }
     }
     K = Kn;
-    auto w_xrows = [&]() {  // W's new column on the accepted fiber's rows (after the R-row writes)
-      if (a.W && upd) {
-        const double sc = ddiv(1.0, __dsqrt_rn(prev_delta));
-        const double* zp = a.zd + (prev_n & 1) * (a.dim + 1);
-        const long long poff = a.c.off[prev_n];
-        const int pm = a.c.len[prev_n];
-        for (long long t = gtid; t < pm; t += gthreads) {
-          const int r = a.c.row[poff + t];
-          a.W[(long long)r * a.Wld + Ko] = (a.c.val[poff + t] - ldg_cg(&zp[r])) * sc;
-        }
-      }
-    };
-    if (last) {
-      if (a.W && upd) {
-        grid_barrier(a.bar, nb);
-        w_xrows();
-      }
-      break;
-    }
+    if (last) break;
     stamp(a.trace, n, 3);
     grid_barrier(a.bar, nb);
     stamp(a.trace, n, 4);
-    w_xrows();
     // ---------------- P2: z over R's rows, residual terms ---------------------
     const int srn = ldg_cg(a.sr_n);
-    last_srn = srn;
     const bool y_fits = K <= a.kvec;
     auto stage_y = [&](int c0, int c1) {
       __syncthreads();
@@ -655,6 +646,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
               const int kfd = tf < L ? ldg_cg(&a.rek[b0 + tf]) : -1;
               const int kst = L > 0 ? ldg_cg(&a.rek[b0]) : -1;
               zdn[row] = z;
+              if (a.W) a.W[(long long)row * a.Wld + K] = -z;  // W's column K on R's rows (relerr.cu)
               a.kf[row] = kfd;
               a.term[blockIdx.x + (long long)nb * (sb0 + s_pos[r])] = s_inx[r] ? 0.0 : dsqr(z);
               // touched order differs from first-appearance order only if
@@ -723,7 +715,8 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     bool bad = false;
     // Terms in the reference's summation order (fiber_basis.cpp:66-77): x's
     // rows ascending, then R's rows in first-touch order.
-    const ResidualTerms get{xv, xr, zdn, (long long)m, tsrc};
+    // (also writes the x rows of W's column K: x - z, see relerr.cu)
+    const ResidualTerms get{xv, xr, zdn, (long long)m, tsrc, a.W ? a.W + K : nullptr, a.Wld};
     // exact sequential residual: warp 0 of every CTA (warp_grid_sum); the
     // other warps wait at the CTA barrier
     stamp(a.trace, n, 7);

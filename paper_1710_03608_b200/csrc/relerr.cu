@@ -77,10 +77,12 @@ __global__ void k_cd(const int64_t* fptr, long long F, const int32_t* row, const
   if (lane == 0) partial[warp] = part;
 }
 
-// sum_j |W^T x_j|^2 with W = R T orthonormal-by-construction (U = T T^T):
-// the same column-chunked sweep as k_cd with one panel instead of two.
+// sum_j |W^T x_j|^2 with W = R T orthonormal by construction (U = T T^T).
+// The panel stores the residuals x_k - R y_k unscaled (written by the filter
+// off its critical path); column c is weighed by wsc[c] = 1/delta_c here.
+// The same column-chunked sweep as k_cd with one panel instead of two.
 __global__ void k_cdw(const int64_t* fptr, long long F, const int32_t* row, const double* val, const double* W,
-                      long long LD, long long K, double* partial) {
+                      const double* wsc, long long LD, long long K, double* partial) {
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -101,7 +103,10 @@ __global__ void k_cdw(const int64_t* fptr, long long F, const int32_t* row, cons
         }
       }
 #pragma unroll
-      for (int u = 0; u < kCW; ++u) part = __fma_rn(ac[u], ac[u], part);
+      for (int u = 0; u < kCW; ++u) {
+        const long long c = c0 + lane + 32 * u;
+        if (c < K) part = __fma_rn(ac[u] * ac[u], wsc[c], part);
+      }
     }
   }
   part = warp_sum(part);
@@ -153,8 +158,8 @@ void error_partials(Ctx* ctx, const Fibers& fb, const Basis& B, double* x_sq, do
   Buf<double> cp(ctx, nwarps);
   if (B.Wok && !getenv("CTD_RELERR_TWO_PANELS")) {
     // one orthonormal panel, maintained by the filter
-    LAUNCH(ctx, k_cdw, cgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, B.W.p, (long long)B.LD, K,
-           cp.p);
+    LAUNCH(ctx, k_cdw, cgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, B.W.p, B.Wsc.p,
+           (long long)B.LD, K, cp.p);
     LAUNCH(ctx, k_reduce, 1, 1024, 0, cp.p, nwarps, cd.p);
     ctx->to_host(x_sq, xsq.p, 1);
     ctx->to_host(cross, cd.p, 1);

@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 
 import paper_1710_03608_b200 as ctd
+from paper_1710_03608_b200 import ctd as api
 from paper_1710_03608_b200 import datagen as g
 
 pytestmark = pytest.mark.gpu
@@ -137,6 +138,25 @@ def test_relative_error(ctx, ref, name):
     assert abs(f.relative_error - e) <= 1e-9 * max(1.0, abs(e)), (f.relative_error, e)
 
 
+@pytest.mark.parametrize("name", ["c1", "rand_fp", "lowrank", "traffic", "cp_small"])
+def test_relative_error_panel_and_two_panel_paths(ctx, ref, name):
+    """The orthonormal-panel pass (factors kept with the panel) and the
+    two-panel fallback (without it) both match the reference."""
+    x = CASES[name]()
+    t = ref.tensor(x.shape, x.flat_idx(), x.val)
+    e = ref.ctd_s(t, 0, 200, 1e-6, 42).extra["relative_error"]
+    d = ctd.DeviceTensor(_st(x), ctx)
+    vals = []
+    for keep in (True, False):
+        h, _ = api.ctd_s_raw(d, 0, 200, 1e-6, 42, ctx=ctx, keep_panel=keep)
+        try:
+            vals.append(api.relative_error_raw(d, h, ctx))
+        finally:
+            api.free_factors(ctx, h)
+    for v in vals:
+        assert abs(v - e) <= 1e-9 * max(1.0, abs(e)), (vals, e)
+
+
 @pytest.mark.parametrize("name,mode", [("c1", 0), ("c1", 2), ("rand_fp", 1), ("rand_int", 0), ("lowrank", 0),
                                        ("traffic", 0), ("order4", 3)])
 def test_core_bitexact(ctx, port, name, mode):
@@ -234,6 +254,7 @@ _KVEC_SCRIPT = r"""
 import sys, numpy as np
 sys.path.insert(0, {root!r})
 import paper_1710_03608_b200 as ctd
+from paper_1710_03608_b200 import ctd as api
 from paper_1710_03608_b200 import datagen as g
 from oracle.bindings import Port
 port = Port()
