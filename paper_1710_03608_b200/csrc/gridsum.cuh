@@ -30,6 +30,7 @@ struct SliceSum {
   Seg agg;
   int nd;       // directs, -1 = overflow
   short last_e; // class/e of the slice's last element; 0x7fff: empty slice
+  double head;  // slice 0: its exact sequential sum (summarized as one direct block)
 };
 static_assert(sizeof(SliceSum) % 8 == 0 && sizeof(SliceDirect) % 8 == 0, "8-byte words");
 
@@ -398,6 +399,22 @@ __device__ double warp_grid_sum(const Get& get, long long nt, unsigned epoch, Sl
   // classify the cached terms independently (their approximate prefixes
   // first: one add chain), so the branchy per-term work overlaps
   const int nc = (int)min((long long)kWarpCache, b1 - b0);
+  // Slice 0 holds the head of the sum, where the small running value crosses
+  // binades often (many directs, slow classification): lane 0 adds it
+  // sequentially instead, and it enters the combine as one direct block.
+  const bool head_slice = (b == 0) && (per <= kWarpCache);
+  double hsum = 0.0;
+  if (head_slice) {
+    for (int l = 0; l < 32; ++l) {
+      const int cl = __shfl_sync(FULL, nc, l);
+#pragma unroll
+      for (int k = 0; k < kWarpCache; ++k) {
+        const double x = __shfl_sync(FULL, xv[k], l);
+        if (k < cl) hsum = dadd(hsum, x);
+      }
+    }
+    hsum = __shfl_sync(FULL, hsum, 0);
+  }
   double Pv[kWarpCache + 1];
   Pv[0] = pre;
 #pragma unroll
@@ -409,14 +426,18 @@ __device__ double warp_grid_sum(const Get& get, long long nt, unsigned epoch, Sl
     ee[k] = 0;
     mm[k] = mono_id();
     cls[k] = CLS_ZERO;
-    if (k < nc) cls[k] = seq_classify_bf(b0 + k == 0, Pv[k], Pv[k + 1], xv[k], mg, &ee[k], &mm[k]);
+    if (k < nc && !head_slice) cls[k] = seq_classify_fp(b0 + k == 0, Pv[k], Pv[k + 1], xv[k], mg, &ee[k], &mm[k]);
   }
   Seg agg{0, mono_id()};
   int nd = 0;
   short le = (short)0x7fff;
+  if (head_slice && nc > 0) {
+    agg.h = 1;
+    le = E_DIRECT;
+  }
 #pragma unroll
   for (int k = 0; k < kWarpCache; ++k) {
-    if (k < nc) {
+    if (k < nc && !head_slice) {
       if (cls[k] == CLS_REG) {
         agg.m = mono_cat(agg.m, mm[k]);
         le = (short)ee[k];
@@ -435,7 +456,7 @@ __device__ double warp_grid_sum(const Get& get, long long nt, unsigned epoch, Sl
     const double Pc = P + x;
     int e = 0;
     Mono m;
-    const int c = seq_classify(i == 0, P, Pc, x, mg, &e, &m);
+    const int c = seq_classify_fp(i == 0, P, Pc, x, mg, &e, &m);
     if (c == CLS_REG) {
       agg.m = mono_cat(agg.m, m);
       le = (short)e;
@@ -500,6 +521,7 @@ __device__ double warp_grid_sum(const Get& get, long long nt, unsigned epoch, Sl
     s.agg = tot;
     s.nd = over ? -1 : ntot;
     s.last_e = (n > 0) ? le : (short)0x7fff;
+    s.head = hsum;
     ps[b] = s;
   }
   __syncwarp();  // orders the other lanes' summary/direct writes before lane 0's release
@@ -517,6 +539,7 @@ __device__ double warp_grid_sum(const Get& get, long long nt, unsigned epoch, Sl
   sv.agg = Seg{0, mono_id()};
   sv.nd = 0;
   sv.last_e = (short)0x7fff;
+  sv.head = 0.0;
   if (cw == 0) {
     // warp 0 alone polls every slice's flag (no polling traffic from the
     // other combine warps), then releases them
@@ -599,7 +622,7 @@ __device__ double warp_grid_sum(const Get& get, long long nt, unsigned epoch, Sl
   int bad = 0;
   if (lane == 0) {
     bool ok = !over_all;
-    double head = 0.0;
+    double head = sv.head;  // slice 0's exact value (0 when it was classified)
     if (ok) {
       // only head -> run -> add is on the dependent path; the run checks are
       // accumulated into `ok` (seq_apply_run's conditions, evaluated lazily)

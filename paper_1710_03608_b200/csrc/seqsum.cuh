@@ -142,6 +142,35 @@ __device__ __forceinline__ int seq_classify_bf(bool first, double Pp, double Pc,
   return (Pc == 0.0) ? CLS_ZERO : (direct ? CLS_DIRECT : CLS_REG);
 }
 
+// seq_classify_bf with the grid increment taken in floating point: t =
+// x 2^(52-e) is exact, (t + 2^52) - 2^52 rounds it to the nearest integer
+// (ties to even) for t < 2^51, and without an exact half-ulp tie the
+// increment does not depend on the parity of the running value.  Ties (or
+// large t) take the integer monoid (seq_mono_bf).  Same results, fewer
+// 64-bit integer instructions.
+__device__ __forceinline__ int seq_classify_fp(bool first, double Pp, double Pc, double x, double mg, int* e_out,
+                                               Mono* m_out) {
+  const int ep = dexp(Pp), ec = dexp(Pc);
+  bool direct = first | !(Pp > 0.0) | !(Pc > 0.0) | !(x < 1.7976931348623157e308) | (ep != ec) | (ec < -960) |
+                (ec > 1020);
+  const int ecc = min(max(ec, -960), 1020);
+  const double lo = pow2(ecc);
+  direct |= ((Pp - lo) <= mg * Pp) | ((2.0 * lo - Pp) <= mg * Pp) | ((Pc - lo) <= mg * Pc) |
+            ((2.0 * lo - Pc) <= mg * Pc);
+  const double t = __dmul_rn(x, pow2(52 - ecc));
+  const double r = __dadd_rn(__dadd_rn(t, 4503599627370496.0), -4503599627370496.0);
+  const double f = __dadd_rn(t, -r);
+  const bool hard = !(t < 2251799813685248.0) | (f == 0.5) | (f == -0.5);
+  if (hard && !direct) {
+    *m_out = seq_mono_bf(x, ecc);
+  } else {
+    const long long ri = (long long)r;
+    *m_out = Mono{ri, ri};
+  }
+  *e_out = ec;
+  return (Pc == 0.0) ? CLS_ZERO : (direct ? CLS_DIRECT : CLS_REG);
+}
+
 // A whole chunk is regular in binade *e when the approximate prefix before it
 // (pre) and after it (post) both lie strictly inside [2^e, 2^(e+1)) with the
 // error margin to spare: the running sum is monotone, so every intermediate
