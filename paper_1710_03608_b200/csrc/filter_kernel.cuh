@@ -217,44 +217,30 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
       const int pm = a.c.len[prev_n];
       for (long long t = gtid; t < pm; t += gthreads) a.W[(long long)a.c.row[poff + t] * a.Wld + K] = 0.0;
     }
-    if (upd) {
+    if (upd && blockIdx.x == nb - 1) {
+      // Ordered append of x_{n-1}'s rows not yet in R (first-appearance
+      // order).  The last CTA does it: U rows are dealt from CTA 0 upward, so
+      // it usually owns none and this overlaps the y chains.
       const long long poff = a.c.off[prev_n];
       const int pm = a.c.len[prev_n];
-      for (long long t = gtid; t < pm; t += gthreads) {
-        const int r = a.c.row[poff + t];
-        const double v = a.c.val[poff + t];
-        a.rrow[rnnz + t] = r;
-        a.rval[rnnz + t] = v;
-        const int L = ldg_cg(&a.rowlen[r]);
-        const long long p = a.rowbase[r] + L;
-        a.rek[p] = Ko;
-        a.rev[p] = v;
-        a.rowlen[r] = L + 1;
-      }
-      if (blockIdx.x == nb - 1) {
-        // Ordered append of x's rows not yet in R (first-appearance order).
-        // The last CTA does it: U rows are dealt from CTA 0 upward, so it
-        // usually owns none and this overlaps the y chains.
-        int srn = ldg_cg(a.sr_n);
-        for (int base = 0; base < pm; base += blockDim.x) {
-          const int t = base + threadIdx.x;
-          const int r = t < pm ? a.c.row[poff + t] : 0;
-          const int isnew = (t < pm) && (ldg_cg(&a.sr_pos[r]) < 0);
-          int tot2;
-          const int pos = block_excl_sum<int>(isnew, shi, &tot2);
-          if (isnew) {
-            a.sr_list[srn + pos] = r;
-            a.sr_pos[r] = srn + pos;
-          }
-          srn += tot2;
+      int srn = ldg_cg(a.sr_n);
+      for (int base = 0; base < pm; base += blockDim.x) {
+        const int t = base + threadIdx.x;
+        const int r = t < pm ? a.c.row[poff + t] : 0;
+        const int isnew = (t < pm) && (ldg_cg(&a.sr_pos[r]) < 0);
+        int tot2;
+        const int pos = block_excl_sum<int>(isnew, shi, &tot2);
+        if (isnew) {
+          a.sr_list[srn + pos] = r;
+          a.sr_pos[r] = srn + pos;
         }
-        if (threadIdx.x == 0) {
-          *a.sr_n = srn;
-          a.kept_cand[Ko - a.K0] = prev_n;
-          a.rptr[Ko + 1] = rnnz + pm;
-        }
+        srn += tot2;
       }
-      rnnz += pm;
+      if (threadIdx.x == 0) {
+        *a.sr_n = srn;
+        a.kept_cand[Ko - a.K0] = prev_n;
+        a.rptr[Ko + 1] = rnnz + a.c.len[prev_n];
+      }
     }
     if (!last) stamp(a.trace, n, 1);
     if (upd || !last) {
@@ -279,12 +265,8 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
       };
       auto yval = [&](long long i) -> double { return sm ? vB[i] : ldg_cg(&yprev[i]); };
       if (sm && pre) {
-        // g (j < Ko) and y_{n-1} were staged during P3 of n-1; add x_{n-1}'s column
-        if (upd && threadIdx.x == 0) {
-          vA[Ko] = a.Gc[(long long)prev_n * nu + n];
-          vB[Ko] = 0.0;
-        }
-        __syncthreads();
+        // g (j < Ko), y_{n-1} and x_{n-1}'s column (speculatively: used only
+        // if n-1 was kept) were staged during P3 of n-1
       } else {
         stage(0, Kn);
       }
@@ -475,6 +457,29 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
           a.trace[(long long)n * kTraceW + 27] = tprobe;
         }
       }
+    }
+    if (upd) {
+      // x_{n-1}'s entries into R's CSC and row index (read by P2 after the
+      // barrier, not by P1): the producer warps do it after their last ring
+      // chunk, while the chain warp finishes (off the critical path)
+      const long long poff = a.c.off[prev_n];
+      const int pm = a.c.len[prev_n];
+      const int warp = threadIdx.x >> 5;
+      const bool doer = last || is_producer(warp);
+      const long long per_cta = last ? blockDim.x : kProdThreads;
+      const long long me = last ? threadIdx.x : (is_producer(warp) ? producer_index(warp, lane) : 0);
+      for (long long t = (long long)blockIdx.x * per_cta + me; doer && t < pm; t += (long long)nb * per_cta) {
+        const int r = a.c.row[poff + t];
+        const double v = a.c.val[poff + t];
+        a.rrow[rnnz + t] = r;
+        a.rval[rnnz + t] = v;
+        const int L = ldg_cg(&a.rowlen[r]);
+        const long long p = a.rowbase[r] + L;
+        a.rek[p] = Ko;
+        a.rev[p] = v;
+        a.rowlen[r] = L + 1;
+      }
+      rnnz += pm;
     }
     K = Kn;
     if (last) break;
@@ -749,7 +754,12 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         a.tag[r] = tg1;
         zd1[r] = 0.0;
       }
-      for (int j = threadIdx.x - 32 * ncw; j < K; j += pw) {
+      for (int j = threadIdx.x - 32 * ncw; j <= K; j += pw) {
+        if (j == K) {  // column K if n is kept: g(x_n, x_{n+1})
+          vA[K] = a.Gc[(long long)n * nu + n1];
+          vB[K] = 0.0;
+          continue;
+        }
         vA[j] = (j < a.K0) ? a.Gb[(long long)j * nu + n1]
                            : a.Gc[(long long)ldg_cg(&a.kept_cand[j - a.K0]) * nu + n1];
         vB[j] = ldg_cg(&ycur[j]);
