@@ -156,6 +156,129 @@ def run_ctd_d(args, ctx, torch):
                      "kept-id append); Eq. 13 core blocks not maintained (SURVEY 8f #2)"}
 
 
+C4 = dict(c=5000, eps=1e-6, seed=42, mode=0, gen_seed=4)
+C5 = dict(shape=[100000, 100000, 1000], nnz=1_000_000_000, c=10000, eps=1e-6, seed=42, mode=0,
+          gen_seed=5)
+
+
+def load_c4():
+    from paper_1710_03608_b200 import datagen
+    seed = C4["gen_seed"]
+    cache = os.path.join(tempfile.gettempdir(), f"ctd_c4_seed{seed}.npz")
+    if os.path.exists(cache):
+        try:
+            z = np.load(cache)
+            return datagen.Tensor(list(z["shape"]), z["idx"], z["val"], {"seed": seed})
+        except Exception:
+            pass
+    x = datagen.c4(seed=seed)
+    try:
+        np.savez(cache, shape=np.array(x.shape), idx=x.idx, val=x.val)
+    except Exception:
+        pass
+    return x
+
+
+def _time_frontend(ctx, dt, cfg, steps, warmup, torch):
+    """Device time of `steps` CTD-S front ends on a resident tensor (CUDA events on
+    the launch stream), plus the per-phase split of the last run."""
+    from paper_1710_03608_b200 import ctd as api
+    for _ in range(warmup):
+        h, info = api.ctd_s_raw(dt, cfg["mode"], cfg["c"], cfg["eps"], cfg["seed"], ctx=ctx)
+        api.free_factors(ctx, h)
+    torch.cuda.synchronize()
+    ctx.set_timing(True)
+    ctx.phase_times(reset=True)
+    l0 = ctx.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    hs = []
+    e0.record()
+    for _ in range(steps):
+        hs.append(api.ctd_s_raw(dt, cfg["mode"], cfg["c"], cfg["eps"], cfg["seed"], ctx=ctx))
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    launches = (ctx.launches - l0) // steps
+    ph = ctx.phase_times(reset=True)
+    ctx.set_timing(False)
+    info = hs[-1][1]
+    for h, _ in hs:
+        api.free_factors(ctx, h)
+    phases = {k: round(v[0] / max(1, v[1]), 3) for k, v in ph.items() if v[1]}
+    return ms, info, phases, launches
+
+
+def run_c4(args, ctx, torch):
+    """BASELINE configs[3] (C4): 1000x1000x100 at 10% density, planted rank-20 CP +
+    N(0, 0.01^2), non-integer fp64; c = 5000 (the filter saturates at 1000 kept and
+    rejects the rest).  Same step scope as the headline (the ctd_s front end)."""
+    from paper_1710_03608_b200 import ctd as api
+    x = load_c4()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    idx_t = torch.from_numpy(np.ascontiguousarray(x.idx.T.astype(np.int32))).to(dev)
+    val_t = torch.from_numpy(x.val).to(dev)
+    dt = api.DeviceTensor.from_device_ptrs(x.shape, x.nnz, [idx_t[k].data_ptr() for k in range(3)],
+                                           val_t.data_ptr(), ctx)
+    ms, info, phases, launches = _time_frontend(ctx, dt, C4, max(1, min(args.steps, 3)), 1, torch)
+    out = {"workload": "C4: CTD-S on 1000x1000x100 at 10% density, planted rank-20 CP + N(0,0.01^2) "
+                       "(non-integer fp64), c=5000, eps=1e-6, mode 0",
+           "nnz": x.nnz, "ms_per_step": round(ms, 3), "nnz_per_s": round(x.nnz / (ms / 1e3), 1),
+           "unique_sampled": info.n_unique, "kept": info.kept, "phases_ms": phases,
+           "gpu_launches_per_step": launches}
+    dt.close()
+    if not args.no_cpu:
+        try:
+            from oracle.bindings import Ref, ref_available
+            if ref_available():
+                R = Ref()
+                fe = R.frontend(R.tensor(x.shape, x.flat_idx(), x.val), C4["mode"], C4["c"], C4["eps"],
+                                C4["seed"])
+                out["cpu_reference"] = {"value": round(x.nnz / fe.seconds, 1), "unit": UNIT,
+                                        "seconds": round(fe.seconds, 3), "cores": 1, "kind": "reference",
+                                        "sample": "full C4 tensor, reference ctd_s front end, "
+                                                  "single-threaded"}
+        except Exception as e:  # pragma: no cover
+            out["cpu_reference"] = {"sample": f"failed: {e}"}
+    return out
+
+
+def run_c5(args, ctx, torch):
+    """BASELINE configs[4] (C5) on one GPU: 1e5x1e5x1e3 traffic with 1e9 coalesced nnz
+    (Zipf(1.2) src/dst, uniform time, log-uniform counts 1..100; int32 indices),
+    c = 10000.  Generated on the device (datagen_gpu, same law as the host generator);
+    the front end is timed on the resident tensor (20 GB of COO, far above L2)."""
+    from paper_1710_03608_b200 import ctd as api
+    from paper_1710_03608_b200 import datagen_gpu
+    free, _ = torch.cuda.mem_get_info()
+    if free < 120e9:
+        return {"skipped": f"needs ~120 GB free device memory, have {free / 1e9:.0f} GB"}
+    t0 = time.perf_counter()
+    idx, val, meta = datagen_gpu.traffic(C5["shape"], C5["nnz"], C5["gen_seed"])
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    torch.cuda.empty_cache()
+    nnz = meta["nnz"]
+    dt = api.DeviceTensor.from_device_ptrs(C5["shape"], nnz, [idx[k].data_ptr() for k in range(3)],
+                                           val.data_ptr(), ctx)
+    ms, info, phases, launches = _time_frontend(ctx, dt, C5, max(1, min(args.steps, 2)), 1, torch)
+    pk, _ = peaks()
+    bs = 44 * nnz + 24 * info.n_fibers
+    mat_ms = phases.get("matricize")
+    out = {"workload": "C5: CTD-S on 1e5x1e5x1e3 traffic, 1e9 coalesced nnz (Zipf(1.2), uniform time, "
+                       "log-uniform counts 1..100, int32 indices), c=10000, eps=1e-6, mode 0; 1 GPU",
+           "nnz": nnz, "draws": meta["draws"], "fibers": info.n_fibers, "generate_s": round(gen_s, 2),
+           "ms_per_step": round(ms, 3), "nnz_per_s": round(nnz / (ms / 1e3), 1),
+           "unique_sampled": info.n_unique, "kept": info.kept, "phases_ms": phases,
+           "gpu_launches_per_step": launches,
+           "step_bytes_44nnz_24F": bs, "step_frac_of_peak": round(bs / (ms / 1e3) / 1e9 / pk, 4),
+           "matricize_gbs": round((32 * nnz + 24 * info.n_fibers) / (mat_ms / 1e3) / 1e9, 1)
+           if mat_ms else None}
+    dt.close()
+    del idx, val
+    torch.cuda.empty_cache()
+    return out
+
+
 def ctd_d_reference_sample():
     """The reference ctd_d_step (oracle/_ref, which also updates the Eq. 13 core) on C3:
     init_stream on the first 10 slices, then 5 timed steps (a bounded sample)."""
@@ -495,6 +618,15 @@ def run_ours(args, rank, world, local_rank):
         if not args.no_cpu:
             ctdd["cpu_reference"] = ctd_d_reference_sample()
 
+    c4 = c5 = None
+    if rank == 0 and world == 1 and not args.no_c4:
+        c4 = run_c4(args, ctx, torch)
+    if rank == 0 and world == 1 and not args.no_c5:
+        del idx_t, val_t
+        dt.close()
+        torch.cuda.empty_cache()
+        c5 = run_c5(args, ctx, torch)
+
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
@@ -523,6 +655,10 @@ def run_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = cpu
     if ctdd is not None:
         line["ctd_d"] = ctdd
+    if c4 is not None:
+        line["c4"] = c4
+    if c5 is not None:
+        line["c5"] = c5
     if rank == 0:
         print(json.dumps(line, default=_np_default), flush=True)
 
@@ -638,6 +774,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ctdd", action="store_true", help="skip the C3 CTD-D per-step latency run")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (planted CP, c=5000) line")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (1e9 nnz) line")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -16,6 +16,9 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
+
+#include <cub/cub.cuh>
 
 #include "bucket.cuh"
 #include "radix.cuh"
@@ -166,6 +169,7 @@ struct SortArgs {
   int wbits, rowbits;
   long long* F_out;
   unsigned* flags;
+  int presorted;                  // oversize buckets already sorted (gkey2 keys, out_val values)
 };
 
 __device__ long long lookback(unsigned long long* st, long long b, long long agg) {
@@ -227,6 +231,9 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(SortArgs a) {
     const uint16_t* I = inb ? sib : sia;
     for (int p = t; p < m; p += T) sv[p] = a.tval[start + I[p]];
     V = sv;
+  } else if (a.presorted) {
+    K = a.gkey2 + start;
+    V = a.out_val + start;
   } else {
     uint32_t* ka = a.tkey + start;
     uint32_t* kb = a.gkey2 + start;
@@ -274,10 +281,101 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(SortArgs a) {
     const long long f = fbase + rank++;
     a.fcol[f] = ((long long)b << a.wbits) + (long long)jl;
     a.fptr[f] = start + p;
-    // column_sq_norms: s += v*v in ascending row order (tensor_ops.cpp:197-198)
+    // column_sq_norms: s += v*v in ascending row order (tensor_ops.cpp:197-198).
+    // The fiber's end first (keys are sorted: binary search for long fibers),
+    // so the value loads do not wait on the loop condition.
+    int e = p + 1;
+    {
+      const int lim = min(m, p + 16);
+      while (e < lim && (K[e] >> a.rowbits) == jl) ++e;
+      if (e == lim && e < m && (K[e] >> a.rowbits) == jl) {
+        int lo = e, hi = m;  // first index in [lo, hi) with a larger column
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if ((K[mid] >> a.rowbits) == jl) lo = mid + 1;
+          else hi = mid;
+        }
+        e = lo;
+      }
+    }
     double s = 0.0;
-    for (int q = p; q < m && (K[q] >> a.rowbits) == jl; ++q) s = dadd(s, dsqr(V[q]));
+    int q = p;
+    if (e - p >= 64) {  // long fiber: L1 prefetch 16 lines ahead of the 16-value batches
+      for (; q + 16 <= e; q += 16) {
+        if (q + 256 < e) asm volatile("prefetch.global.L1 [%0];" ::"l"(V + q + 256));
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = V[q + u];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) s = dadd(s, dsqr(v[u]));
+      }
+    }
+    for (; q < e; ++q) s = dadd(s, dsqr(V[q]));
     a.norm[f] = s;
+  }
+}
+
+// Oversize buckets (more entries than one CTA's shared memory holds: a heavy
+// Zipf column) are sorted together by a device-wide radix sort instead of one
+// CTA per bucket.  Their entries are compacted with 64-bit keys
+// (rank of the bucket among the oversize ones, 32-bit in-bucket key); after
+// the sort the compacted array is the concatenation of the sorted buckets in
+// bucket order, so each entry goes back to its bucket's range.
+// Buckets above each power-of-two size 256..8192 (cap selection).
+__global__ void k_size_dist(const unsigned* count, long long nb, unsigned long long* above) {
+  __shared__ unsigned long long sh[6];
+  if (threadIdx.x < 6) sh[threadIdx.x] = 0;
+  __syncthreads();
+  for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (long long)gridDim.x * blockDim.x) {
+    const unsigned c = count[b];
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+      if (c > (256u << k)) atomicAdd(&sh[k], 1ull);
+  }
+  __syncthreads();
+  if (threadIdx.x < 6 && sh[threadIdx.x]) atomicAdd(&above[threadIdx.x], sh[threadIdx.x]);
+}
+
+__global__ void k_over_count(const unsigned* count, long long nb, int cap, unsigned long long* ocnt,
+                             unsigned* is_over) {
+  const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const bool ov = count[b] > (unsigned)cap;
+  ocnt[b] = ov ? count[b] : 0ull;
+  is_over[b] = ov ? 1u : 0u;
+}
+
+__global__ void k_over_list(const unsigned* is_over, const unsigned* orank, long long nb,
+                            long long* olist) {
+  const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb && is_over[b]) olist[orank[b]] = b;
+}
+
+__global__ void k_over_pack(const long long* olist, const unsigned long long* off,
+                            const unsigned long long* ooff, const uint32_t* tkey, int keybits,
+                            unsigned long long* okey, uint32_t* oidx) {
+  const long long r = blockIdx.x;
+  const long long b = olist[r];
+  const long long start = (long long)off[b], m = (long long)off[b + 1] - start;
+  const long long o = (long long)ooff[b];
+  for (long long p = threadIdx.x; p < m; p += blockDim.x) {
+    okey[o + p] = ((unsigned long long)r << keybits) | tkey[start + p];
+    oidx[o + p] = (uint32_t)(start + p);
+  }
+}
+
+__global__ void k_over_unpack(const long long* olist, const unsigned long long* off,
+                              const unsigned long long* ooff, const unsigned long long* skey,
+                              const uint32_t* sidx, const double* tval, int keybits,
+                              uint32_t* gkey2, double* out_val) {
+  const long long b = olist[blockIdx.x];
+  const long long start = (long long)off[b], m = (long long)off[b + 1] - start;
+  const long long o = (long long)ooff[b];
+  const unsigned long long kmask = keybits >= 32 ? 0xffffffffull : ((1ull << keybits) - 1ull);
+  for (long long p = threadIdx.x; p < m; p += blockDim.x) {
+    gkey2[start + p] = (uint32_t)(skey[o + p] & kmask);
+    out_val[start + p] = tval[sidx[o + p]];
   }
 }
 
@@ -377,13 +475,90 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
   gidx2.alloc(ctx, nnz);
   // Shared-memory capacity sized to the largest bucket (more CTAs per SM).
   const unsigned mx = ctx->read1(maxc.p);
+  if (htrace) {
+    std::vector<unsigned> hc(nb);
+    ctx->to_host(hc.data(), count.p, nb);
+    ctx->sync();
+    long long nover = 0, eover = 0;
+    for (long long b = 0; b < nb; ++b)
+      if (hc[b] > (unsigned)kCap) ++nover, eover += hc[b];
+    fprintf(stderr, "[matricize] nnz=%lld cols=%lld rowbits=%d wbits=%d buckets=%lld max=%u "
+            "oversize=%lld (%lld entries)\n", nnz, (long long)out.cols, rowbits, wbits, nb, mx,
+            nover, eover);
+  }
   HT()
+  // Shared-memory capacity: the smallest power of two holding the largest
+  // bucket (<= kCap).  With many buckets, a large cap costs occupancy on every
+  // CTA (kCap: one CTA per SM), so when few buckets (< 10%) are
+  // above twice the mean size, cap is sized for the rest and the outliers go
+  // through the device-wide sort below.
   int cap = 256;
   while (cap < (int)mx && cap < kCap) cap <<= 1;
+  if (nb > 16ll * ctx->sm_count && nnz < (1ll << 32)) {
+    Buf<unsigned long long> above(ctx, 6);
+    above.zero();
+    LAUNCH(ctx, k_size_dist, (unsigned)std::min<long long>(ceil_div(nb, 256), ctx->sm_count * 4), 256,
+           0, count.p, nb, above.p);
+    unsigned long long ab[6];
+    ctx->to_host(ab, above.p, 6);
+    ctx->sync();
+    const double mean = (double)nnz / (double)nb;
+    int small = 256;
+    while (small < kCap && (double)small < 2.0 * mean) small <<= 1;
+    int k = 0;
+    while ((256 << k) < small) ++k;
+    if (small < cap && (double)ab[k] < 0.1 * (double)nb) cap = small;
+    if (htrace)
+      fprintf(stderr, "[matricize] buckets above 256..8192: %llu %llu %llu %llu %llu %llu; cap %d\n",
+              ab[0], ab[1], ab[2], ab[3], ab[4], ab[5], cap);
+  }
   const int threads = cap <= 2048 ? 256 : kSortThreads;
+  int presorted = 0;
+  if ((int)mx > cap && nnz < (1ll << 32)) {
+    // oversize buckets: one device-wide radix sort over all of them
+    Buf<unsigned long long> ocnt(ctx, nb), ooff(ctx, nb + 1);
+    Buf<unsigned> isov(ctx, nb), orank(ctx, nb + 1);
+    LAUNCH(ctx, k_over_count, ceil_div(nb, 256), 256, 0, count.p, nb, cap, ocnt.p, isov.p);
+    size_t tb1 = 0, tb2 = 0;
+    CUDA_OK(cub::DeviceScan::ExclusiveSum(nullptr, tb1, ocnt.p, ooff.p, nb + 1, ctx->stream));
+    CUDA_OK(cub::DeviceScan::ExclusiveSum(nullptr, tb2, isov.p, orank.p, nb + 1, ctx->stream));
+    Buf<unsigned char> tmp(ctx, std::max(tb1, tb2));
+    CUDA_OK(cub::DeviceScan::ExclusiveSum(tmp.p, tb1, ocnt.p, ooff.p, nb, ctx->stream));
+    CUDA_OK(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, isov.p, orank.p, nb, ctx->stream));
+    ctx->launches += 4;  // two cub scans (init + scan kernels each)
+    unsigned long long last_off = 0, last_cnt = 0;
+    unsigned last_rank = 0, last_ov = 0;
+    ctx->to_host(&last_off, ooff.p + nb - 1, 1);
+    ctx->to_host(&last_cnt, ocnt.p + nb - 1, 1);
+    ctx->to_host(&last_rank, orank.p + nb - 1, 1);
+    ctx->to_host(&last_ov, isov.p + nb - 1, 1);
+    ctx->sync();
+    const long long n_over = (long long)last_rank + last_ov;
+    const long long e_over = (long long)(last_off + last_cnt);
+    if (n_over > 0) {
+      Buf<long long> olist(ctx, n_over);
+      LAUNCH(ctx, k_over_list, ceil_div(nb, 256), 256, 0, isov.p, orank.p, nb, olist.p);
+      const int keybits = wbits + rowbits;
+      const int obits = keybits + bits_for(n_over);
+      Buf<unsigned long long> k1(ctx, e_over), k2(ctx, e_over);
+      Buf<uint32_t> i1(ctx, e_over), i2(ctx, e_over);
+      LAUNCH(ctx, k_over_pack, (unsigned)n_over, 256, 0, olist.p, off.p, ooff.p, tkey.p, keybits,
+             k1.p, i1.p);
+      size_t tb3 = 0;
+      CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tb3, k1.p, k2.p, i1.p, i2.p, e_over, 0, obits,
+                                              ctx->stream));
+      Buf<unsigned char> tmp3(ctx, tb3);
+      CUDA_OK(cub::DeviceRadixSort::SortPairs(tmp3.p, tb3, k1.p, k2.p, i1.p, i2.p, e_over, 0, obits,
+                                              ctx->stream));
+      ctx->launches += 1 + (obits + 7) / 8;  // cub onesweep: histogram + one pass per 8 bits
+      LAUNCH(ctx, k_over_unpack, (unsigned)n_over, 256, 0, olist.p, off.p, ooff.p, k2.p, i2.p,
+             tval.p, keybits, gkey2.p, out.val.p);
+      presorted = 1;
+    }
+  }
   SortArgs sa{cap, off.p, tkey.p, tval.p, gkey2.p, gidx1.p, gidx2.p, out.row.p, out.val.p,
               out.col.p, out.ptr.p, out.norm.p, status.p, ticket.p, nb, nnz, wbits, rowbits,
-              dF.p, ctx->d_flags};
+              dF.p, ctx->d_flags, presorted};
   const size_t smem = (size_t)cap * (4 + 4 + 2 + 2 + 8) + (threads / 32) * kRadix * 4;
   static bool attr_set = false;
   if (!attr_set) {

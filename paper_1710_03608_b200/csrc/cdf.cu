@@ -4,6 +4,10 @@
 //   p_j = fl(n_j / T)                              (sampling.cpp:29)
 //   cum = sequential running sum of p, tail clamped (sampling.cpp:42-54)
 // All three are bit-identical to the reference.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "cdf.cuh"
 #include "seqsum.cuh"
 
@@ -14,7 +18,9 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kPerThread = 8;
 constexpr int kBS = kThreads * kPerThread;  // elements per block
-constexpr int kDMax = 128;                  // directs per block before fallback
+constexpr int kDMax = 128;                  // directs per block before the block is walked
+constexpr int kOver = kDMax + 1;            // bnd[] of a walked block
+constexpr short E_WALKED = -30002;          // element summed by the walker (walked block)
 
 __global__ void k_chunk_sum(const double* __restrict__ x, long long n, double* bsum) {
   __shared__ double sh[33];
@@ -112,17 +118,28 @@ __global__ void k_seq_local(const double* __restrict__ x, long long n, const dou
   Seg carry = block_seg_excl(agg, ssh, &tot_seg);
   int ntot;
   int dpos = block_excl_sum<int>(nd, ish, &ntot);
+  // A block with more directs than its slots (e.g. a CDF creeping up to a
+  // binade edge in tiny steps: every element near the edge is direct) is
+  // "walked": the walker adds all its elements sequentially.  To the carry
+  // scan it is one head at its end (slot b*kDMax) followed by nothing.
   const bool over = ntot > kDMax;
   if (threadIdx.x == 0) {
-    o.bnd[blockIdx.x] = over ? 0 : ntot;
-    o.bagg[blockIdx.x] = tot_seg;
-    if (over) atomicOr(flags, FLAG_SEQSUM);
+    o.bnd[blockIdx.x] = over ? kOver : ntot;
+    o.bagg[blockIdx.x] = over ? Seg{1, mono_id()} : tot_seg;
   }
   // e of the element before this thread's chunk (within the block).
   short prev_e = (short)0x7ffe;  // 0x7ffe: "previous block"
   for (int q = (int)threadIdx.x - 1; q >= 0; --q)
     if (last_e[q] != (short)0x7fff) { prev_e = last_e[q]; break; }
   // Pass C.
+  if (over) {
+#pragma unroll
+    for (int k = 0; k < kPerThread; ++k)
+      if (b0 + k < n) o.e[b0 + k] = E_WALKED;
+    const long long last = min(n, bb + kBS) - 1;
+    if ((last - bb) / kPerThread == (long long)threadIdx.x) o.blast[blockIdx.x] = E_DIRECT;
+    return;
+  }
   {
     double P = pre;
     Mono M = carry.m;
@@ -201,7 +218,7 @@ __global__ void __launch_bounds__(kCarryThreads) k_seq_carry(long long nb, Local
   for (long long b = b0; b < b1; ++b) {
     agg = seg_cat(agg, o.bagg[b]);
     if (o.bnd[b] > 0) {
-      last_slot = (int)(b * kDMax + o.bnd[b] - 1);
+      last_slot = (int)(b * kDMax + (o.bnd[b] == kOver ? 0 : o.bnd[b] - 1));
       ++nd;
     }
   }
@@ -218,7 +235,7 @@ __global__ void __launch_bounds__(kCarryThreads) k_seq_carry(long long nb, Local
     w.inh_head[b] = inh;
     carry = seg_cat(carry, o.bagg[b]);
     if (o.bnd[b] > 0) {
-      inh = (int)(b * kDMax + o.bnd[b] - 1);
+      inh = (int)(b * kDMax + (o.bnd[b] == kOver ? 0 : o.bnd[b] - 1));
       dblocks[pos++] = (int)b;
     }
   }
@@ -228,8 +245,9 @@ __global__ void __launch_bounds__(kCarryThreads) k_seq_carry(long long nb, Local
 }
 
 // Sequential walker over the (few) blocks that hold direct elements.
-__global__ void k_seq_walk(long long nb, LocalOut o, WalkOut w, const int* dblocks,
-                           const int* n_dblocks, unsigned* flags) {
+__global__ void k_seq_walk(const double* __restrict__ x, long long n, long long nb, LocalOut o,
+                           WalkOut w, const int* dblocks, const int* n_dblocks, double* cum,
+                           unsigned* flags, double* diag) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (*flags & FLAG_SEQSUM) return;
   double head = 0.0;
@@ -240,12 +258,32 @@ __global__ void k_seq_walk(long long nb, LocalOut o, WalkOut w, const int* dbloc
     const Mono cin = w.carry_in[b];
     const short prev_last = b > 0 ? o.blast[b - 1] : E_ZERO;
     const int nd = o.bnd[b];
+    if (nd == kOver) {  // walked block: the pending run, then every element in order
+      double acc = head;
+      if (is_reg_e(prev_last)) ok = seq_apply_run(head, prev_last, cin, &acc);
+      if (!ok && diag) {
+        diag[0] = (double)b; diag[1] = -1.0; diag[2] = (double)prev_last; diag[3] = head;
+      }
+      const long long i0 = b * kBS, i1 = min(n, i0 + kBS);
+#pragma unroll 8
+      for (long long i = i0; i < i1; ++i) {
+        acc = dadd(acc, x[i]);
+        if (cum) cum[i] = acc;
+      }
+      head = acc;
+      w.head_val[b * kDMax] = acc;
+      continue;
+    }
     for (int q = 0; q < nd && ok; ++q) {
       const int slot = (int)(b * kDMax + q);
       const Mono M = o.dl_inh[slot] ? mono_cat(cin, o.dl_m[slot]) : o.dl_m[slot];
       const short eb = (o.dl_e[slot] == (short)0x7ffe) ? prev_last : o.dl_e[slot];
       double acc = head;
       if (is_reg_e(eb)) ok = seq_apply_run(head, eb, M, &acc);
+      if (!ok && diag) {
+        diag[0] = (double)b; diag[1] = (double)q; diag[2] = (double)eb; diag[3] = head;
+        diag[4] = (double)M.a0; diag[5] = (double)M.a1; diag[6] = o.dl_x[slot]; diag[7] = (double)nd;
+      }
       acc = dadd(acc, o.dl_x[slot]);
       head = acc;
       w.head_val[slot] = acc;
@@ -253,7 +291,13 @@ __global__ void k_seq_walk(long long nb, LocalOut o, WalkOut w, const int* dbloc
   }
   double total = head;
   const short last_e = o.blast[nb - 1];
-  if (ok && is_reg_e(last_e)) ok = seq_apply_run(head, last_e, w.final_m[0], &total);
+  if (ok && is_reg_e(last_e)) {
+    ok = seq_apply_run(head, last_e, w.final_m[0], &total);
+    if (!ok && diag) {
+      diag[0] = -1.0; diag[2] = (double)last_e; diag[3] = head;
+      diag[4] = (double)w.final_m[0].a0; diag[5] = (double)w.final_m[0].a1;
+    }
+  }
   if (!ok) atomicOr(flags, FLAG_SEQSUM);
   else *w.total = total;
 }
@@ -264,6 +308,7 @@ __global__ void k_seq_final(long long n, LocalOut o, WalkOut w, double* cum,
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const short e = o.e[i];
+  if (e == E_WALKED) return;  // written by the walker
   double c;
   if (e == E_ZERO) {
     c = 0.0;
@@ -324,9 +369,41 @@ void seq_cumsum(Ctx* ctx, const double* x, int64_t n, double* cum, double* d_tot
   LAUNCH(ctx, k_scan_bsum, 1, 1024, 0, bsum.p, nb, bpre.p);
   LAUNCH(ctx, k_seq_local, (unsigned)nb, kThreads, 0, x, (long long)n, bpre.p, o, fl.p);
   LAUNCH(ctx, k_seq_carry, 1, kCarryThreads, 0, nb, o, w, dblocks.p, ndb.p);
-  LAUNCH(ctx, k_seq_walk, 1, 32, 0, nb, o, w, dblocks.p, ndb.p, fl.p);
+  static const bool trace = getenv("CTD_SEQ_TRACE") != nullptr;
+  Buf<double> diag(ctx, 8);
+  if (trace) diag.zero();
+  LAUNCH(ctx, k_seq_walk, 1, 32, 0, x, (long long)n, nb, o, w, dblocks.p, ndb.p, cum, fl.p,
+         trace ? diag.p : nullptr);
   if (cum) LAUNCH(ctx, k_seq_final, ceil_div(n, 256), 256, 0, (long long)n, o, w, cum, fl.p);
   LAUNCH(ctx, k_seq_fallback, 1, 32, 0, x, (long long)n, cum, d_total, fl.p);
+  if (trace) {  // diagnostics: which self-check sent the sum to the fallback
+    std::vector<int> hb(nb);
+    ctx->to_host(hb.data(), bnd.p, nb);
+    const unsigned f = ctx->read1(fl.p);
+    const int nd = ctx->read1(ndb.p);
+    long long tot = 0;
+    int shown = 0;
+    for (long long b = 0; b < nb; ++b) {
+      if (hb[b] == kOver && shown < 6) {
+        ++shown;
+        double xs[8], pb;
+        ctx->to_host(xs, x + b * kBS, std::min<long long>(8, n - b * kBS));
+        ctx->to_host(&pb, bpre.p + b, 1);
+        ctx->sync();
+        fprintf(stderr, "[seq_cumsum] walked block %lld: prefix %.17g, x[0..3] %.17g %.17g %.17g %.17g\n",
+                b, pb, xs[0], xs[1], xs[2], xs[3]);
+      }
+      tot += hb[b] == kOver ? 0 : hb[b];
+    }
+    double dg[8];
+    ctx->to_host(dg, diag.p, 8);
+    ctx->sync();
+    fprintf(stderr, "[seq_cumsum] n=%lld blocks=%lld direct_blocks=%d directs=%lld fallback=%d\n",
+            (long long)n, nb, nd, tot, (int)((f & FLAG_SEQSUM) != 0));
+    if (f & FLAG_SEQSUM)
+      fprintf(stderr, "[seq_cumsum] walk failed: block=%.0f q=%.0f e=%.0f head=%.17g a0=%.0f a1=%.0f x=%.17g nd=%.0f\n",
+              dg[0], dg[1], dg[2], dg[3], dg[4], dg[5], dg[6], dg[7]);
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -153,12 +153,16 @@ __global__ void k_dense_cands(Cands c, double* D, long long n) {
 __global__ void k_gram(const int64_t* lptr_off, const int32_t* llen, const int64_t* lptr, int use_ptr,
                        const int32_t* lrow, const double* lval, long long nleft, const double* D,
                        long long n, double* G, int strictly_upper) {
+  // Warps are ordered column-chunk-major: the warps resident at one time share
+  // a few 32-column chunks of D (dim x 32 doubles each), which stay in L2
+  // while every left vector streams its rows through them.
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nbw = (n + 31) >> 5;
-  const long long a = warp / nbw;
-  if (a >= nleft) return;
-  const long long b = (warp % nbw) * 32 + (threadIdx.x & 31);
-  if (strictly_upper && ((warp % nbw) * 32 + 31) <= a) return;  // whole warp below diagonal
+  const long long a = warp % nleft;
+  const long long bc = warp / nleft;
+  if (bc >= nbw) return;
+  const long long b = bc * 32 + (threadIdx.x & 31);
+  if (strictly_upper && (bc * 32 + 31) <= a) return;  // whole warp below diagonal
   long long off, len;
   if (use_ptr) {
     off = lptr[a];

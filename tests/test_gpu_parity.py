@@ -18,7 +18,23 @@ CASES = {
     "traffic": lambda: g.traffic([500, 500, 20], 20000, 11),
     "cp_small": lambda: g.c4(seed=4, scale_j=60, scale_k=10),
     "order4": lambda: g.random_sparse([8, 9, 10, 11], 0.05, 12),
+    "heavy_fibers": lambda: _heavy_fibers(),
 }
+
+
+def _heavy_fibers():
+    """Mode-0 fibers longer than one CTA's shared-memory bucket (8192 entries):
+    the device-wide radix-sort path of the bucketing (bucket.cu, oversize)."""
+    I = 40000
+    base = g.random_sparse([I, 6, 5], 0.002, 13)
+    extra = []
+    for j, (a, b, n) in enumerate([(0, 0, 15000), (3, 2, 9000), (5, 4, 30000), (1, 1, 8193)]):
+        rows = np.nonzero(g.uniform(50 + j, 0, 0, I) < n / I)[0]
+        extra.append(np.stack([rows, np.full_like(rows, a), np.full_like(rows, b)], axis=1))
+    idx = np.concatenate([base.idx] + extra)
+    val = np.concatenate([base.val] + [np.floor(g.uniform(60 + j, 0, 0, e.shape[0]) * 7) + 1
+                                       for j, e in enumerate(extra)])
+    return g.coalesce([I, 6, 5], idx, val)
 
 
 def _st(x):

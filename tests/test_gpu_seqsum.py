@@ -27,6 +27,12 @@ def _cases():
     yield "subnormal", np.concatenate([np.full(1000, 5e-324), r.random(1000) * 1e-310, r.random(1000)])
     p = r.random(1_000_000) ** 8
     yield "cdf_like", p / p.sum()
+    # a CDF creeping up to 1.0 in tiny steps (C5's law: 8e7 fibers): every term of
+    # the tail lies inside the binade-edge margin, so whole blocks are walked
+    tail = r.random(600_000) * 2e-13
+    yield "edge_creep", np.concatenate([[1.0 - tail.sum() * 0.7], tail, r.random(5000) * 1e-3])
+    yield "edge_creep_mid", np.concatenate([r.random(3000) * 1e-4, [0.5 - 0.3 - 1e-9],
+                                            np.full(300_000, 1e-14), r.random(9000)])
     # growing terms (many crossings)
     yield "geometric", 1.0001 ** np.arange(200_000)
 
