@@ -172,13 +172,22 @@ struct SortArgs {
   int presorted;                  // oversize buckets already sorted (gkey2 keys, out_val values)
 };
 
-__device__ long long lookback(unsigned long long* st, long long b, long long agg) {
+// Decoupled look-back over the buckets' fiber counts.  The count (distinct
+// columns) can be published early (lookback_publish, from a bitmap of the
+// bucket's columns, before the sort) so later buckets never wait on a slow
+// one; lookback() then only walks back and publishes the inclusive prefix.
+__device__ void lookback_publish(unsigned long long* st, long long b, long long agg) {
+  const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62;
+  atomicExch(&st[b], (b == 0 ? kInc : kAgg) | (unsigned long long)agg);
+}
+
+__device__ long long lookback(unsigned long long* st, long long b, long long agg, bool published) {
   const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1;
   if (b == 0) {
-    atomicExch(&st[0], kInc | (unsigned long long)agg);
+    if (!published) atomicExch(&st[0], kInc | (unsigned long long)agg);
     return 0;
   }
-  atomicExch(&st[b], kAgg | (unsigned long long)agg);
+  if (!published) atomicExch(&st[b], kAgg | (unsigned long long)agg);
   long long prefix = 0;
   long long i = b - 1;
   while (true) {
@@ -217,6 +226,28 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(SortArgs a) {
   const int T = blockDim.x, t = threadIdx.x;
   const int keybits = a.wbits + a.rowbits;
   const uint32_t rowmask = a.rowbits ? (0xffffffffu >> (32 - a.rowbits)) : 0u;
+  // early publication of the bucket's fiber count (distinct columns)
+  constexpr int kBmWords = 1024;  // columns per bucket <= 32768
+  __shared__ unsigned bm[kBmWords];
+  __shared__ int s_cnt;
+  const bool early = a.wbits <= 15;
+  if (early) {
+    const int words = ((1 << a.wbits) + 31) >> 5;
+    for (int w = t; w < words; w += T) bm[w] = 0u;
+    if (t == 0) s_cnt = 0;
+    __syncthreads();
+    for (int p = t; p < m; p += T) {
+      const uint32_t jl = a.rowbits < 32 ? (a.tkey[start + p] >> a.rowbits) : 0u;
+      atomicOr(&bm[jl >> 5], 1u << (jl & 31));
+    }
+    __syncthreads();
+    int c = 0;
+    for (int w = t; w < words; w += T) c += __popc(bm[w]);
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((t & 31) == 0 && c) atomicAdd(&s_cnt, c);
+    __syncthreads();
+    if (t == 0) lookback_publish(a.status, b, s_cnt);
+  }
   const bool small = m <= cap;
   const uint32_t* K;
   const double* V;
@@ -265,7 +296,8 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(SortArgs a) {
   long long agg;
   long long rank = block_excl_sum<long long>(nh, sh64, &agg);
   if (t == 0) {
-    s_fbase = lookback(a.status, b, agg);
+    if (early && agg != (long long)s_cnt) atomicOr(a.flags, FLAG_OVERFLOW);  // cannot happen
+    s_fbase = lookback(a.status, b, agg, early);
     if (b == a.nb - 1) {
       *a.F_out = s_fbase + agg;
       a.fptr[s_fbase + agg] = a.nnz;
