@@ -44,6 +44,10 @@ enum ctd_gpu_status {
 #define CTD_GPU_WITH_CORE 0x2u  /* also materialize C = X x_mode R^T (ctd_static.cpp:12-17) */
 #define CTD_GPU_KEEP_PANEL 0x4u /* keep the orthonormal panel W = R T for a later ctd_gpu_relative_error
                                    (implied by CTD_GPU_WITH_ERROR; ~2% of the filter's time) */
+/* ctd_gpu_stream_init flags (init_stream's keep_history / exact_core,
+   ctd_dynamic.hpp:42-45); both imply CTD_GPU_WITH_CORE */
+#define CTD_GPU_KEEP_HISTORY 0x8u /* retain the raw history on the device (core_drift) */
+#define CTD_GPU_EXACT_CORE 0x10u  /* bottom-left block from the history (ctd_dynamic.cpp:207-211) */
 
 typedef struct ctd_gpu_ctx ctd_gpu_ctx;         /* device, stream, scratch pool */
 typedef struct ctd_gpu_tensor ctd_gpu_tensor;   /* SparseTensor (sparse_tensor.hpp:17-60) resident in HBM */
@@ -236,6 +240,10 @@ int ctd_gpu_stream_step(ctd_gpu_stream *s, const ctd_gpu_tensor *slab,
 int64_t ctd_gpu_stream_t(const ctd_gpu_stream *s);
 /* Snapshot of the stream's factors (kept ids, R, U; core when maintained). */
 int ctd_gpu_stream_factors(ctd_gpu_stream *s, ctd_gpu_factors **out);
+/* core_drift (ctd_dynamic.hpp:64-66, ctd_dynamic.cpp:271-301): |C - R^T X_hist|_F
+   against the retained history (CTD_GPU_KEEP_HISTORY or CTD_GPU_EXACT_CORE;
+   otherwise CTD_ERR_ARGUMENT like the reference's ArgumentError). */
+int ctd_gpu_stream_core_drift(ctd_gpu_stream *s, double *out);
 int ctd_gpu_stream_destroy(ctd_gpu_stream *s);
 
 #ifdef __cplusplus

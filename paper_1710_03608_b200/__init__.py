@@ -7,7 +7,7 @@ from .ctd import (ArgumentError, ColumnDistribution, Context, CtdError, DeviceEr
                   DeviceTensor, EmptyInputError, FiberBasis, LRFactors, Matricized,
                   MetricError, NumericError, ShapeError, SparseTensor, StreamState,
                   column_distribution, column_sq_norms, ctd_d_step, ctd_s,
-                  default_step_samples, init_stream, make_fiber_id, matricize,
+                  core_drift, default_step_samples, init_stream, make_fiber_id, matricize,
                   memory_usage, relative_error, sample_with_replacement, unique_first_occurrence)
 
 __version__ = "0.1.0"

@@ -78,6 +78,7 @@ SIGNATURES = [
     ("ctd_gpu_stream_step", _I, [_V, _V, _I64]),
     ("ctd_gpu_stream_t", _I64, [_V]),
     ("ctd_gpu_stream_factors", _I, [_V, _PV]),
+    ("ctd_gpu_stream_core_drift", _I, [_V, C.POINTER(C.c_double)]),
     ("ctd_gpu_stream_destroy", _I, [_V]),
 ]
 

@@ -879,6 +879,14 @@ int ctd_gpu_stream_factors(ctd_gpu_stream* s, ctd_gpu_factors** out) {
   });
 }
 
+int ctd_gpu_stream_core_drift(ctd_gpu_stream* s, double* out) {
+  return guarded([&] {
+    need(s, "stream");
+    need(out, "out");
+    *out = stream_core_drift(s->s);
+  });
+}
+
 int ctd_gpu_stream_destroy(ctd_gpu_stream* s) {
   return guarded([&] { delete s; });
 }

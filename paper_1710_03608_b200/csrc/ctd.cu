@@ -93,7 +93,66 @@ void check_ctd_s_args(const Tensor& x, int mode, int64_t s, double eps) {
   if (!(eps > 0.0)) fail(CTD_ERR_ARGUMENT, "epsilon must be positive");
 }
 
+// History append (concatenate_time, ctd_dynamic.cpp:87-105): plane k of the
+// history holds mode k's indices; the time coordinate is shifted by t_add.
+struct IdxPlanes {
+  const int32_t* p[kMaxOrder];
+};
+__global__ void k_hist_append(IdxPlanes src, const double* sval, long long nnz, int order, long long t_add,
+                              int32_t* didx, long long hcap, double* dval, long long at) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nnz) return;
+  for (int k = 0; k < order; ++k)
+    didx[(long long)k * hcap + at + i] = src.p[k][i] + (k == order - 1 ? (int32_t)t_add : 0);
+  dval[at + i] = sval[i];
+}
+
+void history_append(Stream& st, const Tensor& x, long long t_add) {
+  Ctx* ctx = st.ctx;
+  const long long need_n = st.hnnz + x.nnz;
+  if (need_n > st.hcap) {
+    const long long ncap = std::max<long long>(need_n, 2 * st.hcap + 1024);
+    Buf<int32_t> ni(ctx, (size_t)ncap * st.order);
+    Buf<double> nv(ctx, ncap);
+    for (int k = 0; k < st.order && st.hnnz; ++k)
+      CUDA_OK(cudaMemcpyAsync(ni.p + (size_t)k * ncap, st.hidx.p + (size_t)k * st.hcap, st.hnnz * sizeof(int32_t),
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    if (st.hnnz)
+      CUDA_OK(cudaMemcpyAsync(nv.p, st.hval.p, st.hnnz * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    st.hidx = std::move(ni);
+    st.hval = std::move(nv);
+    st.hcap = ncap;
+  }
+  if (x.nnz) {
+    IdxPlanes pl{};
+    for (int k = 0; k < x.order; ++k) pl.p[k] = x.idx[k];
+    LAUNCH(ctx, k_hist_append, ceil_div(x.nnz, 256), 256, 0, pl, x.val, (long long)x.nnz, x.order, t_add,
+           st.hidx.p, (long long)st.hcap, st.hval.p, (long long)st.hnnz);
+  }
+  st.hnnz = need_n;
+}
+
 }  // namespace
+
+Tensor Stream::history() const {
+  Tensor h;
+  h.ctx = ctx;
+  h.order = order;
+  for (int k = 0; k + 1 < order; ++k) h.shape[k] = slab_shape[k];
+  h.shape[order - 1] = t;
+  h.nnz = hnnz;
+  for (int k = 0; k < order; ++k) h.idx[k] = hidx.p ? hidx.p + (size_t)k * hcap : nullptr;
+  h.val = hval.p;
+  return h;
+}
+
+double stream_core_drift(Stream& st) {
+  // ctd_dynamic.cpp:271-273
+  if (!(st.keep_history || st.exact_core)) fail(CTD_ERR_ARGUMENT, "core drift requires retained history");
+  Fibers hf;
+  matricize(st.ctx, st.history(), st.mode, hf);
+  return core_drift(st.ctx, st.core, hf, *st.basis);
+}
 
 void build_law(Ctx* ctx, const Tensor& x, int mode, Law& law) {
   matricize(ctx, x, mode, law.fb);
@@ -171,7 +230,9 @@ void stream_init(Ctx* ctx, const Tensor& hist, int mode, int64_t s, double eps, 
   if (hist.order < 2) fail(CTD_ERR_ARGUMENT, "a stream needs at least one non-time mode");
   if (mode < 0 || mode >= hist.order - 1) fail(CTD_ERR_ARGUMENT, "mode must precede the time mode");
   Factors f;
-  out.with_core = (flags & CTD_GPU_WITH_CORE) != 0;
+  out.keep_history = (flags & CTD_GPU_KEEP_HISTORY) != 0;
+  out.exact_core = (flags & CTD_GPU_EXACT_CORE) != 0;
+  out.with_core = (flags & (CTD_GPU_WITH_CORE | CTD_GPU_KEEP_HISTORY | CTD_GPU_EXACT_CORE)) != 0;
   run_ctd_s(ctx, hist, mode, s, eps, seed, out.with_core ? CTD_GPU_WITH_CORE : 0, f);
   if (out.with_core) core_from_static(ctx, f.core, out.core);  // matricize(f.C, mode) (:141)
   out.ctx = ctx;
@@ -183,6 +244,7 @@ void stream_init(Ctx* ctx, const Tensor& hist, int mode, int64_t s, double eps, 
   out.seed = seed;
   out.basis = std::move(f.basis);
   out.kept_flat = std::move(f.kept_flat);
+  if (out.keep_history || out.exact_core) history_append(out, hist, 0);  // :143
 }
 
 void stream_step(Stream& st, const Tensor& slab, int64_t d) {
@@ -209,8 +271,15 @@ void stream_step(Stream& st, const Tensor& slab, int64_t d) {
       st.kept_flat.push_back(fr.unique[k] + st.t * fb.cols);
       appended.push_back(fr.unique_fib[k]);
     }
-    if (st.with_core) core_step(ctx, st.core, fb, *st.basis, Kold, uold.p, appended, st.t * fb.cols);
+    if (st.exact_core && !appended.empty()) {  // :207-211
+      Fibers hf;
+      matricize(ctx, st.history(), st.mode, hf);
+      core_step_exact(ctx, st.core, fb, hf, *st.basis, Kold, st.t * fb.cols);
+    } else if (st.with_core) {
+      core_step(ctx, st.core, fb, *st.basis, Kold, uold.p, appended, st.t * fb.cols);
+    }
   }
+  if (st.keep_history || st.exact_core) history_append(st, slab, st.t);  // :225-226
   st.t += 1;  // :227
 }
 

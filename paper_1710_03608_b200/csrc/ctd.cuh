@@ -55,7 +55,16 @@ struct Stream {
   std::vector<int64_t> kept_flat;
   bool with_core = false;  // CTD_GPU_WITH_CORE: maintain the Eq. 13 core
   DevCore core;
+  // retained raw history (StreamState::history, ctd_dynamic.hpp:28-32): the
+  // concatenated slabs as device COO, `order` planes of hcap int32 indices
+  bool keep_history = false, exact_core = false;
+  Buf<int32_t> hidx;
+  Buf<double> hval;
+  int64_t hnnz = 0, hcap = 0;
+  Tensor history() const;
 };
+
+double stream_core_drift(Stream& st);
 
 void stream_init(Ctx* ctx, const Tensor& hist, int mode, int64_t s, double eps, uint64_t seed,
                  unsigned flags, Stream& out);

@@ -19,6 +19,9 @@
 //     ascending j of gram[a,j] * U_old[j,c] (:244-249);
 //   * BL[a, col] = sum over the column's entries (k ascending) of
 //     left[a,k] * core[k,col] (:256-258), entries with |v| >= 1e-14 kept.
+#include <algorithm>
+
+#include "cdf.cuh"
 #include "stream_core.cuh"
 
 namespace ctdgpu {
@@ -110,6 +113,65 @@ __global__ void k_copy_cols(const int64_t* optr, const int32_t* orow, const doub
   }
 }
 
+
+// copy segment i (cnt[i] entries from sbeg[i]) to dbeg[i]; warp per segment
+__global__ void k_copy_segs(const int64_t* sbeg, const int64_t* cnt, const int64_t* dbeg, long long nseg,
+                            const int32_t* srow, const double* sval, int32_t* drow, double* dval) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nseg) return;
+  const int64_t b = sbeg[w], n = cnt[w], d = dbeg[w];
+  for (int64_t i = lane; i < n; i += 32) {
+    drow[d + i] = srow[b + i];
+    dval[d + i] = sval[b + i];
+  }
+}
+
+// per column of a Core: the first entry with row >= K0 (rows ascend)
+__global__ void k_split_rows(const int64_t* ptr, long long cols, const int32_t* row, int K0, int64_t* split) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  int64_t lo = ptr[c], hi = ptr[c + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (row[mid] < K0) lo = mid + 1;
+    else hi = mid;
+  }
+  split[c] = lo;
+}
+
+// core_drift terms of one column pair in the reference's merge order
+// (ctd_dynamic.cpp:282-297); slots past the merged count hold 0 (adding 0 to
+// a non-negative running sum changes nothing)
+__global__ void k_drift_terms(const int64_t* ca, const int64_t* cb, long long n, const int64_t* aptr,
+                              const int32_t* arow, const double* aval, const int64_t* bptr,
+                              const int32_t* brow, const double* bval, const int64_t* toff, double* terms) {
+  const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const int64_t ia = ca[u], ib = cb[u];
+  int64_t p = ia >= 0 ? aptr[ia] : 0, pe = ia >= 0 ? aptr[ia + 1] : 0;
+  int64_t q = ib >= 0 ? bptr[ib] : 0, qe = ib >= 0 ? bptr[ib + 1] : 0;
+  int64_t o = toff[u];
+  const int64_t oe = toff[u + 1];
+  while (p < pe || q < qe) {
+    double t;
+    if (q == qe || (p < pe && arow[p] < brow[q])) {
+      t = dmul(aval[p], aval[p]);
+      ++p;
+    } else if (p == pe || brow[q] < arow[p]) {
+      t = dmul(bval[q], bval[q]);
+      ++q;
+    } else {
+      const double d = dsub(aval[p], bval[q]);
+      t = dmul(d, d);
+      ++p;
+      ++q;
+    }
+    terms[o++] = t;
+  }
+  while (o < oe) terms[o++] = 0.0;
+}
+
 }  // namespace
 
 void core_from_static(Ctx* ctx, const Core& c, DevCore& out) {
@@ -192,6 +254,151 @@ void core_step(Ctx* ctx, DevCore& core, const Fibers& fb, const Basis& B, int64_
   }
   ctx->sync();
   core = std::move(nw);
+}
+
+void core_step_exact(Ctx* ctx, DevCore& core, const Fibers& fb, const Fibers& hf, const Basis& B, int64_t Kold,
+                     int64_t col_offset) {
+  const long long oc = core.cols;
+  Core sc;  // slab columns: R_new^T dX
+  compute_core(ctx, fb, B, sc);
+  // bottom-left: rows >= Kold of R_new^T X_hist (transpose_times(dR, X_hist)
+  // entry by entry: the same merges and the same per-entry drop rule)
+  Core full;
+  std::vector<int64_t> split;
+  if (B.K > Kold) {
+    compute_core(ctx, hf, B, full);
+    if (full.cols) {
+      Buf<int64_t> dptr(ctx, full.cols + 1), dsplit(ctx, full.cols);
+      ctx->to_dev(dptr.p, full.ptr.data(), full.cols + 1);
+      LAUNCH(ctx, k_split_rows, ceil_div(full.cols, 256), 256, 0, dptr.p, (long long)full.cols, full.row.p,
+             (int)Kold, dsplit.p);
+      split.resize(full.cols);
+      ctx->to_host(split.data(), dsplit.p, full.cols);
+      ctx->sync();
+    }
+  }
+  std::vector<int64_t> ocol(oc), optr(oc + 1, 0);
+  if (oc) {
+    ctx->to_host(ocol.data(), core.col.p, oc);
+    ctx->to_host(optr.data(), core.ptr.p, oc + 1);
+    ctx->sync();
+  }
+  // merged column list: old columns and bottom-left columns (ascending ids)
+  std::vector<int64_t> ncol, nptr(1, 0), sbeg, scnt, dbeg;
+  long long i = 0, j = 0;
+  const long long fc = full.cols;
+  auto bl_count = [&](long long c) { return full.ptr[c + 1] - split[c]; };
+  while (i < oc || j < fc) {
+    if (j < fc && bl_count(j) == 0) { ++j; continue; }
+    const bool take_old = j == fc || (i < oc && ocol[i] <= full.col_id[j]);
+    const bool take_bl = i == oc || (j < fc && full.col_id[j] <= ocol[i]);
+    const int64_t cid = take_old ? ocol[i] : full.col_id[j];
+    int64_t n = 0;
+    if (take_old) n += optr[i + 1] - optr[i];
+    if (take_bl) n += bl_count(j);
+    ncol.push_back(cid);
+    nptr.push_back(nptr.back() + n);
+    if (take_old) {
+      sbeg.push_back(optr[i]);
+      scnt.push_back(optr[i + 1] - optr[i]);
+      dbeg.push_back(nptr[nptr.size() - 2]);
+      ++i;
+    }
+    if (take_bl) ++j;
+  }
+  const long long n_old_segs = (long long)sbeg.size();
+  // bottom-left segments (sources in `full`)
+  std::vector<int64_t> bsb, bcnt, bdb;
+  {
+    long long jj = 0;
+    for (size_t c = 0; c < ncol.size(); ++c) {
+      while (jj < fc && full.col_id[jj] < ncol[c]) ++jj;
+      if (jj < fc && full.col_id[jj] == ncol[c] && bl_count(jj) > 0) {
+        const int64_t olen = (nptr[c + 1] - nptr[c]) - bl_count(jj);
+        bsb.push_back(split[jj]);
+        bcnt.push_back(bl_count(jj));
+        bdb.push_back(nptr[c] + olen);
+      }
+    }
+  }
+  const long long nmid = (long long)ncol.size();
+  for (long long s2 = 0; s2 < sc.cols; ++s2) {
+    ncol.push_back(sc.col_id[s2] + col_offset);
+    nptr.push_back(nptr.back() + (sc.ptr[s2 + 1] - sc.ptr[s2]));
+  }
+  DevCore nw;
+  nw.cols = (int64_t)ncol.size();
+  nw.nnz = nptr.back();
+  nw.col.alloc(ctx, nw.cols + 1);
+  nw.ptr.alloc(ctx, nw.cols + 1);
+  nw.row.alloc(ctx, nw.nnz + 1);
+  nw.val.alloc(ctx, nw.nnz + 1);
+  if (nw.cols) ctx->to_dev(nw.col.p, ncol.data(), nw.cols);
+  ctx->to_dev(nw.ptr.p, nptr.data(), nw.cols + 1);
+  auto copy = [&](const std::vector<int64_t>& sb, const std::vector<int64_t>& cn, const std::vector<int64_t>& db,
+                  const int32_t* srow, const double* sval) {
+    const long long ns = (long long)sb.size();
+    if (!ns) return;
+    Buf<int64_t> a(ctx, ns), b(ctx, ns), c(ctx, ns);
+    ctx->to_dev(a.p, sb.data(), ns);
+    ctx->to_dev(b.p, cn.data(), ns);
+    ctx->to_dev(c.p, db.data(), ns);
+    LAUNCH(ctx, k_copy_segs, ceil_div((uint64_t)ns * 32, 256), 256, 0, a.p, b.p, c.p, ns, srow, sval, nw.row.p,
+           nw.val.p);
+    ctx->sync();
+  };
+  if (n_old_segs) copy(sbeg, scnt, dbeg, core.row.p, core.val.p);
+  if (!bsb.empty()) copy(bsb, bcnt, bdb, full.row.p, full.val.p);
+  if (sc.nnz) {
+    const int64_t d = nptr[nmid];
+    CUDA_OK(cudaMemcpyAsync(nw.row.p + d, sc.row.p, sc.nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    CUDA_OK(cudaMemcpyAsync(nw.val.p + d, sc.val.p, sc.nnz * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  ctx->sync();
+  core = std::move(nw);
+}
+
+double core_drift(Ctx* ctx, const DevCore& core, const Fibers& hf, const Basis& B) {
+  Core ex;  // expected = R^T X_hist (transpose_times(R, matricize(history)))
+  compute_core(ctx, hf, B, ex);
+  const long long oc = core.cols, ec = ex.cols;
+  std::vector<int64_t> ocol(oc), optr(oc + 1, 0);
+  if (oc) {
+    ctx->to_host(ocol.data(), core.col.p, oc);
+    ctx->to_host(optr.data(), core.ptr.p, oc + 1);
+    ctx->sync();
+  }
+  std::vector<int64_t> ca, cb, toff(1, 0);
+  long long i = 0, j = 0;
+  while (i < oc || j < ec) {
+    const bool ta = j == ec || (i < oc && ocol[i] <= ex.col_id[j]);
+    const bool tb = i == oc || (j < ec && ex.col_id[j] <= ocol[i]);
+    int64_t n = 0;
+    if (ta) n += optr[i + 1] - optr[i];
+    if (tb) n += ex.ptr[j + 1] - ex.ptr[j];
+    ca.push_back(ta ? i++ : -1);
+    cb.push_back(tb ? j++ : -1);
+    toff.push_back(toff.back() + n);
+  }
+  const long long nu = (long long)ca.size();
+  const int64_t nt = toff.back();
+  if (nt == 0) return 0.0;
+  Buf<int64_t> dca(ctx, nu), dcb(ctx, nu), dto(ctx, nu + 1), dep(ctx, ec + 1);
+  ctx->to_dev(dca.p, ca.data(), nu);
+  ctx->to_dev(dcb.p, cb.data(), nu);
+  ctx->to_dev(dto.p, toff.data(), nu + 1);
+  ctx->to_dev(dep.p, ex.ptr.data(), ec + 1);
+  Buf<double> terms(ctx, nt), cum(ctx, nt), tot(ctx, 1);
+  const int32_t* erow = ex.nnz ? ex.row.p : nullptr;
+  const double* eval = ex.nnz ? ex.val.p : nullptr;
+  LAUNCH(ctx, k_drift_terms, ceil_div(nu, 128), 128, 0, dca.p, dcb.p, nu, core.ptr.p, core.row.p, core.val.p,
+         dep.p, erow, eval, dto.p, terms.p);
+  seq_cumsum(ctx, terms.p, nt, nullptr, tot.p);  // sq: the reference's sequential order, exactly
+  double sq = 0.0;
+  ctx->to_host(&sq, tot.p, 1);
+  ctx->sync();
+  ctx->check_flags("core_drift");
+  return std::sqrt(sq);
 }
 
 }  // namespace ctdgpu

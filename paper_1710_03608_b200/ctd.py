@@ -57,6 +57,8 @@ _ERRORS = {1: ArgumentError, 2: ShapeError, 3: EmptyInputError, 5: MetricError,
 WITH_ERROR = 0x1
 WITH_CORE = 0x2
 KEEP_PANEL = 0x4  # keep the orthonormal panel for a later relative_error (implied by WITH_ERROR)
+KEEP_HISTORY = 0x8  # init_stream(keep_history=True): retain the raw history (core_drift)
+EXACT_CORE = 0x10   # init_stream(exact_core=True): bottom-left block from the history
 
 
 def _check(st: int):
@@ -611,15 +613,29 @@ class StreamState:
 
 
 def init_stream(historical, mode: int, sample_size: int, epsilon: float = 1e-6,
-                seed: int = 42, with_core: bool = False, ctx: Optional[Context] = None) -> StreamState:
-    """init_stream (ctd_dynamic.cpp:129-147).  ``with_core`` maintains the core
-    C(t) through every step (Eq. 13 blocks); ``factors()`` then carries it."""
+                seed: int = 42, keep_history: bool = False, exact_core: bool = False,
+                with_core: bool = False, ctx: Optional[Context] = None) -> StreamState:
+    """init_stream (ctd_dynamic.hpp:42-45, ctd_dynamic.cpp:129-147).  ``with_core``
+    maintains the core C(t) through every step (Eq. 13 blocks); ``factors()`` then
+    carries it.  ``keep_history`` retains the raw history on the device (for
+    ``core_drift``); ``exact_core`` computes the bottom-left block from it
+    (ctd_dynamic.cpp:207-211).  Either implies ``with_core``."""
     ctx = ctx or default_context()
     d = _dev(historical, ctx)
     h = C.c_void_p()
+    flags = ((WITH_CORE if with_core else 0) | (KEEP_HISTORY if keep_history else 0)
+             | (EXACT_CORE if exact_core else 0))
     _check(ctx.L.ctd_gpu_stream_init(ctx.h, d.h, mode, sample_size, epsilon, C.c_uint64(seed),
-                                     WITH_CORE if with_core else 0, C.byref(h)))
+                                     flags, C.byref(h)))
     return StreamState(ctx, h, mode, d.shape[:-1])
+
+
+def core_drift(state: StreamState) -> float:
+    """core_drift (ctd_dynamic.hpp:64-66): |C - R^T X_hist|_F against the retained
+    history; ArgumentError without it (ctd_dynamic.cpp:272-273)."""
+    out = C.c_double()
+    _check(state.ctx.L.ctd_gpu_stream_core_drift(state.h, C.byref(out)))
+    return out.value
 
 
 def ctd_d_step(state: StreamState, slab, sample_size: int) -> StreamState:

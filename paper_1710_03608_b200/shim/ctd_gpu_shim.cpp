@@ -192,10 +192,12 @@ StreamState __wrap__ZN3ctd11init_streamERKNS_12SparseTensorEildmbb(const SparseT
                                                                   index_t sample_size, double epsilon,
                                                                   std::uint64_t seed, bool keep_history,
                                                                   bool exact_core) {
-  if (exact_core) throw ArgumentError("exact_core is not available in the GPU drop-in");
   Tensor t(historical);
   ctd_gpu_stream* s = nullptr;
-  rethrow(ctd_gpu_stream_init(context(), t.h, mode, sample_size, epsilon, seed, CTD_GPU_WITH_CORE, &s));
+  // exact_core: the device stream keeps its own history for the bottom-left
+  // block (ctd_dynamic.cpp:207-211); the host copy below serves core_drift
+  const unsigned flags = CTD_GPU_WITH_CORE | (exact_core ? CTD_GPU_EXACT_CORE : 0u);
+  rethrow(ctd_gpu_stream_init(context(), t.h, mode, sample_size, epsilon, seed, flags, &s));
   StreamState st{FiberBasis(historical.extent(mode)), SparseMatrix(0, 0), historical.shape(), mode, 0, epsilon,
                  seed, {}};
   st.slab_shape.pop_back();
@@ -209,7 +211,8 @@ StreamState __wrap__ZN3ctd11init_streamERKNS_12SparseTensorEildmbb(const SparseT
     st.t = ctd_gpu_stream_t(s);
     st.core = f.core(st.t * st.slab_columns());
   }
-  if (keep_history) st.history = historical;
+  st.exact_core = exact_core;
+  if (keep_history || exact_core) st.history = historical;  // ctd_dynamic.cpp:143
   std::lock_guard<std::mutex> lk(g_mu);
   g_streams[st.kept_fibers.data()] = s;
   return st;

@@ -116,15 +116,15 @@ def test_dropin_errors(ref, dropin):
 
 @pytest.mark.gpu
 @needs_dropin
-@pytest.mark.parametrize("keep_history", [False, True])
-def test_dropin_stream(ref, dropin, keep_history):
+@pytest.mark.parametrize("keep_history,exact_core", [(False, False), (True, False), (True, True)])
+def test_dropin_stream(ref, dropin, keep_history, exact_core):
     x = g.c3_stream(seed=5, n_steps=3, slices_per_step=3, draws_per_slice=2500, n=300,
                     planted_step=2, block=20)
     hist = x.time_slab(0, 3)
     sa = ref.stream(ref.tensor(hist.shape, hist.flat_idx(), hist.val), 0, 120, 1e-6, 7,
-                    keep_history=keep_history)
+                    keep_history=keep_history, exact_core=exact_core)
     sb = dropin.stream(dropin.tensor(hist.shape, hist.flat_idx(), hist.val), 0, 120, 1e-6, 7,
-                       keep_history=keep_history)
+                       keep_history=keep_history, exact_core=exact_core)
     grew = 0
     for t in range(3, x.shape[2]):
         slab = x.time_slab(t, t + 1)

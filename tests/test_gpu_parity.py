@@ -250,6 +250,58 @@ def test_stream_core_vs_port(ctx, port, seed, d):
     assert grew >= 2  # the chain-product (bottom-left) block was exercised
 
 
+def _stream_history_case(ctx, ref, x, h, s, seed, d, keep_history, exact_core):
+    """init_stream(keep_history, exact_core) + ctd_d_step per slab against the
+    compiled reference: kept ids, the whole core and core_drift, bit for bit."""
+    hist = x.time_slab(0, h)
+    st = ctd.init_stream(_st(hist), 0, s, 1e-6, seed, keep_history=keep_history, exact_core=exact_core,
+                         ctx=ctx)
+    rs = ref.stream(ref.tensor(hist.shape, hist.flat_idx(), hist.val), 0, s, 1e-6, seed,
+                    keep_history=keep_history, exact_core=exact_core)
+    drifts = []
+    for t in range(h, x.shape[2]):
+        slab = x.time_slab(t, t + 1)
+        ctd.ctd_d_step(st, _st(slab), d)
+        rs.step(ref.tensor(slab.shape, slab.flat_idx(), slab.val), d)
+        f = st.factors()
+        c = rs.core()
+        assert np.array_equal(f.kept_flat, rs.factors().kept_flat), t
+        assert np.array_equal(_dense_cols(c.cols, f.C_col, f.C_ptr), c.col_ptr), t
+        assert np.array_equal(f.C_row, c.row), t
+        assert np.array_equal(f.C_val.view(np.int64), c.val.view(np.int64)), t
+        dr = ctd.core_drift(st)
+        assert dr == rs.core_drift(), t
+        scale = max(1.0, float(np.sqrt(np.sum(c.val * c.val))))
+        drifts.append(dr / scale)
+    return drifts
+
+
+def test_stream_exact_core_vs_reference(ctx, ref):
+    """test_ctd_dynamic.cpp:61-70: exact_core keeps the core equal to R^T X_hist."""
+    x = g.random_sparse([9, 7, 8], 0.08, 501)
+    drifts = _stream_history_case(ctx, ref, x, 3, 25, 17, 10, True, True)
+    assert max(drifts) <= 1e-12
+
+
+def test_stream_keep_history_drift_vs_reference(ctx, ref):
+    """test_ctd_dynamic.cpp:44-59: on exactly low-rank data the substituted
+    (chain-product) bottom-left block keeps the drift at roundoff."""
+    x = g.low_rank([10, 5, 6], 2, 0.95, 29)
+    drifts = _stream_history_case(ctx, ref, x, 2, 200, 7, 40, True, False)
+    assert max(drifts) <= 1e-10
+    # larger stream with appends every step, exact_core, against the reference
+    y = g.c3_stream(seed=6, n_steps=2, slices_per_step=4, draws_per_slice=1500, n=200,
+                    planted_step=1, block=15)
+    _stream_history_case(ctx, ref, y, 3, 80, 9, 30, False, True)
+
+
+def test_core_drift_requires_history(ctx):
+    x = g.random_sparse([9, 7, 8], 0.08, 501)
+    st = ctd.init_stream(_st(x.time_slab(0, 3)), 0, 25, 1e-6, 17, with_core=True, ctx=ctx)
+    with pytest.raises(ctd.ArgumentError):
+        ctd.core_drift(st)
+
+
 def test_errors(ctx):
     x = g.c1()
     t = _st(x)
