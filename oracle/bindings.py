@@ -398,6 +398,10 @@ class Ref:
             getattr(L, n).restype = i64
         L.ref_stream_core.argtypes = [v, v, v, v]
         L.ref_core_drift.argtypes = [v, C.POINTER(f64)]
+        if hasattr(L, "ref_run_stream"):
+            L.ref_run_stream.argtypes = [v, i32, i64, i64, f64, f64, C.c_uint64, i32, C.POINTER(i64), v, v, v,
+                                         v, v, v]
+            L.ref_tsv_line.argtypes = [i64, f64, f64, f64, i64, C.c_char_p, i64]
 
     def _chk(self, st, what=""):
         if st:
@@ -496,6 +500,28 @@ class Ref:
             return fe
         finally:
             self.L.ref_factors_free(h)
+
+    def run_stream(self, x, mode=0, sample_size=100, step_samples=None, split=0.8, eps=1e-6, seed=42,
+                   exact_core=False) -> dict:
+        """run_stream (stream_harness.cpp:48-107) on a _RefTensor: per-step reports + mean."""
+        T = int(x.shape[-1])
+        n = C.c_int64()
+        step = np.zeros(T + 1, np.int64)
+        err, mem, secs = np.zeros(T + 1), np.zeros(T + 1), np.zeros(T + 1)
+        kept = np.zeros(T + 1, np.int64)
+        mean = np.zeros(4)
+        self._chk(self.L.ref_run_stream(x.h, mode, sample_size, step_samples or 0, split, eps,
+                                        C.c_uint64(seed), int(exact_core), C.byref(n), _p(step), _p(err),
+                                        _p(mem), _p(secs), _p(kept), _p(mean)), "run_stream")
+        k = n.value
+        return {"step": step[:k], "relative_error": err[:k], "memory_usage": mem[:k],
+                "seconds": secs[:k], "kept_fibers": kept[:k], "mean": mean}
+
+    def tsv_line(self, step, err=0.0, secs=0.0, mem=0.0, kept=0) -> str:
+        """tsv_line (evaluation.cpp:51-62); step < 0 gives tsv_header()."""
+        buf = C.create_string_buffer(256)
+        self._chk(self.L.ref_tsv_line(step, err, secs, mem, kept, buf, 256), "tsv_line")
+        return buf.value.decode()
 
     def stream(self, hist, mode, s, eps=1e-6, seed=42, keep_history=False, exact_core=False):
         return _RefStream(self, hist, mode, s, eps, seed, keep_history, exact_core)

@@ -12,6 +12,7 @@
 
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -23,6 +24,7 @@
 #include "ctd/evaluation.hpp"
 #include "ctd/fiber_basis.hpp"
 #include "ctd/sampling.hpp"
+#include "ctd/stream_harness.hpp"
 #include "ctd/tensor_ops.hpp"
 
 using namespace ctd;
@@ -301,6 +303,48 @@ void ref_stream_core(void* s, int64_t* col_ptr, int64_t* rows, double* vals) {
 }
 int ref_core_drift(void* s, double* out) {
   return guard([&] { *out = core_drift(*static_cast<StreamState*>(s)); });
+}
+
+// ---- stream harness (stream_harness.cpp) ----------------------------------
+// Per-step reports of run_stream; arrays hold at least time-extent + 1 entries;
+// mean4 = {error, memory, seconds, kept} of result.mean.
+int ref_run_stream(void* t, int mode, int64_t s, int64_t d, double split, double eps, uint64_t seed,
+                   int exact_core, int64_t* nsteps, int64_t* step, double* err, double* mem, double* secs,
+                   int64_t* kept, double* mean4) {
+  return guard([&] {
+    HarnessOptions o;
+    o.mode = mode;
+    o.sample_size = s;
+    if (d > 0) o.step_samples = d;
+    o.split = split;
+    o.epsilon = eps;
+    o.seed = seed;
+    o.exact_core = exact_core != 0;
+    const StreamRunResult r = run_stream(*static_cast<SparseTensor*>(t), o);
+    *nsteps = static_cast<int64_t>(r.steps.size());
+    for (size_t i = 0; i < r.steps.size(); ++i) {
+      step[i] = r.steps[i].step;
+      err[i] = r.steps[i].eval.relative_error;
+      mem[i] = r.steps[i].eval.memory_usage;
+      secs[i] = r.steps[i].eval.wall_time_seconds;
+      kept[i] = r.steps[i].eval.kept_fibers;
+    }
+    mean4[0] = r.mean.relative_error;
+    mean4[1] = r.mean.memory_usage;
+    mean4[2] = r.mean.wall_time_seconds;
+    mean4[3] = static_cast<double>(r.mean.kept_fibers);
+  });
+}
+int ref_tsv_line(int64_t step, double err, double secs, double mem, int64_t kept, char* buf, int64_t cap) {
+  return guard([&] {
+    EvalReport e;
+    e.relative_error = err;
+    e.wall_time_seconds = secs;
+    e.memory_usage = mem;
+    e.kept_fibers = kept;
+    const std::string line = step < 0 ? tsv_header() : tsv_line(step, e);
+    std::snprintf(buf, static_cast<size_t>(cap), "%s", line.c_str());
+  });
 }
 
 }  // extern "C"

@@ -476,7 +476,8 @@ int ctd_gpu_relative_error(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, ctd_gpu_fa
     }
     {
       PhaseScope ps(&ctx->c, PH_ERROR);
-      *out = relative_error(&ctx->c, fb, *F.basis);
+      *out = (F.has_core && F.core_from_stream) ? relative_error_core(&ctx->c, fb, *F.basis, F.core)
+                                                : relative_error(&ctx->c, fb, *F.basis);
     }
     ctx->c.phase_flush();
   });
@@ -855,6 +856,20 @@ int ctd_gpu_stream_factors(ctd_gpu_stream* s, ctd_gpu_factors** out) {
       CUDA_OK(cudaMemcpyAsync(nb->rrow.p, B.rrow.p, B.rnnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
       CUDA_OK(cudaMemcpyAsync(nb->rval.p, B.rval.p, B.rnnz * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     }
+    // R's row index (relative_error's R U panel reads it)
+    if (B.rowbase.p && B.ricap > 0) {
+      nb->ricap = B.ricap;
+      nb->rowbase.alloc(c, B.dim + 1);
+      nb->rowlen.alloc(c, B.dim + 1);
+      nb->rek.alloc(c, B.ricap);
+      nb->rev.alloc(c, B.ricap);
+      CUDA_OK(cudaMemcpyAsync(nb->rowbase.p, B.rowbase.p, (B.dim + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                              c->stream));
+      CUDA_OK(cudaMemcpyAsync(nb->rowlen.p, B.rowlen.p, B.dim * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                              c->stream));
+      CUDA_OK(cudaMemcpyAsync(nb->rek.p, B.rek.p, B.ricap * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
+      CUDA_OK(cudaMemcpyAsync(nb->rev.p, B.rev.p, B.ricap * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    }
     F.basis = std::move(nb);
     if (S.with_core) {  // StreamState::factors folds the core (:114-127); kept matricized here
       const DevCore& dc = S.core;
@@ -874,6 +889,7 @@ int ctd_gpu_stream_factors(ctd_gpu_stream* s, ctd_gpu_factors** out) {
       }
       c->sync();
       F.has_core = true;
+      F.core_from_stream = true;
     }
     *out = h.release();
   });

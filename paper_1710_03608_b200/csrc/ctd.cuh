@@ -28,6 +28,7 @@ struct Factors {
   bool integer_exact = false;
   bool slow_path = false;
   bool has_core = false;  // CTD_GPU_WITH_CORE: C_(mode) = R^T X_(mode)
+  bool core_from_stream = false;  // C(t) of a CTD-D stream: relative_error uses it explicitly
   Core core;
 };
 

@@ -164,7 +164,94 @@ __global__ void k_reduce(const double* p, long long n, double* out) {
   if (threadIdx.x == 0) *out = s;
 }
 
+// Qt[c][r] = (R U)[r][c] (dense_product, evaluation.cpp:32-43), column-major
+// so that threads over rows read it coalesced.
+__global__ void k_rut(const int64_t* rowbase, const int32_t* rowlen, const int32_t* rek, const double* rev,
+                      const double* U, long long LD, long long dim, long long K, double* Qt) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= dim * K) return;
+  const long long c = e / dim, r = e - c * dim;
+  const long long b = rowbase[r];
+  const int L = rowlen[r];
+  double s = 0.0;
+  for (int t = 0; t < L; ++t) s = __fma_rn(rev[b + t], U[(long long)rek[b + t] * LD + c], s);
+  Qt[e] = s;
+}
+
+// One core column per CTA: |(R U) c_j - x_j|^2 = sum_r y_r^2 over all rows
+// plus, on x_j's rows, (y_r - x_r)^2 - y_r^2 (y = (R U) c_j), and |x_j|^2 of
+// the matched fiber (the unmatched fibers' share is |X|^2 minus these).
+__global__ void k_core_err(const int64_t* ccol, const int64_t* cptr, const int32_t* crow, const double* cval,
+                           long long ncols, const int64_t* fcol, const int64_t* fptr, long long F,
+                           const int32_t* xrow, const double* xval, const double* Qt, long long dim,
+                           double* part_err, double* part_x) {
+  __shared__ double sh[33];
+  for (long long j = blockIdx.x; j < ncols; j += gridDim.x) {
+    const int64_t c0 = cptr[j], c1 = cptr[j + 1];
+    const int64_t id = ccol[j];
+    long long lo = 0, hi = F;  // the X fiber with the same column id (or none)
+    while (lo < hi) {
+      const long long mid = (lo + hi) >> 1;
+      if (fcol[mid] < id) lo = mid + 1;
+      else hi = mid;
+    }
+    const bool has_x = lo < F && fcol[lo] == id;
+    double acc = 0.0, xs = 0.0;
+    for (long long r = threadIdx.x; r < dim; r += blockDim.x) {
+      double y = 0.0;
+      for (int64_t t = c0; t < c1; ++t) y = __fma_rn(Qt[(long long)crow[t] * dim + r], cval[t], y);
+      acc = __fma_rn(y, y, acc);
+    }
+    if (has_x) {
+      for (int64_t e = fptr[lo] + threadIdx.x; e < fptr[lo + 1]; e += blockDim.x) {
+        const long long r = xrow[e];
+        const double x = xval[e];
+        double y = 0.0;
+        for (int64_t t = c0; t < c1; ++t) y = __fma_rn(Qt[(long long)crow[t] * dim + r], cval[t], y);
+        const double d = y - x;
+        acc += d * d - y * y;
+        xs = __fma_rn(x, x, xs);
+      }
+    }
+    acc = block_sum<double>(acc, sh);
+    xs = block_sum<double>(xs, sh);
+    if (threadIdx.x == 0) {
+      part_err[j] = acc;
+      part_x[j] = xs;
+    }
+  }
+}
+
 }  // namespace
+
+double relative_error_core(Ctx* ctx, const Fibers& fb, const Basis& B, const Core& core) {
+  const long long K = B.K, dim = B.dim, nc = core.cols;
+  const unsigned sgrid = (unsigned)ctx->sm_count * 4;
+  Buf<double> sp(ctx, sgrid), xsq(ctx, 1);
+  LAUNCH(ctx, k_sumsq, sgrid, 256, 0, fb.val.p, (long long)fb.nnz, sp.p);
+  LAUNCH(ctx, k_reduce, 1, 1024, 0, sp.p, (long long)sgrid, xsq.p);
+  const double hx = ctx->read1(xsq.p);
+  if (hx == 0.0) fail(CTD_ERR_METRIC, "relative error undefined for a zero tensor");  // evaluation.cpp:93-94
+  if (K == 0 || nc == 0 || core.nnz == 0) return 1.0;
+  Buf<double> Qt(ctx, (size_t)dim * K);
+  LAUNCH(ctx, k_rut, ceil_div((uint64_t)dim * K, 256), 256, 0, B.rowbase.p, B.rowlen.p, B.rek.p, B.rev.p, B.U.p,
+         (long long)B.LD, dim, K, Qt.p);
+  Buf<int64_t> dcol(ctx, nc), dptr(ctx, nc + 1);
+  ctx->to_dev(dcol.p, core.col_id.data(), nc);
+  ctx->to_dev(dptr.p, core.ptr.data(), nc + 1);
+  Buf<double> pe(ctx, nc), px(ctx, nc), se(ctx, 1), sx(ctx, 1);
+  LAUNCH(ctx, k_core_err, (unsigned)std::min<long long>(nc, (long long)ctx->sm_count * 8), 256, 0, dcol.p, dptr.p,
+         core.row.p, core.val.p, nc, fb.col.p, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, Qt.p, dim, pe.p,
+         px.p);
+  LAUNCH(ctx, k_reduce, 1, 1024, 0, pe.p, nc, se.p);
+  LAUNCH(ctx, k_reduce, 1, 1024, 0, px.p, nc, sx.p);
+  double he = 0.0, hxm = 0.0;
+  ctx->to_host(&he, se.p, 1);
+  ctx->to_host(&hxm, sx.p, 1);
+  ctx->sync();
+  // columns without core entries contribute |x_j|^2 (evaluation.cpp:108-111)
+  return (he + (hx - hxm)) / hx;
+}
 
 double relative_error(Ctx* ctx, const Fibers& fb, const Basis& B) {
   double hx = 0.0, hcd = 0.0;
