@@ -402,6 +402,11 @@ class Ref:
             L.ref_run_stream.argtypes = [v, i32, i64, i64, f64, f64, C.c_uint64, i32, C.POINTER(i64), v, v, v,
                                          v, v, v]
             L.ref_tsv_line.argtypes = [i64, f64, f64, f64, i64, C.c_char_p, i64]
+        if hasattr(L, "ref_save_factors"):
+            L.ref_save_factors.argtypes = [v, C.c_char_p]
+            L.ref_load_factors.argtypes = [C.c_char_p, C.POINTER(v)]
+            L.ref_detect_ddos.argtypes = [v, C.POINTER(i64), v, v, v]
+            L.ref_decompose_online.argtypes = [v, i32, i64, f64, C.c_uint64, C.POINTER(v)]
 
     def _chk(self, st, what=""):
         if st:
@@ -500,6 +505,40 @@ class Ref:
             return fe
         finally:
             self.L.ref_factors_free(h)
+
+    def _with_factors(self, h, save_dir=None, detect=False):
+        try:
+            out = {}
+            if save_dir is not None:
+                self._chk(self.L.ref_save_factors(h, save_dir.encode()), "save_factors")
+            if detect:
+                k = int(self.L.ref_factors_kept(h))
+                n = C.c_int64()
+                dst, b = np.zeros(max(k, 1), np.int64), np.zeros(max(k, 1), np.int64)
+                nrm = np.zeros(max(k, 1))
+                self._chk(self.L.ref_detect_ddos(h, C.byref(n), _p(dst), _p(b), _p(nrm)), "detect_ddos")
+                out["detect"] = [(int(dst[i]), int(b[i]), float(nrm[i])) for i in range(n.value)]
+            return out
+        finally:
+            self.L.ref_factors_free(h)
+
+    def ctd_s_bundle(self, t, mode, s, eps, seed, save_dir=None, detect=False) -> dict:
+        """Reference ctd_s, then save_factors / detect_ddos on its factors."""
+        h = C.c_void_p()
+        self._chk(self.L.ref_ctd_s(t.h, mode, s, eps, C.c_uint64(seed), C.byref(h)), "ctd_s")
+        return self._with_factors(h, save_dir, detect)
+
+    def decompose_online(self, t, mode, d, eps, seed, save_dir=None, detect=False) -> dict:
+        h = C.c_void_p()
+        self._chk(self.L.ref_decompose_online(t.h, mode, d, eps, C.c_uint64(seed), C.byref(h)),
+                  "decompose_online")
+        return self._with_factors(h, save_dir, detect)
+
+    def resave(self, src_dir, dst_dir) -> None:
+        """load_factors(src) then save_factors(dst) with the reference."""
+        h = C.c_void_p()
+        self._chk(self.L.ref_load_factors(src_dir.encode(), C.byref(h)), "load_factors")
+        self._with_factors(h, dst_dir)
 
     def run_stream(self, x, mode=0, sample_size=100, step_samples=None, split=0.8, eps=1e-6, seed=42,
                    exact_core=False) -> dict:

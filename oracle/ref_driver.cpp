@@ -20,6 +20,8 @@
 
 #include "ctd/ctd_dynamic.hpp"
 #include "ctd/ctd_static.hpp"
+#include "ctd/ddos.hpp"
+#include "ctd/factor_io.hpp"
 #include "ctd/error.hpp"
 #include "ctd/evaluation.hpp"
 #include "ctd/fiber_basis.hpp"
@@ -344,6 +346,37 @@ int ref_tsv_line(int64_t step, double err, double secs, double mem, int64_t kept
     e.kept_fibers = kept;
     const std::string line = step < 0 ? tsv_header() : tsv_line(step, e);
     std::snprintf(buf, static_cast<size_t>(cap), "%s", line.c_str());
+  });
+}
+
+// ---- factor bundles (factor_io.cpp) and DDoS post-processing (ddos.cpp) ----
+int ref_save_factors(void* f, const char* dir) {
+  return guard([&] { save_factors(static_cast<Factors*>(f)->f, dir); });
+}
+int ref_load_factors(const char* dir, void** out) {
+  return guard([&] {
+    auto fx = std::make_unique<Factors>();
+    fx->f = load_factors(dir);
+    *out = fx.release();
+  });
+}
+// flagged candidates; arrays hold at least kept-count entries
+int ref_detect_ddos(void* f, int64_t* n, int64_t* dst, int64_t* bin, double* norm) {
+  return guard([&] {
+    const auto c = detect_ddos(static_cast<Factors*>(f)->f);
+    *n = static_cast<int64_t>(c.size());
+    for (size_t i = 0; i < c.size(); ++i) {
+      dst[i] = c[i].dst;
+      bin[i] = c[i].bin;
+      norm[i] = c[i].norm;
+    }
+  });
+}
+int ref_decompose_online(void* t, int mode, int64_t d, double eps, uint64_t seed, void** out) {
+  return guard([&] {
+    auto fx = std::make_unique<Factors>();
+    fx->f = decompose_online(*static_cast<SparseTensor*>(t), mode, d, eps, seed);
+    *out = fx.release();
   });
 }
 
