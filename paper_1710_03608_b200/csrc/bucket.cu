@@ -68,14 +68,9 @@ __global__ void k_hist(CooView c, int wbits, unsigned* count, unsigned* flags) {
     const long long j = col_of(c, i, &row, &oob);
     if (oob) atomicOr(flags, FLAG_BOUNDS);
     const unsigned long long b = oob ? kNone : (unsigned long long)(j >> wbits);
-#ifdef CTD_NO_MATCH
-    (void)amask;
-    if (b != kNone) atomicAdd(&count[b], 1u);
-#else
     const unsigned peers = __match_any_sync(amask, b);
     if (b != kNone && (int)(threadIdx.x & 31) == __ffs(peers) - 1)
       atomicAdd(&count[b], (unsigned)__popc(peers));
-#endif
   }
 }
 
@@ -135,11 +130,6 @@ __global__ void k_scatter(CooView c, int wbits, int rowbits, ScatterOut o, unsig
       sq += v * v;
     }
     const unsigned long long b = oob ? kNone : (unsigned long long)(j >> wbits);
-#ifdef CTD_NO_MATCH
-    (void)amask;
-    if (b == kNone) continue;
-    const unsigned long long pos = atomicAdd(&o.cursor[b], 1ull);
-#else
     const unsigned peers = __match_any_sync(amask, b);
     const int leader = __ffs(peers) - 1;
     unsigned long long basepos = 0;
@@ -148,7 +138,6 @@ __global__ void k_scatter(CooView c, int wbits, int rowbits, ScatterOut o, unsig
     basepos = __shfl_sync(peers, basepos, leader);
     if (b == kNone) continue;
     const unsigned long long pos = basepos + __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
-#endif
     o.tkey[pos] = (uint32_t)((((unsigned long long)j & wmask) << rowbits) | (unsigned)row);
     o.tval[pos] = v;
   }
