@@ -376,6 +376,28 @@ def phase_bytes(nnz, F, kept_seq, r_lens):
     }
 
 
+def chain_floor_cycles(kept_seq, r_ptr, r_rows, dim):
+    """The filter's dependency floor: per candidate, the two sequential fp64 add
+    chains the reference's summation order imposes - y = U g (K adds per row,
+    dense_matrix.cpp:42-47) and z = R y (the longest R row's multiplicity,
+    fiber_basis.cpp:56-65) - at the measured DADD latency (8.2 cycles,
+    profiles/r1_ubench.md).  The exact residual sum and the cross-SM exchanges
+    are not counted, so the floor is optimistic."""
+    mult = np.zeros(dim + 1, np.int64)
+    mx = 0
+    K = 0
+    steps = 0
+    for acc in kept_seq:
+        steps += K + mx
+        if acc:
+            rows = r_rows[r_ptr[K]:r_ptr[K + 1]]
+            mult[rows] += 1
+            if rows.size:
+                mx = max(mx, int(mult[rows].max()))
+            K += 1
+    return 8.2 * steps
+
+
 # ---------------------------------------------------------------------------
 
 # phase -> its dominant kernel in the committed ncu captures (profiles/)
@@ -599,6 +621,13 @@ def run_ours(args, rank, world, local_rank):
     roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": pk,
             "unit": "GB/s", "frac": round(achieved / pk, 4), "traffic": ncu_traffic(dom),
             "peak_kind": pk_kind}
+    if dom == "filter":
+        fc = chain_floor_cycles(tr["accepted"], tr["r_ptr"], tr["r_rows"], int(x.shape[C2["mode"]]))
+        clk_hz = 1.965e9
+        roof["latency_floor"] = {
+            "what": "dependent fp64 add chains in the reference's order (y = U g: K adds; z = R y: longest "
+                    "R row), 8.2-cycle DADD latency at 1965 MHz; exchanges and the exact residual sum excluded",
+            "floor_ms": round(fc / clk_hz * 1e3, 3), "frac": round(fc / clk_hz * 1e3 / dms, 4)}
     # SURVEY §8d end-to-end byte formula for the step
     bs = 44 * nnz + 24 * info.n_fibers
 

@@ -562,7 +562,11 @@ def factors_trace(ctx: Context, h, info) -> dict:
     _check(ctx.L.ctd_gpu_factors_trace(h, None, None, _p(acc), None, None))
     cp = np.zeros(k + 1, np.int64)
     _check(ctx.L.ctd_gpu_factors_r(h, _p(cp), None, None))
-    return {"accepted": acc[:nu].astype(bool), "r_lens": np.diff(cp)}
+    rows = np.zeros(max(int(cp[-1]), 1), np.int64)
+    vals = np.zeros(max(int(cp[-1]), 1))
+    _check(ctx.L.ctd_gpu_factors_r(h, _p(cp), _p(rows), _p(vals)))
+    return {"accepted": acc[:nu].astype(bool), "r_lens": np.diff(cp), "r_ptr": cp,
+            "r_rows": rows[:int(cp[-1])]}
 
 
 def factors_result(ctx: Context, h, info):
