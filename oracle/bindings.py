@@ -139,6 +139,10 @@ class Port:
         L.cto_core_matricized.argtypes = [C.POINTER(_CscStruct)] * 3
         L.cto_relative_error.argtypes = [C.POINTER(_CscStruct), f64, C.POINTER(_CscStruct),
                                          v, C.POINTER(_CscStruct), C.POINTER(f64)]
+        L.cto_relerr_dd_direct.argtypes = [C.POINTER(_CscStruct), C.POINTER(_CscStruct), v] + \
+            [C.POINTER(f64)] * 4
+        L.cto_relerr_dd_full.argtypes = [C.POINTER(_CscStruct), C.POINTER(_CscStruct), v] + \
+            [C.POINTER(f64)] * 3
         L.cto_stream_init.argtypes = [i32, v, i64, v, v, i32, i64, f64, C.c_uint64,
                                       C.POINTER(v)]
         L.cto_stream_step.argtypes = [v, i32, v, i64, v, v, i64]
@@ -253,6 +257,27 @@ class Port:
         self._chk(self.L.cto_relative_error(C.byref(a), x_sq, C.byref(b), _p(u), C.byref(c),
                                             C.byref(out)), "relative_error")
         return out.value
+
+    def relerr_dd_direct(self, x: Csc, r: Csc, u: np.ndarray):
+        """Double-double |x_j - R U R^T x_j|^2 summed over the columns of x, and |x|^2,
+        each as (hi, lo) (relerr_dd.c, evaluation.cpp:100-121)."""
+        keep: list = []
+        a, b = self._struct(x, keep), self._struct(r, keep)
+        u = _f64(u).reshape(-1)
+        o = [C.c_double() for _ in range(4)]
+        self._chk(self.L.cto_relerr_dd_direct(C.byref(a), C.byref(b), _p(u), *[C.byref(t) for t in o]),
+                  "relerr_dd_direct")
+        return (o[0].value, o[1].value), (o[2].value, o[3].value)
+
+    def relerr_dd_full(self, x: Csc, r: Csc, u: np.ndarray):
+        """Double-double relative error of the whole matricized tensor x (relerr_dd.c)."""
+        keep: list = []
+        a, b = self._struct(x, keep), self._struct(r, keep)
+        u = _f64(u).reshape(-1)
+        o = [C.c_double() for _ in range(3)]
+        self._chk(self.L.cto_relerr_dd_full(C.byref(a), C.byref(b), _p(u), *[C.byref(t) for t in o]),
+                  "relerr_dd_full")
+        return o[0].value
 
     def ctd_s_error(self, shape, idx, val, mode, s, eps=1e-6, seed=42):
         """Front end + compute_core + relative_error (the reference composition)."""

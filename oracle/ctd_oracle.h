@@ -86,6 +86,15 @@ int cto_core_matricized(const cto_csc *x_mat, const cto_csc *r, cto_csc *out);
 int cto_relative_error(const cto_csc *x_mat, double x_sq, const cto_csc *r,
                        const double *u, const cto_csc *core, double *out);
 
+/* Double-double restatements of relative_error (relerr_dd.c): the error
+ * numerator column by column over the fibers of x (any subset of X's
+ * columns), and the whole-tensor value through the exact expansion
+ * |X|^2 - <U, N> + tr((U G - I) U N), N = C C^T, G = R^T R. */
+int cto_relerr_dd_direct(const cto_csc *x, const cto_csc *r, const double *u,
+                         double *err_hi, double *err_lo, double *xsq_hi, double *xsq_lo);
+int cto_relerr_dd_full(const cto_csc *x, const cto_csc *r, const double *u, double *out,
+                       double *num_hi, double *num_lo);
+
 /* CTD-D (ctd_dynamic.cpp).  The stream keeps R/U (basis), the matricized core
  * and the kept flat ids. */
 typedef struct cto_stream cto_stream;

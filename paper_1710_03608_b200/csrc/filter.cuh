@@ -42,6 +42,13 @@ struct Basis {
   bool Wok = false;
   std::vector<double> Wscale;  // 1/delta of each kept column (host)
   Buf<double> Wsc;             // the same on the device
+  // Q: orthonormal basis of span(R) for the error pass (relerr.cu,
+  // ortho_panel), cached for basis size Qk; Newton-Schulz iterations and the
+  // starting defect |A^T A - I|_F of the last build
+  mutable Buf<double> Q;
+  mutable int64_t Qk = -1, Qld = 0;
+  mutable int Qiters = 0;
+  mutable double Qdefect = 0.0;
 
   Basis(Ctx* c, int64_t d);
   // Copy R's host CSC and U (resume ctor, fiber_basis.cpp:13-19).

@@ -1,88 +1,35 @@
 // Relative reconstruction error |X - R U C|^2 / |X|^2 (relative_error,
 // evaluation.cpp:88-122) without materializing C or a dense reconstruction.
 //
-// With C = R^T X (compute_core, ctd_static.cpp:12-17) and P = R U R^T the
-// error numerator is  sum_j |x_j|^2 - 2 x_j^T P x_j + x_j^T P^2 x_j; U is the
-// inverse Gram, P^2 = P, so it is |X|^2 - sum_j <R^T x_j, (R U)^T x_j>.  Both
-// factors are gathered per nonzero from dense row-major panels
-// Rd = R (dim x K) and Q = R U (dim x K): one streaming pass over the
-// bucketed nonzeros with a K-wide register accumulator per fiber (warp per
-// fiber, lanes across K).  This is a tolerance path (|d| <= 1e-9 max(1,|ref|)),
-// so it uses FMA and a deterministic (fixed-order) reduction.
+// Static factors (C = R^T X, compute_core, ctd_static.cpp:12-17): with Q an
+// orthonormal basis of span(R) (ortho.cu), the numerator is
+// |X|^2 - sum_j |Q^T x_j|^2 up to a term second order in U's backward error
+// (see ortho.cu), evaluated as one streaming pass over the bucketed nonzeros
+// (warp per fiber, lanes across a column tile of Q).  The earlier identity
+// |X|^2 - <X, R U R^T X> carried U's rounding at first order: 3e-9 off at C2
+// (round 1), outside the 1e-9 target.  Stream cores (CTD-D, C != R^T X): the
+// direct column-by-column form, k_core_err.  This is a tolerance path
+// (|d| <= 1e-9 max(1,|ref|), pinned against oracle/relerr_dd.c), so it uses
+// FMA and deterministic (fixed-order) reductions.
 #include "relerr.cuh"
 
+#include <cmath>
 #include <cstdlib>
+
+#include "ortho.cuh"
 
 namespace ctdgpu {
 
 namespace {
 
-__global__ void k_dense_r(const int64_t* rptr, const int32_t* rrow, const double* rval, long long K,
-                          double* Rd) {
-  const long long k = blockIdx.x;
-  if (k >= K) return;
-  for (long long t = rptr[k] + threadIdx.x; t < rptr[k + 1]; t += blockDim.x)
-    Rd[(long long)rrow[t] * K + k] = rval[t];
-}
-
-// Q[r][c] = sum over R's row r entries (k, v): v * U[k][c].
-__global__ void k_ru(const int64_t* rowbase, const int32_t* rowlen, const int32_t* rek, const double* rev,
-                     const double* U, long long LD, long long dim, long long K, double* Q) {
-  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= dim * K) return;
-  const long long r = e / K, c = e - r * K;
-  const long long b = rowbase[r];
-  const int L = rowlen[r];
-  double s = 0.0;
-  for (int t = 0; t < L; ++t) s = __fma_rn(rev[b + t], U[(long long)rek[b + t] * LD + c], s);
-  Q[e] = s;
-}
-
 constexpr int kCW = 4;  // columns per lane per chunk
 
-__global__ void k_cd(const int64_t* fptr, long long F, const int32_t* row, const double* val,
-                     const double* Rd, const double* Q, long long K, double* partial) {
-  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  double part = 0.0;
-  // column chunk outermost: the grid sweeps all fibers against one 128-column
-  // tile of Rd and Q at a time, so the tile (dim x 128 x 16 B) stays in L2 and
-  // the heavy rows' tiles in L1, instead of every fiber walking all of K
-  for (long long c0 = 0; c0 < K; c0 += 32 * kCW) {
-    for (long long f = warp; f < F; f += nwarps) {
-      const long long b = fptr[f], e = fptr[f + 1];
-      double ac[kCW], ad[kCW];
-#pragma unroll
-      for (int u = 0; u < kCW; ++u) ac[u] = ad[u] = 0.0;
-      for (long long t = b; t < e; ++t) {
-        const long long r = row[t];
-        const double v = val[t];
-        const double* rr = Rd + r * K;
-        const double* qq = Q + r * K;
-#pragma unroll
-        for (int u = 0; u < kCW; ++u) {
-          const long long c = c0 + lane + 32 * u;
-          if (c < K) {
-            ac[u] = __fma_rn(v, rr[c], ac[u]);
-            ad[u] = __fma_rn(v, qq[c], ad[u]);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kCW; ++u) part = __fma_rn(ac[u], ad[u], part);
-    }
-  }
-  part = warp_sum(part);
-  if (lane == 0) partial[warp] = part;
-}
-
-// sum_j |W^T x_j|^2 with W = R T orthonormal by construction (U = T T^T).
-// The panel stores the residuals x_k - R y_k unscaled (written by the filter
-// off its critical path); column c is weighed by wsc[c] = 1/delta_c here.
-// The same column-chunked sweep as k_cd with one panel instead of two.
+// sum_j |Q^T x_j|^2 over the fibers with >= 2 entries (Q: dim x K, row-major,
+// leading dimension LD).  Column chunk outermost: the grid sweeps all fibers
+// against one 128-column tile of Q at a time, so the tile (dim x 128 x 8 B)
+// stays in L2 and the heavy rows' tiles in L1.
 __global__ void k_cdw(const int64_t* fptr, long long F, const int32_t* row, const double* val, const double* W,
-                      const double* wsc, long long LD, long long K, double* partial) {
+                      long long LD, long long K, double* partial) {
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -107,7 +54,7 @@ __global__ void k_cdw(const int64_t* fptr, long long F, const int32_t* row, cons
 #pragma unroll
       for (int u = 0; u < kCW; ++u) {
         const long long c = c0 + lane + 32 * u;
-        if (c < K) part = __fma_rn(ac[u] * ac[u], wsc[c], part);
+        if (c < K) part = __fma_rn(ac[u], ac[u], part);
       }
     }
   }
@@ -115,17 +62,16 @@ __global__ void k_cdw(const int64_t* fptr, long long F, const int32_t* row, cons
   if (lane == 0) partial[warp] = part;
 }
 
-// rho[r] = sum_c W[r][c]^2 / delta_c: |W^T x|^2 of a fiber with one entry
-// (r, v) is v^2 rho[r] (63% of C2's fibers).  Warp per row.
-__global__ void k_row_weight(const double* W, const double* wsc, long long LD, long long K, long long dim,
-                             double* rho) {
+// rho[r] = |Q[r][:]|^2: |Q^T x|^2 of a fiber with one entry (r, v) is
+// v^2 rho[r] (63% of C2's fibers).  Warp per row.
+__global__ void k_row_weight(const double* W, long long LD, long long K, long long dim, double* rho) {
   const long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= dim) return;
   double s = 0.0;
   for (long long c = lane; c < K; c += 32) {
     const double w = W[r * LD + c];
-    s = __fma_rn(w * w, wsc[c], s);
+    s = __fma_rn(w, w, s);
   }
   s = warp_sum(s);
   if (lane == 0) rho[r] = s;
@@ -162,6 +108,32 @@ __global__ void k_reduce(const double* p, long long n, double* out) {
   for (long long i = threadIdx.x; i < n; i += blockDim.x) s += p[i];
   s = block_sum<double>(s, sh);
   if (threadIdx.x == 0) *out = s;
+}
+
+// A[r][c] = W[r][c] / sqrt(delta_c): the filter's residual panel with unit
+// columns up to U's rounding (W = R T, U = T T^T), the start of the polar
+// iteration.
+__global__ void k_panel_from_w(const double* W, const double* wsc, long long LDW, long long dim, long long K,
+                               double* A, long long lda) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= dim * K) return;
+  const long long r = t / K, c = t - r * K;
+  A[r * lda + c] = W[r * LDW + c] * sqrt(wsc[c]);
+}
+
+// A[:, k] = R[:, k] / |R[:, k]| (A zeroed), one CTA per kept column: the
+// start of the polar iteration when the filter kept no panel.
+__global__ void k_dense_r_unit(const int64_t* rptr, const int32_t* rrow, const double* rval, long long K, double* A,
+                               long long lda) {
+  __shared__ double sh[33];
+  const long long k = blockIdx.x;
+  if (k >= K) return;
+  double s = 0.0;
+  for (long long t = rptr[k] + threadIdx.x; t < rptr[k + 1]; t += blockDim.x) s = __fma_rn(rval[t], rval[t], s);
+  s = block_sum<double>(s, sh);
+  const double inv = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+  for (long long t = rptr[k] + threadIdx.x; t < rptr[k + 1]; t += blockDim.x)
+    A[(long long)rrow[t] * lda + k] = rval[t] * inv;
 }
 
 // Qt[c][r] = (R U)[r][c] (dense_product, evaluation.cpp:32-43), column-major
@@ -261,6 +233,29 @@ double relative_error(Ctx* ctx, const Fibers& fb, const Basis& B) {
   return (hx - hcd) / hx;
 }
 
+const double* ortho_panel(Ctx* ctx, const Basis& B, int64_t* ldq) {
+  const int64_t K = B.K, dim = B.dim;
+  if (B.Q.p && B.Qk == K) {
+    *ldq = B.Qld;
+    return B.Q.p;
+  }
+  const int64_t ld = (K + 1) & ~int64_t(1);
+  B.Q.alloc(ctx, (size_t)dim * ld);
+  if (B.Wok) {
+    LAUNCH(ctx, k_panel_from_w, ceil_div((uint64_t)dim * K, 256), 256, 0, B.W.p, B.Wsc.p, (long long)B.LD,
+           (long long)dim, (long long)K, B.Q.p, (long long)ld);
+  } else {
+    B.Q.zero();
+    LAUNCH(ctx, k_dense_r_unit, (unsigned)K, 128, 0, B.rptr.p, B.rrow.p, B.rval.p, (long long)K, B.Q.p,
+           (long long)ld);
+  }
+  B.Qiters = orthonormalize(ctx, B.Q.p, dim, K, ld, &B.Qdefect);
+  B.Qk = K;
+  B.Qld = ld;
+  *ldq = ld;
+  return B.Q.p;
+}
+
 void error_partials(Ctx* ctx, const Fibers& fb, const Basis& B, double* x_sq, double* cross) {
   const long long K = B.K, dim = B.dim;
   // |X|^2
@@ -273,30 +268,17 @@ void error_partials(Ctx* ctx, const Fibers& fb, const Basis& B, double* x_sq, do
     *cross = 0.0;
     return;
   }
+  // sum_j |Q^T x_j|^2, Q orthonormal with span(Q) = span(R)
+  int64_t ldq = 0;
+  const double* Q = ortho_panel(ctx, B, &ldq);
   const unsigned cgrid = (unsigned)ctx->sm_count * 8;
   const long long nwarps = (long long)cgrid * 256 / 32;
-  Buf<double> cp(ctx, nwarps);
-  if (B.Wok && !getenv("CTD_RELERR_TWO_PANELS")) {
-    // one orthonormal panel, maintained by the filter
-    Buf<double> rho(ctx, dim + 1), sp1(ctx, sgrid + nwarps);
-    LAUNCH(ctx, k_row_weight, ceil_div((uint64_t)dim * 32, 256), 256, 0, B.W.p, B.Wsc.p, (long long)B.LD, K, dim,
-           rho.p);
-    LAUNCH(ctx, k_single_fibers, sgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, rho.p, sp1.p);
-    LAUNCH(ctx, k_cdw, cgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, B.W.p, B.Wsc.p,
-           (long long)B.LD, K, sp1.p + sgrid);
-    LAUNCH(ctx, k_reduce, 1, 1024, 0, sp1.p, (long long)sgrid + nwarps, cd.p);
-    ctx->to_host(x_sq, xsq.p, 1);
-    ctx->to_host(cross, cd.p, 1);
-    ctx->sync();
-    return;
-  }
-  Buf<double> Rd(ctx, (size_t)dim * K), Q(ctx, (size_t)dim * K);
-  Rd.zero();
-  LAUNCH(ctx, k_dense_r, (unsigned)K, 128, 0, B.rptr.p, B.rrow.p, B.rval.p, K, Rd.p);
-  LAUNCH(ctx, k_ru, ceil_div(dim * K, 256), 256, 0, B.rowbase.p, B.rowlen.p, B.rek.p, B.rev.p, B.U.p,
-         (long long)B.LD, dim, K, Q.p);
-  LAUNCH(ctx, k_cd, cgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, Rd.p, Q.p, K, cp.p);
-  LAUNCH(ctx, k_reduce, 1, 1024, 0, cp.p, nwarps, cd.p);
+  Buf<double> rho(ctx, dim + 1), sp1(ctx, sgrid + nwarps);
+  LAUNCH(ctx, k_row_weight, ceil_div((uint64_t)dim * 32, 256), 256, 0, Q, (long long)ldq, K, dim, rho.p);
+  LAUNCH(ctx, k_single_fibers, sgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, rho.p, sp1.p);
+  LAUNCH(ctx, k_cdw, cgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, Q, (long long)ldq, K,
+         sp1.p + sgrid);
+  LAUNCH(ctx, k_reduce, 1, 1024, 0, sp1.p, (long long)sgrid + nwarps, cd.p);
   ctx->to_host(x_sq, xsq.p, 1);
   ctx->to_host(cross, cd.p, 1);
   ctx->sync();

@@ -15,8 +15,13 @@ double relative_error(Ctx* ctx, const Fibers& fb, const Basis& B);
 double relative_error_core(Ctx* ctx, const Fibers& fb, const Basis& B, const Core& core);
 
 // The two sums relative_error combines, over the fibers of fb (one shard of
-// X in the sharded path): |X|^2 and sum_j x_j^T (R U R^T) x_j, so
-// rel = (|X|^2 - cross) / |X|^2 after summing the shards' partials.
+// X in the sharded path): |X|^2 and sum_j |Q^T x_j|^2 (Q an orthonormal basis
+// of span(R), ortho_panel), so rel = (|X|^2 - cross) / |X|^2 after summing
+// the shards' partials.
 void error_partials(Ctx* ctx, const Fibers& fb, const Basis& B, double* x_sq, double* cross);
+
+// Q = (dim x K, leading dimension *ldq) orthonormal with span(Q) = span(R),
+// built once per basis size (ortho.cu) and cached on the basis.
+const double* ortho_panel(Ctx* ctx, const Basis& B, int64_t* ldq);
 
 }  // namespace ctdgpu
