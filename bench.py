@@ -1,14 +1,22 @@
 #!/usr/bin/env python
 """CTD-S throughput on BASELINE.json configs[1] (C2) on N B200s.
 
-One step = one CTD-S pass over the resident C2 tensor (10^4 x 10^4 x 10^3
+One step = one CTD-S front end over the resident C2 tensor (10^4 x 10^4 x 10^3
 synthetic traffic, 1e7 coalesced nnz, c = 2000, eps = 1e-6, seed 42, mode 0):
 bucketing + exact squared norms, sampling law and CDF, mt19937_64 draws and
-dedup, the bit-exact independence filter + U, and the relative-error pass.
-`value` = nnz / device-timed step (inputs already in HBM); `e2e` = the same
-through the public C-ABI from pinned host COO (H2D + D2H inside the region).
+dedup, the bit-exact independence filter + U -- the scope of the reference's
+ctd_s minus compute_core (C is not materialized: ~4e9 entries at C2, SURVEY
+H3), which is also what `--impl reference` times.  `value` = nnz / device-timed
+step (inputs already in HBM); `e2e` = the same through the public C-ABI from
+pinned host COO (H2D + D2H inside the region).  The relative-error pass
+(evaluation.cpp:88-122) is reported as a second metric (`error_pass`,
+`ctd_s_with_error`), since the reference evaluates it outside ctd_s
+(stream_harness.cpp:72-81).  Secondary objects: C3 (CTD-D latency), C4, C5.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--gpus N > 1 without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (fails if fewer than N GPUs are visible).
 """
 from __future__ import annotations
 
@@ -31,6 +39,19 @@ UNIT = "nnz/s"
 C2 = dict(shape=[10000, 10000, 1000], nnz=10_000_000, c=2000, eps=1e-6, seed=42, mode=0, gen_seed=2)
 WORKLOAD = ("C2: CTD-S on synthetic traffic 1e4x1e4x1e3 (Zipf(1.2) src/dst, uniform time, "
             "log-uniform counts 1..100), 1e7 coalesced nnz, c=2000, eps=1e-6, mode 0")
+STEP_SCOPE = ("ctd_s front end: matricize+norms, column_distribution/CDF, mt19937_64 draws, dedup, "
+              "FiberBasis filter + U (compute_core excluded: C not materialized)")
+
+
+def bench_config(world: int = 1) -> dict:
+    """The `config` object both arms print, identical so the driver can match them."""
+    cfg = {"workload": WORKLOAD, "shape": C2["shape"], "nnz": C2["nnz"], "c": C2["c"], "eps": C2["eps"],
+           "seed": C2["seed"], "mode": C2["mode"], "generator_seed": C2["gen_seed"], "step": STEP_SCOPE,
+           "l2": "inputs larger than L2 (200 MB COO + 120 MB bucketed per step)"}
+    if world > 1:
+        cfg["workload"] = WORKLOAD + f"; weak-scaled: {world} time-concatenated C2 shards"
+        cfg["parallelism"] = f"fiber-range shards x{world} (NCCL)"
+    return cfg
 
 
 def _np_default(o):
@@ -112,7 +133,10 @@ def run_ctd_d(args, ctx, torch):
     d = 500 samples, seed ^ t), each timed alone like stream_harness.cpp:90-92 (step
     only; slabs already resident on the device).  Scope: the step's front end
     (slab bucketing + norms, law/CDF, draws, dedup, bit-exact filter against R(t),
-    kept-id append); the Eq. 13 core blocks are not maintained (SURVEY §8f #2)."""
+    kept-id append); the Eq. 13 core is not maintained over this horizon (its
+    bottom-left block is dense over every historical column: ~1e9+ entries by
+    t = 500).  `same_scope` times the step WITH the Eq. 13 core update
+    on both sides at t = 10..14, where the reference still runs."""
     from paper_1710_03608_b200 import ctd as api
     x = load_c3()
     H = C3["hist_steps"] * C3["slices"]
@@ -142,18 +166,72 @@ def run_ctd_d(args, ctx, torch):
         if d is not None:
             d.close()
     ht.close()
-    return {"workload": "C3: CTD-D on 5000x5000 src x dst, 10 slices/step x 100 steps, Zipf(1.2), "
-                        "counts 1..50, planted 50x50x10 block (+100) at step 60; d=500, eps=1e-6",
-            "history_slices": H, "streamed_slices": len(lat), "history_nnz": hist.nnz,
-            "init_stream_ms": round(init_s * 1e3, 2),
-            "step_ms_p50": round(float(np.percentile(lat_ms, 50)), 3),
-            "step_ms_p99": round(float(np.percentile(lat_ms, 99)), 3),
-            "step_ms_mean": round(float(lat_ms.mean()), 3),
-            "slices_per_s": round(len(lat) / (lat_ms.sum() / 1e3), 1),
-            "nnz_per_s": round(nnz_steps / (lat_ms.sum() / 1e3), 1),
-            "kept_final": len(kept.kept_flat) if hasattr(kept, "kept_flat") else None,
-            "scope": "step front end (bucketing, law, seed^t draws, dedup, bit-exact filter vs R(t), "
-                     "kept-id append); Eq. 13 core blocks not maintained (SURVEY 8f #2)"}
+    st.close()
+    out = {"workload": "C3: CTD-D on 5000x5000 src x dst, 10 slices/step x 100 steps, Zipf(1.2), "
+                       "counts 1..50, planted 50x50x10 block (+100) at step 60; d=500, eps=1e-6",
+           "history_slices": H, "streamed_slices": len(lat), "history_nnz": hist.nnz,
+           "init_stream_ms": round(init_s * 1e3, 2),
+           "step_ms_p50": round(float(np.percentile(lat_ms, 50)), 3),
+           "step_ms_p99": round(float(np.percentile(lat_ms, 99)), 3),
+           "step_ms_mean": round(float(lat_ms.mean()), 3),
+           "step_ms_max": round(float(lat_ms.max()), 3),
+           "slices_per_s": round(len(lat) / (lat_ms.sum() / 1e3), 1),
+           "nnz_per_s": round(nnz_steps / (lat_ms.sum() / 1e3), 1),
+           "kept_final": len(kept.kept_flat) if hasattr(kept, "kept_flat") else None,
+           "scope": "step front end (bucketing, law, seed^t draws, dedup, bit-exact filter vs R(t), "
+                    "kept-id append); Eq. 13 core not maintained over 500 slices (see same_scope)"}
+    out["same_scope"] = ctd_d_same_scope(args, ctx, torch, x)
+    return out
+
+
+def ctd_d_same_scope(args, ctx, torch, x=None):
+    """ctd_d_step WITH the Eq. 13 core update (transpose_times, chain_product,
+    assemble_blocks; ctd_dynamic.cpp:149-229) on both sides, same inputs, same t:
+    init_stream on C3's first 10 slices, then 5 timed steps (t = 10..14)."""
+    from paper_1710_03608_b200 import ctd as api
+    from paper_1710_03608_b200 import datagen
+    x = x if x is not None else load_c3()
+    h = x.time_slab(0, 10)
+    slabs = time_slices(x, 10, 15)
+    shape1 = [C3["n"], C3["n"], 1]
+    nnz = sum(int(v.shape[0]) for _, v in slabs)
+    st = api.init_stream(api.SparseTensor.from_datagen(h), C3["mode"], C3["d"], C3["eps"], C3["seed"],
+                         with_core=True, ctx=ctx)
+    dev = [api.DeviceTensor(api.SparseTensor(shape1, i, v), ctx) for i, v in slabs]
+    torch.cuda.synchronize()
+    lat = []
+    for dt in dev:
+        t0 = time.perf_counter()
+        api.ctd_d_step(st, dt, C3["d"])
+        torch.cuda.synchronize()
+        lat.append(time.perf_counter() - t0)
+    f = st.factors()
+    gpu_core = int(f.C_val.shape[0]) if getattr(f, "C_val", None) is not None else None
+    for d in dev:
+        d.close()
+    st.close()
+    out = {"what": "ctd_d_step incl. the Eq. 13 core (bit-exact with the reference's), t = 10..14 after "
+                   "init_stream on 10 slices of C3", "slab_nnz": nnz,
+           "gpu_step_ms": [round(v * 1e3, 3) for v in lat], "gpu_step_ms_mean": round(float(np.mean(lat)) * 1e3, 3),
+           "core_nnz_after": gpu_core}
+    if not args.no_cpu:
+        try:
+            from oracle.bindings import Ref, ref_available
+            if ref_available():
+                R = Ref()
+                rs = R.stream(R.tensor(h.shape, h.flat_idx(), h.val), C3["mode"], C3["d"], C3["eps"], C3["seed"])
+                secs = []
+                for idx, val in slabs:
+                    sl = datagen.Tensor(shape1, idx, val)
+                    secs.append(rs.step(R.tensor(sl.shape, sl.flat_idx(), sl.val), C3["d"]))
+                out["reference_step_ms"] = [round(v * 1e3, 3) for v in secs]
+                out["reference_step_ms_mean"] = round(float(np.mean(secs)) * 1e3, 3)
+                out["reference"] = {"kind": "reference", "cores": 1, "cpu": _cpu_model(),
+                                    "sample": "the reference ctd_d_step (oracle/_ref) on the same slabs, single-threaded"}
+                out["speedup_mean"] = round(float(np.mean(secs)) / float(np.mean(lat)), 1)
+        except Exception as e:  # pragma: no cover
+            out["reference"] = {"sample": f"failed: {e}"}
+    return out
 
 
 C4 = dict(c=5000, eps=1e-6, seed=42, mode=0, gen_seed=4)
@@ -246,7 +324,10 @@ def run_c5(args, ctx, torch):
     """BASELINE configs[4] (C5) on one GPU: 1e5x1e5x1e3 traffic with 1e9 coalesced nnz
     (Zipf(1.2) src/dst, uniform time, log-uniform counts 1..100; int32 indices),
     c = 10000.  Generated on the device (datagen_gpu, same law as the host generator);
-    the front end is timed on the resident tensor (20 GB of COO, far above L2)."""
+    the front end is timed on the resident tensor (20 GB of COO, far above L2), then
+    end to end from pinned host COO (32 GB in the reference's int64 layout), and the
+    reference front end on a 1/100 time-scaled C5 (full C5 does not finish: ~1e9 nnz
+    std::sort + a filter over fibers of ~1e4-1e5 entries)."""
     from paper_1710_03608_b200 import ctd as api
     from paper_1710_03608_b200 import datagen_gpu
     free, _ = torch.cuda.mem_get_info()
@@ -261,7 +342,7 @@ def run_c5(args, ctx, torch):
     dt = api.DeviceTensor.from_device_ptrs(C5["shape"], nnz, [idx[k].data_ptr() for k in range(3)],
                                            val.data_ptr(), ctx)
     ms, info, phases, launches = _time_frontend(ctx, dt, C5, max(1, min(args.steps, 2)), 1, torch)
-    pk, _ = peaks()
+    pk, pk_kind = peaks()
     bs = 44 * nnz + 24 * info.n_fibers
     mat_ms = phases.get("matricize")
     out = {"workload": "C5: CTD-S on 1e5x1e5x1e3 traffic, 1e9 coalesced nnz (Zipf(1.2), uniform time, "
@@ -270,36 +351,87 @@ def run_c5(args, ctx, torch):
            "ms_per_step": round(ms, 3), "nnz_per_s": round(nnz / (ms / 1e3), 1),
            "unique_sampled": info.n_unique, "kept": info.kept, "phases_ms": phases,
            "gpu_launches_per_step": launches,
-           "step_bytes_44nnz_24F": bs, "step_frac_of_peak": round(bs / (ms / 1e3) / 1e9 / pk, 4),
-           "matricize_gbs": round((32 * nnz + 24 * info.n_fibers) / (mat_ms / 1e3) / 1e9, 1)
-           if mat_ms else None}
+           "step_bytes_44nnz_24F": bs, "step_frac_of_peak": round(bs / (ms / 1e3) / 1e9 / pk, 4)}
+    if mat_ms:
+        mb = 32 * nnz + 24 * info.n_fibers
+        out["roofline"] = {"bound": "hbm", "kernel": "matricize (bucketing + norms)", "achieved": round(mb / (mat_ms / 1e3) / 1e9, 1),
+                           "peak": pk, "unit": "GB/s", "frac": round(mb / (mat_ms / 1e3) / 1e9 / pk, 4),
+                           "bytes": mb, "peak_kind": pk_kind,
+                           "note": "the HBM-bound phase at C5; the filter (latency-bound) is in phases_ms"}
+    # error pass at C5 (the second metric)
+    try:
+        h, _ = api.ctd_s_raw(dt, C5["mode"], C5["c"], C5["eps"], C5["seed"], ctx=ctx, keep_panel=True)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        rel = api.relative_error_raw(dt, h, ctx)
+        torch.cuda.synchronize()
+        out["error_pass"] = {"ms_first": round((time.perf_counter() - t1) * 1e3, 2), "relative_error": rel}
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rel = api.relative_error_raw(dt, h, ctx)
+        e1.record()
+        torch.cuda.synchronize()
+        out["error_pass"]["ms_cached_panel"] = round(e0.elapsed_time(e1), 2)
+        api.free_factors(ctx, h)
+    except Exception as e:  # pragma: no cover
+        out["error_pass"] = {"failed": str(e)}
     dt.close()
+    # e2e: the reference's host layout (int64 AoS + fp64) from pinned memory
+    if not args.no_e2e:
+        try:
+            out["e2e"] = c5_e2e(ctx, idx, val, nnz, torch)
+        except Exception as e:  # pragma: no cover
+            out["e2e"] = {"failed": str(e)}
     del idx, val
     torch.cuda.empty_cache()
+    if not args.no_cpu:
+        out["cpu_baseline"] = c5_cpu_baseline()
     return out
 
 
-def ctd_d_reference_sample():
-    """The reference ctd_d_step (oracle/_ref, which also updates the Eq. 13 core) on C3:
-    init_stream on the first 10 slices, then 5 timed steps (a bounded sample)."""
+def c5_e2e(ctx, idx, val, nnz, torch):
+    from paper_1710_03608_b200 import ctd as api
+    ih = torch.empty((nnz, 3), dtype=torch.int64, pin_memory=True)
+    vh = torch.empty(nnz, dtype=torch.float64, pin_memory=True)
+    step = 1 << 27
+    for a in range(0, nnz, step):
+        b = min(nnz, a + step)
+        ih[a:b].copy_(torch.stack([idx[0][a:b], idx[1][a:b], idx[2][a:b]], 1).to(torch.int64))
+    vh.copy_(val)
+    torch.cuda.synchronize()
+    del idx, val
+    torch.cuda.empty_cache()
+    t0 = time.perf_counter()
+    t = api.DeviceTensor.from_host_ptrs(C5["shape"], nnz, ih.data_ptr(), vh.data_ptr(), ctx)
+    h, info = api.ctd_s_raw(t, C5["mode"], C5["c"], C5["eps"], C5["seed"], ctx=ctx)
+    kept, u = api.factors_result(ctx, h, info)
+    api.free_factors(ctx, h)
+    t.close()
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    return {"value": round(nnz / sec, 1), "unit": UNIT, "ms_per_step": round(sec * 1e3, 1),
+            "h2d_bytes_per_step": nnz * (3 * 8 + 8), "d2h_bytes_per_step": int(kept.nbytes + u.nbytes),
+            "path": "ctd_gpu_tensor_from_host (pinned int64 AoS + fp64, 32 GB) -> ctd_gpu_ctd_s -> kept ids + U"}
+
+
+def c5_cpu_baseline():
+    """The reference front end on C5 scaled 1/100 in time (1e5 x 1e5 x 10, 1e7 nnz,
+    c = 10000): the full C5 does not fit the reference's budget (DNF)."""
     try:
         from oracle.bindings import Ref, ref_available
+        from paper_1710_03608_b200 import datagen
         if not ref_available():
-            return None
-        x = load_c3()
+            return {"value": None, "sample": "unavailable: oracle/_ref/libctdref.so not built"}
+        x = datagen.traffic([100000, 100000, 10], 10_000_000, C5["gen_seed"])
         R = Ref()
-        h = x.time_slab(0, 10)
-        st = R.stream(R.tensor(h.shape, h.flat_idx(), h.val), C3["mode"], C3["d"], C3["eps"], C3["seed"])
-        secs = []
-        for i, (idx, val) in enumerate(time_slices(x, 10, 15)):
-            from paper_1710_03608_b200 import datagen
-            sl = datagen.Tensor([C3["n"], C3["n"], 1], idx, val)
-            secs.append(st.step(R.tensor(sl.shape, sl.flat_idx(), sl.val), C3["d"]))
-        return {"step_ms_mean": round(float(np.mean(secs)) * 1e3, 2), "cores": 1, "kind": "reference",
-                "sample": "reference ctd_d_step (includes its Eq. 13 core update) at t = 10..14 "
-                          "after init_stream on 10 slices; single-threaded"}
+        t = R.tensor(x.shape, x.flat_idx(), x.val)
+        fe = R.frontend(t, C5["mode"], C5["c"], C5["eps"], C5["seed"])
+        return {"value": round(x.nnz / fe.seconds, 1), "unit": UNIT, "cores": 1, "kind": "reference",
+                "seconds": round(fe.seconds, 3), "cpu": _cpu_model(),
+                "sample": "reference ctd_s front end on C5 scaled 1/100 in time (1e5x1e5x10, 1e7 nnz, same "
+                          "generator law, c=10000), single-threaded; full C5: DNF (1e9 nnz)"}
     except Exception as e:  # pragma: no cover
-        return {"sample": f"failed: {e}"}
+        return {"value": None, "sample": f"failed: {e}"}
 
 
 # ---------------------------------------------------------------------------
@@ -357,14 +489,17 @@ class Clocks:
 # algorithmic bytes (frozen before measuring)
 
 def phase_bytes(nnz, F, kept_seq, r_lens):
-    """Algorithmic HBM bytes per phase for one CTD-S step."""
+    """Algorithmic HBM bytes per phase for one CTD-S step.  Filter:
+    per candidate one read of U (y = U g, the update fused into the same pass)
+    and of R's row index (z = R y, 12 B/entry); per accept one write of the
+    (K+1)^2 U."""
     filt = 0
     K = 0
     rn = 0
     for j, acc in enumerate(kept_seq):
         filt += 8 * K * K + 12 * rn          # y = U g reads U; z reads R's row index
         if acc:
-            filt += 16 * (K + 1) * (K + 1)  # U update read + write
+            filt += 8 * (K + 1) * (K + 1)   # U update written once
             rn += r_lens[K]
             K += 1
     return {
@@ -463,12 +598,14 @@ def run_sharded(args, rank, world, local_rank):
     ctx.set_timing(True)
     ctx.phase_times(reset=True)
     l0 = ctx.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local_rank) as clk:
-        t0 = time.perf_counter()
+        e0.record()
         for _ in range(args.steps):
             r = step()
+        e1.record()
         torch.cuda.synchronize()
-        sec = (time.perf_counter() - t0) / args.steps
+        sec = e0.elapsed_time(e1) / 1e3 / args.steps
     torch.distributed.barrier()
     launches = ctx.launches - l0
     phases = ctx.phase_times(reset=True)
@@ -504,11 +641,10 @@ def run_sharded(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded splitmix64 generator, SURVEY §8d)",
-        "config": {"workload": WORKLOAD + f"; weak-scaled: {world} time-concatenated C2 shards",
-                   "nnz": nnz, "global_shape": gshape, "parallelism": f"fiber-range shards x{world} (NCCL)",
+        "config": bench_config(world),
+        "result": {"nnz_global": nnz, "global_shape": gshape,
                    "kept": int(r.kept_flat.shape[0]), "unique_sampled": int(r.unique.shape[0]),
-                   "relative_error": rel, "fibers_global": r.n_fibers,
-                   "l2": "inputs larger than L2 (200 MB COO per rank)"},
+                   "relative_error": rel, "fibers_global": r.n_fibers},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": None, "peak": pk, "unit": "GB/s",
                      "frac": None, "traffic": ncu_traffic(dom), "peak_kind": pk_kind,
                      "note": "multi-rank step includes host collectives; per-kernel roofline in the N=1 line"},
@@ -579,10 +715,17 @@ def run_ours(args, rank, world, local_rank):
     # timed steps above, which match the reference's ctd_s)
     torch.cuda.synchronize()
     p0 = time.perf_counter()
+    q0, q1, q2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    q0.record()
     hlast, _ = api.ctd_s_raw(dt, mode, c, eps, seed, with_error=False, ctx=ctx, keep_panel=True)
+    q1.record()
     torch.cuda.synchronize()
     panel_front_ms = (time.perf_counter() - p0) * 1e3
     rel = api.relative_error_raw(dt, hlast, ctx)
+    q2.record()
+    torch.cuda.synchronize()
+    panel_front_ms_dev = q0.elapsed_time(q1)
+    err_first_ms = q1.elapsed_time(q2)
     ctx.set_timing(True)
     ctx.phase_times(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -628,8 +771,9 @@ def run_ours(args, rank, world, local_rank):
             "what": "dependent fp64 add chains in the reference's order (y = U g: K adds; z = R y: longest "
                     "R row), 8.2-cycle DADD latency at 1965 MHz; exchanges and the exact residual sum excluded",
             "floor_ms": round(fc / clk_hz * 1e3, 3), "frac": round(fc / clk_hz * 1e3 / dms, 4)}
-    # SURVEY §8d end-to-end byte formula for the step
-    bs = 44 * nnz + 24 * info.n_fibers
+    # SURVEY §8d byte formula for the front-end step (the 12 B/nnz error-pass
+    # re-read of 44 nnz + 24 F belongs to error_pass)
+    bs = 32 * nnz + 24 * info.n_fibers
 
     # ---- e2e through the public C-ABI from pinned host COO
     e2e = None
@@ -644,8 +788,6 @@ def run_ours(args, rank, world, local_rank):
     ctdd = None
     if rank == 0 and world == 1 and not args.no_ctdd:
         ctdd = run_ctd_d(args, ctx, torch)
-        if not args.no_cpu:
-            ctdd["cpu_reference"] = ctd_d_reference_sample()
 
     c4 = c5 = None
     if rank == 0 and world == 1 and not args.no_c4:
@@ -661,21 +803,27 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded splitmix64 generator, SURVEY §8d)",
-        "config": {"workload": WORKLOAD, "nnz": nnz, "fibers": info.n_fibers,
-                   "step": "ctd_s front end: matricize+norms, law/CDF, mt19937_64 draws, dedup, "
-                           "bit-exact filter + U (C not materialized, as the CPU baseline)",
-                   "unique_sampled": info.n_unique, "kept": info.kept,
+        "config": bench_config(1),
+        "result": {"nnz": nnz, "fibers": info.n_fibers, "unique_sampled": info.n_unique, "kept": info.kept,
                    "relative_error": rel,
-                   "l2": "inputs larger than L2 (200 MB COO + 120 MB bucketed per step)",
-                   "parallelism": f"fiber-range shards x{world}" if world > 1 else "1 GPU",
-                   "step_bytes_44nnz_24F": bs,
-                   "step_frac_of_peak": round(bs / (ms / 1e3) / 1e9 / pk, 4)},
+                   "step_bytes_32nnz_24F": bs, "step_frac_of_peak": round(bs / (ms / 1e3) / 1e9 / pk, 4),
+                   "step_bytes_note": "front end: read COO (20 B) + write bucketed row/val (12 B) per nnz, "
+                                      "fiber col/ptr/norm (24 B) per fiber; the error pass's 12 B/nnz "
+                                      "re-read is charged to error_pass"},
         "roofline": roof, "phases": per_phase, "gpu_launches": launches,
         "error_pass": {"ms": round(err_ms, 3), "kernel_ms": round(err_kernel_ms, 3),
                        "nnz_per_s": round(nnz / (err_ms / 1e3), 1),
-                       "what": "relative_error(X, factors): matricize + one pass over all nnz against the orthonormal panel W = R T (U = T T^T)",
-                       "panel": "W kept by the filter on request (CTD_GPU_KEEP_PANEL)",
+                       "bytes": 32 * nnz + 24 * info.n_fibers + 12 * nnz,
+                       "gbs": round((44 * nnz + 24 * info.n_fibers) / (err_ms / 1e3) / 1e9, 1),
+                       "first_call_ms": round(err_first_ms, 3),
+                       "what": "relative_error(X, factors): matricize + |X|^2 - sum_j |Q^T x_j|^2 over all nnz, "
+                               "Q orthonormal with span(Q) = span(R) (ortho.cu: DMMA polar iteration from the "
+                               "filter's residual panel, cached on the factors after the first call)",
                        "front_end_with_panel_ms": round(panel_front_ms, 3)},
+        "ctd_s_with_error": {"ms_per_step": round(panel_front_ms_dev + err_first_ms, 3),
+                             "nnz_per_s": round(nnz / ((panel_front_ms_dev + err_first_ms) / 1e3), 1),
+                             "what": "front end (keeping the panel) + the first relative_error call (panel "
+                                     "orthonormalization + sweep), device-timed"},
         "clocks": clk.summary(),
     }
     if e2e:
@@ -758,8 +906,10 @@ def _cpu_model():
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's own CPU implementation (oracle/_ref),
-    rank 0 only, each step a bounded sample of C2 (the first T' time slices)."""
+    """--impl reference: the reference's own CPU implementation (oracle/_ref, the
+    unmodified proj/core compiled from /root/reference), rank 0 only, every step the
+    full C2 front end -- the same config and step scope as our arm (the
+    reference has no threading, so one host core)."""
     if rank != 0:
         return
     from oracle.bindings import Ref, ref_available
@@ -767,31 +917,44 @@ def run_reference(args, rank, world):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libctdref.so not built"}))
         return
     x = load_c2(0)
-    n_steps = args.steps + args.warmup
-    frac = 1.0 if n_steps <= 6 else max(0.05, 6.0 / n_steps)
-    T1 = max(1, int(round(C2["shape"][2] * frac)))
-    xs = x if T1 >= C2["shape"][2] else x.time_slab(0, T1)
     R = Ref()
-    t = R.tensor(xs.shape, xs.flat_idx(), xs.val)
+    t = R.tensor(x.shape, x.flat_idx(), x.val)
     secs = []
-    for i in range(n_steps):
+    for i in range(args.steps + args.warmup):
         fe = R.frontend(t, C2["mode"], C2["c"], C2["eps"], C2["seed"])
         if i >= args.warmup:
             secs.append(fe.seconds)
     sec = float(np.mean(secs))
-    value = xs.nnz / sec
-    sample = (f"reference ctd_s front end on the first {T1} of 1000 time slices of C2 "
-              f"({xs.nnz} nnz); single-threaded (the reference has no threading)")
+    value = x.nnz / sec
+    sample = ("the full C2 tensor every step: reference ctd_s front end (matricize -> column_distribution "
+              "-> sample_with_replacement -> unique_first_occurrence -> FiberBasis loop); single-threaded "
+              "(the reference has no threading); input SparseTensor built once outside the timer")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "sample_nnz": xs.nnz},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64 generator, SURVEY §8d)",
+        "config": bench_config(1),
+        "result": {"nnz": x.nnz, "kept": int(len(fe.kept_flat)), "unique_sampled": int(len(fe.unique)),
+                   "step_seconds": [round(v, 3) for v in secs]},
         "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": 1, "kind": "reference",
                          "sample": sample, "cpu": _cpu_model()},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def _relaunch(args) -> int:
+    """--gpus N > 1 outside torchrun: re-launch under torch.distributed.run with N
+    ranks on this node, or fail loudly when fewer than N GPUs are visible."""
+    import torch
+    have = torch.cuda.device_count()
+    if args.impl == "ours" and have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} requested but only {have} GPU(s) visible", file=sys.stderr)
+        return 2
+    port = 29500 + (os.getpid() % 1000)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -806,9 +969,14 @@ def main():
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 (planted CP, c=5000) line")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (1e9 nnz) line")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -820,6 +988,10 @@ def main():
             backend = "gloo"
         else:
             backend = "nccl"
+            if torch.cuda.device_count() < world:
+                print(f"bench.py: {world} ranks but only {torch.cuda.device_count()} GPU(s) visible",
+                      file=sys.stderr)
+                sys.exit(2)
         torch.cuda.set_device(local_rank)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.distributed.init_process_group(backend)

@@ -499,12 +499,9 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
                           cudaMemcpyDeviceToDevice, ctx->stream));
   ScatterOut so{cursor.p, tkey.p, tval.p, intok.p, sumsq.p};
   LAUNCH(ctx, k_scatter, grid, 256, 0, c, wbits, rowbits, so, ctx->d_flags);
-  // Oversize buckets need global sort buffers; allocate lazily (rare).
-  // The buffers are sized nnz so every bucket owns its slice.
+  // Oversize buckets need global sort buffers (sized nnz so every bucket owns
+  // its slice), allocated below only when some bucket exceeds the capacity.
   Buf<uint32_t> gkey2, gidx1, gidx2;
-  gkey2.alloc(ctx, nnz);
-  gidx1.alloc(ctx, nnz);
-  gidx2.alloc(ctx, nnz);
   // Shared-memory capacity sized to the largest bucket (more CTAs per SM).
   const unsigned mx = ctx->read1(maxc.p);
   if (htrace) {
@@ -546,6 +543,13 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
   }
   const int threads = cap <= 2048 ? 256 : kSortThreads;
   int presorted = 0;
+  if ((int)mx > cap) {
+    gkey2.alloc(ctx, nnz);  // presorted oversize keys (or the in-kernel sort's second buffer)
+    if (nnz >= (1ll << 32)) {  // the in-kernel global-memory sort of oversize buckets
+      gidx1.alloc(ctx, nnz);
+      gidx2.alloc(ctx, nnz);
+    }
+  }
   if ((int)mx > cap && nnz < (1ll << 32)) {
     // oversize buckets: one device-wide radix sort over all of them
     Buf<unsigned long long> ocnt(ctx, nb), ooff(ctx, nb + 1);
@@ -592,12 +596,11 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
               out.col.p, out.ptr.p, out.norm.p, status.p, ticket.p, nb, nnz, wbits, rowbits,
               dF.p, ctx->d_flags, presorted};
   const size_t smem = (size_t)cap * (4 + 4 + 2 + 2 + 8) + (threads / 32) * kRadix * 4;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_done = 0;
+  if (first_on_device(&attr_done, ctx->device)) {
     const size_t smax = (size_t)kCap * (4 + 4 + 2 + 2 + 8) + (kSortThreads / 32) * kRadix * 4;
     CUDA_OK(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smax));
-    attr_set = true;
   }
   LAUNCH(ctx, k_bucket_sort, (unsigned)nb, threads, smem, sa);
   HT()

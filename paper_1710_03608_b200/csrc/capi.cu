@@ -61,6 +61,16 @@ void need(const void* p, const char* what) {
   if (!p) fail(CTD_ERR_ARGUMENT, std::string(what) + " is NULL");
 }
 
+// Every entry point runs on its context's device, whatever the calling
+// thread's current device is (several contexts on several devices may share
+// one process).
+void bind_device(const Ctx* c) {
+  if (!c) return;
+  int cur = -1;
+  CUDA_OK(cudaGetDevice(&cur));
+  if (cur != c->device) CUDA_OK(cudaSetDevice(c->device));
+}
+
 __global__ void k_narrow(const int64_t* in, long long nnz, int order, int32_t* out, unsigned* flags) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nnz * order) return;
@@ -150,6 +160,7 @@ int ctd_gpu_ctx_create(int device, void* stream, ctd_gpu_ctx** out) {
 int ctd_gpu_ctx_set_stream(ctd_gpu_ctx* ctx, void* stream) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     ctx->c.stream = static_cast<cudaStream_t>(stream);
   });
 }
@@ -157,6 +168,7 @@ int ctd_gpu_ctx_set_stream(ctd_gpu_ctx* ctx, void* stream) {
 int ctd_gpu_ctx_synchronize(ctd_gpu_ctx* ctx) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     ctx->c.sync();
   });
 }
@@ -177,6 +189,7 @@ int64_t ctd_gpu_ctx_launches(const ctd_gpu_ctx* ctx) { return ctx ? ctx->c.launc
 int ctd_gpu_ctx_set_timing(ctd_gpu_ctx* ctx, int enable) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     ctx->c.phase_flush();
     ctx->c.timing = enable != 0;
   });
@@ -185,6 +198,7 @@ int ctd_gpu_ctx_set_timing(ctd_gpu_ctx* ctx, int enable) {
 int ctd_gpu_ctx_phase_times(ctd_gpu_ctx* ctx, double* ms, int64_t* counts, int reset) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     ctx->c.phase_flush();
     for (int i = 0; i < Ctx::kPhases; ++i) {
       if (ms) ms[i] = ctx->c.phase_ms[i];
@@ -206,6 +220,7 @@ int ctd_gpu_tensor_from_host(ctd_gpu_ctx* ctx, int order, const int64_t* shape, 
                              const int64_t* indices, const double* values, ctd_gpu_tensor** out) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     need(out, "out");
     if (order > 0) need(shape, "shape");
     if (nnz < 0) fail(CTD_ERR_SHAPE, "index data does not match entry count");
@@ -242,6 +257,7 @@ int ctd_gpu_tensor_from_device(ctd_gpu_ctx* ctx, int order, const int64_t* shape
                                ctd_gpu_tensor** out) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     need(out, "out");
     if (order > 0) need(shape, "shape");
     if (nnz < 0) fail(CTD_ERR_SHAPE, "index data does not match entry count");
@@ -273,6 +289,7 @@ int ctd_gpu_matricize(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int mode, int64
                       double* sq_norms) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     need(x, "x");
     Ctx* c = &ctx->c;
     Fibers fb;
@@ -291,6 +308,7 @@ int ctd_gpu_column_distribution(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int m
                                 double* total_sq_norm, double* probs, double* cumulative) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     need(x, "x");
     Ctx* c = &ctx->c;
     Law law;
@@ -306,6 +324,7 @@ int ctd_gpu_sample_with_replacement(ctd_gpu_ctx* ctx, const double* probs, int64
                                     uint64_t seed, int64_t* out) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     if (count < 0) fail(CTD_ERR_ARGUMENT, "sample count must be non-negative");  // sampling.cpp:36
     if (count == 0) return;
     need(out, "out");
@@ -326,6 +345,7 @@ int ctd_gpu_sample_with_replacement(ctd_gpu_ctx* ctx, const double* probs, int64
 int ctd_gpu_seq_cumsum(ctd_gpu_ctx* ctx, const double* x, int64_t n, double* out) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     if (n <= 0) return;
     need(x, "x");
     need(out, "out");
@@ -342,6 +362,7 @@ int ctd_gpu_unique_first_occurrence(ctd_gpu_ctx* ctx, const int64_t* drawn, int6
                                     int64_t* n_out) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     need(n_out, "n_out");
     *n_out = 0;
     if (n <= 0) return;
@@ -363,6 +384,7 @@ int ctd_gpu_ctd_s(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int mode, int64_t s
                   uint64_t seed, unsigned flags, ctd_gpu_factors** out) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     need(x, "x");
     need(out, "out");
     auto h = std::make_unique<ctd_gpu_factors>();
@@ -375,6 +397,7 @@ int ctd_gpu_ctd_s(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int mode, int64_t s
 int ctd_gpu_factors_info_get(const ctd_gpu_factors* f, ctd_gpu_factors_info* info) {
   return guarded([&] {
     need(f, "factors");
+    bind_device(f->f.ctx);
     need(info, "info");
     const Factors& F = f->f;
     std::memset(info, 0, sizeof(*info));
@@ -401,6 +424,7 @@ int ctd_gpu_factors_info_get(const ctd_gpu_factors* f, ctd_gpu_factors_info* inf
 int ctd_gpu_factors_kept_flat(const ctd_gpu_factors* f, int64_t* out) {
   return guarded([&] {
     need(f, "factors");
+    bind_device(f->f.ctx);
     need(out, "out");
     std::memcpy(out, f->f.kept_flat.data(), f->f.kept_flat.size() * sizeof(int64_t));
   });
@@ -409,6 +433,7 @@ int ctd_gpu_factors_kept_flat(const ctd_gpu_factors* f, int64_t* out) {
 int ctd_gpu_factors_r(const ctd_gpu_factors* f, int64_t* col_ptr, int64_t* rows, double* vals) {
   return guarded([&] {
     need(f, "factors");
+    bind_device(f->f.ctx);
     basis_r(*f->f.basis, col_ptr, rows, vals);
   });
 }
@@ -416,6 +441,7 @@ int ctd_gpu_factors_r(const ctd_gpu_factors* f, int64_t* col_ptr, int64_t* rows,
 int ctd_gpu_factors_u(const ctd_gpu_factors* f, double* u) {
   return guarded([&] {
     need(f, "factors");
+    bind_device(f->f.ctx);
     need(u, "u");
     basis_u(*f->f.basis, u);
   });
@@ -425,6 +451,7 @@ int ctd_gpu_factors_core(const ctd_gpu_factors* f, int64_t* c_cols, int64_t* col
                          int64_t* rows, double* vals) {
   return guarded([&] {
     need(f, "factors");
+    bind_device(f->f.ctx);
     const Factors& F = f->f;
     if (!F.has_core) fail(CTD_ERR_ARGUMENT, "factors were computed without CTD_GPU_WITH_CORE");
     const Core& c = F.core;
@@ -446,6 +473,7 @@ int ctd_gpu_factors_trace(const ctd_gpu_factors* f, int64_t* drawn, int64_t* uni
                           int32_t* degenerate, double* delta) {
   return guarded([&] {
     need(f, "factors");
+    bind_device(f->f.ctx);
     const Factors& F = f->f;
     if (drawn) std::memcpy(drawn, F.drawn.data(), F.drawn.size() * sizeof(int64_t));
     if (unique) std::memcpy(unique, F.unique.data(), F.unique.size() * sizeof(int64_t));
@@ -462,8 +490,10 @@ int ctd_gpu_factors_destroy(ctd_gpu_factors* f) {
 int ctd_gpu_relative_error(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, ctd_gpu_factors* f, double* out) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     need(x, "x");
     need(f, "factors");
+    bind_device(f->f.ctx);
     need(out, "out");
     Factors& F = f->f;
     if (x->t.order != F.order) fail(CTD_ERR_SHAPE, "factor shape does not match the tensor");
@@ -487,6 +517,7 @@ int ctd_gpu_memory_usage(const ctd_gpu_tensor* x, const ctd_gpu_factors* f, doub
   return guarded([&] {
     need(x, "x");
     need(f, "factors");
+    bind_device(f->f.ctx);
     need(out, "out");
     if (x->t.nnz == 0) fail(CTD_ERR_METRIC, "memory usage undefined for an empty tensor");  // evaluation.cpp:125-126
     const Factors& F = f->f;
@@ -505,6 +536,7 @@ int ctd_gpu_memory_usage(const ctd_gpu_tensor* x, const ctd_gpu_factors* f, doub
 int ctd_gpu_basis_create(ctd_gpu_ctx* ctx, int64_t dim, ctd_gpu_basis** out) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     need(out, "out");
     if (dim < 0) fail(CTD_ERR_ARGUMENT, "basis dimension must be non-negative");
     auto h = std::make_unique<ctd_gpu_basis>();
@@ -525,6 +557,7 @@ int ctd_gpu_basis_try_append(ctd_gpu_basis* b, int64_t dim, int64_t nnz, const i
                              double epsilon, int32_t* accepted, int32_t* degenerate, double* delta, double* y) {
   return guarded([&] {
     need(b, "basis");
+    bind_device(b->ctx);
     Basis& B = *b->b;
     Ctx* c = b->ctx;
     if (dim != B.dim) fail(CTD_ERR_SHAPE, "fiber length does not match basis");  // fiber_basis.cpp:45
@@ -566,6 +599,7 @@ int ctd_gpu_sample_fibers(ctd_gpu_ctx* ctx, int64_t n_fibers, const int64_t* fib
                           int64_t* n_unique) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     need(unique, "unique");
     need(n_unique, "n_unique");
     if (sample_size < 1) fail(CTD_ERR_ARGUMENT, "sample size must be at least 1");  // sampling.cpp:36
@@ -609,6 +643,7 @@ int ctd_gpu_basis_append_batch(ctd_gpu_basis* b, int64_t n, const int64_t* cand_
                                double* delta) {
   return guarded([&] {
     need(b, "basis");
+    bind_device(b->ctx);
     if (n < 0) fail(CTD_ERR_ARGUMENT, "negative candidate count");
     if (n == 0) return;
     need(cand_ptr, "cand_ptr");
@@ -663,6 +698,7 @@ int64_t ctd_gpu_basis_r_nnz(const ctd_gpu_basis* b) { return b ? b->b->rnnz : -1
 int ctd_gpu_basis_r(const ctd_gpu_basis* b, int64_t* col_ptr, int64_t* rows, double* vals) {
   return guarded([&] {
     need(b, "basis");
+    bind_device(b->ctx);
     need(col_ptr, "col_ptr");
     basis_r(*b->b, col_ptr, rows, vals);
   });
@@ -672,7 +708,9 @@ int ctd_gpu_basis_error_partials(ctd_gpu_ctx* ctx, const ctd_gpu_basis* b, const
                                  double* x_sq, double* cross) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     need(b, "basis");
+    bind_device(b->ctx);
     need(x, "x");
     need(x_sq, "x_sq");
     need(cross, "cross");
@@ -707,6 +745,7 @@ __global__ void k_gather_fibers(const int64_t* src, const int64_t* dst, const in
 int ctd_gpu_shard_create(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int mode, ctd_gpu_shard** out) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     need(x, "x");
     need(out, "out");
     if (mode < 0 || mode >= x->t.order) fail(CTD_ERR_ARGUMENT, "mode out of range");
@@ -732,6 +771,7 @@ int64_t ctd_gpu_shard_n_fibers(const ctd_gpu_shard* s) { return s ? s->fb.F : -1
 int ctd_gpu_shard_fibers(const ctd_gpu_shard* s, int64_t* fiber_col, double* sq_norms) {
   return guarded([&] {
     need(s, "shard");
+    bind_device(s->ctx);
     const int64_t F = s->fb.F;
     if (fiber_col && F) std::memcpy(fiber_col, s->col.data(), F * sizeof(int64_t));
     if (sq_norms && F) {
@@ -745,6 +785,7 @@ int ctd_gpu_shard_gather(const ctd_gpu_shard* s, int64_t n, const int64_t* cols,
                          int64_t* rows, double* vals) {
   return guarded([&] {
     need(s, "shard");
+    bind_device(s->ctx);
     need(cand_ptr, "cand_ptr");
     if (n < 0) fail(CTD_ERR_ARGUMENT, "negative count");
     std::vector<int64_t> src(n), len(n);
@@ -776,7 +817,9 @@ int ctd_gpu_shard_gather(const ctd_gpu_shard* s, int64_t n, const int64_t* cols,
 int ctd_gpu_shard_error_partials(const ctd_gpu_shard* s, const ctd_gpu_basis* b, double* x_sq, double* cross) {
   return guarded([&] {
     need(s, "shard");
+    bind_device(s->ctx);
     need(b, "basis");
+    bind_device(b->ctx);
     need(x_sq, "x_sq");
     need(cross, "cross");
     if (s->fb.rows != b->b->dim) fail(CTD_ERR_SHAPE, "fiber length does not match basis");
@@ -792,6 +835,7 @@ int ctd_gpu_shard_destroy(ctd_gpu_shard* s) {
 int ctd_gpu_basis_u(const ctd_gpu_basis* b, double* u) {
   return guarded([&] {
     need(b, "basis");
+    bind_device(b->ctx);
     need(u, "u");
     basis_u(*b->b, u);
   });
@@ -801,6 +845,7 @@ int ctd_gpu_stream_init(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* historical, int 
                         double epsilon, uint64_t seed, unsigned flags, ctd_gpu_stream** out) {
   return guarded([&] {
     need(ctx, "ctx");
+    bind_device(&ctx->c);
     need(historical, "historical");
     need(out, "out");
     auto h = std::make_unique<ctd_gpu_stream>();
@@ -812,6 +857,7 @@ int ctd_gpu_stream_init(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* historical, int 
 int ctd_gpu_stream_step(ctd_gpu_stream* s, const ctd_gpu_tensor* slab, int64_t sample_size) {
   return guarded([&] {
     need(s, "stream");
+    bind_device(s->s.ctx);
     need(slab, "slab");
     stream_step(s->s, slab->t, sample_size);
   });
@@ -822,6 +868,7 @@ int64_t ctd_gpu_stream_t(const ctd_gpu_stream* s) { return s ? s->s.t : -1; }
 int ctd_gpu_stream_factors(ctd_gpu_stream* s, ctd_gpu_factors** out) {
   return guarded([&] {
     need(s, "stream");
+    bind_device(s->s.ctx);
     need(out, "out");
     // Snapshot: kept ids and a copy of the basis (R, U).
     auto h = std::make_unique<ctd_gpu_factors>();
@@ -898,6 +945,7 @@ int ctd_gpu_stream_factors(ctd_gpu_stream* s, ctd_gpu_factors** out) {
 int ctd_gpu_stream_core_drift(ctd_gpu_stream* s, double* out) {
   return guarded([&] {
     need(s, "stream");
+    bind_device(s->s.ctx);
     need(out, "out");
     *out = stream_core_drift(s->s);
   });

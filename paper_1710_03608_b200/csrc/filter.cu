@@ -235,9 +235,17 @@ struct FArgs {
   unsigned* sflag;   // [grid] slice-summary epoch flags
   double* W;         // optional [dim][Wld] orthonormal panel R T (error pass), column k written at accept k
   long long Wld;
+  // resumable segments (speculative rejection batches, spec.cu)
+  int n_begin;       // first candidate of this launch
+  int Kstart;        // basis size at n_begin
+  long long rnnz_start;
+  int prev_n0;       // last exactly processed candidate before n_begin (a rejection), or -1
+  int exit_run;      // return after this many consecutive rejections (0: never)
+  int* next_out;     // first unprocessed candidate (n_u when done)
 };
 
 constexpr int kTraceW = 32;  // clock64 slots per candidate
+constexpr int kSpecRun = 8;  // consecutive rejections that hand over to the batch certifier
 __device__ __forceinline__ void stamp(long long* tr, int n, int k) {
   if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[(long long)n * kTraceW + k] = clock64();
 }
@@ -423,11 +431,9 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   ctx->zero(ctx->d_bar, 2 * sizeof(unsigned));
   int per_sm = 0;
   const size_t dsmem = kFilterSmem;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_done = 0;
+  if (first_on_device(&attr_done, ctx->device))
     CUDA_OK(cudaFuncSetAttribute(k_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
-    attr = true;
-  }
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter, kFThreads, dsmem));
   if (per_sm < 1) fail(CTD_ERR_DEVICE, "filter kernel cannot be resident");
   unsigned grid = (unsigned)ctx->sm_count;  // one CTA per SM
@@ -436,11 +442,52 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
     if (gv > 0 && gv < (int)grid) grid = (unsigned)gv;
   }
   void* args[] = {&fa};
+  // Exact kernel segments; after kSpecRun consecutive rejections the kernel
+  // returns and the following candidates are certified in batches
+  // (spec.cu) until one needs the exact path again.
+  Buf<int> dnext(ctx, 1);
+  fa.next_out = dnext.p;
+  fa.n_begin = 0;
+  fa.Kstart = (int)K0;
+  fa.rnnz_start = B.rnnz;
+  fa.prev_n0 = -1;
+  static const bool no_spec = getenv("CTD_NO_SPEC") != nullptr;
+  fa.exit_run = (!no_spec && !want_y && n > kSpecRun) ? kSpecRun : 0;
+  int64_t spec_b = 256;
   ctx->phase_end();
   ctx->phase_begin(PH_FILTER);
-  CUDA_OK(cudaLaunchCooperativeKernel((const void*)k_filter, dim3(grid), dim3(kFThreads), args, dsmem,
-                                      ctx->stream));
-  ctx->launches++;
+  for (;;) {
+    CUDA_OK(cudaLaunchCooperativeKernel((const void*)k_filter, dim3(grid), dim3(kFThreads), args, dsmem,
+                                        ctx->stream));
+    ctx->launches++;
+    if (!fa.exit_run) break;
+    int nx = 0;
+    long long kk = 0, rr = 0;
+    ctx->to_host(&nx, dnext.p, 1);
+    ctx->to_host(&kk, fK.p, 1);
+    ctx->to_host(&rr, fR.p, 1);
+    ctx->sync();
+    if (nx >= n) break;
+    int64_t pos = nx;
+    for (;;) {
+      const int64_t L = spec_certify(B, c, xsq.p, Gb.p, Gc.p, kept.p, K0, kk, pos, spec_b, eps, acc.p, deg.p, dl.p,
+                                     res.p);
+      out.n_spec += L;
+      pos += L;
+      if (pos >= n) break;
+      if (L < spec_b) {
+        spec_b = std::max<int64_t>(64, spec_b / 2);
+        break;
+      }
+      spec_b = std::min<int64_t>(spec_b * 2, 4096);
+    }
+    if (pos >= n) break;
+    fa.n_begin = (int)pos;
+    fa.Kstart = (int)kk;
+    fa.rnnz_start = rr;
+    fa.prev_n0 = nx - 1;
+    ctx->zero(ctx->d_bar, 2 * sizeof(unsigned));
+  }
   ctx->phase_end();
   // ---- results
   out.accepted.resize(n);

@@ -70,11 +70,20 @@ struct BatchOut {
   std::vector<int32_t> kept_cand;  // candidates accepted, in order
   std::vector<double> y_last;      // y of the last candidate (U R^T x)
   bool slow_path = false;
+  int64_t n_spec = 0;              // rejections certified in batches (spec.cu)
 };
 
 // Runs the reference filter loop (ctd_static.cpp:40-44) over all candidates
 // in order against the basis, appending the accepted ones.
 void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want_y);
+
+// Speculative rejection batches (spec.cu): evaluates candidates [pos, pos+b)
+// against the current basis (K columns; Gram tables Gb [K0][n], Gc [n][n],
+// kept_cand[k - K0] the candidate behind basis column k) and returns how many
+// leading ones are certified rejections, writing their outcomes.
+int64_t spec_certify(Basis& B, const Cands& c, const double* xsq, const double* Gb, const double* Gc,
+                     const int* kept_cand, int64_t K0, int64_t K, int64_t pos, int64_t b, double eps, int32_t* acc,
+                     int32_t* deg, double* dl, double* res_out);
 
 // Host copies of the basis.
 void basis_u(const Basis& B, double* u /* K*K row-major */);

@@ -180,13 +180,20 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
   const int lane = threadIdx.x & 31;
   const long long LD = a.LD;
   const int nu = a.n_u;
-  int K = a.K0;
-  long long rnnz = a.rnnz0;
+  // A launch resumes at candidate n_begin with the basis state a previous
+  // segment left (K, rnnz; the last exactly processed candidate prev_n0, a
+  // rejection, whose rows in W's column K are cleared below) and, with
+  // exit_run > 0, returns after exit_run consecutive rejections so the host
+  // can certify the following candidates in a batch (spec.cu).
+  int K = a.Kstart;
+  long long rnnz = a.rnnz_start;
   bool prev_acc = false;
   double prev_delta = 0.0;
-  int prev_n = -1;
+  int prev_n = a.prev_n0;
+  int run = 0;
+  int next = nu;
   bool pre = false;  // candidate n's setup (tags, z half, g and y staging) done during P3 of n-1
-  for (int n = 0; n <= nu; ++n) {
+  for (int n = a.n_begin; n <= nu; ++n) {
     const bool last = (n == nu);
     if (!last) stamp(a.trace, n, 0);
     const bool upd = prev_acc;
@@ -793,9 +800,16 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     prev_delta = res;
     prev_n = n;
     stamp(a.trace, n, 9);
+    // every CTA took the same decision, so they all leave together
+    run = reject ? run + 1 : 0;
+    if (a.exit_run > 0 && run >= a.exit_run && n + 1 < nu) {
+      next = n + 1;
+      break;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *a.final_K = K;
     *a.final_rnnz = rnnz;
+    if (a.next_out) *a.next_out = next;
   }
 }

@@ -34,7 +34,7 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 // K-slices of 16 double-buffered through shared memory.  blockIdx.z selects
 // a split of the reduction range; with `partial` the raw sums go to
 // C + z*M*N (ldc = N) for k_reduce_splits.
-template <bool TA>
+template <bool TA, bool ABS>
 __global__ void __launch_bounds__(128) k_gemm(long long M, long long N, long long Kr, const double* __restrict__ A,
                                               long long lda, const double* __restrict__ B, long long ldb,
                                               double* __restrict__ C, long long ldc, long long kchunk, double alpha,
@@ -65,6 +65,10 @@ __global__ void __launch_bounds__(128) k_gemm(long long M, long long N, long lon
       }
       const long long gk = k0 + (e >> 6), gn = n0 + (e & 63);
       rb[i] = (gk < kend && gn < N) ? B[gk * ldb + gn] : 0.0;
+      if (ABS) {
+        ra[i] = fabs(ra[i]);
+        rb[i] = fabs(rb[i]);
+      }
     }
   };
   auto store = [&](int buf) {
@@ -200,7 +204,8 @@ __global__ void k_copy_panel(const double* src, double* dst, long long n, long l
 }  // namespace
 
 void gemm_f64(Ctx* ctx, bool trans_a, int64_t M, int64_t N, int64_t Kr, const double* A, int64_t lda,
-              const double* B, int64_t ldb, double* C, int64_t ldc, double alpha, double beta, double gamma) {
+              const double* B, int64_t ldb, double* C, int64_t ldc, double alpha, double beta, double gamma,
+              bool abs_operands) {
   if (M <= 0 || N <= 0) return;
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int64_t want = (int64_t)ctx->sm_count * 4;
@@ -221,12 +226,19 @@ void gemm_f64(Ctx* ctx, bool trans_a, int64_t M, int64_t N, int64_t Kr, const do
     out = part.p;
     ldo = N;
   }
-  if (trans_a)
-    LAUNCH(ctx, k_gemm<true>, grid, 128, 0, (long long)M, (long long)N, (long long)Kr, A, (long long)lda, B,
-           (long long)ldb, out, ldo, (long long)kchunk, alpha, beta, gamma, splits > 1 ? 1 : 0);
+  const int is_part = splits > 1 ? 1 : 0;
+  if (trans_a && !abs_operands)
+    LAUNCH(ctx, (k_gemm<true, false>), grid, 128, 0, (long long)M, (long long)N, (long long)Kr, A, (long long)lda, B,
+           (long long)ldb, out, ldo, (long long)kchunk, alpha, beta, gamma, is_part);
+  else if (trans_a)
+    LAUNCH(ctx, (k_gemm<true, true>), grid, 128, 0, (long long)M, (long long)N, (long long)Kr, A, (long long)lda, B,
+           (long long)ldb, out, ldo, (long long)kchunk, alpha, beta, gamma, is_part);
+  else if (!abs_operands)
+    LAUNCH(ctx, (k_gemm<false, false>), grid, 128, 0, (long long)M, (long long)N, (long long)Kr, A, (long long)lda,
+           B, (long long)ldb, out, ldo, (long long)kchunk, alpha, beta, gamma, is_part);
   else
-    LAUNCH(ctx, k_gemm<false>, grid, 128, 0, (long long)M, (long long)N, (long long)Kr, A, (long long)lda, B,
-           (long long)ldb, out, ldo, (long long)kchunk, alpha, beta, gamma, splits > 1 ? 1 : 0);
+    LAUNCH(ctx, (k_gemm<false, true>), grid, 128, 0, (long long)M, (long long)N, (long long)Kr, A, (long long)lda,
+           B, (long long)ldb, out, ldo, (long long)kchunk, alpha, beta, gamma, is_part);
   if (splits > 1)
     LAUNCH(ctx, k_reduce_splits, ceil_div((uint64_t)M * N, 256), 256, 0, part.p, (int)splits, (long long)M,
            (long long)N, C, (long long)ldc, alpha, beta, gamma);

@@ -8,9 +8,11 @@ namespace ctdgpu {
 // B is row-major [Kr x N] (ldb).  trans_a: A is stored [Kr x M] (lda) and
 // op(A) = A^T (the Gram / SYRK shape, reduction over the long dimension);
 // otherwise A is row-major [M x Kr].  C is row-major (ldc).  Deterministic:
-// split-K partials are reduced in a fixed order.
+// split-K partials are reduced in a fixed order.  abs_operands: |op(A)| |B|
+// (the magnitudes rounding-error bounds are built from).
 void gemm_f64(Ctx* ctx, bool trans_a, int64_t M, int64_t N, int64_t Kr, const double* A, int64_t lda,
-              const double* B, int64_t ldb, double* C, int64_t ldc, double alpha, double beta, double gamma);
+              const double* B, int64_t ldb, double* C, int64_t ldc, double alpha, double beta, double gamma,
+              bool abs_operands = false);
 
 // Orthonormalizes the columns of A (n x K, row-major, lda) in place: A <- A
 // (A^T A)^(-1/2), the polar factor, by the Newton-Schulz iteration with the

@@ -24,5 +24,5 @@ def test_phase_bytes():
     pb = bench.phase_bytes(nnz=100, F=10, kept_seq=acc, r_lens=np.array([3, 4]))
     assert pb["matricize"] == 32 * 100 + 24 * 10
     assert pb["law"] == 24 * 10
-    # cand 0: K=0 -> 0 + accept 16*1; cand 1: K=1 -> 8 + 12*3; cand 2: K=1 -> 8 + 36 + accept 16*4
-    assert pb["filter"] == 16 + (8 + 36) + (8 + 36 + 64)
+    # cand 0: K=0 -> 0 + accept 8*1; cand 1: K=1 -> 8 + 12*3; cand 2: K=1 -> 8 + 36 + accept 8*4
+    assert pb["filter"] == 8 + (8 + 36) + (8 + 36 + 32)
