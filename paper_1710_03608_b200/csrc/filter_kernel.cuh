@@ -231,16 +231,27 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
       const long long poff = a.c.off[prev_n];
       const int pm = a.c.len[prev_n];
       int srn = ldg_cg(a.sr_n);
-      for (int base = 0; base < pm; base += blockDim.x) {
-        const int t = base + threadIdx.x;
-        const int r = t < pm ? a.c.row[poff + t] : 0;
-        const int isnew = (t < pm) && (ldg_cg(&a.sr_pos[r]) < 0);
-        int tot2;
-        const int pos = block_excl_sum<int>(isnew, shi, &tot2);
-        if (isnew) {
-          a.sr_list[srn + pos] = r;
-          a.sr_pos[r] = srn + pos;
+      // 4 consecutive entries per thread per block scan (C5 fibers hold
+      // 1e4-1e5 entries; this CTA's append is what the others wait for)
+      for (int base = 0; base < pm; base += 4 * blockDim.x) {
+        const int t0 = base + 4 * threadIdx.x;
+        int rr[4], nw[4], cnt = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + u;
+          rr[u] = t < pm ? a.c.row[poff + t] : 0;
+          nw[u] = (t < pm) && (ldg_cg(&a.sr_pos[rr[u]]) < 0);
+          cnt += nw[u];
         }
+        int tot2;
+        int pos = block_excl_sum<int>(cnt, shi, &tot2);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (nw[u]) {
+            a.sr_list[srn + pos] = rr[u];
+            a.sr_pos[rr[u]] = srn + pos;
+            ++pos;
+          }
         srn += tot2;
       }
       if (threadIdx.x == 0) {

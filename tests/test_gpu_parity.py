@@ -350,3 +350,4 @@ def test_filter_global_operand_path():
     r = subprocess.run([sys.executable, "-c", _KVEC_SCRIPT.format(root=root)], env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
