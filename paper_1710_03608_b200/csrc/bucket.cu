@@ -419,7 +419,10 @@ int bits_for(long long n) {  // bits needed to represent 0..n-1
 
 }  // namespace
 
-void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
+// The general path: any entry order (bucket scatter + per-bucket radix sort
+// by (column, row)).  matricize() uses it when the input's rows are not
+// ascending inside its columns (onesweep.cu needs that order).
+static void matricize_sort(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
   static const bool htrace = getenv("CTD_HOST_TRACE") != nullptr;
   std::chrono::steady_clock::time_point ht[8];
   int nht = 0;
@@ -623,6 +626,16 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
     fprintf(stderr, " ms\n");
   }
 #undef HT
+}
+
+void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
+  if (mode < 0 || mode >= x.order)
+    fail(CTD_ERR_ARGUMENT, "mode " + std::to_string(mode) + " out of range for order " +
+                               std::to_string(x.order));
+  static const bool legacy = getenv("CTD_BUCKET_LEGACY") != nullptr;  // A/B hook
+  if (!legacy && matricize_onesweep(ctx, x, mode, out)) return;
+  out = Fibers{};
+  matricize_sort(ctx, x, mode, out);
 }
 
 }  // namespace ctdgpu

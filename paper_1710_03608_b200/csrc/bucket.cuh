@@ -23,6 +23,12 @@ struct Fibers {
   double sum_sq = 0.0;         // sum of v^2 (any order; exact when integer_exact)
 };
 
+// Dispatches to matricize_onesweep (the stable LSD partition, for inputs
+// whose rows ascend inside every column, i.e. any normalized SparseTensor)
+// and falls back to the general bucket sort otherwise.
 void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out);
+// Returns false (nothing usable in out) when the input's rows do not ascend
+// inside a column; raises the usual input errors otherwise.
+bool matricize_onesweep(Ctx* ctx, const Tensor& x, int mode, Fibers& out);
 
 }  // namespace ctdgpu

@@ -116,6 +116,13 @@ __global__ void k_copy_rows(const long long* oldbase, const long long* newbase, 
   }
 }
 
+// W[:, col] = 0 (the panel's scratch column before a new batch: the last
+// candidate of the previous batch may have left its residual there)
+__global__ void k_zero_col(double* W, long long ld, long long dim, long long col) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < dim) W[r * ld + col] = 0.0;
+}
+
 __global__ void k_copy_u(const double* src, long long ld_src, double* dst, long long ld_dst, long long k) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= k * k) return;
@@ -363,6 +370,8 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   if (B.Wok) {
     fa.W = B.W.p;
     fa.Wld = B.LD;
+    if (K0 > 0) LAUNCH(ctx, k_zero_col, ceil_div((uint64_t)B.dim, 256), 256, 0, B.W.p, (long long)B.LD, (long long)B.dim,
+                       (long long)K0);
   }
   fa.c = c;
   fa.xsq = xsq.p;

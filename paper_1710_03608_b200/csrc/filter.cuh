@@ -45,10 +45,13 @@ struct Basis {
   // Q: orthonormal basis of span(R) for the error pass (relerr.cu,
   // ortho_panel), cached for basis size Qk; Newton-Schulz iterations and the
   // starting defect |A^T A - I|_F of the last build
+  // (Qcompl: the panel is (I - R U R^T)^T instead, Qcols = dim, for a basis
+  // whose R U R^T is no projector; Sdefect = |Q^T R U R^T Q - I|_F)
   mutable Buf<double> Q;
-  mutable int64_t Qk = -1, Qld = 0;
+  mutable int64_t Qk = -1, Qld = 0, Qcols = 0;
   mutable int Qiters = 0;
-  mutable double Qdefect = 0.0;
+  mutable double Qdefect = 0.0, Sdefect = 0.0;
+  mutable bool Qcompl = false;
 
   Basis(Ctx* c, int64_t d);
   // Copy R's host CSC and U (resume ctor, fiber_basis.cpp:13-19).

@@ -1,0 +1,491 @@
+// COO -> mode-alpha fiber bucketing for a normalized (lexicographically
+// sorted) SparseTensor: the HBM-bound form of matricize (tensor_ops.cpp:
+// 118-135) + the SparseMatrix COO constructor (sparse_matrix.cpp:22-67) +
+// column_sq_norms (tensor_ops.cpp:194-202).
+//
+// In a lexicographically sorted COO every mode-alpha column (all other
+// coordinates fixed) already lists its rows in ascending order, so the
+// reference's (col, row) order is a STABLE sort by the column id j alone.
+// That is an LSD radix sort of 32-bit keys with (row, value) payload, done as
+// single-pass "onesweep" partitions of <= 9 bits each (C5: 27 bits, 3 passes;
+// C2: 24 bits, 3; C4: 17 bits, 2):
+//   k_os_hist   one read of the COO: the digit histograms of every pass, plus
+//               the input checks (bounds, stored zeros, integrality, sum v^2)
+//   k_os_pass   per 4096-entry tile: stable rank of every entry among equal
+//               digits (warp match + per-warp counters), the tile's digit
+//               counts published and prefixed across tiles by a decoupled
+//               look-back, the tile reordered by digit in shared memory and
+//               written out in contiguous per-digit runs
+//   k_os_heads* fiber heads (j changes) -> fiber ids and offsets; rows must
+//               strictly ascend inside a column (duplicates -> ArgumentError;
+//               an unsorted input falls back to the general bucket sort)
+//   k_os_norms  each fiber's squared norm summed in ascending-row order, a
+//               thread per fiber; long fibers through the exact parallel
+//               sequential sum (seqsum.cuh): bit-identical to the reference.
+// Traffic per entry: 12 B (histogram) + 20 B read / 16 B write (first pass) +
+// 32 B per further pass + 12 B (heads/norms), no atomics on the data path and
+// no partial-sector scatter (bucket.cu's atomic scatter moved 3.3x its bytes).
+#include <cstdlib>
+#include <vector>
+
+#include "bucket.cuh"
+#include "seqsum.cuh"
+
+namespace ctdgpu {
+
+namespace {
+
+constexpr int kOsThreads = 512;
+constexpr int kOsItems = 8;
+constexpr int kOsTile = kOsThreads * kOsItems;  // entries per tile
+constexpr int kOsWarps = kOsThreads / 32;
+constexpr int kOsMaxBits = 9;
+constexpr int kOsMaxPass = 4;
+constexpr int kOsHeadsPer = 1024;  // entries per block in the heads kernels
+constexpr int kOsLong = 1024;      // fibers longer than this: block-wide exact norm
+
+struct Coo {
+  int order, mode;
+  long long nnz;
+  const int32_t* idx[kMaxOrder];
+  const double* val;
+  long long stride[kMaxOrder];
+  long long shape[kMaxOrder];
+};
+
+__device__ __forceinline__ uint32_t coo_col(const Coo& c, long long i, int* row, bool* oob) {
+  unsigned long long j = 0;
+  bool bad = false;
+  int r = 0;
+  for (int k = 0; k < c.order; ++k) {
+    const long long v = c.idx[k][i];
+    bad |= (v < 0) | (v >= c.shape[k]);
+    if (k == c.mode) r = (int)v;
+    else j += (unsigned long long)v * (unsigned long long)c.stride[k];
+  }
+  *row = r;
+  *oob = bad;
+  return (uint32_t)j;
+}
+
+__global__ void k_os_hist(Coo c, int npass, int dbits, unsigned long long* hist, unsigned* flags, int* intok,
+                          double* sumsq) {
+  __shared__ unsigned sh[kOsMaxPass << kOsMaxBits];
+  const int bins = 1 << dbits;
+  for (int t = threadIdx.x; t < npass * bins; t += blockDim.x) sh[t] = 0u;
+  __syncthreads();
+  double sq = 0.0;
+  bool iok = true, oobf = false, zf = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < c.nnz;
+       i += (long long)gridDim.x * blockDim.x) {
+    int row;
+    bool oob;
+    const uint32_t j = coo_col(c, i, &row, &oob);
+    const double v = c.val[i];
+    oobf |= oob;
+    zf |= (v == 0.0);
+    iok &= (v == rint(v)) && (fabs(v) <= 67108864.0);
+    sq += v * v;
+    for (int p = 0; p < npass; ++p) atomicAdd(&sh[p * bins + ((j >> (p * dbits)) & (bins - 1))], 1u);
+  }
+  sq = warp_sum(sq);
+  const bool all_ok = __all_sync(0xffffffffu, iok);
+  const bool any_oob = __any_sync(0xffffffffu, oobf), any_zero = __any_sync(0xffffffffu, zf);
+  if ((threadIdx.x & 31) == 0) {
+    if (sq != 0.0) atomicAdd(sumsq, sq);
+    if (!all_ok) atomicExch(intok, 0);
+    if (any_oob) atomicOr(flags, FLAG_BOUNDS);
+    if (any_zero) atomicOr(flags, FLAG_ZERO);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < npass * bins; t += blockDim.x)
+    if (sh[t]) atomicAdd(&hist[t], (unsigned long long)sh[t]);
+}
+
+// Exclusive scan of every pass's histogram (one block).
+__global__ void k_os_scan_hist(const unsigned long long* hist, int npass, int bins, unsigned long long* base) {
+  __shared__ unsigned long long sh[33];
+  for (int p = 0; p < npass; ++p) {
+    const unsigned long long v = threadIdx.x < bins ? hist[p * bins + threadIdx.x] : 0ull;
+    const unsigned long long e = block_excl_sum<unsigned long long>(v, sh, nullptr);
+    if (threadIdx.x < bins) base[p * bins + threadIdx.x] = e;
+  }
+}
+
+struct PassArgs {
+  Coo c;
+  int first;
+  const uint32_t* jin;
+  const int32_t* rin;
+  const double* vin;
+  uint32_t* jout;
+  int32_t* rout;
+  double* vout;
+  long long n;
+  int shift, dbits;
+  const unsigned long long* digit_base;  // [bins] global start of each digit
+  unsigned long long* status;            // [tiles][bins] look-back words
+  unsigned* ticket;
+};
+
+__global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int bins = 1 << a.dbits;
+  double* tv = reinterpret_cast<double*>(smem);                                  // [tile]
+  unsigned long long* gbase = reinterpret_cast<unsigned long long*>(tv + kOsTile);  // [bins]
+  uint32_t* tj = reinterpret_cast<uint32_t*>(gbase + bins);                      // [tile]
+  int32_t* tr = reinterpret_cast<int32_t*>(tj + kOsTile);                        // [tile]
+  unsigned* whist = reinterpret_cast<unsigned*>(tr + kOsTile);                   // [warps][bins]
+  unsigned* doff = whist + kOsWarps * bins;                                      // [bins]
+  __shared__ long long s_tile;
+  __shared__ unsigned sh32[33];
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
+  for (int t = threadIdx.x; t < kOsWarps * bins; t += blockDim.x) whist[t] = 0u;
+  __syncthreads();
+  const long long tile = s_tile;
+  const long long start = tile * kOsTile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned mask = (unsigned)bins - 1u;
+  unsigned* wh = whist + warp * bins;
+  uint32_t jv[kOsItems];
+  int32_t rv[kOsItems];
+  double vv[kOsItems];
+  unsigned lr[kOsItems];
+  // warp w owns the contiguous items [w*256, w*256+256) of the tile, 32 per
+  // round: ranks follow the item order (stable)
+#pragma unroll
+  for (int r = 0; r < kOsItems; ++r) {
+    const long long i = start + (long long)warp * (32 * kOsItems) + r * 32 + lane;
+    const bool act = i < a.n;
+    uint32_t j = 0;
+    int row = 0;
+    double v = 0.0;
+    if (act) {
+      if (a.first) {
+        bool oob;
+        j = coo_col(a.c, i, &row, &oob);
+        v = a.c.val[i];
+      } else {
+        j = a.jin[i];
+        row = a.rin[i];
+        v = a.vin[i];
+      }
+    }
+    jv[r] = j;
+    rv[r] = row;
+    vv[r] = v;
+    const unsigned amask = __ballot_sync(0xffffffffu, act);
+    if (act) {
+      const unsigned d = (j >> a.shift) & mask;
+      const unsigned peers = __match_any_sync(amask, d);
+      const unsigned b0 = wh[d];
+      lr[r] = b0 + __popc(peers & ((1u << lane) - 1u));
+      __syncwarp(amask);
+      if (lane == __ffs(peers) - 1) wh[d] = b0 + __popc(peers);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive offsets of the warps, and the tile's total
+  unsigned tot = 0;
+  if ((int)threadIdx.x < bins) {
+    const int d = threadIdx.x;
+    for (int w = 0; w < kOsWarps; ++w) {
+      const unsigned cnt = whist[w * bins + d];
+      whist[w * bins + d] = tot;
+      tot += cnt;
+    }
+  }
+  const unsigned excl = block_excl_sum<unsigned>(tot, sh32, nullptr);
+  if ((int)threadIdx.x < bins) {
+    const int d = threadIdx.x;
+    doff[d] = excl;
+    // decoupled look-back over the tiles' counts of digit d
+    const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = kAgg - 1ull;
+    unsigned long long* st = a.status + tile * bins + d;
+    if (tile == 0) {
+      atomicExch(st, kInc | (unsigned long long)tot);
+      gbase[d] = a.digit_base[d];
+    } else {
+      atomicExch(st, kAgg | (unsigned long long)tot);
+      unsigned long long prefix = 0;
+      long long i = tile - 1;
+      while (true) {
+        const unsigned long long s = *((volatile unsigned long long*)(a.status + i * bins + d));
+        const unsigned long long f = s >> 62;
+        if (f == 0) {
+          __nanosleep(32);
+          continue;
+        }
+        prefix += s & kVal;
+        if (f == 2) break;
+        --i;
+      }
+      atomicExch(st, kInc | (prefix + tot));
+      gbase[d] = a.digit_base[d] + prefix;
+    }
+  }
+  __syncthreads();
+  // the tile reordered by digit (stable) in shared memory
+#pragma unroll
+  for (int r = 0; r < kOsItems; ++r) {
+    const long long i = start + (long long)warp * (32 * kOsItems) + r * 32 + lane;
+    if (i < a.n) {
+      const unsigned d = (jv[r] >> a.shift) & mask;
+      const unsigned pos = doff[d] + whist[warp * bins + d] + lr[r];
+      tj[pos] = jv[r];
+      tr[pos] = rv[r];
+      tv[pos] = vv[r];
+    }
+  }
+  __syncthreads();
+  // contiguous per-digit runs to global memory
+  const int tn = (int)min((long long)kOsTile, a.n - start);
+  for (int s = threadIdx.x; s < tn; s += blockDim.x) {
+    const uint32_t j = tj[s];
+    const unsigned d = (j >> a.shift) & mask;
+    const unsigned long long gp = gbase[d] + (unsigned long long)(s - (int)doff[d]);
+    a.jout[gp] = j;
+    a.rout[gp] = tr[s];
+    a.vout[gp] = tv[s];
+  }
+}
+
+// Fiber heads: a head where j changes.  Inside a column rows must strictly
+// ascend: equal -> duplicate coordinates, descending -> the input was not
+// lexicographically sorted (the caller falls back to the general sort).
+__device__ __forceinline__ bool os_head(const uint32_t* j, long long p) { return p == 0 || j[p] != j[p - 1]; }
+
+__global__ void k_os_heads_count(const uint32_t* j, const int32_t* row, long long n, unsigned* bcnt, unsigned* flags,
+                                 unsigned* unsorted) {
+  __shared__ unsigned sh[33];
+  const long long b0 = (long long)blockIdx.x * kOsHeadsPer;
+  unsigned c = 0;
+  bool dup = false, bad = false;
+  for (int t = threadIdx.x; t < kOsHeadsPer; t += blockDim.x) {
+    const long long p = b0 + t;
+    if (p >= n) break;
+    if (os_head(j, p)) {
+      ++c;
+    } else {
+      const int r0 = row[p - 1], r1 = row[p];
+      dup |= (r1 == r0);
+      bad |= (r1 < r0);
+    }
+  }
+  unsigned tot;
+  block_excl_sum<unsigned>(c, sh, &tot);
+  if (threadIdx.x == 0) bcnt[blockIdx.x] = tot;
+  if (__any_sync(0xffffffffu, dup) && (threadIdx.x & 31) == 0) atomicOr(flags, FLAG_DUPLICATE);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(unsorted, 1u);
+}
+
+__global__ void k_os_scan_blocks(const unsigned* bcnt, long long nb, unsigned long long* bbase, long long* F_out,
+                                 int64_t* fptr, long long n) {
+  __shared__ unsigned long long sh[33];
+  unsigned long long carry = 0;
+  for (long long b0 = 0; b0 < nb; b0 += blockDim.x) {
+    const long long b = b0 + threadIdx.x;
+    const unsigned long long v = b < nb ? bcnt[b] : 0ull;
+    unsigned long long tot;
+    const unsigned long long e = block_excl_sum<unsigned long long>(v, sh, &tot);
+    if (b < nb) bbase[b] = carry + e;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    *F_out = (long long)carry;
+    fptr[carry] = n;
+  }
+}
+
+__global__ void k_os_heads_write(const uint32_t* j, long long n, const unsigned long long* bbase, int64_t* fcol,
+                                 int64_t* fptr) {
+  __shared__ unsigned sh[33];
+  const long long b0 = (long long)blockIdx.x * kOsHeadsPer;
+  // consecutive entries per thread so the block scan follows entry order
+  constexpr int kPer = kOsHeadsPer / 256;
+  const long long p0 = b0 + (long long)threadIdx.x * kPer;
+  unsigned c = 0;
+  for (int u = 0; u < kPer; ++u)
+    if (p0 + u < n && os_head(j, p0 + u)) ++c;
+  unsigned f = block_excl_sum<unsigned>(c, sh, nullptr);
+  const unsigned long long base = bbase[blockIdx.x];
+  for (int u = 0; u < kPer; ++u) {
+    const long long p = p0 + u;
+    if (p < n && os_head(j, p)) {
+      fcol[base + f] = j[p];
+      fptr[base + f] = p;
+      ++f;
+    }
+  }
+}
+
+// column_sq_norms: s += v*v in ascending row order (tensor_ops.cpp:197-198).
+__global__ void k_os_norms(const int64_t* fptr, const long long* F_in, const double* val, double* norm, int* longl,
+                           int* nlong) {
+  const long long F = *F_in;
+  for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < F; f += (long long)gridDim.x * blockDim.x) {
+    const long long b = fptr[f], e = fptr[f + 1];
+    if (e - b > kOsLong) {
+      longl[atomicAdd(nlong, 1)] = (int)f;
+      continue;
+    }
+    double s = 0.0;
+    long long q = b;
+    for (; q + 4 <= e; q += 4) {
+      const double v0 = val[q], v1 = val[q + 1], v2 = val[q + 2], v3 = val[q + 3];
+      s = dadd(s, dsqr(v0));
+      s = dadd(s, dsqr(v1));
+      s = dadd(s, dsqr(v2));
+      s = dadd(s, dsqr(v3));
+    }
+    for (; q < e; ++q) s = dadd(s, dsqr(val[q]));
+    norm[f] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_os_norms_long(const int64_t* fptr, const int* longl, const int* nlong,
+                                                       const double* val, double* norm, unsigned* flags) {
+  __shared__ SeqSumSmem S;
+  const int nl = *nlong;
+  for (int q = blockIdx.x; q < nl; q += gridDim.x) {
+    const long long f = longl[q];
+    const double* v = val + fptr[f];
+    auto get = [v](long long i) { return dsqr(v[i]); };
+    bool bad = false;
+    const double s = block_exact_sum(get, fptr[f + 1] - fptr[f], S, &bad);
+    if (threadIdx.x == 0) {
+      norm[f] = s;
+      if (bad) atomicOr(flags, FLAG_SEQSUM);
+    }
+    __syncthreads();
+  }
+}
+
+int os_bits_for(unsigned long long n) {
+  int b = 0;
+  while (b < 63 && (1ull << b) < n) ++b;
+  return b;
+}
+
+}  // namespace
+
+bool matricize_onesweep(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
+  Coo c{};
+  c.order = x.order;
+  c.mode = mode;
+  c.nnz = x.nnz;
+  c.val = x.val;
+  long long acc = 1;
+  for (int k = 0; k < x.order; ++k) {  // fiber_strides, tensor_ops.cpp:106-116
+    c.idx[k] = x.idx[k];
+    c.shape[k] = x.shape[k];
+    if (k == mode) {
+      c.stride[k] = 0;
+      continue;
+    }
+    c.stride[k] = acc;
+    acc *= x.shape[k];
+  }
+  const long long nnz = x.nnz;
+  if (acc > (1ll << 32) || nnz >= (1ll << 40) || nnz == 0) return false;
+  out.rows = x.shape[mode];
+  out.cols = acc;
+  out.nnz = nnz;
+  out.mode = mode;
+  const int bits = std::max(1, os_bits_for((unsigned long long)acc));
+  const int npass = (bits + kOsMaxBits - 1) / kOsMaxBits;
+  const int dbits = (bits + npass - 1) / npass;
+  const int bins = 1 << dbits;
+  // validation, histograms
+  Buf<unsigned long long> hist(ctx, (size_t)npass * bins), dbase(ctx, (size_t)npass * bins);
+  hist.zero();
+  Buf<int> intok(ctx, 1);
+  Buf<double> sumsq(ctx, 1);
+  sumsq.zero();
+  {
+    const int one = 1;
+    ctx->to_dev(intok.p, &one, 1);
+  }
+  const unsigned hgrid = (unsigned)std::min<long long>((nnz + 255) / 256, (long long)ctx->sm_count * 8);
+  LAUNCH(ctx, k_os_hist, hgrid, 256, 0, c, npass, dbits, hist.p, ctx->d_flags, intok.p, sumsq.p);
+  LAUNCH(ctx, k_os_scan_hist, 1, 512, 0, hist.p, npass, bins, dbase.p);
+  // LSD passes: ping-pong, the last one into the output arrays
+  out.row.alloc(ctx, nnz);
+  out.val.alloc(ctx, nnz);
+  Buf<uint32_t> ja(ctx, nnz), jb(ctx, npass > 1 ? nnz : 1);
+  Buf<int32_t> ra(ctx, npass > 1 ? nnz : 1);
+  Buf<double> va(ctx, npass > 1 ? nnz : 1);
+  const long long tiles = (nnz + kOsTile - 1) / kOsTile;
+  Buf<unsigned long long> status(ctx, (size_t)tiles * bins);
+  Buf<unsigned> ticket(ctx, 1);
+  const size_t smem = (size_t)kOsTile * (8 + 4 + 4) + (size_t)bins * 8 + (size_t)(kOsWarps + 1) * bins * 4;
+  static unsigned long long attr_done = 0;
+  if (first_on_device(&attr_done, ctx->device)) {
+    const size_t smax = (size_t)kOsTile * 16 + ((size_t)1 << kOsMaxBits) * (8 + (kOsWarps + 1) * 4);
+    CUDA_OK(cudaFuncSetAttribute(k_os_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+  }
+  for (int p = 0; p < npass; ++p) {
+    // pass p reads the previous pass's output; the destinations alternate so
+    // that the last pass lands in (jfinal, out.row, out.val)
+    const bool last = p == npass - 1;
+    PassArgs pa{};
+    pa.c = c;
+    pa.first = p == 0;
+    const bool to_a = ((npass - 1 - p) & 1) == 0;  // last pass -> the "a"/output side
+    uint32_t* jdst = to_a ? ja.p : jb.p;
+    const uint32_t* jsrc = to_a ? jb.p : ja.p;
+    pa.jin = jsrc;
+    pa.rin = to_a ? ra.p : out.row.p;
+    pa.vin = to_a ? va.p : out.val.p;
+    pa.jout = jdst;
+    pa.rout = to_a ? out.row.p : ra.p;
+    pa.vout = to_a ? out.val.p : va.p;
+    (void)last;
+    pa.n = nnz;
+    pa.shift = p * dbits;
+    pa.dbits = dbits;
+    pa.digit_base = dbase.p + (size_t)p * bins;
+    pa.status = status.p;
+    pa.ticket = ticket.p;
+    status.zero();
+    ticket.zero();
+    LAUNCH(ctx, k_os_pass, (unsigned)tiles, kOsThreads, smem, pa);
+  }
+  // fibers: heads, offsets, norms
+  const uint32_t* jf = ja.p;
+  const long long hb = (nnz + kOsHeadsPer - 1) / kOsHeadsPer;
+  Buf<unsigned> bcnt(ctx, hb), uns(ctx, 1);
+  Buf<unsigned long long> bbase(ctx, hb);
+  uns.zero();
+  Buf<long long> dF(ctx, 1);
+  out.col.alloc(ctx, nnz + 1);
+  out.ptr.alloc(ctx, nnz + 1);
+  out.norm.alloc(ctx, nnz + 1);
+  LAUNCH(ctx, k_os_heads_count, (unsigned)hb, 256, 0, jf, out.row.p, nnz, bcnt.p, ctx->d_flags, uns.p);
+  LAUNCH(ctx, k_os_scan_blocks, 1, 1024, 0, bcnt.p, hb, bbase.p, dF.p, out.ptr.p, nnz);
+  LAUNCH(ctx, k_os_heads_write, (unsigned)hb, 256, 0, jf, nnz, bbase.p, out.col.p, out.ptr.p);
+  Buf<int> longl(ctx, nnz / kOsLong + 2), nlong(ctx, 1);
+  nlong.zero();
+  const unsigned ngrid = (unsigned)std::min<long long>((nnz + 255) / 256, (long long)ctx->sm_count * 16);
+  LAUNCH(ctx, k_os_norms, ngrid, 256, 0, out.ptr.p, dF.p, out.val.p, out.norm.p, longl.p, nlong.p);
+  LAUNCH(ctx, k_os_norms_long, (unsigned)ctx->sm_count * 4, 256, 0, out.ptr.p, longl.p, nlong.p, out.val.p,
+         out.norm.p, ctx->d_flags);
+  long long F = 0;
+  int iok = 0;
+  double ssq = 0.0;
+  unsigned unsorted = 0;
+  ctx->to_host(&F, dF.p, 1);
+  ctx->to_host(&iok, intok.p, 1);
+  ctx->to_host(&ssq, sumsq.p, 1);
+  ctx->to_host(&unsorted, uns.p, 1);
+  ctx->sync();
+  if (unsorted) return false;  // rows not ascending inside a column: general sort
+  out.F = F;
+  out.sum_sq = ssq;
+  out.integer_exact = iok && ssq < 4503599627370496.0;  // 2^52
+  ctx->check_flags("matricize");
+  return true;
+}
+
+}  // namespace ctdgpu

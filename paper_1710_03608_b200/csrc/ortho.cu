@@ -17,6 +17,8 @@
 #include "ortho.cuh"
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 namespace ctdgpu {
 
@@ -244,6 +246,17 @@ void gemm_f64(Ctx* ctx, bool trans_a, int64_t M, int64_t N, int64_t Kr, const do
            (long long)N, C, (long long)ldc, alpha, beta, gamma);
 }
 
+double frob_defect(Ctx* ctx, const double* H, int64_t K) {
+  const unsigned nb = (unsigned)std::min<int64_t>(ctx->sm_count * 2, ceil_div((uint64_t)K * K, 256));
+  Buf<double> dp(ctx, 2 * (size_t)nb), dv(ctx, 2);
+  LAUNCH(ctx, k_defect, nb, 256, 0, H, (long long)K, dp.p);
+  LAUNCH(ctx, k_defect_final, 1, 256, 0, dp.p, (int)nb, dv.p);
+  double hv[2];
+  ctx->to_host(hv, dv.p, 2);
+  ctx->sync();
+  return std::sqrt(hv[0]);
+}
+
 int orthonormalize(Ctx* ctx, double* A, int64_t n, int64_t K, int64_t lda, double* defect, int max_iter) {
   *defect = 0.0;
   if (K == 0 || n == 0) return 0;
@@ -260,6 +273,9 @@ int orthonormalize(Ctx* ctx, double* A, int64_t n, int64_t K, int64_t lda, doubl
     ctx->to_host(hv, dv.p, 2);
     ctx->sync();
     const double e = std::sqrt(hv[0]);
+    static const bool trace = getenv("CTD_ORTHO_TRACE") != nullptr;
+    if (trace) fprintf(stderr, "[ortho] n=%lld K=%lld it=%d |A^T A - I|_F=%.3e |A^T A|_F=%.3e\n", (long long)n,
+                       (long long)K, it, e, std::sqrt(hv[1]));
     if (!std::isfinite(e)) fail(CTD_ERR_NUMERIC, "orthonormalize: non-finite Gram matrix");
     if (!scaled && e > 0.5) {
       // |A|_2^2 <= |A^T A|_F: scale so every singular value is <= 1, where

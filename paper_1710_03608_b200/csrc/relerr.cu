@@ -136,6 +136,34 @@ __global__ void k_dense_r_unit(const int64_t* rptr, const int32_t* rrow, const d
     A[(long long)rrow[t] * lda + k] = rval[t] * inv;
 }
 
+// Dense copies of R: Rd[r][k] (row-major dim x K) and Rt[k][r] (K x dim),
+// both zeroed beforehand; one CTA per kept column.
+__global__ void k_dense_r2(const int64_t* rptr, const int32_t* rrow, const double* rval, long long K, double* Rd,
+                           long long ldd, double* Rt, long long ldt) {
+  const long long k = blockIdx.x;
+  if (k >= K) return;
+  for (long long t = rptr[k] + threadIdx.x; t < rptr[k + 1]; t += blockDim.x) {
+    const long long r = rrow[t];
+    if (Rd) Rd[r * ldd + k] = rval[t];
+    if (Rt) Rt[k * ldt + r] = rval[t];
+  }
+}
+
+__global__ void k_transpose(const double* A, long long rows, long long cols, long long lda, double* At,
+                            long long ldt) {
+  __shared__ double tile[32][33];
+  const long long r0 = (long long)blockIdx.y * 32, c0 = (long long)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const long long r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? A[r * lda + c] : 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const long long c = c0 + i, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) At[c * ldt + r] = tile[threadIdx.x][i];
+  }
+}
+
 // Qt[c][r] = (R U)[r][c] (dense_product, evaluation.cpp:32-43), column-major
 // so that threads over rows read it coalesced.
 __global__ void k_rut(const int64_t* rowbase, const int32_t* rowlen, const int32_t* rek, const double* rev,
@@ -233,26 +261,87 @@ double relative_error(Ctx* ctx, const Fibers& fb, const Basis& B) {
   return (hx - hcd) / hx;
 }
 
+namespace {
+
+constexpr long long kComplMaxDim = 16384;  // the dense complement I - R U R^T up to this I_alpha
+constexpr double kSDefectMax = 1e-6;       // |Q^T R U R^T Q - I|_F above this: U is no inverse Gram of R
+
+void transpose(Ctx* ctx, const double* A, long long rows, long long cols, long long lda, double* At, long long ldt) {
+  LAUNCH(ctx, k_transpose, dim3(ceil_div(cols, 32), ceil_div(rows, 32)), dim3(32, 8), 0, A, rows, cols, lda, At, ldt);
+}
+
+// |S - I|_F with S = Q^T R U R^T Q: how far R U R^T is from the projector
+// onto span(R) (the neglected term of the orthonormal pass is <= its square).
+double s_defect(Ctx* ctx, const Basis& B, const double* Q, int64_t ldq) {
+  const int64_t K = B.K, dim = B.dim;
+  Buf<double> Rd(ctx, (size_t)dim * K), Bm(ctx, (size_t)K * K), BmT(ctx, (size_t)K * K), T2(ctx, (size_t)K * K),
+      S(ctx, (size_t)K * K);
+  Rd.zero();
+  LAUNCH(ctx, k_dense_r2, (unsigned)K, 128, 0, B.rptr.p, B.rrow.p, B.rval.p, (long long)K, Rd.p, (long long)K,
+         (double*)nullptr, 0ll);
+  gemm_f64(ctx, true, K, K, dim, Q, ldq, Rd.p, K, Bm.p, K, 1.0, 0.0, 0.0);     // Q^T R
+  gemm_f64(ctx, false, K, K, K, Bm.p, K, B.U.p, B.LD, T2.p, K, 1.0, 0.0, 0.0);  // (Q^T R) U
+  transpose(ctx, Bm.p, K, K, K, BmT.p, K);
+  gemm_f64(ctx, false, K, K, K, T2.p, K, BmT.p, K, S.p, K, 1.0, 0.0, 0.0);      // ... R^T Q
+  return frob_defect(ctx, S.p, K);
+}
+
+// The sweep panel P = (I - R U R^T)^T (dim x dim): sum_j |P^T x_j|^2 is the
+// error numerator itself, the reference's expression (evaluation.cpp:113-119)
+// summed in another order -- for bases whose R U R^T is not a projector
+// (more kept fibers than I_alpha, or R beyond fp64's reach).
+void build_complement(Ctx* ctx, const Basis& B) {
+  const int64_t K = B.K, dim = B.dim;
+  if (dim > kComplMaxDim)
+    fail(CTD_ERR_NUMERIC, "relative_error: R U R^T is not a projector and I_alpha is too large for the dense pass");
+  Buf<double> Rt(ctx, (size_t)K * dim), T(ctx, (size_t)dim * K), Cm(ctx, (size_t)dim * dim);
+  Rt.zero();
+  LAUNCH(ctx, k_dense_r2, (unsigned)K, 128, 0, B.rptr.p, B.rrow.p, B.rval.p, (long long)K, (double*)nullptr, 0ll,
+         Rt.p, (long long)dim);
+  gemm_f64(ctx, true, dim, K, K, Rt.p, dim, B.U.p, B.LD, T.p, K, 1.0, 0.0, 0.0);  // R U
+  gemm_f64(ctx, false, dim, dim, K, T.p, K, Rt.p, dim, Cm.p, dim, -1.0, 0.0, 1.0);  // I - R U R^T
+  B.Q.alloc(ctx, (size_t)dim * dim);
+  transpose(ctx, Cm.p, dim, dim, dim, B.Q.p, dim);
+  B.Qld = dim;
+  B.Qcols = dim;
+  B.Qcompl = true;
+}
+
+}  // namespace
+
 const double* ortho_panel(Ctx* ctx, const Basis& B, int64_t* ldq) {
   const int64_t K = B.K, dim = B.dim;
   if (B.Q.p && B.Qk == K) {
     *ldq = B.Qld;
     return B.Q.p;
   }
-  const int64_t ld = (K + 1) & ~int64_t(1);
-  B.Q.alloc(ctx, (size_t)dim * ld);
-  if (B.Wok) {
-    LAUNCH(ctx, k_panel_from_w, ceil_div((uint64_t)dim * K, 256), 256, 0, B.W.p, B.Wsc.p, (long long)B.LD,
-           (long long)dim, (long long)K, B.Q.p, (long long)ld);
-  } else {
-    B.Q.zero();
-    LAUNCH(ctx, k_dense_r_unit, (unsigned)K, 128, 0, B.rptr.p, B.rrow.p, B.rval.p, (long long)K, B.Q.p,
-           (long long)ld);
+  B.Qcompl = false;
+  bool compl_ = K > dim;
+  if (!compl_) {
+    const int64_t ld = (K + 1) & ~int64_t(1);
+    B.Q.alloc(ctx, (size_t)dim * ld);
+    if (B.Wok) {
+      LAUNCH(ctx, k_panel_from_w, ceil_div((uint64_t)dim * K, 256), 256, 0, B.W.p, B.Wsc.p, (long long)B.LD,
+             (long long)dim, (long long)K, B.Q.p, (long long)ld);
+    } else {
+      B.Q.zero();
+      LAUNCH(ctx, k_dense_r_unit, (unsigned)K, 128, 0, B.rptr.p, B.rrow.p, B.rval.p, (long long)K, B.Q.p,
+             (long long)ld);
+    }
+    try {
+      B.Qiters = orthonormalize(ctx, B.Q.p, dim, K, ld, &B.Qdefect);
+      B.Sdefect = s_defect(ctx, B, B.Q.p, ld);
+      compl_ = !(B.Sdefect <= kSDefectMax);
+    } catch (const Fail& f) {
+      if (f.code != CTD_ERR_NUMERIC) throw;
+      compl_ = true;  // rank-deficient to fp64: R U R^T is no projector either
+    }
+    B.Qld = ld;
+    B.Qcols = K;
   }
-  B.Qiters = orthonormalize(ctx, B.Q.p, dim, K, ld, &B.Qdefect);
+  if (compl_) build_complement(ctx, B);
   B.Qk = K;
-  B.Qld = ld;
-  *ldq = ld;
+  *ldq = B.Qld;
   return B.Q.p;
 }
 
@@ -268,20 +357,24 @@ void error_partials(Ctx* ctx, const Fibers& fb, const Basis& B, double* x_sq, do
     *cross = 0.0;
     return;
   }
-  // sum_j |Q^T x_j|^2, Q orthonormal with span(Q) = span(R)
+  // sum_j |Q^T x_j|^2, Q orthonormal with span(Q) = span(R) (or, for a basis
+  // whose R U R^T is no projector, the residual energy itself)
   int64_t ldq = 0;
   const double* Q = ortho_panel(ctx, B, &ldq);
+  const long long nc = B.Qcols;
   const unsigned cgrid = (unsigned)ctx->sm_count * 8;
   const long long nwarps = (long long)cgrid * 256 / 32;
   Buf<double> rho(ctx, dim + 1), sp1(ctx, sgrid + nwarps);
-  LAUNCH(ctx, k_row_weight, ceil_div((uint64_t)dim * 32, 256), 256, 0, Q, (long long)ldq, K, dim, rho.p);
+  LAUNCH(ctx, k_row_weight, ceil_div((uint64_t)dim * 32, 256), 256, 0, Q, (long long)ldq, nc, dim, rho.p);
   LAUNCH(ctx, k_single_fibers, sgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, rho.p, sp1.p);
-  LAUNCH(ctx, k_cdw, cgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, Q, (long long)ldq, K,
+  LAUNCH(ctx, k_cdw, cgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, Q, (long long)ldq, nc,
          sp1.p + sgrid);
   LAUNCH(ctx, k_reduce, 1, 1024, 0, sp1.p, (long long)sgrid + nwarps, cd.p);
+  double s = 0.0;
   ctx->to_host(x_sq, xsq.p, 1);
-  ctx->to_host(cross, cd.p, 1);
+  ctx->to_host(&s, cd.p, 1);
   ctx->sync();
+  *cross = B.Qcompl ? *x_sq - s : s;
 }
 
 }  // namespace ctdgpu
