@@ -19,9 +19,10 @@
 //   k_os_heads* fiber heads (j changes) -> fiber ids and offsets; rows must
 //               strictly ascend inside a column (duplicates -> ArgumentError;
 //               an unsorted input falls back to the general bucket sort)
-//   k_os_norms  each fiber's squared norm summed in ascending-row order, a
-//               thread per fiber; long fibers through the exact parallel
-//               sequential sum (seqsum.cuh): bit-identical to the reference.
+//   norms       each fiber's squared norm summed in ascending-row order: a
+//               thread per fiber (<= 32 entries), a warp (<= 1024), or the
+//               block-wide exact sequential sum (seqsum.cuh): bit-identical
+//               to the reference.
 // Traffic per entry: 12 B (histogram) + 20 B read / 16 B write (first pass) +
 // 32 B per further pass + 12 B (heads/norms), no atomics on the data path and
 // no partial-sector scatter (bucket.cu's atomic scatter moved 3.3x its bytes).
@@ -42,6 +43,7 @@ constexpr int kOsWarps = kOsThreads / 32;
 constexpr int kOsMaxBits = 9;
 constexpr int kOsMaxPass = 4;
 constexpr int kOsHeadsPer = 1024;  // entries per block in the heads kernels
+constexpr int kOsShort = 32;       // fibers up to this long: norm summed by one thread
 constexpr int kOsLong = 1024;      // fibers longer than this: block-wide exact norm
 
 struct Coo {
@@ -114,7 +116,7 @@ __global__ void k_os_scan_hist(const unsigned long long* hist, int npass, int bi
 
 struct PassArgs {
   Coo c;
-  int first;
+  int first, last;
   const uint32_t* jin;
   const int32_t* rin;
   const double* vin;
@@ -148,36 +150,43 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
   const unsigned mask = (unsigned)bins - 1u;
   unsigned* wh = whist + warp * bins;
   uint32_t jv[kOsItems];
-  int32_t rv[kOsItems];
-  double vv[kOsItems];
+  int32_t rv[kOsItems];  // first pass: the row comes with j from the COO
   unsigned lr[kOsItems];
   // warp w owns the contiguous items [w*256, w*256+256) of the tile, 32 per
-  // round: ranks follow the item order (stable)
+  // round: ranks follow the item order (stable).  Only the keys are loaded
+  // now (all rounds in flight together); rows and values are read in the
+  // scatter below, which keeps the item state in registers (no spills).
 #pragma unroll
   for (int r = 0; r < kOsItems; ++r) {
     const long long i = start + (long long)warp * (32 * kOsItems) + r * 32 + lane;
-    const bool act = i < a.n;
     uint32_t j = 0;
     int row = 0;
-    double v = 0.0;
-    if (act) {
+    if (i < a.n) {
       if (a.first) {
         bool oob;
         j = coo_col(a.c, i, &row, &oob);
-        v = a.c.val[i];
       } else {
-        j = a.jin[i];
-        row = a.rin[i];
-        v = a.vin[i];
+        j = __ldcs(a.jin + i);
       }
     }
     jv[r] = j;
     rv[r] = row;
-    vv[r] = v;
+  }
+#pragma unroll
+  for (int r = 0; r < kOsItems; ++r) {
+    const long long i = start + (long long)warp * (32 * kOsItems) + r * 32 + lane;
+    const bool act = i < a.n;
     const unsigned amask = __ballot_sync(0xffffffffu, act);
     if (act) {
-      const unsigned d = (j >> a.shift) & mask;
-      const unsigned peers = __match_any_sync(amask, d);
+      const unsigned d = (jv[r] >> a.shift) & mask;
+      // lanes with the same digit: one ballot per digit bit (cheaper than
+      // MATCH.ANY on this part)
+      unsigned peers = amask;
+      for (int b = 0; b < a.dbits; ++b) {
+        const unsigned bit = (d >> b) & 1u;
+        const unsigned bal = __ballot_sync(amask, bit);
+        peers &= bit ? bal : ~bal;
+      }
       const unsigned b0 = wh[d];
       lr[r] = b0 + __popc(peers & ((1u << lane) - 1u));
       __syncwarp(amask);
@@ -208,18 +217,30 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
       gbase[d] = a.digit_base[d];
     } else {
       atomicExch(st, kAgg | (unsigned long long)tot);
+      // walk back 8 tiles per round trip (independent loads): a wave of
+      // resident tiles otherwise serializes on one load latency per tile
       unsigned long long prefix = 0;
       long long i = tile - 1;
-      while (true) {
-        const unsigned long long s = *((volatile unsigned long long*)(a.status + i * bins + d));
-        const unsigned long long f = s >> 62;
-        if (f == 0) {
-          __nanosleep(32);
-          continue;
+      bool done = false;
+      while (!done) {
+        unsigned long long w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          w[k] = (i - k >= 0) ? *((volatile unsigned long long*)(a.status + (i - k) * bins + d)) : kInc;
+        int k = 0;
+        for (; k < 8; ++k) {
+          const unsigned long long f = w[k] >> 62;
+          if (f == 0) break;  // not published yet: re-read from this tile
+          prefix += w[k] & kVal;
+          if (f == 2) {
+            done = true;
+            break;
+          }
         }
-        prefix += s & kVal;
-        if (f == 2) break;
-        --i;
+        if (!done) {
+          i -= k;
+          if (k < 8) __nanosleep(32);
+        }
       }
       atomicExch(st, kInc | (prefix + tot));
       gbase[d] = a.digit_base[d] + prefix;
@@ -234,8 +255,8 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
       const unsigned d = (jv[r] >> a.shift) & mask;
       const unsigned pos = doff[d] + whist[warp * bins + d] + lr[r];
       tj[pos] = jv[r];
-      tr[pos] = rv[r];
-      tv[pos] = vv[r];
+      tr[pos] = a.first ? rv[r] : __ldcs(a.rin + i);
+      tv[pos] = a.first ? a.c.val[i] : __ldcs(a.vin + i);
     }
   }
   __syncthreads();
@@ -245,9 +266,15 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
     const uint32_t j = tj[s];
     const unsigned d = (j >> a.shift) & mask;
     const unsigned long long gp = gbase[d] + (unsigned long long)(s - (int)doff[d]);
-    a.jout[gp] = j;
-    a.rout[gp] = tr[s];
-    a.vout[gp] = tv[s];
+    if (a.last) {  // read next by the heads / norms (and, at C2 size, from L2)
+      a.jout[gp] = j;
+      a.rout[gp] = tr[s];
+      a.vout[gp] = tv[s];
+    } else {  // consumed by the next pass only: streaming stores
+      __stcs(a.jout + gp, j);
+      __stcs(a.rout + gp, tr[s]);
+      __stcs(a.vout + gp, tv[s]);
+    }
   }
 }
 
@@ -320,27 +347,50 @@ __global__ void k_os_heads_write(const uint32_t* j, long long n, const unsigned 
   }
 }
 
-// column_sq_norms: s += v*v in ascending row order (tensor_ops.cpp:197-198).
-__global__ void k_os_norms(const int64_t* fptr, const long long* F_in, const double* val, double* norm, int* longl,
-                           int* nlong) {
+// column_sq_norms (tensor_ops.cpp:197-198): each fiber's v^2 summed in
+// ascending row order.  Fibers up to kOsShort entries: a thread each; longer
+// ones are listed for a warp each (k_os_norms_mid) or, beyond kOsLong, the
+// block-wide exact sequential sum (k_os_norms_long).
+__global__ void k_os_norms(const int64_t* fptr, const long long* F_in, const double* val, double* norm, int* midl,
+                           int* nmid) {
   const long long F = *F_in;
   for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < F; f += (long long)gridDim.x * blockDim.x) {
     const long long b = fptr[f], e = fptr[f + 1];
-    if (e - b > kOsLong) {
-      longl[atomicAdd(nlong, 1)] = (int)f;
+    if (e - b > kOsShort) {
+      midl[atomicAdd(nmid, 1)] = (int)f;
       continue;
     }
     double s = 0.0;
-    long long q = b;
-    for (; q + 4 <= e; q += 4) {
-      const double v0 = val[q], v1 = val[q + 1], v2 = val[q + 2], v3 = val[q + 3];
-      s = dadd(s, dsqr(v0));
-      s = dadd(s, dsqr(v1));
-      s = dadd(s, dsqr(v2));
-      s = dadd(s, dsqr(v3));
-    }
-    for (; q < e; ++q) s = dadd(s, dsqr(val[q]));
+    for (long long q = b; q < e; ++q) s = dadd(s, dsqr(val[q]));
     norm[f] = s;
+  }
+}
+
+// A warp per listed fiber: 32 values loaded per round (the next round's in
+// flight), then added in order by every lane through shuffles.
+__global__ void k_os_norms_mid(const int64_t* fptr, const int* list, const int* nlist, const double* val,
+                               double* norm, int* longl, int* nlong) {
+  const int nl = *nlist;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (long long q0 = warp; q0 < nl; q0 += nw) {
+    const long long f = list[q0];
+    const long long b = fptr[f], e = fptr[f + 1];
+    if (e - b > kOsLong) {
+      if (lane == 0) longl[atomicAdd(nlong, 1)] = (int)f;
+      continue;
+    }
+    double s = 0.0;
+    double cur = (b + lane < e) ? val[b + lane] : 0.0;
+    for (long long base = b; base < e; base += 32) {
+      const double nxt = (base + 32 + lane < e) ? val[base + 32 + lane] : 0.0;
+      const double sq = dsqr(cur);
+      const int cnt = (int)min(32ll, e - base);
+      for (int t = 0; t < cnt; ++t) s = dadd(s, __shfl_sync(0xffffffffu, sq, t));
+      cur = nxt;
+    }
+    if (lane == 0) norm[f] = s;
   }
 }
 
@@ -441,7 +491,7 @@ bool matricize_onesweep(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
     pa.jout = jdst;
     pa.rout = to_a ? out.row.p : ra.p;
     pa.vout = to_a ? out.val.p : va.p;
-    (void)last;
+    pa.last = last ? 1 : 0;
     pa.n = nnz;
     pa.shift = p * dbits;
     pa.dbits = dbits;
@@ -465,10 +515,13 @@ bool matricize_onesweep(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
   LAUNCH(ctx, k_os_heads_count, (unsigned)hb, 256, 0, jf, out.row.p, nnz, bcnt.p, ctx->d_flags, uns.p);
   LAUNCH(ctx, k_os_scan_blocks, 1, 1024, 0, bcnt.p, hb, bbase.p, dF.p, out.ptr.p, nnz);
   LAUNCH(ctx, k_os_heads_write, (unsigned)hb, 256, 0, jf, nnz, bbase.p, out.col.p, out.ptr.p);
-  Buf<int> longl(ctx, nnz / kOsLong + 2), nlong(ctx, 1);
+  Buf<int> midl(ctx, nnz / kOsShort + 2), nmid(ctx, 1), longl(ctx, nnz / kOsLong + 2), nlong(ctx, 1);
+  nmid.zero();
   nlong.zero();
   const unsigned ngrid = (unsigned)std::min<long long>((nnz + 255) / 256, (long long)ctx->sm_count * 16);
-  LAUNCH(ctx, k_os_norms, ngrid, 256, 0, out.ptr.p, dF.p, out.val.p, out.norm.p, longl.p, nlong.p);
+  LAUNCH(ctx, k_os_norms, ngrid, 256, 0, out.ptr.p, dF.p, out.val.p, out.norm.p, midl.p, nmid.p);
+  LAUNCH(ctx, k_os_norms_mid, (unsigned)ctx->sm_count * 8, 256, 0, out.ptr.p, midl.p, nmid.p, out.val.p, out.norm.p,
+         longl.p, nlong.p);
   LAUNCH(ctx, k_os_norms_long, (unsigned)ctx->sm_count * 4, 256, 0, out.ptr.p, longl.p, nlong.p, out.val.p,
          out.norm.p, ctx->d_flags);
   long long F = 0;
