@@ -143,6 +143,7 @@ class Port:
             [C.POINTER(f64)] * 4
         L.cto_relerr_dd_full.argtypes = [C.POINTER(_CscStruct), C.POINTER(_CscStruct), v] + \
             [C.POINTER(f64)] * 3
+        L.cto_filter_par.argtypes = [i64, i64, v, v, v, f64, v, v, v, C.POINTER(i64), v]
         L.cto_stream_init.argtypes = [i32, v, i64, v, v, i32, i64, f64, C.c_uint64,
                                       C.POINTER(v)]
         L.cto_stream_step.argtypes = [v, i32, v, i64, v, v, i64]
@@ -278,6 +279,22 @@ class Port:
         self._chk(self.L.cto_relerr_dd_full(C.byref(a), C.byref(b), _p(u), *[C.byref(t) for t in o]),
                   "relerr_dd_full")
         return o[0].value
+
+    def filter_par(self, dim, cand_ptr, rows, vals, eps=1e-6):
+        """The filter loop over candidate fibers (CSC) from an empty basis,
+        multi-threaded, bit-identical to FiberBasis (filter_par.c).  Returns
+        (accepted, degenerate, delta, U)."""
+        cand_ptr, rows, vals = _i64(cand_ptr), _i64(rows), _f64(vals)
+        n = cand_ptr.shape[0] - 1
+        acc = np.zeros(max(n, 1), np.int32)
+        deg = np.zeros(max(n, 1), np.int32)
+        dl = np.zeros(max(n, 1))
+        u = np.zeros(max(n * n, 1))
+        k = C.c_int64()
+        self._chk(self.L.cto_filter_par(dim, n, _p(cand_ptr), _p(rows), _p(vals), eps, _p(acc), _p(deg), _p(dl),
+                                        C.byref(k), _p(u)), "filter_par")
+        K = k.value
+        return acc[:n], deg[:n], dl[:n], u[:K * K].reshape(K, K).copy()
 
     def ctd_s_error(self, shape, idx, val, mode, s, eps=1e-6, seed=42):
         """Front end + compute_core + relative_error (the reference composition)."""

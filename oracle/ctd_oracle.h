@@ -95,6 +95,12 @@ int cto_relerr_dd_direct(const cto_csc *x, const cto_csc *r, const double *u,
 int cto_relerr_dd_full(const cto_csc *x, const cto_csc *r, const double *u, double *out,
                        double *num_hi, double *num_lo);
 
+/* The filter loop (ctd_static.cpp:40-44 over try_append_fiber) from an empty
+ * basis, multi-threaded but bit-identical to cto_basis_try_append
+ * (filter_par.c).  u_out holds n*n doubles; *k_out receives K. */
+int cto_filter_par(int64_t dim, int64_t n, const int64_t *cand_ptr, const int64_t *rows, const double *vals,
+                   double eps, int *accepted, int *degenerate, double *delta, int64_t *k_out, double *u_out);
+
 /* CTD-D (ctd_dynamic.cpp).  The stream keeps R/U (basis), the matricized core
  * and the kept flat ids. */
 typedef struct cto_stream cto_stream;

@@ -46,11 +46,16 @@ struct Basis {
   // ortho_panel), cached for basis size Qk; Newton-Schulz iterations and the
   // starting defect |A^T A - I|_F of the last build
   // (Qcompl: the panel is (I - R U R^T)^T instead, Qcols = dim, for a basis
-  // whose R U R^T is no projector; Sdefect = |Q^T R U R^T Q - I|_F)
+  // whose R U R^T is no projector)
   mutable Buf<double> Q;
   mutable int64_t Qk = -1, Qld = 0, Qcols = 0;
   mutable int Qiters = 0;
-  mutable double Qdefect = 0.0, Sdefect = 0.0;
+  mutable double Qdefect = 0.0;
+  // P = Q E^T: the second-order correction panel of the error pass (relerr.cu
+  // build_correction), kept when |E|_F^2 >= 1e-13
+  mutable Buf<double> P;
+  mutable bool Pok = false;
+  mutable double Enorm = 0.0;
   mutable bool Qcompl = false;
 
   Basis(Ctx* c, int64_t d);

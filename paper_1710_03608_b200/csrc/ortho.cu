@@ -257,6 +257,17 @@ double frob_defect(Ctx* ctx, const double* H, int64_t K) {
   return std::sqrt(hv[0]);
 }
 
+double frob_norm(Ctx* ctx, const double* H, int64_t K) {
+  const unsigned nb = (unsigned)std::min<int64_t>(ctx->sm_count * 2, ceil_div((uint64_t)K * K, 256));
+  Buf<double> dp(ctx, 2 * (size_t)nb), dv(ctx, 2);
+  LAUNCH(ctx, k_defect, nb, 256, 0, H, (long long)K, dp.p);
+  LAUNCH(ctx, k_defect_final, 1, 256, 0, dp.p, (int)nb, dv.p);
+  double hv[2];
+  ctx->to_host(hv, dv.p, 2);
+  ctx->sync();
+  return std::sqrt(hv[1]);
+}
+
 int orthonormalize(Ctx* ctx, double* A, int64_t n, int64_t K, int64_t lda, double* defect, int max_iter) {
   *defect = 0.0;
   if (K == 0 || n == 0) return 0;

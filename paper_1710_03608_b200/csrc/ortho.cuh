@@ -14,8 +14,9 @@ void gemm_f64(Ctx* ctx, bool trans_a, int64_t M, int64_t N, int64_t Kr, const do
               const double* B, int64_t ldb, double* C, int64_t ldc, double alpha, double beta, double gamma,
               bool abs_operands = false);
 
-// |H - I|_F of a K x K matrix.
+// |H - I|_F and |H|_F of a K x K matrix.
 double frob_defect(Ctx* ctx, const double* H, int64_t K);
+double frob_norm(Ctx* ctx, const double* H, int64_t K);
 
 // Orthonormalizes the columns of A (n x K, row-major, lda) in place: A <- A
 // (A^T A)^(-1/2), the polar factor, by the Newton-Schulz iteration with the

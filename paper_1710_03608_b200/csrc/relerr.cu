@@ -14,6 +14,7 @@
 #include "relerr.cuh"
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "ortho.cuh"
@@ -164,6 +165,51 @@ __global__ void k_transpose(const double* A, long long rows, long long cols, lon
   }
 }
 
+// Z = A B - I in double-double (A, B: K x K, row-major, lda / ldb), rounded
+// to fp64.  A = G = R^T R is exact for integer data and B = U is exact, so
+// Z = U's backward error G U - I comes out to ~1e-32 cond(G) where fp64
+// would lose it to cancellation.  16 x 16 tiles through shared memory.
+__device__ __forceinline__ void dd_add(double& hi, double& lo, double a, double b) {
+  // (hi, lo) += (a, b) with the error-free sum of the high parts
+  const double s = hi + a;
+  const double bb = s - hi;
+  const double e = (hi - (s - bb)) + (a - bb);
+  const double t = lo + b + e;
+  hi = s + t;
+  lo = t - (hi - s);
+}
+__global__ void k_dd_gemm_mi(const double* A, long long lda, const double* B, long long ldb, long long K, double* Z) {
+  __shared__ double As[16][17], Bs[16][17];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const long long row = (long long)blockIdx.y * 16 + ty, col = (long long)blockIdx.x * 16 + tx;
+  double hi = 0.0, lo = 0.0;
+  for (long long k0 = 0; k0 < K; k0 += 16) {
+    As[ty][tx] = (row < K && k0 + tx < K) ? A[row * lda + k0 + tx] : 0.0;
+    Bs[ty][tx] = (k0 + ty < K && col < K) ? B[(k0 + ty) * ldb + col] : 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const double a = As[ty][t], b = Bs[t][tx];
+      const double p = a * b;
+      const double e = __fma_rn(a, b, -p);  // exact product error
+      dd_add(hi, lo, p, e);
+    }
+    __syncthreads();
+  }
+  if (row < K && col < K) {
+    if (row == col) dd_add(hi, lo, -1.0, 0.0);
+    Z[row * K + col] = hi + lo;
+  }
+}
+
+// Y = alpha Z + beta I (K x K).
+__global__ void k_axpi(const double* Z, long long K, double alpha, double beta, double* Y) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K * K) return;
+  const long long r = t / K, c = t - r * K;
+  Y[t] = alpha * Z[t] + ((r == c) ? beta : 0.0);
+}
+
 // Qt[c][r] = (R U)[r][c] (dense_product, evaluation.cpp:32-43), column-major
 // so that threads over rows read it coalesced.
 __global__ void k_rut(const int64_t* rowbase, const int32_t* rowlen, const int32_t* rek, const double* rev,
@@ -264,36 +310,20 @@ double relative_error(Ctx* ctx, const Fibers& fb, const Basis& B) {
 namespace {
 
 constexpr long long kComplMaxDim = 16384;  // the dense complement I - R U R^T up to this I_alpha
-constexpr double kSDefectMax = 1e-6;       // |Q^T R U R^T Q - I|_F above this: U is no inverse Gram of R
 
 void transpose(Ctx* ctx, const double* A, long long rows, long long cols, long long lda, double* At, long long ldt) {
   LAUNCH(ctx, k_transpose, dim3(ceil_div(cols, 32), ceil_div(rows, 32)), dim3(32, 8), 0, A, rows, cols, lda, At, ldt);
 }
 
-// |S - I|_F with S = Q^T R U R^T Q: how far R U R^T is from the projector
-// onto span(R) (the neglected term of the orthonormal pass is <= its square).
-double s_defect(Ctx* ctx, const Basis& B, const double* Q, int64_t ldq) {
-  const int64_t K = B.K, dim = B.dim;
-  Buf<double> Rd(ctx, (size_t)dim * K), Bm(ctx, (size_t)K * K), BmT(ctx, (size_t)K * K), T2(ctx, (size_t)K * K),
-      S(ctx, (size_t)K * K);
-  Rd.zero();
-  LAUNCH(ctx, k_dense_r2, (unsigned)K, 128, 0, B.rptr.p, B.rrow.p, B.rval.p, (long long)K, Rd.p, (long long)K,
-         (double*)nullptr, 0ll);
-  gemm_f64(ctx, true, K, K, dim, Q, ldq, Rd.p, K, Bm.p, K, 1.0, 0.0, 0.0);     // Q^T R
-  gemm_f64(ctx, false, K, K, K, Bm.p, K, B.U.p, B.LD, T2.p, K, 1.0, 0.0, 0.0);  // (Q^T R) U
-  transpose(ctx, Bm.p, K, K, K, BmT.p, K);
-  gemm_f64(ctx, false, K, K, K, T2.p, K, BmT.p, K, S.p, K, 1.0, 0.0, 0.0);      // ... R^T Q
-  return frob_defect(ctx, S.p, K);
-}
-
 // The sweep panel P = (I - R U R^T)^T (dim x dim): sum_j |P^T x_j|^2 is the
 // error numerator itself, the reference's expression (evaluation.cpp:113-119)
 // summed in another order -- for bases whose R U R^T is not a projector
-// (more kept fibers than I_alpha, or R beyond fp64's reach).
+// (more kept fibers than I_alpha, or R rank-deficient to fp64, where the
+// polar iteration cannot converge).
 void build_complement(Ctx* ctx, const Basis& B) {
   const int64_t K = B.K, dim = B.dim;
   if (dim > kComplMaxDim)
-    fail(CTD_ERR_NUMERIC, "relative_error: R U R^T is not a projector and I_alpha is too large for the dense pass");
+    fail(CTD_ERR_NUMERIC, "relative_error: R is rank-deficient and I_alpha is too large for the dense pass");
   Buf<double> Rt(ctx, (size_t)K * dim), T(ctx, (size_t)dim * K), Cm(ctx, (size_t)dim * dim);
   Rt.zero();
   LAUNCH(ctx, k_dense_r2, (unsigned)K, 128, 0, B.rptr.p, B.rrow.p, B.rval.p, (long long)K, (double*)nullptr, 0ll,
@@ -305,6 +335,77 @@ void build_complement(Ctx* ctx, const Basis& B) {
   B.Qld = dim;
   B.Qcols = dim;
   B.Qcompl = true;
+}
+
+}  // namespace
+
+namespace {
+
+// The second-order term of the orthonormal pass (ortho.cu): with
+// Delta = U - G^-1 and B = Q^T R, the error numerator is
+//   |X|^2 - sum_j |Q^T x_j|^2 + sum_j |E Q^T x_j|^2,   E = B Delta B^T,
+// exactly.  Delta is U's backward error: U Z (I + Z)^-1 with Z = G U - I in
+// double-double (k_dd_gemm_mi).  When |E|_F^2 is below 1e-13 the
+// term is below that bound relative to |X|^2 and is skipped (C2, C4); at C5
+// (heavy overlapping fibers, cond(G) ~ 1e10) it is ~1e-9 and the panel
+// P = Q E^T is swept like Q.
+void build_correction(Ctx* ctx, const Basis& B) {
+  const int64_t K = B.K, dim = B.dim;
+  const int64_t ldq = B.Qld;
+  B.Pok = false;
+  Buf<double> Rd(ctx, (size_t)dim * K), G(ctx, (size_t)K * K), Z(ctx, (size_t)K * K), D(ctx, (size_t)K * K),
+      Bm(ctx, (size_t)K * K), BmT(ctx, (size_t)K * K), T1(ctx, (size_t)K * K), E(ctx, (size_t)K * K);
+  Rd.zero();
+  LAUNCH(ctx, k_dense_r2, (unsigned)K, 128, 0, B.rptr.p, B.rrow.p, B.rval.p, (long long)K, Rd.p, (long long)K,
+         (double*)nullptr, 0ll);
+  gemm_f64(ctx, true, K, K, dim, Rd.p, K, Rd.p, K, G.p, K, 1.0, 0.0, 0.0);          // G = R^T R
+  LAUNCH(ctx, k_dd_gemm_mi, dim3(ceil_div(K, 16), ceil_div(K, 16)), dim3(16, 16), 0, G.p, (long long)K, B.U.p,
+         (long long)B.LD, (long long)K, Z.p);                                       // Z = G U - I
+  // Delta = U - G^-1 = U Z (I + Z)^-1 (G^-1 = U (G U)^-1): the inverse by
+  // Newton's iteration Y <- 2Y - Y (I + Z) Y from Y = I - Z (quadratic;
+  // |Z| ~ 0.2 at C5, where the first-order U Z leaves ~10% of the term)
+  {
+    const double zF = frob_norm(ctx, Z.p, K);
+    Buf<double> IZ(ctx, (size_t)K * K), Y(ctx, (size_t)K * K), M(ctx, (size_t)K * K), Y2(ctx, (size_t)K * K);
+    LAUNCH(ctx, k_axpi, ceil_div((uint64_t)K * K, 256), 256, 0, Z.p, (long long)K, 1.0, 1.0, IZ.p);   // I + Z
+    LAUNCH(ctx, k_axpi, ceil_div((uint64_t)K * K, 256), 256, 0, Z.p, (long long)K, -1.0, 1.0, Y.p);   // I - Z
+    bool conv = false;
+    double d = 0.0;
+    for (int it = 0; it < 40; ++it) {
+      gemm_f64(ctx, false, K, K, K, IZ.p, K, Y.p, K, M.p, K, 1.0, 0.0, 0.0);  // (I + Z) Y
+      d = frob_defect(ctx, M.p, K);
+      if (!(d >= 1e-13)) {
+        conv = d == d;
+        break;
+      }
+      if (!(d < 1e6)) break;  // diverging
+      CUDA_OK(cudaMemcpyAsync(Y2.p, Y.p, (size_t)K * K * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+      gemm_f64(ctx, false, K, K, K, Y2.p, K, M.p, K, Y.p, K, -1.0, 2.0, 0.0);  // Y = 2Y - Y M
+    }
+    if (getenv("CTD_ORTHO_TRACE"))
+      fprintf(stderr, "[ortho] |G U - I|_F=%.3e, (I+Z)^-1 Newton %s (defect %.2e)\n", zF,
+              conv ? "converged" : "failed: first order", d);
+    if (conv) {
+      gemm_f64(ctx, false, K, K, K, Z.p, K, Y.p, K, M.p, K, 1.0, 0.0, 0.0);     // Z (I + Z)^-1
+      gemm_f64(ctx, false, K, K, K, B.U.p, B.LD, M.p, K, D.p, K, 1.0, 0.0, 0.0);
+    } else {
+      gemm_f64(ctx, false, K, K, K, B.U.p, B.LD, Z.p, K, D.p, K, 1.0, 0.0, 0.0);  // first order only
+    }
+  }
+  gemm_f64(ctx, true, K, K, dim, B.Q.p, ldq, Rd.p, K, Bm.p, K, 1.0, 0.0, 0.0);      // B = Q^T R
+  gemm_f64(ctx, false, K, K, K, Bm.p, K, D.p, K, T1.p, K, 1.0, 0.0, 0.0);
+  transpose(ctx, Bm.p, K, K, K, BmT.p, K);
+  gemm_f64(ctx, false, K, K, K, T1.p, K, BmT.p, K, E.p, K, 1.0, 0.0, 0.0);         // E = B Delta B^T
+  const double eF = frob_norm(ctx, E.p, K);
+  B.Enorm = eF;
+  if (getenv("CTD_ORTHO_TRACE")) fprintf(stderr, "[ortho] K=%lld |E|_F=%.3e (second-order term %s)\n", (long long)K, eF,
+                                         eF * eF >= 1e-13 ? "swept" : "below 1e-13, skipped");
+  if (!(eF * eF >= 1e-13)) return;
+  Buf<double> Et(ctx, (size_t)K * K);
+  transpose(ctx, E.p, K, K, K, Et.p, K);
+  B.P.alloc(ctx, (size_t)dim * ldq);
+  gemm_f64(ctx, false, dim, K, K, B.Q.p, ldq, Et.p, K, B.P.p, ldq, 1.0, 0.0, 0.0);  // P = Q E^T
+  B.Pok = true;
 }
 
 }  // namespace
@@ -330,16 +431,18 @@ const double* ortho_panel(Ctx* ctx, const Basis& B, int64_t* ldq) {
     }
     try {
       B.Qiters = orthonormalize(ctx, B.Q.p, dim, K, ld, &B.Qdefect);
-      B.Sdefect = s_defect(ctx, B, B.Q.p, ld);
-      compl_ = !(B.Sdefect <= kSDefectMax);
     } catch (const Fail& f) {
       if (f.code != CTD_ERR_NUMERIC) throw;
       compl_ = true;  // rank-deficient to fp64: R U R^T is no projector either
     }
     B.Qld = ld;
     B.Qcols = K;
+    if (!compl_) build_correction(ctx, B);
   }
-  if (compl_) build_complement(ctx, B);
+  if (compl_) {
+    B.Pok = false;
+    build_complement(ctx, B);
+  }
   B.Qk = K;
   *ldq = B.Qld;
   return B.Q.p;
@@ -370,11 +473,21 @@ void error_partials(Ctx* ctx, const Fibers& fb, const Basis& B, double* x_sq, do
   LAUNCH(ctx, k_cdw, cgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, Q, (long long)ldq, nc,
          sp1.p + sgrid);
   LAUNCH(ctx, k_reduce, 1, 1024, 0, sp1.p, (long long)sgrid + nwarps, cd.p);
+  double s2 = 0.0;
+  if (B.Pok) {  // the second-order term sum_j |E Q^T x_j|^2 (build_correction)
+    Buf<double> cd2(ctx, 1);
+    LAUNCH(ctx, k_row_weight, ceil_div((uint64_t)dim * 32, 256), 256, 0, B.P.p, (long long)ldq, nc, dim, rho.p);
+    LAUNCH(ctx, k_single_fibers, sgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, rho.p, sp1.p);
+    LAUNCH(ctx, k_cdw, cgrid, 256, 0, fb.ptr.p, (long long)fb.F, fb.row.p, fb.val.p, B.P.p, (long long)ldq, nc,
+           sp1.p + sgrid);
+    LAUNCH(ctx, k_reduce, 1, 1024, 0, sp1.p, (long long)sgrid + nwarps, cd2.p);
+    s2 = ctx->read1(cd2.p);
+  }
   double s = 0.0;
   ctx->to_host(x_sq, xsq.p, 1);
   ctx->to_host(&s, cd.p, 1);
   ctx->sync();
-  *cross = B.Qcompl ? *x_sq - s : s;
+  *cross = B.Qcompl ? *x_sq - s : s - s2;
 }
 
 }  // namespace ctdgpu

@@ -3,11 +3,12 @@
 * C2 (configs[1]) and C4 (configs[3]): the whole CTD-S front end on the GPU
   against the C restatement on the identical tensor, bit for bit (draws,
   unique list, every decision and delta, kept ids, R, U).
-* C5 (configs[4], 1e9 nnz on one GPU; generated on the device): size-independent
-  properties plus bounded oracle checks - fiber norms against an independent
-  exact integer reduction, the sampling law/draws/dedup against the restatement
-  on the full 1e8-fiber law, and the first filter decisions and deltas against
-  the restatement's FiberBasis fed the same candidate fibers.
+* C5 (configs[4], 1e9 nnz on one GPU; generated on the device): fiber norms
+  against an independent exact integer reduction, the sampling law/draws/dedup
+  against the restatement on the full 1e8-fiber law, every filter decision,
+  delta and U against the multi-threaded restatement of FiberBasis fed the same
+  candidate fibers, and the relative error of a 128-fiber subset against the
+  double-double oracle.
 """
 import os
 
@@ -86,9 +87,9 @@ def test_c5_scale_properties(ctx, port):
     assert int(fnorm.astype(np.int64).sum()) == int((val.to(torch.int64) ** 2).sum())
     del ref_norm, sq
     torch.cuda.empty_cache()
-    # -- the front end
+    # -- the front end (with the error pass: it keeps the orthonormal panel)
     c, eps, seed = 10000, 1e-6, 42
-    f = ctd.ctd_s(dt, 0, c, eps, seed, ctx=ctx)
+    f = ctd.ctd_s(dt, 0, c, eps, seed, with_error=True, ctx=ctx)
     # law + draws + dedup: the restatement on the full dense law (N_alpha = 1e8)
     p = np.zeros(J * T)
     p[fcol] = fnorm
@@ -99,20 +100,55 @@ def test_c5_scale_properties(ctx, port):
     assert np.array_equal(f.drawn, drawn)
     uniq = port.unique_first_occurrence(drawn)
     assert np.array_equal(f.unique, uniq)
-    # filter: the first n decisions against the restatement's FiberBasis
-    n = int(os.environ.get("CTD_C5_PREFIX", "600"))
+    # filter: EVERY decision, delta and U against the multi-threaded restatement
+    # of FiberBasis (oracle/filter_par.c, bit-identical to the sequential one:
+    # tests/test_filter_par.py) fed the same candidate fibers
+    n = int(os.environ.get("CTD_C5_PREFIX", str(len(uniq))))
     cand = torch.from_numpy(uniq[:n]).to(col.device)
     sel = torch.nonzero(torch.isin(col, cand)).squeeze(1)
     scol, order = torch.sort(col[sel], stable=True)   # lexicographic input: rows ascend per fiber
     rows = idx[0][sel][order].to(torch.int64).cpu().numpy()
     vals = val[sel][order].cpu().numpy()
     scol = scol.cpu().numpy()
-    b = port.basis(I)
-    for k, j in enumerate(uniq[:n]):
-        lo, hi = np.searchsorted(scol, [j, j + 1])
-        acc, _, delta, _ = b.try_append(rows[lo:hi], vals[lo:hi], eps)
-        assert acc == bool(f.accepted[k]), k
-        assert delta == f.delta[k], k
-    assert np.array_equal(f.kept_flat[:b.size()], uniq[:n][f.accepted[:n].astype(bool)])
-    assert np.array_equal(f.U, f.U.T)
+    lo = np.searchsorted(scol, uniq[:n])
+    hi = np.searchsorted(scol, uniq[:n] + 1)
+    cp = np.concatenate([[0], np.cumsum(hi - lo)]).astype(np.int64)
+    crow = np.concatenate([rows[a:b] for a, b in zip(lo, hi)])
+    cval = np.concatenate([vals[a:b] for a, b in zip(lo, hi)])
+    acc, deg, dl, U = port.filter_par(I, cp, crow, cval, eps)
+    assert np.array_equal(acc.astype(bool), f.accepted[:n].astype(bool))
+    assert np.array_equal(deg.astype(bool), f.degenerate[:n].astype(bool))
+    assert np.array_equal(dl.view(np.int64), f.delta[:n].view(np.int64))
+    if n == len(uniq):
+        assert np.array_equal(U.view(np.int64), f.U.view(np.int64))
+    assert np.array_equal(f.kept_flat[:int(acc.sum())], uniq[:n][acc.astype(bool)])
+    # relative error: the error is a sum over fibers, so a fiber subset X_S of
+    # C5 (the heaviest, random ones, kept ones) through the same factors is
+    # checked against the double-double column-by-column oracle
+    # (oracle/relerr_dd.c, pinned to the reference by test_relerr_oracle.py)
+    assert 0.0 <= f.relative_error <= 1.0
+    rng = np.random.default_rng(5)
+    heavy = fcol[np.argsort(fnorm)[-40:]]
+    pick = np.unique(np.concatenate([heavy, rng.choice(fcol, 80, replace=False), uniq[:8]]))
+    pt = torch.from_numpy(pick).to(col.device)
+    ssel = torch.nonzero(torch.isin(col, pt)).squeeze(1)     # input order: lexicographic
+    sidx = [idx[k][ssel].contiguous() for k in range(3)]
+    sval = val[ssel].contiguous()
+    sub = api.DeviceTensor.from_device_ptrs(shape, int(ssel.shape[0]), [t.data_ptr() for t in sidx],
+                                            sval.data_ptr(), ctx)
+    v_gpu = ctd.relative_error(sub, f, ctx)
+    sub.close()
+    scol2, order2 = torch.sort(col[ssel], stable=True)
+    srow = idx[0][ssel][order2].to(torch.int64).cpu().numpy()
+    svv = val[ssel][order2].cpu().numpy()
+    scol2 = scol2.cpu().numpy()
+    lo2 = np.searchsorted(scol2, pick)
+    hi2 = np.searchsorted(scol2, pick + 1)
+    from oracle.bindings import Csc
+    xs = Csc(I, len(pick), np.concatenate([[0], np.cumsum(hi2 - lo2)]).astype(np.int64), srow, svv)
+    R = Csc(I, f.kept_count(), f.R_col_ptr.astype(np.int64), f.R_row.astype(np.int64), f.R_val)
+    (eh, el), (xh, xl) = port.relerr_dd_direct(xs, R, f.U)
+    want = (eh + el) / (xh + xl)
+    assert abs(v_gpu - want) <= 1e-9 * max(1.0, abs(want)), (v_gpu, want)
+    assert abs(v_gpu - want) <= 1e-12 * max(1.0, abs(want)), (v_gpu, want)
     dt.close()
