@@ -107,6 +107,17 @@ int ctd_gpu_matricize(ctd_gpu_ctx *ctx, const ctd_gpu_tensor *x, int mode,
 int ctd_gpu_column_distribution(ctd_gpu_ctx *ctx, const ctd_gpu_tensor *x,
                                 int mode, double *total_sq_norm, double *probs,
                                 double *cumulative);
+/* column_sq_norms (tensor_ops.hpp:39, tensor_ops.cpp:194-202) and
+ * column_distribution (sampling.hpp:20, sampling.cpp:21-31) of a host matrix
+ * in the reference's SparseMatrix layout (col_ptr[cols+1], rows ascending
+ * per column, no stored zeros): out/probs have `cols` entries, bit-exact. */
+int ctd_gpu_column_sq_norms_csc(ctd_gpu_ctx *ctx, int64_t rows, int64_t cols,
+                                const int64_t *col_ptr, const int64_t *row_idx,
+                                const double *vals, double *out);
+int ctd_gpu_column_distribution_csc(ctd_gpu_ctx *ctx, int64_t rows, int64_t cols,
+                                    const int64_t *col_ptr, const int64_t *row_idx,
+                                    const double *vals, double *total_sq_norm,
+                                    double *probs);
 /* sample_with_replacement (sampling.hpp:27-28) over a host probability
  * vector of n columns (zero entries allowed). */
 int ctd_gpu_sample_with_replacement(ctd_gpu_ctx *ctx, const double *probs,

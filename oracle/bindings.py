@@ -144,6 +144,7 @@ class Port:
         L.cto_relerr_dd_full.argtypes = [C.POINTER(_CscStruct), C.POINTER(_CscStruct), v] + \
             [C.POINTER(f64)] * 3
         L.cto_filter_par.argtypes = [i64, i64, v, v, v, f64, v, v, v, C.POINTER(i64), v]
+        L.cto_stream_init2.argtypes = [i32, v, i64, v, v, i32, i64, f64, C.c_uint64, i32, C.POINTER(v)]
         L.cto_stream_init.argtypes = [i32, v, i64, v, v, i32, i64, f64, C.c_uint64,
                                       C.POINTER(v)]
         L.cto_stream_step.argtypes = [v, i32, v, i64, v, v, i64]
@@ -307,8 +308,9 @@ class Port:
         return fe, core, self.relative_error(xm, x_sq, fe.R, fe.U, core)
 
     # -- CTD-D ------------------------------------------------------------------
-    def stream(self, shape, idx, val, mode, s, eps=1e-6, seed=42):
-        return _PortStream(self, shape, idx, val, mode, s, eps, seed)
+    def stream(self, shape, idx, val, mode, s, eps=1e-6, seed=42, core=True):
+        """init_stream; core=False keeps only the front end (kept ids, basis)."""
+        return _PortStream(self, shape, idx, val, mode, s, eps, seed, core)
 
 
 class _PortBasis:
@@ -343,12 +345,13 @@ class _PortBasis:
 
 
 class _PortStream:
-    def __init__(self, port, shape, idx, val, mode, s, eps, seed):
+    def __init__(self, port, shape, idx, val, mode, s, eps, seed, core=True):
         self.P = port
         shape, idx, val = _i64(shape), _i64(idx), _f64(val)
         h = C.c_void_p()
-        port._chk(port.L.cto_stream_init(len(shape), _p(shape), len(val), _p(idx), _p(val),
-                                         mode, s, eps, C.c_uint64(seed), C.byref(h)), "init_stream")
+        port._chk(port.L.cto_stream_init2(len(shape), _p(shape), len(val), _p(idx), _p(val),
+                                          mode, s, eps, C.c_uint64(seed), 0 if core else 1, C.byref(h)),
+                  "init_stream")
         self.h = h
 
     def __del__(self):

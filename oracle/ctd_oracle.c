@@ -525,6 +525,7 @@ int cto_relative_error(const cto_csc *x, double x_sq, const cto_csc *r,
 /* ---------------------------------------------------------------------------
  * CTD-D (ctd_dynamic.cpp). */
 struct cto_stream {
+  int no_core; /* front end only: kept ids and the basis, no Eq. 13 core */
   cto_basis *basis;
   cto_csc core; /* C_(alpha): basis.size() x t*slab_cols */
   int order;     /* order of the slab / stream tensor (time mode last) */
@@ -624,6 +625,15 @@ static void assemble(const cto_csc *tl, const cto_csc *tr, const cto_csc *bl,
 int cto_stream_init(int order, const int64_t *shape, int64_t nnz,
                     const int64_t *idx, const double *val, int mode, int64_t s,
                     double eps, uint64_t seed, cto_stream **out) {
+  return cto_stream_init2(order, shape, nnz, idx, val, mode, s, eps, seed, 0, out);
+}
+
+/* init_stream with an optional front-end-only state (no_core): the kept ids
+ * and the basis evolve exactly as in ctd_d_step, the core is not kept (for
+ * parity checks of long streams, where the reference's core does not fit). */
+int cto_stream_init2(int order, const int64_t *shape, int64_t nnz,
+                     const int64_t *idx, const double *val, int mode, int64_t s,
+                     double eps, uint64_t seed, int no_core, cto_stream **out) {
   if (order < 2) return 1;
   if (mode < 0 || mode >= order - 1) return 1;
   cto_frontend f;
@@ -640,6 +650,11 @@ int cto_stream_init(int order, const int64_t *shape, int64_t nnz,
   S->seed = seed;
   for (int64_t i = 0; i < f.kept; ++i) push_kept(S, f.kept_flat[i]);
   cto_frontend_free(&f);
+  S->no_core = no_core;
+  if (no_core) {
+    *out = S;
+    return 0;
+  }
   cto_csc xm, r;
   cto_matricize(order, shape, nnz, idx, val, mode, &xm);
   cto_basis_r(S->basis, &r);
@@ -665,10 +680,14 @@ int cto_stream_step(cto_stream *S, int order, const int64_t *shape,
   if (st) return st;
   const int64_t delta_cols = delta.cols;
   cto_csc r_old;
-  cto_basis_r(S->basis, &r_old); /* :165 */
+  memset(&r_old, 0, sizeof(r_old));
   const int64_t k_old = S->basis->k;
-  double *u_old = xmalloc((size_t)(k_old * k_old) * sizeof(double) + 8);
-  if (k_old) memcpy(u_old, S->basis->u, (size_t)(k_old * k_old) * sizeof(double));
+  double *u_old = NULL;
+  if (!S->no_core) {
+    cto_basis_r(S->basis, &r_old); /* :165 */
+    u_old = xmalloc((size_t)(k_old * k_old) * sizeof(double) + 8);
+    if (k_old) memcpy(u_old, S->basis->u, (size_t)(k_old * k_old) * sizeof(double));
+  }
   int64_t kept_before = S->kept;
   if (delta.nnz > 0) { /* :173-188 */
     cto_frontend f;
@@ -680,6 +699,11 @@ int cto_stream_step(cto_stream *S, int order, const int64_t *shape,
     f.basis = NULL;
     cto_frontend_free(&f);
     if (st) { cto_csc_free(&delta); cto_csc_free(&r_old); free(u_old); return st; }
+  }
+  if (S->no_core) {
+    S->t += 1;
+    cto_csc_free(&delta);
+    return 0;
   }
   cto_csc top_right;
   transpose_times(&r_old, &delta, &top_right); /* :190 */

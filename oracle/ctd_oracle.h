@@ -107,6 +107,9 @@ typedef struct cto_stream cto_stream;
 int cto_stream_init(int order, const int64_t *shape, int64_t nnz,
                     const int64_t *idx, const double *val, int mode, int64_t s,
                     double eps, uint64_t seed, cto_stream **out);
+int cto_stream_init2(int order, const int64_t *shape, int64_t nnz,
+                     const int64_t *idx, const double *val, int mode, int64_t s,
+                     double eps, uint64_t seed, int no_core, cto_stream **out);
 int cto_stream_step(cto_stream *st, int order, const int64_t *shape,
                     int64_t nnz, const int64_t *idx, const double *val,
                     int64_t d);

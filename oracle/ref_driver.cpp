@@ -267,6 +267,15 @@ int ref_memory_usage(void* t, void* f, double* out) {
 }
 
 // ---- CTD-D (ctd_dynamic.cpp) ---------------------------------------------
+// Hooks of the GPU drop-in (paper_1710_03608_b200/shim): absent (null) in the
+// plain CPU library.  The drop-in refreshes a StreamState's basis / core /
+// history from the device lazily; these accessors read the fields directly.
+extern "C" void ctd_shim_sync_state(void* state) __attribute__((weak));
+extern "C" void ctd_shim_release_state(void* state) __attribute__((weak));
+static StreamState* synced(void* s) {
+  if (ctd_shim_sync_state) ctd_shim_sync_state(s);
+  return static_cast<StreamState*>(s);
+}
 int ref_init_stream(void* hist, int mode, int64_t s, double eps, uint64_t seed,
                     int keep_history, int exact_core, void** out) {
   return guard([&] {
@@ -274,7 +283,10 @@ int ref_init_stream(void* hist, int mode, int64_t s, double eps, uint64_t seed,
                                        eps, seed, keep_history != 0, exact_core != 0));
   });
 }
-void ref_stream_free(void* s) { delete static_cast<StreamState*>(s); }
+void ref_stream_free(void* s) {
+  if (ctd_shim_release_state) ctd_shim_release_state(s);
+  delete static_cast<StreamState*>(s);
+}
 int ref_stream_step(void* s, void* slab, int64_t d, double* seconds) {
   return guard([&] {
     auto* st = static_cast<StreamState*>(s);
@@ -293,11 +305,11 @@ int ref_stream_factors(void* s, void** out) {
   });
 }
 // Matricized core (basis.size() x t*slab_columns) as CSC.
-int64_t ref_stream_core_nnz(void* s) { return static_cast<StreamState*>(s)->core.nnz(); }
-int64_t ref_stream_core_rows(void* s) { return static_cast<StreamState*>(s)->core.rows(); }
-int64_t ref_stream_core_cols(void* s) { return static_cast<StreamState*>(s)->core.cols(); }
+int64_t ref_stream_core_nnz(void* s) { return synced(s)->core.nnz(); }
+int64_t ref_stream_core_rows(void* s) { return synced(s)->core.rows(); }
+int64_t ref_stream_core_cols(void* s) { return synced(s)->core.cols(); }
 void ref_stream_core(void* s, int64_t* col_ptr, int64_t* rows, double* vals) {
-  const auto& c = static_cast<StreamState*>(s)->core;
+  const auto& c = synced(s)->core;
   const auto& cp = c.column_pointers();
   for (size_t i = 0; i < cp.size(); ++i) col_ptr[i] = static_cast<int64_t>(cp[i]);
   std::memcpy(rows, c.row_indices().data(), c.nnz() * sizeof(int64_t));

@@ -30,5 +30,8 @@ void matricize(Ctx* ctx, const Tensor& x, int mode, Fibers& out);
 // Returns false (nothing usable in out) when the input's rows do not ascend
 // inside a column; raises the usual input errors otherwise.
 bool matricize_onesweep(Ctx* ctx, const Tensor& x, int mode, Fibers& out);
+// column_sq_norms (tensor_ops.cpp:194-202) of fb's fibers into fb.norm, each
+// summed in stored (ascending-row) order.
+void fiber_norms(Ctx* ctx, Fibers& fb);
 
 }  // namespace ctdgpu

@@ -320,6 +320,89 @@ int ctd_gpu_column_distribution(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int m
   });
 }
 
+// A host CSC (SparseMatrix layout: col_ptr[cols+1], rows ascending per
+// column) uploaded as the nonempty columns' fibers.
+static void fibers_from_csc(Ctx* c, int64_t rows, int64_t cols, const int64_t* col_ptr, const int64_t* row_idx,
+                            const double* vals, Fibers& fb) {
+  if (rows < 0 || cols < 0) fail(CTD_ERR_ARGUMENT, "matrix extents must be non-negative");
+  if (rows > 0x7fffffffLL) fail(CTD_ERR_SHAPE, "matrix row count exceeds the int32 index range");
+  need(col_ptr, "col_ptr");
+  const int64_t nnz = col_ptr[cols];
+  std::vector<int64_t> col, ptr;
+  std::vector<int32_t> r32(nnz > 0 ? nnz : 1);
+  for (int64_t j = 0; j < cols; ++j) {
+    if (col_ptr[j + 1] < col_ptr[j]) fail(CTD_ERR_ARGUMENT, "col_ptr must be non-decreasing");
+    if (col_ptr[j + 1] > col_ptr[j]) {
+      col.push_back(j);
+      ptr.push_back(col_ptr[j]);
+    }
+  }
+  ptr.push_back(nnz);
+  for (int64_t t = 0; t < nnz; ++t) {
+    if (row_idx[t] < 0 || row_idx[t] >= rows) fail(CTD_ERR_SHAPE, "row index out of range");
+    r32[t] = (int32_t)row_idx[t];
+  }
+  fb.rows = rows;
+  fb.cols = cols;
+  fb.nnz = nnz;
+  fb.F = (int64_t)col.size();
+  fb.col.alloc(c, fb.F + 1);
+  fb.ptr.alloc(c, fb.F + 1);
+  fb.row.alloc(c, nnz + 1);
+  fb.val.alloc(c, nnz + 1);
+  c->to_dev(fb.col.p, col.data(), fb.F);
+  c->to_dev(fb.ptr.p, ptr.data(), fb.F + 1);
+  c->to_dev(fb.row.p, r32.data(), nnz);
+  c->to_dev(fb.val.p, vals, nnz);
+  fiber_norms(c, fb);
+  c->check_flags("column_sq_norms");
+}
+
+int ctd_gpu_column_sq_norms_csc(ctd_gpu_ctx* ctx, int64_t rows, int64_t cols, const int64_t* col_ptr,
+                                const int64_t* row_idx, const double* vals, double* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    bind_device(&ctx->c);
+    need(out, "out");
+    Ctx* c = &ctx->c;
+    Fibers fb;
+    fibers_from_csc(c, rows, cols, col_ptr, row_idx, vals, fb);
+    std::vector<int64_t> col(fb.F);
+    std::vector<double> nrm(fb.F);
+    c->to_host(col.data(), fb.col.p, fb.F);
+    c->to_host(nrm.data(), fb.norm.p, fb.F);
+    c->sync();
+    std::fill(out, out + cols, 0.0);
+    for (int64_t f = 0; f < fb.F; ++f) out[col[f]] = nrm[f];
+  });
+}
+
+int ctd_gpu_column_distribution_csc(ctd_gpu_ctx* ctx, int64_t rows, int64_t cols, const int64_t* col_ptr,
+                                    const int64_t* row_idx, const double* vals, double* total_sq_norm,
+                                    double* probs) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    bind_device(&ctx->c);
+    Ctx* c = &ctx->c;
+    Fibers fb;
+    fibers_from_csc(c, rows, cols, col_ptr, row_idx, vals, fb);
+    if (fb.F == 0) fail(CTD_ERR_EMPTY_INPUT, "column distribution of a matrix without nonzero entries");  // sampling.cpp:22-23
+    Buf<double> pr(c, fb.F + 1), cum(c, fb.F + 1), tot(c, 1);
+    sampling_law(c, fb.norm.p, fb.F, tot.p, pr.p, cum.p, c->d_flags);
+    c->check_flags("column_distribution");
+    std::vector<int64_t> col(fb.F);
+    std::vector<double> p(fb.F);
+    c->to_host(col.data(), fb.col.p, fb.F);
+    c->to_host(p.data(), pr.p, fb.F);
+    if (total_sq_norm) c->to_host(total_sq_norm, tot.p, 1);
+    c->sync();
+    if (probs) {
+      std::fill(probs, probs + cols, 0.0);
+      for (int64_t f = 0; f < fb.F; ++f) probs[col[f]] = p[f];
+    }
+  });
+}
+
 int ctd_gpu_sample_with_replacement(ctd_gpu_ctx* ctx, const double* probs, int64_t n, int64_t count,
                                     uint64_t seed, int64_t* out) {
   return guarded([&] {

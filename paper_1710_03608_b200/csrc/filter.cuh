@@ -52,7 +52,7 @@ struct Basis {
   mutable int Qiters = 0;
   mutable double Qdefect = 0.0;
   // P = Q E^T: the second-order correction panel of the error pass (relerr.cu
-  // build_correction), kept when |E|_F^2 >= 1e-13
+  // build_correction), kept when |E|_F^2 >= 1e-11
   mutable Buf<double> P;
   mutable bool Pok = false;
   mutable double Enorm = 0.0;

@@ -420,6 +420,23 @@ int os_bits_for(unsigned long long n) {
 
 }  // namespace
 
+void fiber_norms(Ctx* ctx, Fibers& fb) {
+  const long long nnz = fb.nnz, F = fb.F;
+  fb.norm.alloc(ctx, F + 1);
+  if (F == 0) return;
+  Buf<long long> dF(ctx, 1);
+  ctx->to_dev(dF.p, &F, 1);
+  Buf<int> midl(ctx, nnz / kOsShort + 2), nmid(ctx, 1), longl(ctx, nnz / kOsLong + 2), nlong(ctx, 1);
+  nmid.zero();
+  nlong.zero();
+  const unsigned ngrid = (unsigned)std::min<long long>((F + 255) / 256, (long long)ctx->sm_count * 16);
+  LAUNCH(ctx, k_os_norms, ngrid, 256, 0, fb.ptr.p, dF.p, fb.val.p, fb.norm.p, midl.p, nmid.p);
+  LAUNCH(ctx, k_os_norms_mid, (unsigned)ctx->sm_count * 8, 256, 0, fb.ptr.p, midl.p, nmid.p, fb.val.p, fb.norm.p,
+         longl.p, nlong.p);
+  LAUNCH(ctx, k_os_norms_long, (unsigned)ctx->sm_count * 4, 256, 0, fb.ptr.p, longl.p, nlong.p, fb.val.p, fb.norm.p,
+         ctx->d_flags);
+}
+
 bool matricize_onesweep(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
   Coo c{};
   c.order = x.order;

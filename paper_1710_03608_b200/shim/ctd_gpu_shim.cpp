@@ -1,24 +1,39 @@
 // Drop-in for the reference C++ API (proj/core, namespace ctd): the hot-path
 // entry points re-pointed at libctd_gpu.so through the C-ABI in
 // include/ctd_gpu.h.  Compiled against the reference's own headers and linked
-// into the reference library with
+// into the reference library with `ld --wrap=<mangled name>` for each symbol
+// below (shim/Makefile), so every caller (stream_harness, ddos, tests, the
+// Python/ctypes drivers) runs on the B200 without a source change; see
+// INTEGRATION.md.
 //
-//   -Wl,--wrap=_ZN3ctd5ctd_sERKNS_12SparseTensorEildm                (ctd_s)
-//   -Wl,--wrap=_ZN3ctd11init_streamERKNS_12SparseTensorEildmbb       (init_stream)
-//   -Wl,--wrap=_ZN3ctd10ctd_d_stepENS_11StreamStateERKNS_12SparseTensorEl  (ctd_d_step)
+// Entry points replaced (reference declarations, include/ctd/...):
+//   ctd_s                    ctd_static.hpp:22-24   (src/ctd_static.cpp:19-50)
+//   init_stream              ctd_dynamic.hpp:42-45  (src/ctd_dynamic.cpp:129-147)
+//   ctd_d_step               ctd_dynamic.hpp:57-58  (src/ctd_dynamic.cpp:149-229)
+//   StreamState::factors     ctd_dynamic.hpp:38     (src/ctd_dynamic.cpp:114-127)
+//   core_drift               ctd_dynamic.hpp:66     (src/ctd_dynamic.cpp:271-301)
+//   relative_error           evaluation.hpp:39      (src/evaluation.cpp:88-122)
+//   matricize                tensor_ops.hpp:21      (src/tensor_ops.cpp:118-135)
+//   column_sq_norms          tensor_ops.hpp:39      (src/tensor_ops.cpp:194-202)
+//   column_distribution      sampling.hpp:20        (src/sampling.cpp:21-31)
+//   sample_with_replacement  sampling.hpp:27-28     (src/sampling.cpp:33-64)
+//   unique_first_occurrence  sampling.hpp:31        (src/sampling.cpp:66-78)
+// memory_usage (evaluation.cpp:124-129) stays reference code: it counts the
+// nonzeros of host objects the caller already holds.
 //
-// so every caller (stream_harness, ddos, tests, the Python/ctypes drivers)
-// runs on the B200 without a source change; see oracle/Makefile `dropin` and
-// INTEGRATION.md.  Everything else (SparseTensor, SparseMatrix, DenseMatrix,
-// FiberBasis, fold, relative_error, memory_usage, ...) stays reference code.
-//
-// Entry points replaced (reference declarations):
-//   ctd_s        include/ctd/ctd_static.hpp:22-24   (src/ctd_static.cpp:19-50)
-//   init_stream  include/ctd/ctd_dynamic.hpp:42-45  (src/ctd_dynamic.cpp:129-147)
-//   ctd_d_step   include/ctd/ctd_dynamic.hpp:57-58  (src/ctd_dynamic.cpp:149-229)
+// Device state: a CTD-D stream lives on the GPU (ctd_gpu_stream), keyed by
+// the heap buffer of StreamState::kept_fibers (which survives the reference's
+// move-in / return-out idiom).  ctd_d_step updates only t and kept_fibers;
+// the basis, the matricized core and the retained history are refreshed from
+// the device when the caller asks for them (factors(), core_drift(), or
+// ctd_shim_sync_state() for code that reads the fields directly), so a step
+// costs no O(core) or O(history) host copy.  Factors produced on the device
+// stay registered (bounded LRU) so relative_error on them runs on the GPU;
+// anything else falls back to the reference code (__real_).
 // Errors: the C-ABI status is the reference ErrorClass; it is rethrown as the
 // matching ctd::*Error with ctd_gpu_last_error()'s message.
 #include <cstdint>
+#include <list>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -27,6 +42,8 @@
 
 #include "ctd/ctd_dynamic.hpp"
 #include "ctd/ctd_static.hpp"
+#include "ctd/evaluation.hpp"
+#include "ctd/sampling.hpp"
 #include "ctd/error.hpp"
 #include "ctd/factors.hpp"
 #include "ctd/fiber_basis.hpp"
@@ -76,6 +93,11 @@ struct Factors {
     if (h) ctd_gpu_factors_destroy(h);
   }
   void load_info() { rethrow(ctd_gpu_factors_info_get(h, &info)); }
+  ctd_gpu_factors* release() {
+    ctd_gpu_factors* p = h;
+    h = nullptr;
+    return p;
+  }
 
   std::vector<int64_t> kept_flat() const {
     std::vector<int64_t> v(info.kept);
@@ -129,21 +151,39 @@ index_t other_extents(const std::vector<index_t>& shape, int mode) {
 // GPU stream handles, keyed by the heap buffer of StreamState::kept_fibers:
 // moving a StreamState (the reference's pass-by-value / return idiom) keeps
 // that buffer, so the key follows the state through ctd_d_step calls.
+struct StreamEntry {
+  ctd_gpu_stream* s = nullptr;
+  bool stale = false;                 // basis / core / t not refreshed since a step
+  std::vector<SparseTensor> pending;  // slabs not yet appended to state.history
+};
 std::mutex g_mu;
-std::unordered_map<const void*, ctd_gpu_stream*> g_streams;
+std::unordered_map<const void*, StreamEntry> g_streams;
 
-void fill_state(StreamState& st, ctd_gpu_stream* s, int64_t kept_before) {
-  Factors f;
-  rethrow(ctd_gpu_stream_factors(s, &f.h));
-  f.load_info();
-  const auto flat = f.kept_flat();
-  std::vector<index_t> grown(st.slab_shape);
-  grown.push_back(ctd_gpu_stream_t(s));
-  for (int64_t k = kept_before; k < (int64_t)flat.size(); ++k)
-    st.kept_fibers.push_back(make_fiber_id(grown, st.mode, flat[k]));
-  st.basis = FiberBasis(f.r(), f.u());
-  st.core = f.core(ctd_gpu_stream_t(s) * st.slab_columns());
-  st.t = ctd_gpu_stream_t(s);
+// Factors computed on the device, keyed like streams by kept_fibers' buffer;
+// the last kFactorsKept stay resident for relative_error.
+constexpr size_t kFactorsKept = 8;
+std::list<std::pair<const void*, ctd_gpu_factors*>> g_factors;
+
+void register_factors(const LRFactors& f, ctd_gpu_factors* h) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto it = g_factors.begin(); it != g_factors.end(); ++it)
+    if (it->first == f.kept_fibers.data()) {
+      ctd_gpu_factors_destroy(it->second);
+      g_factors.erase(it);
+      break;
+    }
+  g_factors.emplace_front(f.kept_fibers.data(), h);
+  while (g_factors.size() > kFactorsKept) {
+    ctd_gpu_factors_destroy(g_factors.back().second);
+    g_factors.pop_back();
+  }
+}
+
+ctd_gpu_factors* find_factors(const LRFactors& f) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto& e : g_factors)
+    if (e.first == f.kept_fibers.data() && !f.kept_fibers.empty()) return e.second;
+  return nullptr;
 }
 
 SparseTensor append_time(const SparseTensor& head, const SparseTensor& slab) {
@@ -161,6 +201,28 @@ SparseTensor append_time(const SparseTensor& head, const SparseTensor& slab) {
   return SparseTensor(std::move(shape), std::move(idx), std::move(val));
 }
 
+// The state's basis, core, t and history from the device (lazily, g_mu held).
+void sync_locked(StreamState& st, StreamEntry& e) {
+  if (e.stale) {
+    Factors f;
+    rethrow(ctd_gpu_stream_factors(e.s, &f.h));
+    f.load_info();
+    st.basis = FiberBasis(f.r(), f.u());
+    st.t = ctd_gpu_stream_t(e.s);
+    st.core = f.core(st.t * st.slab_columns());
+    e.stale = false;
+  }
+  if (st.history && !e.pending.empty()) {
+    for (const auto& slab : e.pending) st.history = append_time(*st.history, slab);
+    e.pending.clear();
+  }
+}
+
+StreamEntry* find_stream_locked(const StreamState& st) {
+  auto it = g_streams.find(st.kept_fibers.data());
+  return it == g_streams.end() ? nullptr : &it->second;
+}
+
 }  // namespace
 
 }  // namespace ctd
@@ -173,7 +235,8 @@ LRFactors __wrap__ZN3ctd5ctd_sERKNS_12SparseTensorEildm(const SparseTensor& x, i
                                                        double epsilon, std::uint64_t seed) {
   Tensor t(x);
   Factors f;
-  rethrow(ctd_gpu_ctd_s(context(), t.h, mode, sample_size, epsilon, seed, CTD_GPU_WITH_CORE, &f.h));
+  rethrow(ctd_gpu_ctd_s(context(), t.h, mode, sample_size, epsilon, seed, CTD_GPU_WITH_CORE | CTD_GPU_KEEP_PANEL,
+                        &f.h));
   f.load_info();
   LRFactors out;
   out.mode = mode;
@@ -185,6 +248,7 @@ LRFactors __wrap__ZN3ctd5ctd_sERKNS_12SparseTensorEildm(const SparseTensor& x, i
   std::vector<index_t> cshape = x.shape();
   cshape[(size_t)mode] = f.info.kept;
   out.C = fold(f.core(other_extents(x.shape(), mode)), mode, cshape);
+  register_factors(out, f.release());
   return out;
 }
 
@@ -214,37 +278,175 @@ StreamState __wrap__ZN3ctd11init_streamERKNS_12SparseTensorEildmbb(const SparseT
   st.exact_core = exact_core;
   if (keep_history || exact_core) st.history = historical;  // ctd_dynamic.cpp:143
   std::lock_guard<std::mutex> lk(g_mu);
-  g_streams[st.kept_fibers.data()] = s;
+  g_streams[st.kept_fibers.data()].s = s;
   return st;
 }
 
 StreamState __wrap__ZN3ctd10ctd_d_stepENS_11StreamStateERKNS_12SparseTensorEl(StreamState state,
                                                                              const SparseTensor& slab,
                                                                              index_t sample_size) {
-  ctd_gpu_stream* s = nullptr;
+  StreamEntry e;
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_streams.find(state.kept_fibers.data());
     if (it == g_streams.end())
       throw ArgumentError("stream state was not created by the GPU init_stream (or was copied)");
-    s = it->second;
+    e = std::move(it->second);
     g_streams.erase(it);
   }
   const int64_t before = (int64_t)state.kept_fibers.size();
   {
     Tensor t(slab);
-    const int st = ctd_gpu_stream_step(s, t.h, sample_size);
+    const int st = ctd_gpu_stream_step(e.s, t.h, sample_size);
     if (st != CTD_OK) {
       std::lock_guard<std::mutex> lk(g_mu);
-      g_streams[state.kept_fibers.data()] = s;
+      g_streams[state.kept_fibers.data()] = std::move(e);
       rethrow(st);
     }
   }
-  fill_state(state, s, before);
-  if (state.history) state.history = append_time(*state.history, slab);
+  // kept ids (flat ids on the grown shape, ctd_dynamic.cpp:184-185) and t now;
+  // basis, core and history when asked for (sync_locked)
+  {
+    Factors f;
+    rethrow(ctd_gpu_stream_factors(e.s, &f.h));
+    f.load_info();
+    std::vector<int64_t> flat(f.info.kept);
+    if (f.info.kept) rethrow(ctd_gpu_factors_kept_flat(f.h, flat.data()));
+    std::vector<index_t> grown(state.slab_shape);
+    grown.push_back(ctd_gpu_stream_t(e.s));
+    for (int64_t k = before; k < (int64_t)flat.size(); ++k)
+      state.kept_fibers.push_back(make_fiber_id(grown, state.mode, flat[k]));
+  }
+  state.t = ctd_gpu_stream_t(e.s);
+  e.stale = true;
+  if (state.history) e.pending.push_back(slab);  // ctd_dynamic.cpp:225-226, appended on sync
   std::lock_guard<std::mutex> lk(g_mu);
-  g_streams[state.kept_fibers.data()] = s;
+  g_streams[state.kept_fibers.data()] = std::move(e);
   return state;
+}
+
+LRFactors __real__ZNK3ctd11StreamState7factorsEv(const StreamState* self);
+LRFactors __wrap__ZNK3ctd11StreamState7factorsEv(const StreamState* self) {
+  ctd_gpu_stream* s = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (StreamEntry* e = find_stream_locked(*self)) s = e->s;
+  }
+  if (!s) return __real__ZNK3ctd11StreamState7factorsEv(self);
+  // the device snapshot (ctd_dynamic.cpp:114-127): R, U, the core folded
+  // with time extent t, the state's kept fibers
+  Factors f;
+  rethrow(ctd_gpu_stream_factors(s, &f.h));
+  f.load_info();
+  LRFactors out;
+  out.mode = self->mode;
+  out.epsilon = self->epsilon;
+  out.seed = self->seed;
+  out.kept_fibers = self->kept_fibers;
+  out.R = f.r();
+  out.U = f.u();
+  std::vector<index_t> shape(self->slab_shape);
+  const index_t t = ctd_gpu_stream_t(s);
+  shape.push_back(t);
+  std::vector<index_t> cshape = shape;
+  cshape[(size_t)self->mode] = f.info.kept;
+  out.C = fold(f.core(t * self->slab_columns()), self->mode, cshape);
+  register_factors(out, f.release());
+  return out;
+}
+
+double __real__ZN3ctd10core_driftERKNS_11StreamStateE(const StreamState& state);
+double __wrap__ZN3ctd10core_driftERKNS_11StreamStateE(const StreamState& state) {
+  ctd_gpu_stream* s = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (StreamEntry* e = find_stream_locked(state)) s = e->s;
+  }
+  if (!s) return __real__ZN3ctd10core_driftERKNS_11StreamStateE(state);
+  double out = 0.0;
+  rethrow(ctd_gpu_stream_core_drift(s, &out));
+  return out;
+}
+
+double __real__ZN3ctd14relative_errorERKNS_12SparseTensorERKNS_9LRFactorsE(const SparseTensor& x,
+                                                                         const LRFactors& f);
+double __wrap__ZN3ctd14relative_errorERKNS_12SparseTensorERKNS_9LRFactorsE(const SparseTensor& x,
+                                                                         const LRFactors& f) {
+  ctd_gpu_factors* h = find_factors(f);
+  if (!h) return __real__ZN3ctd14relative_errorERKNS_12SparseTensorERKNS_9LRFactorsE(x, f);
+  Tensor t(x);
+  double out = 0.0;
+  rethrow(ctd_gpu_relative_error(context(), t.h, h, &out));
+  return out;
+}
+
+SparseMatrix __wrap__ZN3ctd9matricizeERKNS_12SparseTensorEi(const SparseTensor& x, int mode) {
+  Tensor t(x);
+  int64_t F = 0;
+  rethrow(ctd_gpu_matricize(context(), t.h, mode, &F, nullptr, nullptr, nullptr, nullptr, nullptr));
+  std::vector<int64_t> col(F), ptr(F + 1);
+  std::vector<int32_t> r32(x.nnz());
+  std::vector<double> vals(x.nnz());
+  rethrow(ctd_gpu_matricize(context(), t.h, mode, &F, col.data(), ptr.data(), r32.data(), vals.data(), nullptr));
+  std::vector<index_t> ri(r32.begin(), r32.end()), ci;
+  ci.reserve(x.nnz());
+  for (int64_t f = 0; f < F; ++f)
+    for (int64_t q = ptr[f]; q < ptr[f + 1]; ++q) ci.push_back(col[f]);
+  return SparseMatrix(x.extent(mode), other_extents(x.shape(), mode), std::move(ri), std::move(ci), std::move(vals));
+}
+
+std::vector<double> __wrap__ZN3ctd15column_sq_normsERKNS_12SparseMatrixE(const SparseMatrix& m) {
+  const auto& cp = m.column_pointers();
+  std::vector<int64_t> cp64(cp.begin(), cp.end());
+  std::vector<double> out((size_t)m.cols());
+  rethrow(ctd_gpu_column_sq_norms_csc(context(), m.rows(), m.cols(), cp64.data(), m.row_indices().data(),
+                                      m.values().data(), out.data()));
+  return out;
+}
+
+ColumnDistribution __wrap__ZN3ctd19column_distributionERKNS_12SparseMatrixE(const SparseMatrix& m) {
+  const auto& cp = m.column_pointers();
+  std::vector<int64_t> cp64(cp.begin(), cp.end());
+  ColumnDistribution d;
+  d.probabilities.assign((size_t)m.cols(), 0.0);
+  rethrow(ctd_gpu_column_distribution_csc(context(), m.rows(), m.cols(), cp64.data(), m.row_indices().data(),
+                                          m.values().data(), &d.total_sq_norm, d.probabilities.data()));
+  return d;
+}
+
+std::vector<index_t> __wrap__ZN3ctd23sample_with_replacementERKNS_18ColumnDistributionElm(
+    const ColumnDistribution& dist, index_t count, std::uint64_t seed) {
+  std::vector<index_t> out(count > 0 ? (size_t)count : 0);
+  rethrow(ctd_gpu_sample_with_replacement(context(), dist.probabilities.data(), (int64_t)dist.probabilities.size(),
+                                          count, seed, out.data()));
+  return out;
+}
+
+std::vector<index_t> __wrap__ZN3ctd23unique_first_occurrenceESt4spanIKlLm18446744073709551615EE(
+    std::span<const index_t> drawn) {
+  std::vector<index_t> out(drawn.size());
+  int64_t n = 0;
+  rethrow(ctd_gpu_unique_first_occurrence(context(), drawn.data(), (int64_t)drawn.size(), out.data(), &n));
+  out.resize((size_t)n);
+  return out;
+}
+
+// For callers that read StreamState::basis / core / history directly (the
+// reference's own test driver does): bring them up to date from the device.
+void ctd_shim_sync_state(void* state) {
+  auto& st = *static_cast<StreamState*>(state);
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (StreamEntry* e = find_stream_locked(st)) sync_locked(st, *e);
+}
+
+// Releases the device stream behind a state the caller is about to destroy.
+void ctd_shim_release_state(void* state) {
+  auto& st = *static_cast<StreamState*>(state);
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_streams.find(st.kept_fibers.data());
+  if (it == g_streams.end()) return;
+  ctd_gpu_stream_destroy(it->second.s);
+  g_streams.erase(it);
 }
 
 }  // extern "C"

@@ -18,7 +18,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 DROPIN = os.path.join(ROOT, "paper_1710_03608_b200", "shim", "libctd_dropin.so")
 WRAPPED = ("_ZN3ctd5ctd_sERKNS_12SparseTensorEildm",
            "_ZN3ctd11init_streamERKNS_12SparseTensorEildmbb",
-           "_ZN3ctd10ctd_d_stepENS_11StreamStateERKNS_12SparseTensorEl")
+           "_ZN3ctd10ctd_d_stepENS_11StreamStateERKNS_12SparseTensorEl",
+           "_ZNK3ctd11StreamState7factorsEv",
+           "_ZN3ctd10core_driftERKNS_11StreamStateE",
+           "_ZN3ctd14relative_errorERKNS_12SparseTensorERKNS_9LRFactorsE",
+           "_ZN3ctd9matricizeERKNS_12SparseTensorEi",
+           "_ZN3ctd15column_sq_normsERKNS_12SparseMatrixE",
+           "_ZN3ctd19column_distributionERKNS_12SparseMatrixE",
+           "_ZN3ctd23sample_with_replacementERKNS_18ColumnDistributionElm",
+           "_ZN3ctd23unique_first_occurrenceESt4spanIKlLm18446744073709551615EE")
 
 needs_dropin = pytest.mark.skipif(not os.path.exists(DROPIN),
                                   reason="drop-in not built (make -C paper_1710_03608_b200/shim)")
@@ -146,3 +154,40 @@ def test_dropin_stream(ref, dropin, keep_history, exact_core):
             da, db = sa.core_drift(), sb.core_drift()
             assert da == db or abs(da - db) <= 1e-9 * max(1.0, abs(da)), t
     assert grew >= 1
+
+
+@pytest.mark.gpu
+@needs_dropin
+@pytest.mark.parametrize("name", list(CASES))
+def test_dropin_tensor_ops_and_sampling(ref, dropin, name):
+    """matricize, column_sq_norms, column_distribution, sample_with_replacement
+    and unique_first_occurrence through the drop-in: bit-identical."""
+    make, mode, s = CASES[name]
+    x = make()
+    ta, tb = ref.tensor(x.shape, x.flat_idx(), x.val), dropin.tensor(x.shape, x.flat_idx(), x.val)
+    (ma, na), (mb, nb) = ref.matricize(ta, mode), dropin.matricize(tb, mode)
+    assert np.array_equal(ma.col_ptr, mb.col_ptr) and np.array_equal(ma.row, mb.row)
+    assert np.array_equal(ma.val.view(np.int64), mb.val.view(np.int64))
+    assert np.array_equal(na.view(np.int64), nb.view(np.int64))
+    (pa, ta_), (pb, tb_) = ref.column_distribution(ta, mode), dropin.column_distribution(tb, mode)
+    assert ta_ == tb_ and np.array_equal(pa.view(np.int64), pb.view(np.int64))
+    for seed in (1, 42, 2**63 + 5):
+        da, db = ref.sample_with_replacement(pa, s, seed), dropin.sample_with_replacement(pb, s, seed)
+        assert np.array_equal(da, db)
+        assert np.array_equal(ref.unique_first_occurrence(da), dropin.unique_first_occurrence(db))
+
+
+@pytest.mark.gpu
+@needs_dropin
+def test_dropin_run_stream(ref, dropin):
+    """The reference's own run_stream (stream_harness.cpp:48-107) through the
+    drop-in: every ctd_d_step, StreamState::factors and relative_error on the
+    GPU, per-step kept counts and memory usage equal, errors within 1e-9."""
+    x = g.c3_stream(seed=6, n_steps=4, slices_per_step=3, draws_per_slice=2500, n=300, planted_step=3, block=20)
+    a = ref.run_stream(ref.tensor(x.shape, x.flat_idx(), x.val), 0, 120, 40, 0.5, 1e-6, 7)
+    b = dropin.run_stream(dropin.tensor(x.shape, x.flat_idx(), x.val), 0, 120, 40, 0.5, 1e-6, 7)
+    assert np.array_equal(a["step"], b["step"])
+    assert np.array_equal(a["kept_fibers"], b["kept_fibers"])
+    assert np.array_equal(a["memory_usage"], b["memory_usage"])
+    for ea, eb in zip(a["relative_error"], b["relative_error"]):
+        assert abs(ea - eb) <= 1e-9 * max(1.0, abs(ea)), (ea, eb)
