@@ -258,9 +258,11 @@ StreamState __wrap__ZN3ctd11init_streamERKNS_12SparseTensorEildmbb(const SparseT
                                                                   bool exact_core) {
   Tensor t(historical);
   ctd_gpu_stream* s = nullptr;
-  // exact_core: the device stream keeps its own history for the bottom-left
-  // block (ctd_dynamic.cpp:207-211); the host copy below serves core_drift
-  const unsigned flags = CTD_GPU_WITH_CORE | (exact_core ? CTD_GPU_EXACT_CORE : 0u);
+  // keep_history / exact_core: the device stream keeps its own history (the
+  // bottom-left block, ctd_dynamic.cpp:207-211, and core_drift); the host
+  // copy is appended lazily on sync
+  const unsigned flags = CTD_GPU_WITH_CORE | (exact_core ? CTD_GPU_EXACT_CORE : 0u) |
+                        (keep_history ? CTD_GPU_KEEP_HISTORY : 0u);
   rethrow(ctd_gpu_stream_init(context(), t.h, mode, sample_size, epsilon, seed, flags, &s));
   StreamState st{FiberBasis(historical.extent(mode)), SparseMatrix(0, 0), historical.shape(), mode, 0, epsilon,
                  seed, {}};
