@@ -252,7 +252,7 @@ struct FArgs {
 };
 
 constexpr int kTraceW = 32;  // clock64 slots per candidate
-constexpr int kSpecRun = 8;  // consecutive rejections that hand over to the batch certifier
+constexpr int kSpecRun = 2;  // consecutive rejections that hand over to the batch certifier
 __device__ __forceinline__ void stamp(long long* tr, int n, int k) {
   if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[(long long)n * kTraceW + k] = clock64();
 }
@@ -462,7 +462,7 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   fa.prev_n0 = -1;
   static const bool no_spec = getenv("CTD_NO_SPEC") != nullptr;
   fa.exit_run = (!no_spec && !want_y && n > kSpecRun) ? kSpecRun : 0;
-  int64_t spec_b = 256;
+  int64_t spec_b = 64;
   ctx->phase_end();
   ctx->phase_begin(PH_FILTER);
   for (;;) {
@@ -484,8 +484,8 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
       out.n_spec += L;
       pos += L;
       if (pos >= n) break;
-      if (L < spec_b) {
-        spec_b = std::max<int64_t>(64, spec_b / 2);
+      if (L < spec_b) {  // the next batch sized to the run just seen
+        spec_b = std::min<int64_t>(4096, std::max<int64_t>(32, 2 * L + 32));
         break;
       }
       spec_b = std::min<int64_t>(spec_b * 2, 4096);

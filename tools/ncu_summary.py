@@ -28,6 +28,7 @@ METRICS = {
     "launch__grid_size": "grid",
     "launch__block_size": "block",
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active": "dmma_pipe_pct",
     "lts__t_bytes.sum": "l2_bytes",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
@@ -40,16 +41,25 @@ def short(name):
 
 
 def launches(path):
+    """Per kernel: launch times (s) and DRAM bytes, from an ncu --csv metrics list."""
     rows = list(csv.reader(open(path)))
     h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[h]
-    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    agg = collections.OrderedDict()
+    ki, ni, vi, ui = (hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"),
+                      hdr.index("Metric Unit"))
+    ii = hdr.index("ID")
+    per = collections.OrderedDict()
     for r in rows[h + 1:]:
         if len(r) <= vi:
             continue
-        v = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1e-9)
-        agg.setdefault(short(r[ki]), []).append(v)
+        v = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1e-9 if "time" in r[ni] else 1.0)
+        per.setdefault((r[ii], short(r[ki])), {})[r[ni]] = v
+    agg = collections.OrderedDict()
+    for (_, k), m in per.items():
+        a = agg.setdefault(k, {"t": [], "rd": 0.0, "wr": 0.0})
+        a["t"].append(m.get("gpu__time_duration.sum", 0.0))
+        a["rd"] += m.get("dram__bytes_read.sum", 0.0)
+        a["wr"] += m.get("dram__bytes_write.sum", 0.0)
     return agg
 
 
@@ -76,19 +86,24 @@ def main():
     ap.add_argument("--round", default="r1")
     ap.add_argument("--launches")
     ap.add_argument("--reports", nargs="*", default=[])
+    ap.add_argument("--name", default="launches", help="output file suffix for the launch list")
+    ap.add_argument("--command", default="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu")
     a = ap.parse_args()
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     if a.launches:
         agg = launches(a.launches)
-        tot = sum(sum(v) for v in agg.values())
-        lines = [f"# {a.round}: kernel launch list (ncu gpu__time_duration, --clock-control none)", "",
-                 "Command: `ncu --metrics gpu__time_duration.sum --clock-control none --csv "
-                 "python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu` (warm-up + timed steps "
-                 "+ error pass; cold-cache and serialised, so compare shares, not absolutes).", "",
-                 "| kernel | launches | total ms | mean ms | share |", "|---|---|---|---|---|"]
-        for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-            lines.append(f"| {k} | {len(v)} | {sum(v) * 1e3:.3f} | {sum(v) / len(v) * 1e3:.4f} | {sum(v) / tot:.3f} |")
-        open(os.path.join(ROOT, "profiles", f"{a.round}_launches.md"), "w").write("\n".join(lines) + "\n")
+        tot = sum(sum(v["t"]) for v in agg.values())
+        lines = [f"# {a.round}: kernel launch list (ncu gpu__time_duration + DRAM bytes, --clock-control none)", "",
+                 f"Command: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
+                 f"--clock-control none --csv {a.command}` (cold-cache and serialised: compare shares, not "
+                 "absolutes).", "",
+                 "| kernel | launches | total ms | mean ms | share | DRAM read MB | DRAM write MB |",
+                 "|---|---|---|---|---|---|---|"]
+        for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]["t"])):
+            t = v["t"]
+            lines.append(f"| {k} | {len(t)} | {sum(t) * 1e3:.3f} | {sum(t) / len(t) * 1e3:.4f} | "
+                         f"{sum(t) / tot:.3f} | {v['rd'] / 1e6:.1f} | {v['wr'] / 1e6:.1f} |")
+        open(os.path.join(ROOT, "profiles", f"{a.round}_{a.name}.md"), "w").write("\n".join(lines) + "\n")
     kern = []
     for p in a.reports:
         kern += report(p)
@@ -96,12 +111,13 @@ def main():
         json.dump(kern, open(os.path.join(ROOT, "profiles", f"{a.round}_kernels.json"), "w"), indent=1)
         lines = [f"# {a.round}: ncu --set full captures (per launch)", "",
                  "| kernel | time ms | DRAM read MB | DRAM write MB | DRAM % peak | SM % | warps active % | "
-                 "FP64 pipe % | regs | grid x block |", "|---|---|---|---|---|---|---|---|---|---|"]
+                 "FP64 pipe % | DMMA pipe % | regs | grid x block |", "|---|---|---|---|---|---|---|---|---|---|---|"]
         for d in kern:
             g = lambda k, s=1.0, f="{:.2f}": (f.format(d[k] * s) if d.get(k) is not None else "-")
             lines.append(f"| {d['kernel']} | {g('time', 1e3, '{:.3f}')} | {g('dram_read', 1e-6, '{:.1f}')} | "
                          f"{g('dram_write', 1e-6, '{:.1f}')} | {g('dram_pct')} | {g('sm_pct')} | "
-                         f"{g('warps_active_pct')} | {g('fp64_pipe_pct')} | {g('regs', 1, '{:.0f}')} | "
+                         f"{g('warps_active_pct')} | {g('fp64_pipe_pct')} | {g('dmma_pipe_pct')} | "
+                         f"{g('regs', 1, '{:.0f}')} | "
                          f"{g('grid', 1, '{:.0f}')} x {g('block', 1, '{:.0f}')} |")
         open(os.path.join(ROOT, "profiles", f"{a.round}_kernels.md"), "w").write("\n".join(lines) + "\n")
 
