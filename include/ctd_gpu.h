@@ -234,6 +234,22 @@ int ctd_gpu_shard_gather(const ctd_gpu_shard *s, int64_t n, const int64_t *cols,
 int ctd_gpu_shard_error_partials(const ctd_gpu_shard *s, const ctd_gpu_basis *b,
                                  double *x_sq, double *cross);
 int ctd_gpu_shard_destroy(ctd_gpu_shard *s);
+/* The sampling law chained across the shards' ascending fiber ranges instead
+ * of all-gathering every fiber (column_distribution / sample_with_replacement,
+ * sampling.cpp:21-64, whose sums are sequential over the columns):
+ *   seq_total: the sequential sum of this shard's squared norms resumed from
+ *     `start` (the running value after the earlier shards) -> *total;
+ *   cdf: p = n / total and this shard's segment of the cumulative array
+ *     resumed from `start` (kept on the shard); *end is its last value and
+ *     *has_positive whether any p > 0;
+ *   clamp: the tail clamp to 1.0 from the last positive p (the shard holding
+ *     the global last positive column calls it);
+ *   draw: the replicated mt19937_64(seed) uniforms; cols[i] = the fiber
+ *     upper_bound selects when it lies in this shard, else -1. */
+int ctd_gpu_shard_seq_total(const ctd_gpu_shard *s, double start, double *total);
+int ctd_gpu_shard_cdf(ctd_gpu_shard *s, double total, double start, double *end, int *has_positive);
+int ctd_gpu_shard_clamp(ctd_gpu_shard *s);
+int ctd_gpu_shard_draw(const ctd_gpu_shard *s, int64_t count, uint64_t seed, int64_t *cols);
 /* relative_error's two sums over the fibers of x (one shard):
  * x_sq = |X_p|^2 and cross = sum_j x_j^T (R U R^T) x_j; after summing the
  * shards, rel = (x_sq - cross) / x_sq. */

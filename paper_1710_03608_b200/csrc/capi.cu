@@ -34,6 +34,9 @@ struct ctd_gpu_shard {
   Ctx* ctx;
   Fibers fb;                       // the shard's bucketed fibers, resident in HBM
   std::vector<int64_t> col, ptr;   // host copies for owner lookups
+  Buf<double> cum;                 // this shard's segment of the global CDF (ctd_gpu_shard_cdf)
+  Buf<int> last_pos;               // last fiber with p > 0, or -1
+  double cum_lo = 0.0, cum_hi = 0.0;
 };
 
 namespace {
@@ -908,6 +911,104 @@ int ctd_gpu_shard_error_partials(const ctd_gpu_shard* s, const ctd_gpu_basis* b,
     if (s->fb.rows != b->b->dim) fail(CTD_ERR_SHAPE, "fiber length does not match basis");
     PhaseScope ps(s->ctx, PH_ERROR);
     error_partials(s->ctx, s->fb, *b->b, x_sq, cross);
+  });
+}
+
+// ---- the sampling law chained across fiber-range shards ---------------------
+namespace {
+
+// cum[0..n] of [start, x[0], ..., x[n-1]]: the reference's sequential sum
+// resumed from `start` (the running value at the end of the earlier shards).
+void seq_from(Ctx* c, double start, const double* x, int64_t n, Buf<double>& ext, double* end) {
+  ext.alloc(c, n + 1);
+  c->to_dev(ext.p, &start, 1);
+  if (n > 0)
+    CUDA_OK(cudaMemcpyAsync(ext.p + 1, x, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  Buf<double> out(c, n + 1), tot(c, 1);
+  seq_cumsum(c, ext.p, n + 1, out.p, tot.p);
+  *end = c->read1(tot.p);
+  ext = std::move(out);
+}
+
+__global__ void k_shard_draw(const uint64_t* raw, long long count, double lo, double hi, const double* cum,
+                             long long F, const int64_t* fcol, int64_t* out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const double u = (double)(raw[i] >> 11) * (1.0 / 9007199254740992.0);  // sampling.cpp:15-17
+  int64_t col = -1;
+  if (u >= lo && u < hi) {  // upper_bound (sampling.cpp:59-61) lands in this shard
+    long long a = 0, b = F;
+    while (a < b) {
+      const long long m = (a + b) >> 1;
+      if (cum[m] > u) b = m;
+      else a = m + 1;
+    }
+    col = a < F ? fcol[a] : -1;
+  }
+  out[i] = col;
+}
+
+}  // namespace
+
+int ctd_gpu_shard_seq_total(const ctd_gpu_shard* s, double start, double* total) {
+  return guarded([&] {
+    need(s, "shard");
+    bind_device(s->ctx);
+    need(total, "total");
+    Buf<double> ext;
+    seq_from(s->ctx, start, s->fb.norm.p, s->fb.F, ext, total);
+  });
+}
+
+int ctd_gpu_shard_cdf(ctd_gpu_shard* s, double total, double start, double* end, int* has_positive) {
+  return guarded([&] {
+    need(s, "shard");
+    bind_device(s->ctx);
+    need(end, "end");
+    if (!(total > 0.0)) fail(CTD_ERR_EMPTY_INPUT, "sampling from an all-zero distribution");
+    Ctx* c = s->ctx;
+    const int64_t F = s->fb.F;
+    Buf<double> pr(c, F + 1), dt(c, 1);
+    c->to_dev(dt.p, &total, 1);
+    s->last_pos.alloc(c, 1);
+    probs_from_norms(c, s->fb.norm.p, F, dt.p, pr.p, s->last_pos.p);
+    Buf<double> ext;
+    seq_from(c, start, pr.p, F, ext, end);
+    s->cum.alloc(c, F + 1);
+    if (F > 0) CUDA_OK(cudaMemcpyAsync(s->cum.p, ext.p + 1, F * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    const int lp = c->read1(s->last_pos.p);
+    if (has_positive) *has_positive = lp >= 0;
+    s->cum_lo = start;
+    s->cum_hi = *end;
+  });
+}
+
+int ctd_gpu_shard_clamp(ctd_gpu_shard* s) {
+  return guarded([&] {
+    need(s, "shard");
+    bind_device(s->ctx);
+    if (!s->cum.p || !s->last_pos.p) fail(CTD_ERR_ARGUMENT, "ctd_gpu_shard_cdf first");
+    clamp_from(s->ctx, s->cum.p, s->fb.F, s->last_pos.p);
+    s->cum_hi = 1.0;
+  });
+}
+
+int ctd_gpu_shard_draw(const ctd_gpu_shard* s, int64_t count, uint64_t seed, int64_t* cols) {
+  return guarded([&] {
+    need(s, "shard");
+    bind_device(s->ctx);
+    if (count < 0) fail(CTD_ERR_ARGUMENT, "sample count must be non-negative");
+    if (count == 0) return;
+    need(cols, "cols");
+    if (!s->cum.p) fail(CTD_ERR_ARGUMENT, "ctd_gpu_shard_cdf first");
+    Ctx* c = s->ctx;
+    Buf<uint64_t> raw(c, count);
+    mt19937_64(c, seed, count, raw.p);
+    Buf<int64_t> out(c, count);
+    LAUNCH(c, k_shard_draw, ceil_div(count, 256), 256, 0, raw.p, (long long)count, s->cum_lo, s->cum_hi, s->cum.p,
+           (long long)s->fb.F, s->fb.col.p, out.p);
+    c->to_host(cols, out.p, count);
+    c->sync();
   });
 }
 

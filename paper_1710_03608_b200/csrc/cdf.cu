@@ -448,6 +448,18 @@ void sampling_law(Ctx* ctx, const double* norms, int64_t F, double* d_total, dou
   LAUNCH(ctx, k_clamp, ceil_div(F > 0 ? F : 1, 256), 256, 0, cum, (long long)F, lp.p, d_law_flags);
 }
 
+void probs_from_norms(Ctx* ctx, const double* norms, int64_t F, const double* d_total, double* probs,
+                      int* d_last_pos) {
+  CUDA_OK(cudaMemsetAsync(d_last_pos, 0xff, sizeof(int), ctx->stream));
+  if (F > 0) LAUNCH(ctx, k_probs, ceil_div(F, 256), 256, 0, norms, (long long)F, d_total, probs, d_last_pos);
+}
+
+void clamp_from(Ctx* ctx, double* cum, int64_t n, const int* d_last_pos) {
+  Buf<unsigned> fl(ctx, 1);
+  fl.zero();
+  if (n > 0) LAUNCH(ctx, k_clamp, ceil_div(n, 256), 256, 0, cum, (long long)n, d_last_pos, fl.p);
+}
+
 void clamped_cdf(Ctx* ctx, const double* probs, int64_t n, double* cum, unsigned* d_flags) {
   Buf<int> lp(ctx, 1);
   CUDA_OK(cudaMemsetAsync(lp.p, 0xff, sizeof(int), ctx->stream));

@@ -4,11 +4,15 @@ partitioned by contiguous fiber-id range.
 Per rank (reference functions in parentheses):
   1. bucket the local shard and compute its fibers' exact squared norms
      (matricize + column_sq_norms, tensor_ops.cpp:118-135,194-202);
-  2. all-gather the fibers' global column ids and norms; because the shards are
-     contiguous ascending fiber ranges the concatenation is the global fiber
-     list in column order, so every rank computes the identical bit-exact law,
-     draws and dedup (column_distribution / sample_with_replacement /
-     unique_first_occurrence, sampling.cpp:21-78);
+  2. the sampling law's two sequential sums (the normalizer and the CDF,
+     sampling.cpp:26-27,42-49) run over the columns in order, and the shards are
+     ascending column ranges, so each sum is CHAINED across the ranks: rank r
+     resumes it from the running value rank r-1 passes on (one double per hop)
+     over its own fibers only, bit-exact.  Every rank then generates the same
+     mt19937_64 uniforms and resolves the draws that fall in its CDF segment;
+     an all-gather of the (draw, fiber) pairs and a replicated dedup give the
+     unique list (sample_with_replacement / unique_first_occurrence,
+     sampling.cpp:33-78).  Law work per rank is its shard, whatever N is;
   3. the owner of each unique candidate contributes its fiber; an all-gather
      assembles every candidate in draw order on every rank;
   4. the filter and U recurrence run replicated (deterministic: identical
@@ -110,6 +114,28 @@ class Comm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t.cpu().numpy()
 
+    def chain(self, fn, start: float = 0.0):
+        """Sequential hand-off in rank order: rank r receives the value rank r-1
+        produced (rank 0 starts from `start`), applies fn, passes the result on.
+        Returns (value received, value produced)."""
+        v = self.torch.tensor([start], dtype=self.torch.float64, device=self.device)
+        if self.rank > 0:
+            self.dist.recv(v, src=self.global_rank(self.rank - 1), group=self.group)
+        c_in = float(v.item())
+        c_out = fn(c_in)
+        if self.rank < self.world - 1:
+            v = self.torch.tensor([c_out], dtype=self.torch.float64, device=self.device)
+            self.dist.send(v, dst=self.global_rank(self.rank + 1), group=self.group)
+        return c_in, c_out
+
+    def bcast(self, value: float, src: int) -> float:
+        v = self.torch.tensor([value], dtype=self.torch.float64, device=self.device)
+        self.dist.broadcast(v, src=self.global_rank(src), group=self.group)
+        return float(v.item())
+
+    def global_rank(self, r: int) -> int:
+        return r if self.group is None else self.dist.get_global_rank(self.group, r)
+
 
 # ---------------------------------------------------------------------------
 # per-rank kernels (the C-ABI library)
@@ -138,6 +164,14 @@ class GpuKernels:
             shape, idx, val = x
             x = api.DeviceTensor(api.SparseTensor(list(shape), idx, val), self.ctx)
         return _GpuShard(self, x, mode)
+
+    def unique(self, drawn):
+        drawn = np.ascontiguousarray(drawn, np.int64)
+        out = np.zeros(max(drawn.shape[0], 1), np.int64)
+        n = C.c_int64()
+        api._check(self.L.ctd_gpu_unique_first_occurrence(self.ctx.h, api._p(drawn), drawn.shape[0], api._p(out),
+                                                          C.byref(n)))
+        return out[:n.value].copy()
 
     def sample_fibers(self, col, norm, s, seed):
         col = np.ascontiguousarray(col, dtype=np.int64)
@@ -179,6 +213,26 @@ class _GpuShard:
         xs, cr = C.c_double(), C.c_double()
         api._check(self.k.L.ctd_gpu_shard_error_partials(self.h, basis.h, C.byref(xs), C.byref(cr)))
         return xs.value, cr.value
+
+    # the chained sampling law (ctd_gpu_shard_seq_total / _cdf / _clamp / _draw)
+    def seq_total(self, start):
+        out = C.c_double()
+        api._check(self.k.L.ctd_gpu_shard_seq_total(self.h, C.c_double(start), C.byref(out)))
+        return out.value
+
+    def cdf(self, total, start):
+        end, pos = C.c_double(), C.c_int()
+        api._check(self.k.L.ctd_gpu_shard_cdf(self.h, C.c_double(total), C.c_double(start), C.byref(end),
+                                              C.byref(pos)))
+        return end.value, bool(pos.value)
+
+    def clamp(self):
+        api._check(self.k.L.ctd_gpu_shard_clamp(self.h))
+
+    def draw(self, count, seed):
+        out = np.zeros(max(count, 1), np.int64)
+        api._check(self.k.L.ctd_gpu_shard_draw(self.h, count, C.c_uint64(seed), api._p(out)))
+        return out[:count]
 
     def close(self):
         if getattr(self, "h", None):
@@ -262,6 +316,87 @@ class ShardedResult:
     stats: dict = field(default_factory=dict)
 
 
+def _check_ranges(sh, comm) -> int:
+    """Shards must be disjoint ascending fiber ranges in rank order (checked on
+    every rank's first/last column); returns the global fiber count."""
+    ends = np.array([sh.col[0], sh.col[-1]] if sh.col.shape[0] else [-1, -1], dtype=np.int64)
+    last = -1
+    for e in comm.allgather(ends):
+        if e[0] < 0:
+            continue
+        if e[0] <= last:
+            raise api.ArgumentError("shards must hold disjoint ascending fiber ranges in rank order")
+        last = e[1]
+    return int(comm.allreduce_sum(np.array([sh.col.shape[0]], dtype=np.int64))[0])
+
+
+def _sample_sharded(sh, comm, k, count: int, seed: int):
+    """column_distribution + sample_with_replacement + unique_first_occurrence
+    (sampling.cpp:21-78) over the ranks' fiber ranges: the normalizer and the
+    CDF are sequential sums over the columns in order, so each is chained rank
+    to rank (one double per hop, every rank summing only its own fibers); the
+    rank whose CDF segment holds a uniform resolves that draw."""
+    _, t_last = comm.chain(sh.seq_total, 0.0)
+    total = comm.bcast(t_last, comm.world - 1)
+    if not (total > 0.0):
+        raise api.EmptyInputError("column distribution of a tensor without nonzero entries")
+    flag = {}
+
+    def cdf(start):
+        end, has = sh.cdf(total, start)
+        flag["has"] = has
+        return end
+
+    comm.chain(cdf, 0.0)
+    flags = comm.allgather(np.array([1 if flag["has"] else 0], dtype=np.int64))
+    if comm.rank == max(r for r, f in enumerate(flags) if f[0]):
+        sh.clamp()  # the tail clamp on the rank holding the last positive column (:54)
+    mine = sh.draw(count, seed)
+    got = comm.allgather(np.stack([np.nonzero(mine >= 0)[0], mine[mine >= 0]], 1).reshape(-1).astype(np.int64))
+    drawn = np.full(count, -1, np.int64)
+    for g in got:
+        g = g.reshape(-1, 2)
+        drawn[g[:, 0]] = g[:, 1]
+    if (drawn < 0).any():
+        raise api.CtdError("a draw fell in no shard's CDF segment")
+    return total, k.unique(drawn)
+
+
+def _gather_candidates(sh, comm, unique):
+    """The unique candidates' fibers from their owners, all-gathered and laid
+    out in draw order (CSC: ptr, rows, vals) on every rank."""
+    pos = np.searchsorted(sh.col, unique)
+    ok = pos < sh.col.shape[0]
+    mine = np.zeros(unique.shape[0], bool)
+    mine[ok] = sh.col[pos[ok]] == unique[ok]
+    which = np.nonzero(mine)[0].astype(np.int64)
+    lptr, lrows, lvals = sh.gather(unique[which])
+    g_which = comm.allgather(which)
+    g_lens = comm.allgather(np.diff(lptr).astype(np.int64))
+    g_rows = comm.allgather(lrows.astype(np.int64))
+    g_vals = comm.allgather(lvals.astype(np.float64))
+    n_u = unique.shape[0]
+    owner = np.full(n_u, -1, np.int64)
+    cand_len = np.zeros(n_u, np.int64)
+    for r, (w, ln) in enumerate(zip(g_which, g_lens)):
+        owner[w] = r
+        cand_len[w] = ln
+    if n_u and owner.min() < 0:
+        raise api.CtdError("a drawn fiber has no owner (shards do not cover the fiber space)")
+    cptr = np.concatenate([[0], np.cumsum(cand_len)]).astype(np.int64)
+    crow = np.zeros(int(cptr[-1]), np.int64)
+    cval = np.zeros(int(cptr[-1]))
+    for w, ln, rr, vv in zip(g_which, g_lens, g_rows, g_vals):
+        if w.size == 0:
+            continue
+        n_e = int(ln.sum())
+        src0 = np.concatenate([[0], np.cumsum(ln)[:-1]])
+        dst_idx = np.repeat(cptr[w] - src0, ln) + np.arange(n_e)
+        crow[dst_idx] = rr[:n_e]
+        cval[dst_idx] = vv[:n_e]
+    return cptr, crow, cval
+
+
 def ctd_s_sharded(shape, local, mode: int, sample_size: int, epsilon: float = 1e-6, seed: int = 42,
                   comm: Optional[Comm] = None, kernels=None, with_error: bool = False) -> ShardedResult:
     """CTD-S front end over fiber-range shards; every rank returns the same
@@ -291,45 +426,13 @@ def ctd_s_sharded(shape, local, mode: int, sample_size: int, epsilon: float = 1e
     # 1. local bucketing + exact norms (resident)
     sh = k.shard(local if isinstance(local, api.DeviceTensor) else (shape, local[0], local[1]), mode)
     mark()
-    # 2. global fiber list (ranks own ascending ranges) -> replicated law/draws/dedup
-    gcol = np.concatenate(comm.allgather(sh.col.astype(np.int64)))
-    gnorm = np.concatenate(comm.allgather(sh.norm.astype(np.float64)))
-    if gcol.shape[0] > 1 and not np.all(gcol[1:] > gcol[:-1]):
-        raise api.ArgumentError("shards must hold disjoint ascending fiber ranges in rank order")
+    n_fibers = _check_ranges(sh, comm)
     mark()
-    total, unique = k.sample_fibers(gcol, gnorm, sample_size, seed)
+    # 2. the law, chained across the ranks; draws and dedup
+    total, unique = _sample_sharded(sh, comm, k, sample_size, seed)
     mark()
     # 3. candidate payloads from their owners, assembled in draw order
-    pos = np.searchsorted(sh.col, unique)
-    ok = pos < sh.col.shape[0]
-    mine = np.zeros(unique.shape[0], bool)
-    mine[ok] = sh.col[pos[ok]] == unique[ok]
-    which = np.nonzero(mine)[0].astype(np.int64)
-    lptr, lrows, lvals = sh.gather(unique[which])
-    g_which = comm.allgather(which)
-    g_lens = comm.allgather(np.diff(lptr).astype(np.int64))
-    g_rows = comm.allgather(lrows.astype(np.int64))
-    g_vals = comm.allgather(lvals.astype(np.float64))
-    n_u = unique.shape[0]
-    owner = np.full(n_u, -1, np.int64)
-    cand_len = np.zeros(n_u, np.int64)
-    for r, (w, ln) in enumerate(zip(g_which, g_lens)):
-        owner[w] = r
-        cand_len[w] = ln
-    if n_u and owner.min() < 0:
-        raise api.CtdError("a drawn fiber has no owner (shards do not cover the fiber space)")
-    cptr = np.concatenate([[0], np.cumsum(cand_len)]).astype(np.int64)
-    crow = np.zeros(int(cptr[-1]), np.int64)
-    cval = np.zeros(int(cptr[-1]))
-    for w, ln, rr, vv in zip(g_which, g_lens, g_rows, g_vals):
-        if w.size == 0:
-            continue
-        # scatter each owned candidate's entries to its slot in draw order
-        n_e = int(ln.sum())
-        src0 = np.concatenate([[0], np.cumsum(ln)[:-1]])
-        dst_idx = np.repeat(cptr[w] - src0, ln) + np.arange(n_e)
-        crow[dst_idx] = rr[:n_e]
-        cval[dst_idx] = vv[:n_e]
+    cptr, crow, cval = _gather_candidates(sh, comm, unique)
     mark()
     # 4. replicated filter + U recurrence
     dim = int(shape[mode])
@@ -340,10 +443,10 @@ def ctd_s_sharded(shape, local, mode: int, sample_size: int, epsilon: float = 1e
     rp, rr, rv = B.r()
     mark()
     if trace:
-        names = ["shard", "allgather fibers", "law+draws", "candidates", "filter+U/R"]
+        names = ["shard", "range check", "law+draws", "candidates", "filter+U/R"]
         print("[dist trace] rank %d: " % comm.rank + " ".join(
             f"{n}={1e3 * (b - a):.1f}ms" for n, a, b in zip(names, tm[:-1], tm[1:])), flush=True)
-    res = ShardedResult(kept, U, rp, rr, rv, unique, acc, deg, dl, float(total), None, int(gcol.shape[0]),
+    res = ShardedResult(kept, U, rp, rr, rv, unique, acc, deg, dl, float(total), None, n_fibers,
                         {"local_fibers": int(sh.col.shape[0]), "candidate_nnz": int(cptr[-1])})
     # 5. error partials, all-reduced
     if with_error:
@@ -355,3 +458,57 @@ def ctd_s_sharded(shape, local, mode: int, sample_size: int, epsilon: float = 1e
     B.close()
     sh.close()
     return res
+
+
+# ---------------------------------------------------------------------------
+# CTD-D over fiber-range shards
+
+class ShardedStream:
+    """init_stream / ctd_d_step (ctd_dynamic.cpp:129-229) with every slab split
+    by fiber range across the ranks: each step buckets the rank's part of the
+    slab, runs the chained law with seed ^ t (:177), gathers the candidates and
+    filters them against the replicated basis (:178-187).  Every rank holds the
+    same kept ids (flat ids j + t * slab_columns on the grown shape, :184-185),
+    R and U.  The Eq. 13 core is not maintained (the front end of the step,
+    as the C3 latency line measures it)."""
+
+    def __init__(self, hist_shape, local, mode: int, sample_size: int, epsilon: float = 1e-6, seed: int = 42,
+                 comm: Optional[Comm] = None, kernels=None):
+        self.comm = comm or Comm()
+        self.k = kernels or GpuKernels()
+        if len(hist_shape) < 2 or not (0 <= mode < len(hist_shape) - 1):
+            raise api.ArgumentError("mode must precede the time mode")
+        self.mode, self.eps, self.seed = mode, epsilon, seed
+        self.slab_shape = list(hist_shape[:-1])
+        self.slab_cols = int(np.prod([n for i, n in enumerate(self.slab_shape) if i != mode], dtype=np.int64))
+        self.t = int(hist_shape[-1])
+        sh = self.k.shard((list(hist_shape), local[0], local[1]), mode)
+        _check_ranges(sh, self.comm)
+        _, unique = _sample_sharded(sh, self.comm, self.k, sample_size, seed)
+        cptr, crow, cval = _gather_candidates(sh, self.comm, unique)
+        sh.close()
+        self.B = self.k.basis(int(hist_shape[mode]))
+        acc, _, _ = self.B.append_batch(cptr, crow, cval, epsilon)
+        self.kept_flat = list(unique[np.nonzero(acc)[0]])
+
+    def step(self, local, sample_size: int):
+        """One slab of time extent 1; `local` = this rank's (idx, val) of it (slab
+        index space, time coordinate 0) in its fiber range."""
+        idx, val = local
+        nnz = int(self.comm.allreduce_sum(np.array([len(val)], dtype=np.int64))[0])
+        if nnz > 0:
+            sh = self.k.shard((self.slab_shape + [1], idx, val), self.mode)
+            _check_ranges(sh, self.comm)
+            _, unique = _sample_sharded(sh, self.comm, self.k, sample_size, self.seed ^ self.t)
+            cptr, crow, cval = _gather_candidates(sh, self.comm, unique)
+            sh.close()
+            acc, _, _ = self.B.append_batch(cptr, crow, cval, self.eps)
+            self.kept_flat += [int(j) + self.t * self.slab_cols for j in unique[np.nonzero(acc)[0]]]
+        self.t += 1
+        return self
+
+    def U(self):
+        return self.B.u()
+
+    def close(self):
+        self.B.close()

@@ -26,12 +26,16 @@ class OracleKernels:
         uniq = self.P.unique_first_occurrence(drawn)
         return total, np.asarray(col, dtype=np.int64)[uniq]
 
+    def unique(self, drawn):
+        return self.P.unique_first_occurrence(drawn)
+
     def basis(self, dim):
         return _OracleBasis(self.P.basis(dim))
 
 
 class _OracleShard:
     def __init__(self, P, shape, idx, val, mode):
+        self.P = P
         m = P.matricize(shape, np.asarray(idx).reshape(-1), val, mode)
         counts = np.diff(m.col_ptr)
         cols = np.nonzero(counts > 0)[0].astype(np.int64)
@@ -40,6 +44,38 @@ class _OracleShard:
         self.lf = LocalFibers(cols, np.concatenate([[0], np.cumsum(counts[cols])]).astype(np.int64),
                               m.row[sel].astype(np.int64), m.val[sel], P.column_sq_norms(m)[cols])
         self.col, self.norm = self.lf.col, self.lf.norm
+
+    # the chained law (sampling.cpp:26-27,42-54): sequential sums resumed from
+    # the running value of the earlier shards
+    def seq_total(self, start):
+        t = float(start)
+        for v in self.norm:
+            t += float(v)
+        return t
+
+    def cdf(self, total, start):
+        self.probs = np.asarray(self.norm, dtype=np.float64) / total
+        c = float(start)
+        self.cum = np.zeros(self.probs.shape[0])
+        for i, p in enumerate(self.probs):
+            c += float(p)
+            self.cum[i] = c
+        self.lo, self.hi = float(start), c
+        pos = np.nonzero(self.probs > 0)[0]
+        self.last_pos = int(pos[-1]) if pos.size else -1
+        return c, self.last_pos >= 0
+
+    def clamp(self):
+        self.cum[self.last_pos:] = 1.0
+        self.hi = 1.0
+
+    def draw(self, count, seed):
+        raw = self.P.mt19937_64(seed, count)
+        u = (raw >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+        out = np.full(count, -1, np.int64)
+        sel = (u >= self.lo) & (u < self.hi)
+        out[sel] = self.col[np.searchsorted(self.cum, u[sel], side="right")]
+        return out
 
     def gather(self, cols):
         lf = self.lf

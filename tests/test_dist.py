@@ -1,7 +1,7 @@
 """Sharded CTD-S (paper_1710_03608_b200.dist) with world_size 2.
 
 CPU: two gloo ranks run the sharded host logic (fiber-range shards, all-gather
-of fiber norms and candidate payloads, replicated filter, all-reduced error
+of candidate payloads, the sampling law chained rank to rank, replicated filter, all-reduced error
 partials) with oracle-backed per-rank kernels; the replicated result must equal
 the single-process oracle bit for bit (kept ids, decisions, U) and the error
 within 1e-9.  GPU: the same with the C-ABI kernels (two ranks on one device,
@@ -130,3 +130,75 @@ def test_sharded_gpu_two_ranks_equal_single_gpu(case, mode, s, tmp_path):
         assert np.array_equal(r["kept"], f.kept_flat)
         assert np.array_equal(r["U"].view(np.int64), f.U.view(np.int64))
         assert abs(float(r["rel"]) - f.relative_error) <= 1e-9 * max(1.0, abs(f.relative_error))
+
+
+def _stream_worker(rank, world, port, backend, out):
+    import torch.distributed as tdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x = datagen.c3_stream(seed=5, n_steps=3, slices_per_step=3, draws_per_slice=2500, n=300, planted_step=2,
+                              block=20)
+        hist = x.time_slab(0, 3)
+        if backend == "oracle":
+            from oracle.bindings import Port
+            from dist_oracle_kernels import OracleKernels
+            k = OracleKernels(Port())
+        else:
+            k = dist.GpuKernels()
+        comm = dist.Comm()
+        hb = dist.fiber_range_bounds(hist.shape, 0, hist.idx, world)
+        st = dist.ShardedStream(hist.shape, dist.shard(hist.shape, hist.idx, hist.val, 0, hb, rank), 0, 120, 1e-6,
+                                7, comm=comm, kernels=k)
+        kept = [np.array(st.kept_flat, np.int64)]
+        for t in range(3, x.shape[2]):
+            sl = x.time_slab(t, t + 1)
+            sb = dist.fiber_range_bounds(sl.shape, 0, sl.idx, world)
+            st.step(dist.shard(sl.shape, sl.idx, sl.val, 0, sb, rank), 40)
+            kept.append(np.array(st.kept_flat, np.int64))
+        np.savez(os.path.join(out, f"s{rank}.npz"), U=st.U(), t=st.t,
+                 **{f"k{i}": k_ for i, k_ in enumerate(kept)})
+        st.close()
+    finally:
+        tdist.destroy_process_group()
+
+
+def _run_stream(backend, tmp_path, world=2):
+    import torch.multiprocessing as mp
+    mp.spawn(_stream_worker, args=(world, _free_port(), backend, str(tmp_path)), nprocs=world, join=True)
+    return [dict(np.load(tmp_path / f"s{r}.npz")) for r in range(world)]
+
+
+def test_sharded_stream_equals_single_process(port, tmp_path):
+    """CTD-D with every slab split by fiber range over two ranks (gloo, CPU
+    kernels): kept ids after every step and U equal the single-process
+    restatement's stream (front end; the core is not kept on either side)."""
+    res = _run_stream("oracle", tmp_path)
+    x = datagen.c3_stream(seed=5, n_steps=3, slices_per_step=3, draws_per_slice=2500, n=300, planted_step=2, block=20)
+    hist = x.time_slab(0, 3)
+    ps = port.stream(hist.shape, hist.flat_idx(), hist.val, 0, 120, 1e-6, 7, core=False)
+    want = [ps.kept_flat()]
+    for t in range(3, x.shape[2]):
+        sl = x.time_slab(t, t + 1)
+        ps.step(sl.shape, sl.flat_idx(), sl.val, 40)
+        want.append(ps.kept_flat())
+    for r in res:
+        for i, w in enumerate(want):
+            assert np.array_equal(r[f"k{i}"], w), i
+        assert int(r["t"]) == x.shape[2]
+        assert np.array_equal(r["U"].view(np.int64), ps.U().view(np.int64))
+
+
+@pytest.mark.gpu
+def test_sharded_stream_gpu_two_ranks(port, tmp_path):
+    res = _run_stream("gpu", tmp_path)
+    x = datagen.c3_stream(seed=5, n_steps=3, slices_per_step=3, draws_per_slice=2500, n=300, planted_step=2, block=20)
+    hist = x.time_slab(0, 3)
+    ps = port.stream(hist.shape, hist.flat_idx(), hist.val, 0, 120, 1e-6, 7, core=False)
+    for t in range(3, x.shape[2]):
+        sl = x.time_slab(t, t + 1)
+        ps.step(sl.shape, sl.flat_idx(), sl.val, 40)
+    for r in res:
+        assert np.array_equal(r[f"k{x.shape[2] - 3}"], ps.kept_flat())
+        assert np.array_equal(r["U"].view(np.int64), ps.U().view(np.int64))
