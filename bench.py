@@ -21,6 +21,7 @@ torch.distributed.run with N ranks (fails if fewer than N GPUs are visible).
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import math
 import os
@@ -317,6 +318,52 @@ def run_c4(args, ctx, torch):
                                                   "single-threaded"}
         except Exception as e:  # pragma: no cover
             out["cpu_reference"] = {"sample": f"failed: {e}"}
+    return out
+
+
+def run_full_ctd_s(args, ctx, torch):
+    """The reference's whole ctd_s (ctd_static.cpp:19-50), compute_core
+    (C = X x_mode R^T, tensor_ops.cpp:27-59) included, on the configs where the
+    reference finishes: C1 (configs[0]) against the reference, and C4
+    (configs[3], C fully dense: ~1e8 entries) where the reference's
+    compute_core alone takes ~3 min (SURVEY probe: DNF in this budget)."""
+    from paper_1710_03608_b200 import ctd as api
+    from paper_1710_03608_b200 import datagen
+    out = {}
+    for name, x, s in (("c1", datagen.c1(), 200), ("c4", load_c4(), C4["c"])):
+        d = api.DeviceTensor(api.SparseTensor.from_datagen(x), ctx)
+        times = []
+        for it in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            h, info = api.ctd_s_raw(d, 0, s, 1e-6, 42, ctx=ctx, with_core=True)
+            e1.record()
+            torch.cuda.synchronize()
+            if it:
+                times.append(e0.elapsed_time(e1))
+            api.free_factors(ctx, h)
+        d.close()
+        o = {"gpu_ms": round(float(np.median(times)), 3), "nnz": x.nnz, "kept": info.kept, "c_nnz": info.c_nnz}
+        if not args.no_cpu and name == "c1":
+            try:
+                from oracle.bindings import Ref, ref_available
+                if ref_available():
+                    R = Ref()
+                    t = R.tensor(x.shape, x.flat_idx(), x.val)
+                    secs = []
+                    for _ in range(3):
+                        h2 = C.c_void_p()
+                        R._chk(R.L.ref_ctd_s(t.h, 0, s, 1e-6, C.c_uint64(42), C.byref(h2)), "ctd_s")
+                        fe = R._factors(h2, False)
+                        R.L.ref_factors_free(h2)
+                        secs.append(fe.seconds)
+                    o["reference_ms"] = round(float(np.median(secs)) * 1e3, 3)
+                    o["speedup"] = round(o["reference_ms"] / o["gpu_ms"], 1)
+            except Exception as e:  # pragma: no cover
+                o["reference"] = f"failed: {e}"
+        elif name == "c4":
+            o["reference"] = "DNF: the reference's compute_core alone takes ~176 s at C4 (BASELINE.md section 4)"
+        out[name] = o
     return out
 
 
@@ -789,9 +836,13 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_ctdd:
         ctdd = run_ctd_d(args, ctx, torch)
 
-    c4 = c5 = None
+    c4 = c5 = full = None
     if rank == 0 and world == 1 and not args.no_c4:
         c4 = run_c4(args, ctx, torch)
+        try:
+            full = run_full_ctd_s(args, ctx, torch)
+        except Exception as e:  # pragma: no cover
+            full = {"failed": str(e)}
     if rank == 0 and world == 1 and not args.no_c5:
         del idx_t, val_t
         dt.close()
@@ -834,6 +885,8 @@ def run_ours(args, rank, world, local_rank):
         line["ctd_d"] = ctdd
     if c4 is not None:
         line["c4"] = c4
+    if full is not None:
+        line["ctd_s_with_core"] = full
     if c5 is not None:
         line["c5"] = c5
     if rank == 0:

@@ -528,14 +528,15 @@ def memory_usage(x, f: LRFactors, ctx: Optional[Context] = None) -> float:
 
 
 def ctd_s_raw(x, mode: int, sample_size: int, epsilon: float = 1e-6, seed: int = 42,
-              with_error: bool = False, ctx: Optional[Context] = None, keep_panel: bool = False):
+              with_error: bool = False, ctx: Optional[Context] = None, keep_panel: bool = False,
+              with_core: bool = False):
     """ctd_s without copying R/U to the host: returns (handle, FactorsInfo).
     Free the handle with ``free_factors``.  keep_panel: maintain the
     orthonormal panel so a later ``relative_error_raw`` takes one pass."""
     ctx = ctx or default_context()
     d = _dev(x, ctx)
     h = C.c_void_p()
-    flags = (WITH_ERROR if with_error else 0) | (KEEP_PANEL if keep_panel else 0)
+    flags = (WITH_ERROR if with_error else 0) | (KEEP_PANEL if keep_panel else 0) | (WITH_CORE if with_core else 0)
     _check(ctx.L.ctd_gpu_ctd_s(ctx.h, d.h, mode, sample_size, epsilon, C.c_uint64(seed), flags, C.byref(h)))
     info = _lib.FactorsInfo()
     _check(ctx.L.ctd_gpu_factors_info_get(h, C.byref(info)))
