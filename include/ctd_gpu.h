@@ -48,6 +48,9 @@ enum ctd_gpu_status {
    ctd_dynamic.hpp:42-45); both imply CTD_GPU_WITH_CORE */
 #define CTD_GPU_KEEP_HISTORY 0x8u /* retain the raw history on the device (core_drift) */
 #define CTD_GPU_EXACT_CORE 0x10u  /* bottom-left block from the history (ctd_dynamic.cpp:207-211) */
+#define CTD_GPU_LAZY_CORE 0x20u   /* maintain the Eq. 13 core as recorded blocks (the slab's columns and the
+                                     chain product's left factor (dR^T R) U per step), applied when the core
+                                     is read (stream factors, core_drift); implies CTD_GPU_WITH_CORE */
 
 typedef struct ctd_gpu_ctx ctd_gpu_ctx;         /* device, stream, scratch pool */
 typedef struct ctd_gpu_tensor ctd_gpu_tensor;   /* SparseTensor (sparse_tensor.hpp:17-60) resident in HBM */
@@ -265,12 +268,20 @@ int ctd_gpu_stream_init(ctd_gpu_ctx *ctx, const ctd_gpu_tensor *historical,
 int ctd_gpu_stream_step(ctd_gpu_stream *s, const ctd_gpu_tensor *slab,
                         int64_t sample_size);
 int64_t ctd_gpu_stream_t(const ctd_gpu_stream *s);
+/* kept_fibers.size() (-1 for a null stream). */
+int64_t ctd_gpu_stream_n_kept(const ctd_gpu_stream *s);
 /* Snapshot of the stream's factors (kept ids, R, U; core when maintained). */
 int ctd_gpu_stream_factors(ctd_gpu_stream *s, ctd_gpu_factors **out);
 /* core_drift (ctd_dynamic.hpp:64-66, ctd_dynamic.cpp:271-301): |C - R^T X_hist|_F
    against the retained history (CTD_GPU_KEEP_HISTORY or CTD_GPU_EXACT_CORE;
    otherwise CTD_ERR_ARGUMENT like the reference's ArgumentError). */
 int ctd_gpu_stream_core_drift(ctd_gpu_stream *s, double *out);
+/* CTD_GPU_LAZY_CORE: the recorded, not yet applied core updates (count and
+   device bytes); ctd_gpu_stream_core_sync applies them (factors and
+   core_drift do so themselves).  No reference counterpart: the reference
+   applies every update inside ctd_d_step (ctd_dynamic.cpp:149-229). */
+int ctd_gpu_stream_core_pending(const ctd_gpu_stream *s, int64_t *records, int64_t *bytes);
+int ctd_gpu_stream_core_sync(ctd_gpu_stream *s);
 int ctd_gpu_stream_destroy(ctd_gpu_stream *s);
 
 #ifdef __cplusplus

@@ -45,6 +45,8 @@ SIGNATURES = [
     ("ctd_gpu_tensor_destroy", _I, [_V]),
     ("ctd_gpu_matricize", _I, [_V, _V, _I, _P, _P, _P, _P, _P, _P]),
     ("ctd_gpu_column_distribution", _I, [_V, _V, _I, _P, _P, _P]),
+    ("ctd_gpu_column_sq_norms_csc", _I, [_V, _I64, _I64, _P, _P, _P, _P]),
+    ("ctd_gpu_column_distribution_csc", _I, [_V, _I64, _I64, _P, _P, _P, _P, _P]),
     ("ctd_gpu_sample_with_replacement", _I, [_V, _P, _I64, _I64, _U64, _P]),
     ("ctd_gpu_seq_cumsum", _I, [_V, _P, _I64, _P]),
     ("ctd_gpu_unique_first_occurrence", _I, [_V, _P, _I64, _P, _P]),
@@ -74,11 +76,18 @@ SIGNATURES = [
     ("ctd_gpu_shard_gather", _I, [_V, _I64, _P, _P, _P, _P]),
     ("ctd_gpu_shard_error_partials", _I, [_V, _V, _P, _P]),
     ("ctd_gpu_shard_destroy", _I, [_V]),
+    ("ctd_gpu_shard_seq_total", _I, [_V, _D, _P]),
+    ("ctd_gpu_shard_cdf", _I, [_V, _D, _D, _P, _P]),
+    ("ctd_gpu_shard_clamp", _I, [_V]),
+    ("ctd_gpu_shard_draw", _I, [_V, _I64, _U64, _P]),
     ("ctd_gpu_stream_init", _I, [_V, _V, _I, _I64, _D, _U64, C.c_uint, _PV]),
     ("ctd_gpu_stream_step", _I, [_V, _V, _I64]),
     ("ctd_gpu_stream_t", _I64, [_V]),
+    ("ctd_gpu_stream_n_kept", _I64, [_V]),
     ("ctd_gpu_stream_factors", _I, [_V, _PV]),
     ("ctd_gpu_stream_core_drift", _I, [_V, C.POINTER(C.c_double)]),
+    ("ctd_gpu_stream_core_pending", _I, [_V, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("ctd_gpu_stream_core_sync", _I, [_V]),
     ("ctd_gpu_stream_destroy", _I, [_V]),
 ]
 

@@ -215,7 +215,7 @@ int ctd_gpu_ctx_phase_times(ctd_gpu_ctx* ctx, double* ms, int64_t* counts, int r
 }
 
 const char* ctd_gpu_phase_name(int i) {
-  static const char* names[] = {"matricize", "law", "sample", "filter_prep", "filter", "error", "h2d", "other"};
+  static const char* names[] = {"matricize", "law", "sample", "filter_prep", "filter", "error", "h2d", "core"};
   return (i >= 0 && i < Ctx::kPhases) ? names[i] : "";
 }
 
@@ -1048,6 +1048,7 @@ int ctd_gpu_stream_step(ctd_gpu_stream* s, const ctd_gpu_tensor* slab, int64_t s
 }
 
 int64_t ctd_gpu_stream_t(const ctd_gpu_stream* s) { return s ? s->s.t : -1; }
+int64_t ctd_gpu_stream_n_kept(const ctd_gpu_stream* s) { return s ? (int64_t)s->s.kept_flat.size() : -1; }
 
 int ctd_gpu_stream_factors(ctd_gpu_stream* s, ctd_gpu_factors** out) {
   return guarded([&] {
@@ -1103,6 +1104,7 @@ int ctd_gpu_stream_factors(ctd_gpu_stream* s, ctd_gpu_factors** out) {
     }
     F.basis = std::move(nb);
     if (S.with_core) {  // StreamState::factors folds the core (:114-127); kept matricized here
+      stream_core_sync(s->s);
       const DevCore& dc = S.core;
       Core& cc = F.core;
       cc.rows = B.K;
@@ -1132,6 +1134,24 @@ int ctd_gpu_stream_core_drift(ctd_gpu_stream* s, double* out) {
     bind_device(s->s.ctx);
     need(out, "out");
     *out = stream_core_drift(s->s);
+  });
+}
+
+int ctd_gpu_stream_core_pending(const ctd_gpu_stream* s, int64_t* records, int64_t* bytes) {
+  return guarded([&] {
+    need(s, "stream");
+    need(records, "records");
+    need(bytes, "bytes");
+    *records = (int64_t)s->s.pending.size();
+    *bytes = (int64_t)s->s.arena.bytes();
+  });
+}
+
+int ctd_gpu_stream_core_sync(ctd_gpu_stream* s) {
+  return guarded([&] {
+    need(s, "stream");
+    bind_device(s->s.ctx);
+    stream_core_sync(s->s);
   });
 }
 

@@ -146,9 +146,16 @@ Tensor Stream::history() const {
   return h;
 }
 
+void stream_core_sync(Stream& st) {
+  for (const CoreRecord& r : st.pending) core_apply(st.ctx, st.core, r);
+  st.pending.clear();
+  st.arena.clear();
+}
+
 double stream_core_drift(Stream& st) {
   // ctd_dynamic.cpp:271-273
   if (!(st.keep_history || st.exact_core)) fail(CTD_ERR_ARGUMENT, "core drift requires retained history");
+  stream_core_sync(st);
   Fibers hf;
   matricize(st.ctx, st.history(), st.mode, hf);
   return core_drift(st.ctx, st.core, hf, *st.basis);
@@ -212,7 +219,7 @@ void run_ctd_s(Ctx* ctx, const Tensor& x, int mode, int64_t s, double eps, uint6
     out.rel_error = relative_error(ctx, fb, *out.basis);
   }
   if (flags & CTD_GPU_WITH_CORE) {  // factors.C = compute_core(x, R, mode) (ctd_static.cpp:47)
-    PhaseScope ps(ctx, PH_OTHER);
+    PhaseScope ps(ctx, PH_CORE);
     compute_core(ctx, fb, *out.basis, out.core);
     out.has_core = true;
   }
@@ -232,7 +239,8 @@ void stream_init(Ctx* ctx, const Tensor& hist, int mode, int64_t s, double eps, 
   Factors f;
   out.keep_history = (flags & CTD_GPU_KEEP_HISTORY) != 0;
   out.exact_core = (flags & CTD_GPU_EXACT_CORE) != 0;
-  out.with_core = (flags & (CTD_GPU_WITH_CORE | CTD_GPU_KEEP_HISTORY | CTD_GPU_EXACT_CORE)) != 0;
+  out.with_core = (flags & (CTD_GPU_WITH_CORE | CTD_GPU_KEEP_HISTORY | CTD_GPU_EXACT_CORE | CTD_GPU_LAZY_CORE)) != 0;
+  out.lazy_core = (flags & CTD_GPU_LAZY_CORE) != 0 && !out.exact_core;
   run_ctd_s(ctx, hist, mode, s, eps, seed, out.with_core ? CTD_GPU_WITH_CORE : 0, f);
   if (out.with_core) core_from_static(ctx, f.core, out.core);  // matricize(f.C, mode) (:141)
   out.ctx = ctx;
@@ -260,10 +268,12 @@ void stream_step(Stream& st, const Tensor& slab, int64_t d) {
     matricize(ctx, slab, st.mode, fb);
     // snapshot U^(t) for the core update (:165-167)
     const int64_t Kold = st.basis->K;
-    Buf<double> uold(ctx, st.with_core ? (size_t)Kold * Kold + 1 : 1);
-    if (st.with_core && Kold)
+    Buf<double>& uold = st.uold;
+    if (st.with_core && Kold) {
+      if (uold.n < (size_t)Kold * Kold) uold.alloc(ctx, (size_t)Kold * Kold * 3 / 2 + 1);  // amortized growth
       CUDA_OK(cudaMemcpy2DAsync(uold.p, Kold * sizeof(double), st.basis->U.p, st.basis->LD * sizeof(double),
                                 Kold * sizeof(double), Kold, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
     Front fr;
     front_end(ctx, fb, *st.basis, d, st.eps, st.seed ^ (uint64_t)st.t, fr, false);
     std::vector<int32_t> appended;
@@ -271,10 +281,14 @@ void stream_step(Stream& st, const Tensor& slab, int64_t d) {
       st.kept_flat.push_back(fr.unique[k] + st.t * fb.cols);
       appended.push_back(fr.unique_fib[k]);
     }
+    PhaseScope ps(ctx, PH_CORE);
     if (st.exact_core && !appended.empty()) {  // :207-211
       Fibers hf;
       matricize(ctx, st.history(), st.mode, hf);
       core_step_exact(ctx, st.core, fb, hf, *st.basis, Kold, st.t * fb.cols);
+    } else if (st.lazy_core) {
+      st.pending.emplace_back();
+      core_record(ctx, fb, *st.basis, Kold, uold.p, appended, st.t * fb.cols, &st.arena, st.pending.back());
     } else if (st.with_core) {
       core_step(ctx, st.core, fb, *st.basis, Kold, uold.p, appended, st.t * fb.cols);
     }

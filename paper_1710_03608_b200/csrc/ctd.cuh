@@ -56,6 +56,12 @@ struct Stream {
   std::vector<int64_t> kept_flat;
   bool with_core = false;  // CTD_GPU_WITH_CORE: maintain the Eq. 13 core
   DevCore core;
+  // CTD_GPU_LAZY_CORE: each step records its core inputs (CoreRecord) and the
+  // records are applied when the core is read (stream_core_sync)
+  bool lazy_core = false;
+  std::vector<CoreRecord> pending;
+  CoreArena arena;
+  Buf<double> uold;  // U^(t) snapshot for the core update (capacity grows)
   // retained raw history (StreamState::history, ctd_dynamic.hpp:28-32): the
   // concatenated slabs as device COO, `order` planes of hcap int32 indices
   bool keep_history = false, exact_core = false;
@@ -66,6 +72,8 @@ struct Stream {
 };
 
 double stream_core_drift(Stream& st);
+// Applies the lazily recorded core updates (a no-op for an eager stream).
+void stream_core_sync(Stream& st);
 
 void stream_init(Ctx* ctx, const Tensor& hist, int mode, int64_t s, double eps, uint64_t seed,
                  unsigned flags, Stream& out);

@@ -110,7 +110,7 @@ struct Ctx {
   }
 };
 
-enum Phase { PH_MATRICIZE = 0, PH_LAW, PH_SAMPLE, PH_FILTER_PREP, PH_FILTER, PH_ERROR, PH_H2D, PH_OTHER };
+enum Phase { PH_MATRICIZE = 0, PH_LAW, PH_SAMPLE, PH_FILTER_PREP, PH_FILTER, PH_ERROR, PH_H2D, PH_CORE };
 
 // Scoped phase marker (no-op unless ctx->timing).
 struct PhaseScope {

@@ -20,6 +20,9 @@
 //   * BL[a, col] = sum over the column's entries (k ascending) of
 //     left[a,k] * core[k,col] (:256-258), entries with |v| >= 1e-14 kept.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "cdf.cuh"
 #include "stream_core.cuh"
@@ -57,6 +60,89 @@ __global__ void k_gram_old(const int32_t* fib, int A, const int64_t* fptr, const
     }
     __syncthreads();
   }
+}
+
+// The same gram by columns of R: gram[a][k] = the sum over R_k's rows r
+// ascending (the rows of the merge in transpose_times) of x_a[r] * R[r,k],
+// with fiber a scattered densely into shared memory.  Rows of R_k absent from
+// fiber a hold 0 there and are skipped (adding the product 0 * R[r,k] would
+// not change the sum either).  A thread per (a, k): A x K_old independent
+// sums instead of one CTA per appended fiber with a barrier per row.
+__global__ void __launch_bounds__(256) k_gram_cols(const int32_t* fib, const int64_t* fptr, const int32_t* frow,
+                                                   const double* fval, int dim, const int64_t* rptr,
+                                                   const int32_t* rrow, const double* rval, int Kold,
+                                                   double* gram) {
+  extern __shared__ double xs[];  // [dim]
+  const int a = blockIdx.y;
+  const int f = fib[a];
+  for (int r = threadIdx.x; r < dim; r += blockDim.x) xs[r] = 0.0;
+  __syncthreads();
+  for (int64_t t = fptr[f] + threadIdx.x; t < fptr[f + 1]; t += blockDim.x) xs[frow[t]] = fval[t];
+  __syncthreads();
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= Kold) return;
+  double acc = 0.0;
+  for (int64_t e = rptr[k]; e < rptr[k + 1]; ++e) {
+    const double x = xs[rrow[e]];
+    if (x != 0.0) acc = dadd(acc, dmul(x, rval[e]));  // av[p] * bv[q], a = dR
+  }
+  gram[(long long)a * Kold + k] = fabs(acc) >= kDropTol ? acc : 0.0;
+}
+
+// Ordered compaction of each gram row's stored entries (j ascending): the
+// chain product's inner loop visits only them.
+__global__ void __launch_bounds__(256) k_gram_compact(const double* gram, int Kold, int32_t* nzj, double* nzg,
+                                                      int* nzn) {
+  __shared__ int s_warp[8];
+  const int a = blockIdx.x;
+  const double* g = gram + (long long)a * Kold;
+  int base = 0;
+  for (int j0 = 0; j0 < Kold; j0 += 256) {
+    const int j = j0 + threadIdx.x;
+    const double v = j < Kold ? g[j] : 0.0;
+    const bool nz = v != 0.0;
+    const unsigned bal = __ballot_sync(0xffffffffu, nz);
+    if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = __popc(bal);
+    __syncthreads();
+    int before = 0, all = 0;
+    for (int w = 0; w < 8; ++w) {
+      if (w < (int)(threadIdx.x >> 5)) before += s_warp[w];
+      all += s_warp[w];
+    }
+    before += __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
+    if (nz) {
+      nzj[(long long)a * Kold + base + before] = j;
+      nzg[(long long)a * Kold + base + before] = v;
+    }
+    base += all;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) nzn[a] = base;
+}
+
+// left[a][c] over the compacted entries; blockIdx.x = a varies fastest so the
+// CTAs of all appended rows stream through the same rows of U_old together
+// (one HBM read of U_old, the other A-1 from L2).
+__global__ void __launch_bounds__(256) k_left_nz(const int32_t* nzj, const double* nzg, const int* nzn, int Kold,
+                                                 const double* uold, double* left) {
+  const int a = blockIdx.x;
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= Kold) return;
+  const int n = nzn[a];
+  const int32_t* jj = nzj + (long long)a * Kold;
+  const double* gg = nzg + (long long)a * Kold;
+  double acc = 0.0;
+  int i = 0;
+  for (; i + 4 <= n; i += 4) {
+    const double u0 = uold[(long long)jj[i] * Kold + c], u1 = uold[(long long)jj[i + 1] * Kold + c];
+    const double u2 = uold[(long long)jj[i + 2] * Kold + c], u3 = uold[(long long)jj[i + 3] * Kold + c];
+    acc = dadd(acc, dmul(gg[i], u0));
+    acc = dadd(acc, dmul(gg[i + 1], u1));
+    acc = dadd(acc, dmul(gg[i + 2], u2));
+    acc = dadd(acc, dmul(gg[i + 3], u3));
+  }
+  for (; i < n; ++i) acc = dadd(acc, dmul(gg[i], uold[(long long)jj[i] * Kold + c]));
+  left[(long long)a * Kold + c] = acc;
 }
 
 // left[a][c] = sum_{j: gram[a][j] != 0, ascending} gram[a][j] * U_old[j][c]
@@ -189,28 +275,143 @@ void core_from_static(Ctx* ctx, const Core& c, DevCore& out) {
   }
 }
 
-void core_step(Ctx* ctx, DevCore& core, const Fibers& fb, const Basis& B, int64_t Kold, const double* uold,
-               const std::vector<int32_t>& appended_fib, int64_t col_offset) {
+void* CoreArena::take(Ctx*, size_t bytes) {
+  bytes = (bytes + 255) & ~size_t(255);
+  if (chunks.empty() || used + bytes > chunks.back().second) {
+    // geometric growth: O(log) cudaMalloc calls over a long stream (each can
+    // stall the step by tens of ms under load)
+    const size_t n = std::max({bytes, chunk_bytes, this->bytes() / 2});
+    void* p = nullptr;
+    static const bool trace = getenv("CTD_ARENA_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    CUDA_OK(cudaMalloc(&p, n));
+    if (trace) {
+      cudaMemPool_t pool;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetDefaultMemPool(&pool, dev);
+      uint64_t res = 0, used_b = 0;
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used_b);
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      fprintf(stderr, "[arena] chunk %zu MB in %.2f ms (%zu chunks) pool reserved %.1f GB used %.1f GB free %.1f GB\n",
+              n >> 20, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+              chunks.size() + 1, res / 1e9, used_b / 1e9, fr / 1e9);
+    }
+    chunks.emplace_back(static_cast<char*>(p), n);
+    used = 0;
+  }
+  void* p = chunks.back().first + used;
+  used += bytes;
+  return p;
+}
+
+void CoreArena::clear() {
+  for (auto& c : chunks) cudaFree(c.first);
+  chunks.clear();
+  used = 0;
+}
+
+size_t CoreArena::bytes() const {
+  size_t b = 0;
+  for (const auto& c : chunks) b += c.second;
+  return b;
+}
+
+void core_record(Ctx* ctx, const Fibers& fb, const Basis& B, int64_t Kold, const double* uold,
+                 const std::vector<int32_t>& appended_fib, int64_t col_offset, CoreArena* arena,
+                 CoreRecord& rec) {
   const int A = (int)appended_fib.size();
-  const long long oc = core.cols;
+  rec.A = A;
+  rec.Kold = Kold;
+  rec.col_offset = col_offset;
+  static const bool trace = getenv("CTD_CORE_TRACE") != nullptr;
+  double tm[4] = {0, 0, 0, 0};
+  auto lap = [&](int i) {
+    if (!trace) return;
+    static std::chrono::steady_clock::time_point t0;
+    ctx->sync();
+    const auto now = std::chrono::steady_clock::now();
+    if (i >= 0) tm[i] = std::chrono::duration<double, std::milli>(now - t0).count();
+    t0 = now;
+  };
+  lap(-1);
   // slab columns: R_new^T dX (top-right rows < K_old, bottom-right rows >= K_old)
-  Core sc;
-  compute_core(ctx, fb, B, sc);
-  // bottom-left counts over the old columns
-  Buf<double> left(ctx, (size_t)A * Kold + 1);
-  Buf<long long> blc(ctx, oc + 1);
-  const unsigned wgrid = ceil_div((uint64_t)oc * 32, 256);
-  if (A > 0 && Kold > 0 && oc > 0) {
+  {
+    Core sc;
+    compute_core(ctx, fb, B, sc);
+    lap(0);
+    rec.cols = sc.cols;
+    rec.nnz = sc.nnz;
+    rec.col_id = std::move(sc.col_id);
+    rec.ptr = std::move(sc.ptr);
+    if (sc.nnz && arena) {
+      int32_t* r = static_cast<int32_t*>(arena->take(ctx, sc.nnz * sizeof(int32_t)));
+      double* v = static_cast<double*>(arena->take(ctx, sc.nnz * sizeof(double)));
+      CUDA_OK(cudaMemcpyAsync(r, sc.row.p, sc.nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+      CUDA_OK(cudaMemcpyAsync(v, sc.val.p, sc.nnz * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+      rec.row = r;
+      rec.val = v;
+    } else if (sc.nnz) {
+      rec.own_sc = std::move(sc);
+      rec.row = rec.own_sc.row.p;
+      rec.val = rec.own_sc.val.p;
+    }
+    lap(1);
+  }
+  if (A > 0 && Kold > 0) {
+    double* left;
+    if (arena) {
+      left = static_cast<double*>(arena->take(ctx, (size_t)A * Kold * sizeof(double)));
+    } else {
+      rec.own_left.alloc(ctx, (size_t)A * Kold);
+      left = rec.own_left.p;
+    }
+    rec.left = left;
     Buf<int32_t> fib(ctx, A);
     ctx->to_dev(fib.p, appended_fib.data(), A);
     Buf<double> gram(ctx, (size_t)A * Kold);
-    const size_t smem = (size_t)Kold * sizeof(double);
-    if (smem > 200 * 1024) fail(CTD_ERR_ARGUMENT, "core update supports at most 25600 kept fibers");
-    CUDA_OK(cudaFuncSetAttribute(k_gram_old, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    LAUNCH(ctx, k_gram_old, (unsigned)std::min(A, ctx->sm_count * 4), 256, smem, fib.p, A, fb.ptr.p, fb.row.p,
-           fb.val.p, B.rowbase.p, B.rowlen.p, B.rek.p, B.rev.p, (int)Kold, gram.p);
-    LAUNCH(ctx, k_left, ceil_div((uint64_t)A * Kold, 256), 256, 0, gram.p, A, (int)Kold, uold, left.p);
-    LAUNCH(ctx, k_bottom_left, wgrid, 256, 0, 0, core.ptr.p, core.row.p, core.val.p, oc, left.p, A, (int)Kold,
+    const size_t xsmem = (size_t)B.dim * sizeof(double);
+    if (xsmem <= 96 * 1024 && !getenv("CTD_CORE_LEGACY")) {
+      if (xsmem > 48 * 1024)
+        CUDA_OK(cudaFuncSetAttribute(k_gram_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem));
+      const dim3 grid(ceil_div((uint64_t)Kold, 256), A);
+      LAUNCH(ctx, k_gram_cols, grid, 256, xsmem, fib.p, fb.ptr.p, fb.row.p, fb.val.p, (int)B.dim, B.rptr.p,
+             B.rrow.p, B.rval.p, (int)Kold, gram.p);
+    } else {
+      const size_t smem = (size_t)Kold * sizeof(double);
+      if (smem > 200 * 1024) fail(CTD_ERR_ARGUMENT, "core update supports at most 25600 kept fibers");
+      CUDA_OK(cudaFuncSetAttribute(k_gram_old, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      LAUNCH(ctx, k_gram_old, (unsigned)std::min(A, ctx->sm_count * 4), 256, smem, fib.p, A, fb.ptr.p, fb.row.p,
+             fb.val.p, B.rowbase.p, B.rowlen.p, B.rek.p, B.rev.p, (int)Kold, gram.p);
+    }
+    if (!getenv("CTD_CORE_LEGACY")) {
+      Buf<int32_t> nzj(ctx, (size_t)A * Kold);
+      Buf<double> nzg(ctx, (size_t)A * Kold);
+      Buf<int> nzn(ctx, A);
+      LAUNCH(ctx, k_gram_compact, A, 256, 0, gram.p, (int)Kold, nzj.p, nzg.p, nzn.p);
+      const dim3 grid(A, ceil_div((uint64_t)Kold, 256));
+      LAUNCH(ctx, k_left_nz, grid, 256, 0, nzj.p, nzg.p, nzn.p, (int)Kold, uold, left);
+    } else {
+      LAUNCH(ctx, k_left, ceil_div((uint64_t)A * Kold, 256), 256, 0, gram.p, A, (int)Kold, uold, left);
+    }
+    lap(2);
+  }
+  if (trace && tm[0] + tm[1] + tm[2] > 10.0)
+    fprintf(stderr, "[core_record] K=%lld A=%d F=%lld nnz=%lld: compute_core %.2f copy %.2f gram+left %.2f ms\n",
+            (long long)B.K, A, (long long)fb.F, (long long)rec.nnz, tm[0], tm[1], tm[2]);
+}
+
+void core_apply(Ctx* ctx, DevCore& core, const CoreRecord& rec) {
+  const int A = rec.A;
+  const int64_t Kold = rec.Kold;
+  const long long oc = core.cols;
+  // bottom-left counts over the old columns
+  Buf<long long> blc(ctx, oc + 1);
+  const unsigned wgrid = ceil_div((uint64_t)oc * 32, 256);
+  if (A > 0 && Kold > 0 && oc > 0) {
+    LAUNCH(ctx, k_bottom_left, wgrid, 256, 0, 0, core.ptr.p, core.row.p, core.val.p, oc, rec.left, A, (int)Kold,
            blc.p, (const int64_t*)nullptr, (int32_t*)nullptr, (double*)nullptr);
   } else if (oc > 0) {
     CUDA_OK(cudaMemsetAsync(blc.p, 0, (oc + 1) * sizeof(long long), ctx->stream));
@@ -225,13 +426,13 @@ void core_step(Ctx* ctx, DevCore& core, const Fibers& fb, const Basis& B, int64_
     optr[0] = 0;
   }
   ctx->sync();
-  const long long nc = oc + sc.cols;
+  const long long nc = oc + rec.cols;
   std::vector<int64_t> nptr(nc + 1, 0), ncol(nc);
   for (long long c = 0; c < oc; ++c) nptr[c + 1] = nptr[c] + (optr[c + 1] - optr[c]) + hb[c];
-  for (long long s = 0; s < sc.cols; ++s) nptr[oc + s + 1] = nptr[oc + s] + (sc.ptr[s + 1] - sc.ptr[s]);
+  for (long long s = 0; s < rec.cols; ++s) nptr[oc + s + 1] = nptr[oc + s] + (rec.ptr[s + 1] - rec.ptr[s]);
   if (oc) ctx->to_host(ncol.data(), core.col.p, oc);
   ctx->sync();
-  for (long long s = 0; s < sc.cols; ++s) ncol[oc + s] = sc.col_id[s] + col_offset;
+  for (long long s = 0; s < rec.cols; ++s) ncol[oc + s] = rec.col_id[s] + rec.col_offset;
   DevCore nw;
   nw.cols = nc;
   nw.nnz = nptr[nc];
@@ -244,16 +445,23 @@ void core_step(Ctx* ctx, DevCore& core, const Fibers& fb, const Basis& B, int64_
   if (oc) {
     LAUNCH(ctx, k_copy_cols, wgrid, 256, 0, core.ptr.p, core.row.p, core.val.p, oc, nw.ptr.p, nw.row.p, nw.val.p);
     if (A > 0 && Kold > 0)
-      LAUNCH(ctx, k_bottom_left, wgrid, 256, 0, 1, core.ptr.p, core.row.p, core.val.p, oc, left.p, A, (int)Kold,
+      LAUNCH(ctx, k_bottom_left, wgrid, 256, 0, 1, core.ptr.p, core.row.p, core.val.p, oc, rec.left, A, (int)Kold,
              (long long*)nullptr, nw.ptr.p, nw.row.p, nw.val.p);
   }
-  if (sc.nnz) {
+  if (rec.nnz) {
     const int64_t d = nptr[oc];
-    CUDA_OK(cudaMemcpyAsync(nw.row.p + d, sc.row.p, sc.nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
-    CUDA_OK(cudaMemcpyAsync(nw.val.p + d, sc.val.p, sc.nnz * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    CUDA_OK(cudaMemcpyAsync(nw.row.p + d, rec.row, rec.nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    CUDA_OK(cudaMemcpyAsync(nw.val.p + d, rec.val, rec.nnz * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   }
   ctx->sync();
   core = std::move(nw);
+}
+
+void core_step(Ctx* ctx, DevCore& core, const Fibers& fb, const Basis& B, int64_t Kold, const double* uold,
+               const std::vector<int32_t>& appended_fib, int64_t col_offset) {
+  CoreRecord rec;
+  core_record(ctx, fb, B, Kold, uold, appended_fib, col_offset, nullptr, rec);
+  core_apply(ctx, core, rec);
 }
 
 void core_step_exact(Ctx* ctx, DevCore& core, const Fibers& fb, const Fibers& hf, const Basis& B, int64_t Kold,

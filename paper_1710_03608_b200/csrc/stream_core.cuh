@@ -17,7 +17,49 @@ struct DevCore {
 
 void core_from_static(Ctx* ctx, const Core& c, DevCore& out);
 
-// One ctd_d_step core update (Eq. 13).  B is the basis after this step's
+// The inputs of one core update, computed when the step runs (they depend on
+// the basis and U of that moment) and applied to the core later: the slab's
+// columns R_new^T dX (top-right + bottom-right) and the chain product's dense
+// left factor W = (dR^T R_old) U_old (A x Kold), which the bottom-left block
+// applies to the core as it stood before the step (the
+// block-append core with the bottom-left kept as W and expanded lazily).
+// Bump allocator over large device chunks for the records: they are kept
+// until the core is read, so per-record pool allocations would fragment the
+// stream-ordered pool and grow it at every step.  Chunks come from
+// cudaMalloc: growing the stream-ordered pool by 1 GB costs ~12 ms (47 ms
+// worst) on a B200, cudaMalloc ~0.6 ms (tools/alloc_probe.cu).
+struct CoreArena {
+  std::vector<std::pair<char*, size_t>> chunks;
+  size_t used = 0;
+  static constexpr size_t chunk_bytes = size_t(1) << 30;  // smallest chunk
+  CoreArena() = default;
+  CoreArena(const CoreArena&) = delete;
+  CoreArena& operator=(const CoreArena&) = delete;
+  ~CoreArena() { clear(); }
+  void* take(Ctx* ctx, size_t bytes);
+  void clear();  // synchronizes the device (cudaFree)
+  size_t bytes() const;
+};
+
+struct CoreRecord {
+  // slab columns R_new^T dX: col_id/ptr on the host, row/val in the arena
+  int64_t cols = 0, nnz = 0;
+  std::vector<int64_t> col_id, ptr;
+  const int32_t* row = nullptr;
+  const double* val = nullptr;
+  const double* left = nullptr;  // [A][Kold] in the arena
+  Core own_sc;                   // without an arena: the record owns its blocks
+  Buf<double> own_left;
+  int A = 0;
+  int64_t Kold = 0;
+  int64_t col_offset = 0;
+};
+void core_record(Ctx* ctx, const Fibers& fb, const Basis& B, int64_t Kold, const double* uold,
+                 const std::vector<int32_t>& appended_fib, int64_t col_offset, CoreArena* arena,
+                 CoreRecord& out);
+void core_apply(Ctx* ctx, DevCore& core, const CoreRecord& rec);
+
+// One ctd_d_step core update (Eq. 13) = core_record + core_apply.  B is the basis after this step's
 // appends, Kold its size before them and uold (Kold x Kold, row-major) U
 // before them; appended_fib the appended candidates' fiber indices into fb in
 // acceptance order; col_offset = t * slab_columns.

@@ -59,6 +59,7 @@ WITH_CORE = 0x2
 KEEP_PANEL = 0x4  # keep the orthonormal panel for a later relative_error (implied by WITH_ERROR)
 KEEP_HISTORY = 0x8  # init_stream(keep_history=True): retain the raw history (core_drift)
 EXACT_CORE = 0x10   # init_stream(exact_core=True): bottom-left block from the history
+LAZY_CORE = 0x20    # init_stream(lazy_core=True): core updates recorded per step, applied on read
 
 
 def _check(st: int):
@@ -605,6 +606,19 @@ class StreamState:
         _check(self.ctx.L.ctd_gpu_stream_factors(self.h, C.byref(h)))
         return _read_factors(self.ctx, h, self.slab_shape + [self.t], self.mode, trace=False)
 
+    def n_kept(self) -> int:
+        return int(self.ctx.L.ctd_gpu_stream_n_kept(self.h))
+
+    def core_pending(self):
+        """(records, device bytes) of the lazily kept core updates (lazy_core)."""
+        r, b = C.c_int64(), C.c_int64()
+        _check(self.ctx.L.ctd_gpu_stream_core_pending(self.h, C.byref(r), C.byref(b)))
+        return r.value, b.value
+
+    def core_sync(self):
+        """Applies the lazily kept core updates (factors() and core_drift do this)."""
+        _check(self.ctx.L.ctd_gpu_stream_core_sync(self.h))
+
     def close(self):
         if getattr(self, "h", None):
             self.ctx.L.ctd_gpu_stream_destroy(self.h)
@@ -619,17 +633,21 @@ class StreamState:
 
 def init_stream(historical, mode: int, sample_size: int, epsilon: float = 1e-6,
                 seed: int = 42, keep_history: bool = False, exact_core: bool = False,
-                with_core: bool = False, ctx: Optional[Context] = None) -> StreamState:
+                with_core: bool = False, lazy_core: bool = False,
+                ctx: Optional[Context] = None) -> StreamState:
     """init_stream (ctd_dynamic.hpp:42-45, ctd_dynamic.cpp:129-147).  ``with_core``
     maintains the core C(t) through every step (Eq. 13 blocks); ``factors()`` then
     carries it.  ``keep_history`` retains the raw history on the device (for
     ``core_drift``); ``exact_core`` computes the bottom-left block from it
-    (ctd_dynamic.cpp:207-211).  Either implies ``with_core``."""
+    (ctd_dynamic.cpp:207-211).  Either implies ``with_core``.  ``lazy_core``
+    maintains the same core as per-step records (the slab's columns and the
+    chain product's left factor) applied when the core is read; it implies
+    ``with_core`` and is ignored with ``exact_core``."""
     ctx = ctx or default_context()
     d = _dev(historical, ctx)
     h = C.c_void_p()
     flags = ((WITH_CORE if with_core else 0) | (KEEP_HISTORY if keep_history else 0)
-             | (EXACT_CORE if exact_core else 0))
+             | (EXACT_CORE if exact_core else 0) | (LAZY_CORE if lazy_core else 0))
     _check(ctx.L.ctd_gpu_stream_init(ctx.h, d.h, mode, sample_size, epsilon, C.c_uint64(seed),
                                      flags, C.byref(h)))
     return StreamState(ctx, h, mode, d.shape[:-1])

@@ -261,7 +261,8 @@ StreamState __wrap__ZN3ctd11init_streamERKNS_12SparseTensorEildmbb(const SparseT
   // keep_history / exact_core: the device stream keeps its own history (the
   // bottom-left block, ctd_dynamic.cpp:207-211, and core_drift); the host
   // copy is appended lazily on sync
-  const unsigned flags = CTD_GPU_WITH_CORE | (exact_core ? CTD_GPU_EXACT_CORE : 0u) |
+  // the core is kept as per-step records and assembled when read (bit-identical)
+  const unsigned flags = CTD_GPU_WITH_CORE | CTD_GPU_LAZY_CORE | (exact_core ? CTD_GPU_EXACT_CORE : 0u) |
                         (keep_history ? CTD_GPU_KEEP_HISTORY : 0u);
   rethrow(ctd_gpu_stream_init(context(), t.h, mode, sample_size, epsilon, seed, flags, &s));
   StreamState st{FiberBasis(historical.extent(mode)), SparseMatrix(0, 0), historical.shape(), mode, 0, epsilon,

@@ -173,11 +173,16 @@ def test_relative_error_panel_and_two_panel_paths(ctx, ref, name):
         assert abs(v - e) <= 1e-9 * max(1.0, abs(e)), (vals, e)
 
 
+@pytest.mark.parametrize("heavy_rows", [None, "1", "6"])
 @pytest.mark.parametrize("name,mode", [("c1", 0), ("c1", 2), ("rand_fp", 1), ("rand_int", 0), ("lowrank", 0),
-                                       ("traffic", 0), ("order4", 3)])
-def test_core_bitexact(ctx, port, name, mode):
+                                       ("traffic", 0), ("order4", 3), ("cp_small", 0)])
+def test_core_bitexact(ctx, port, name, mode, heavy_rows, monkeypatch):
     """compute_core (ctd_static.cpp:12-17): C_(mode) = R^T X_(mode) entry for entry,
-    including the 1e-14 drop rule, against the oracle's multiply_columns."""
+    including the 1e-14 drop rule, against the oracle's multiply_columns.
+    ``heavy_rows`` moves the split between the row-merge CTAs and the
+    transposed walk over R's columns (k_core_heavy) so both paths are covered."""
+    if heavy_rows is not None:
+        monkeypatch.setenv("CTD_CORE_HEAVY_ROWS", heavy_rows)
     x = CASES[name]()
     f = ctd.ctd_s(_st(x), mode, 150, 1e-6, 42, with_core=True, ctx=ctx)
     xm = port.matricize(x.shape, x.idx.reshape(-1), x.val, mode)
@@ -224,14 +229,21 @@ def _dense_cols(ncols, C_col, C_ptr):
     return cp
 
 
-@pytest.mark.parametrize("seed,d", [(5, 60), (6, 25)])
-def test_stream_core_vs_port(ctx, port, seed, d):
+@pytest.mark.parametrize("seed,d,lazy,read_every,legacy", [(5, 60, False, 1, False), (6, 25, False, 1, False),
+                                                          (5, 60, True, 1, False), (6, 25, True, 3, False),
+                                                          (6, 25, False, 1, True)])
+def test_stream_core_vs_port(ctx, port, seed, d, lazy, read_every, legacy, monkeypatch):
     """CTD-D with the core maintained (Eq. 13: top-right R^T dX, chain-product
-    bottom-left, bottom-right dR^T dX, assemble_blocks) bit for bit."""
+    bottom-left, bottom-right dR^T dX, assemble_blocks) bit for bit; with
+    ``lazy`` the steps only record their blocks and the core is assembled when
+    it is read (every ``read_every`` steps, so several records are pending);
+    ``legacy`` runs the row-merge gram / per-(a, c) chain-product kernels."""
+    if legacy:
+        monkeypatch.setenv("CTD_CORE_LEGACY", "1")
     x = g.c3_stream(seed=seed, n_steps=3, slices_per_step=3, draws_per_slice=2500, n=300,
                     planted_step=2, block=20)
     hist = x.time_slab(0, 3)
-    st = ctd.init_stream(_st(hist), 0, 120, 1e-6, 7, with_core=True, ctx=ctx)
+    st = ctd.init_stream(_st(hist), 0, 120, 1e-6, 7, with_core=True, lazy_core=lazy, ctx=ctx)
     ps = port.stream(hist.shape, hist.flat_idx(), hist.val, 0, 120, 1e-6, 7)
     grew = 0
     for t in range(3, x.shape[2]):
@@ -240,6 +252,8 @@ def test_stream_core_vs_port(ctx, port, seed, d):
         ctd.ctd_d_step(st, _st(slab), d)
         ps.step(slab.shape, slab.flat_idx(), slab.val, d)
         grew += len(ps.kept_flat()) > k0
+        if (t - 2) % read_every and t + 1 < x.shape[2]:
+            continue
         f = st.factors()
         c = ps.core()
         assert np.array_equal(f.kept_flat, ps.kept_flat()), t
@@ -250,12 +264,12 @@ def test_stream_core_vs_port(ctx, port, seed, d):
     assert grew >= 2  # the chain-product (bottom-left) block was exercised
 
 
-def _stream_history_case(ctx, ref, x, h, s, seed, d, keep_history, exact_core):
+def _stream_history_case(ctx, ref, x, h, s, seed, d, keep_history, exact_core, lazy=False):
     """init_stream(keep_history, exact_core) + ctd_d_step per slab against the
     compiled reference: kept ids, the whole core and core_drift, bit for bit."""
     hist = x.time_slab(0, h)
     st = ctd.init_stream(_st(hist), 0, s, 1e-6, seed, keep_history=keep_history, exact_core=exact_core,
-                         ctx=ctx)
+                         lazy_core=lazy, ctx=ctx)
     rs = ref.stream(ref.tensor(hist.shape, hist.flat_idx(), hist.val), 0, s, 1e-6, seed,
                     keep_history=keep_history, exact_core=exact_core)
     drifts = []
@@ -289,6 +303,7 @@ def test_stream_keep_history_drift_vs_reference(ctx, ref):
     x = g.low_rank([10, 5, 6], 2, 0.95, 29)
     drifts = _stream_history_case(ctx, ref, x, 2, 200, 7, 40, True, False)
     assert max(drifts) <= 1e-10
+    assert _stream_history_case(ctx, ref, x, 2, 200, 7, 40, True, False, lazy=True) == drifts
     # larger stream with appends every step, exact_core, against the reference
     y = g.c3_stream(seed=6, n_steps=2, slices_per_step=4, draws_per_slice=1500, n=200,
                     planted_step=1, block=15)
