@@ -66,6 +66,10 @@ const char *ctd_gpu_version(void);
  * context is ordered on that stream. */
 int ctd_gpu_ctx_create(int device, void *stream, ctd_gpu_ctx **out);
 int ctd_gpu_ctx_set_stream(ctd_gpu_ctx *ctx, void *stream);
+/* Returns the context's cached device blocks and the stream-ordered pool's
+   unused reserve to the driver (for other allocators in the process, e.g.
+   torch.cuda.empty_cache's counterpart). */
+int ctd_gpu_ctx_trim(ctd_gpu_ctx *ctx);
 int ctd_gpu_ctx_synchronize(ctd_gpu_ctx *ctx);
 int ctd_gpu_ctx_destroy(ctd_gpu_ctx *ctx);
 /* Launch counter of this library's kernels on the context (for bench.py). */
@@ -276,11 +280,13 @@ int ctd_gpu_stream_factors(ctd_gpu_stream *s, ctd_gpu_factors **out);
    against the retained history (CTD_GPU_KEEP_HISTORY or CTD_GPU_EXACT_CORE;
    otherwise CTD_ERR_ARGUMENT like the reference's ArgumentError). */
 int ctd_gpu_stream_core_drift(ctd_gpu_stream *s, double *out);
-/* CTD_GPU_LAZY_CORE: the recorded, not yet applied core updates (count and
-   device bytes); ctd_gpu_stream_core_sync applies them (factors and
-   core_drift do so themselves).  No reference counterpart: the reference
-   applies every update inside ctd_d_step (ctd_dynamic.cpp:149-229). */
-int ctd_gpu_stream_core_pending(const ctd_gpu_stream *s, int64_t *records, int64_t *bytes);
+/* CTD_GPU_LAZY_CORE: the recorded, not yet applied core updates (records,
+   slab-column entries, and bytes = 12 per entry + 8 per left-factor value);
+   ctd_gpu_stream_core_sync applies them (factors and core_drift do so
+   themselves).  No reference counterpart: the reference applies every update
+   inside ctd_d_step (ctd_dynamic.cpp:149-229). */
+int ctd_gpu_stream_core_pending(const ctd_gpu_stream *s, int64_t *records, int64_t *entries,
+                                int64_t *bytes);
 int ctd_gpu_stream_core_sync(ctd_gpu_stream *s);
 int ctd_gpu_stream_destroy(ctd_gpu_stream *s);
 

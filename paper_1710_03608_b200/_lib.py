@@ -33,6 +33,7 @@ SIGNATURES = [
     ("ctd_gpu_version", C.c_char_p, []),
     ("ctd_gpu_ctx_create", _I, [_I, _V, _PV]),
     ("ctd_gpu_ctx_set_stream", _I, [_V, _V]),
+    ("ctd_gpu_ctx_trim", _I, [_V]),
     ("ctd_gpu_ctx_synchronize", _I, [_V]),
     ("ctd_gpu_ctx_destroy", _I, [_V]),
     ("ctd_gpu_ctx_launches", _I64, [_V]),
@@ -86,7 +87,7 @@ SIGNATURES = [
     ("ctd_gpu_stream_n_kept", _I64, [_V]),
     ("ctd_gpu_stream_factors", _I, [_V, _PV]),
     ("ctd_gpu_stream_core_drift", _I, [_V, C.POINTER(C.c_double)]),
-    ("ctd_gpu_stream_core_pending", _I, [_V, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("ctd_gpu_stream_core_pending", _I, [_V, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("ctd_gpu_stream_core_sync", _I, [_V]),
     ("ctd_gpu_stream_destroy", _I, [_V]),
 ]

@@ -137,9 +137,9 @@ int ctd_gpu_ctx_create(int device, void* stream, ctd_gpu_ctx** out) {
     uint64_t thr = UINT64_MAX;
     CUDA_OK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     // Prewarm the stream-ordered pool so steady-state calls never map memory
-    // (CTD_GPU_POOL_MB, default 8192; the pool keeps it: threshold above).
+    // (CTD_GPU_POOL_MB, default 1024: buffers below Ctx::kBigBytes; the pool keeps it).
     {
-      size_t mb = 8192;
+      size_t mb = 1024;
       if (const char* e = getenv("CTD_GPU_POOL_MB")) mb = (size_t)atoll(e);
       size_t free_b = 0, total_b = 0;
       CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
@@ -164,7 +164,20 @@ int ctd_gpu_ctx_set_stream(ctd_gpu_ctx* ctx, void* stream) {
   return guarded([&] {
     need(ctx, "ctx");
     bind_device(&ctx->c);
+    CUDA_OK(cudaStreamSynchronize(ctx->c.stream));  // cached blocks are reused in stream order
     ctx->c.stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+int ctd_gpu_ctx_trim(ctd_gpu_ctx* ctx) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    bind_device(&ctx->c);
+    ctx->c.big_trim();
+    cudaMemPool_t pool;
+    CUDA_OK(cudaDeviceGetDefaultMemPool(&pool, ctx->c.device));
+    CUDA_OK(cudaStreamSynchronize(ctx->c.stream));
+    CUDA_OK(cudaMemPoolTrimTo(pool, 0));
   });
 }
 
@@ -181,6 +194,7 @@ int ctd_gpu_ctx_destroy(ctd_gpu_ctx* ctx) {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->c.stream);
     ctx_register(&ctx->c, false);
+    ctx->c.big_release_all();
     cudaFree(ctx->c.d_flags);
     cudaFree(ctx->c.d_bar);
     delete ctx;
@@ -1137,13 +1151,15 @@ int ctd_gpu_stream_core_drift(ctd_gpu_stream* s, double* out) {
   });
 }
 
-int ctd_gpu_stream_core_pending(const ctd_gpu_stream* s, int64_t* records, int64_t* bytes) {
+int ctd_gpu_stream_core_pending(const ctd_gpu_stream* s, int64_t* records, int64_t* entries, int64_t* bytes) {
   return guarded([&] {
     need(s, "stream");
     need(records, "records");
+    need(entries, "entries");
     need(bytes, "bytes");
     *records = (int64_t)s->s.pending.size();
-    *bytes = (int64_t)s->s.arena.bytes();
+    *entries = s->s.pending_entries;
+    *bytes = s->s.pending_bytes;
   });
 }
 

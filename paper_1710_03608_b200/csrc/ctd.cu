@@ -150,6 +150,7 @@ void stream_core_sync(Stream& st) {
   for (const CoreRecord& r : st.pending) core_apply(st.ctx, st.core, r);
   st.pending.clear();
   st.arena.clear();
+  st.pending_entries = st.pending_bytes = 0;
 }
 
 double stream_core_drift(Stream& st) {
@@ -289,6 +290,9 @@ void stream_step(Stream& st, const Tensor& slab, int64_t d) {
     } else if (st.lazy_core) {
       st.pending.emplace_back();
       core_record(ctx, fb, *st.basis, Kold, uold.p, appended, st.t * fb.cols, &st.arena, st.pending.back());
+      const CoreRecord& r = st.pending.back();
+      st.pending_entries += r.nnz;
+      st.pending_bytes += 12 * r.nnz + 8 * (int64_t)r.A * r.Kold;
     } else if (st.with_core) {
       core_step(ctx, st.core, fb, *st.basis, Kold, uold.p, appended, st.t * fb.cols);
     }

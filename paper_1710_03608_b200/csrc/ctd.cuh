@@ -61,6 +61,7 @@ struct Stream {
   bool lazy_core = false;
   std::vector<CoreRecord> pending;
   CoreArena arena;
+  int64_t pending_entries = 0, pending_bytes = 0;  // slab-column entries; 12/entry + 8 per left value
   Buf<double> uold;  // U^(t) snapshot for the core update (capacity grows)
   // retained raw history (StreamState::history, ctd_dynamic.hpp:28-32): the
   // concatenated slabs as device COO, `order` planes of hcap int32 indices

@@ -1,8 +1,12 @@
 // Context, device buffers and tensor handles.
 #pragma once
 
+#include <algorithm>
+#include <cstdlib>
+#include <map>
 #include <mutex>
 #include <set>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -39,16 +43,96 @@ struct Ctx {
   unsigned* d_bar = nullptr;     // grid-barrier words for persistent kernels
   int64_t launches = 0;          // kernels launched on this context
 
+  // Buffers of kBigBytes or more come from a per-context cache of cudaMalloc
+  // blocks instead of the stream-ordered pool: growing the pool costs ~12 ms
+  // per GB on a B200 against ~0.6 ms for cudaMalloc (tools/alloc_probe.cu),
+  // and C5's ~60 GB of per-call temporaries made a cold call ~4x slower.
+  // Reuse is stream-ordered because every kernel of a context runs on its
+  // one stream (set_stream synchronizes the old stream first).
+  // Cached free bytes are capped (a quarter of the device, at most 48 GB, or
+  // CTD_GPU_CACHE_GB; the excess is returned at once); ctd_gpu_ctx_trim
+  // returns the rest (like torch.cuda.empty_cache).
+  static constexpr size_t kBigBytes = size_t(64) << 20;
+  std::multimap<size_t, void*> big_free;
+  std::unordered_map<void*, size_t> big_live;
+  size_t big_free_bytes = 0, big_cap = 0;
+  std::mutex big_mu;
+
+  void* big_alloc(size_t n) {
+    n = (n + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+    std::lock_guard<std::mutex> lk(big_mu);
+    auto it = big_free.lower_bound(n);
+    if (it != big_free.end() && it->first <= n + n / 4 + (size_t(64) << 20)) {
+      void* p = it->second;
+      big_live.emplace(p, it->first);
+      big_free_bytes -= it->first;
+      big_free.erase(it);
+      return p;
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, n) != cudaSuccess) {
+      cudaGetLastError();
+      big_trim_locked();  // give the cached blocks and the pool's reserve back, retry
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+      CUDA_OK(cudaMalloc(&p, n));
+    }
+    big_live.emplace(p, n);
+    return p;
+  }
+  void big_trim_locked() {
+    if (big_free.empty()) return;
+    cudaStreamSynchronize(stream);
+    for (auto& b : big_free) cudaFree(b.second);
+    big_free.clear();
+    big_free_bytes = 0;
+  }
+  void big_trim() {
+    std::lock_guard<std::mutex> lk(big_mu);
+    big_trim_locked();
+  }
+  // context teardown: every cached and live block
+  void big_release_all() {
+    std::lock_guard<std::mutex> lk(big_mu);
+    big_trim_locked();
+    for (auto& b : big_live) cudaFree(b.first);
+    big_live.clear();
+  }
+
   void* alloc_bytes(size_t n) {
     void* p = nullptr;
     if (n == 0) n = 16;
+    if (n >= kBigBytes) return big_alloc(n);
     CUDA_OK(cudaMallocAsync(&p, n, stream));
     return p;
   }
   template <typename T>
   T* alloc(size_t n) { return static_cast<T*>(alloc_bytes(n * sizeof(T))); }
   void release(void* p) {
-    if (p) cudaFreeAsync(p, stream);
+    if (!p) return;
+    {
+      std::lock_guard<std::mutex> lk(big_mu);
+      auto it = big_live.find(p);
+      if (it != big_live.end()) {
+        const size_t n = it->second;
+        big_live.erase(it);
+        if (big_cap == 0) {
+          size_t fr = 0, tot = 0;
+          big_cap = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? std::min(tot / 4, size_t(48) << 30)
+                                                              : (size_t(32) << 30);
+          if (const char* e = getenv("CTD_GPU_CACHE_GB")) big_cap = (size_t)atoll(e) << 30;
+        }
+        if (big_free_bytes + n > big_cap) {
+          cudaStreamSynchronize(stream);  // queued kernels may still use it
+          cudaFree(p);
+        } else {
+          big_free.emplace(n, p);
+          big_free_bytes += n;
+        }
+        return;
+      }
+    }
+    cudaFreeAsync(p, stream);
   }
   void sync() { CUDA_OK(cudaStreamSynchronize(stream)); }
   void zero(void* p, size_t bytes) { CUDA_OK(cudaMemsetAsync(p, 0, bytes, stream)); }

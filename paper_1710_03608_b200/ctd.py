@@ -105,6 +105,11 @@ class Context:
         _check(self.L.ctd_gpu_ctx_phase_times(self.h, _p(ms), _p(n), int(reset)))
         return {self.L.ctd_gpu_phase_name(i).decode(): (float(ms[i]), int(n[i])) for i in range(8)}
 
+    def trim(self):
+        """Returns cached device memory to the driver (torch.cuda.empty_cache's
+        counterpart for this context)."""
+        _check(self.L.ctd_gpu_ctx_trim(self.h))
+
     def close(self):
         if getattr(self, "h", None):
             self.L.ctd_gpu_ctx_destroy(self.h)
@@ -610,10 +615,11 @@ class StreamState:
         return int(self.ctx.L.ctd_gpu_stream_n_kept(self.h))
 
     def core_pending(self):
-        """(records, device bytes) of the lazily kept core updates (lazy_core)."""
-        r, b = C.c_int64(), C.c_int64()
-        _check(self.ctx.L.ctd_gpu_stream_core_pending(self.h, C.byref(r), C.byref(b)))
-        return r.value, b.value
+        """(records, slab-column entries, bytes) of the lazily kept core updates
+        (lazy_core)."""
+        r, e, b = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(self.ctx.L.ctd_gpu_stream_core_pending(self.h, C.byref(r), C.byref(e), C.byref(b)))
+        return r.value, e.value, b.value
 
     def core_sync(self):
         """Applies the lazily kept core updates (factors() and core_drift do this)."""

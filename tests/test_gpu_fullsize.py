@@ -60,6 +60,7 @@ def test_c5_scale_properties(ctx, port):
     from paper_1710_03608_b200 import ctd as api
     from paper_1710_03608_b200 import datagen_gpu, dist
 
+    ctx.trim()  # the library's cached blocks from earlier tests back to the driver
     torch.cuda.empty_cache()
     free, total = torch.cuda.mem_get_info()
     if free < 120e9:
@@ -76,6 +77,7 @@ def test_c5_scale_properties(ctx, port):
     sh = dist.GpuKernels(ctx).shard(dt, 0)
     fcol, fnorm = sh.col.copy(), sh.norm.copy()
     sh.close()
+    ctx.trim()
     col = idx[1].to(torch.int64) + idx[2].to(torch.int64) * J   # mode-0 column j = dst + t*J
     sq = val * val
     ref_norm = torch.zeros(J * T, dtype=torch.float64, device=val.device)
@@ -90,6 +92,7 @@ def test_c5_scale_properties(ctx, port):
     # -- the front end (with the error pass: it keeps the orthonormal panel)
     c, eps, seed = 10000, 1e-6, 42
     f = ctd.ctd_s(dt, 0, c, eps, seed, with_error=True, ctx=ctx)
+    ctx.trim()
     # law + draws + dedup: the restatement on the full dense law (N_alpha = 1e8)
     p = np.zeros(J * T)
     p[fcol] = fnorm
