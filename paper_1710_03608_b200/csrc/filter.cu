@@ -146,12 +146,17 @@ __global__ void __launch_bounds__(256) k_xsq(Cands c, double* xsq, unsigned* fla
 }
 
 // Dense candidate matrix D[row][cand] (dim x n), zeroed beforehand.
-__global__ void k_dense_cands(Cands c, double* D, long long n) {
+// The candidates as a dense table in 32-column chunks: D[(bc * dim + r) * 32 +
+// (cand & 31)], bc = cand / 32, so one chunk (dim x 32 doubles) is contiguous
+// and the Gram pass can keep it L2-resident while every left vector streams
+// through it.
+__global__ void k_dense_cands(Cands c, double* D, long long dim, const int32_t* pos) {
   const long long cand = blockIdx.x;
   if (cand >= c.n) return;
   const long long off = c.off[cand];
-  for (int t = threadIdx.x; t < c.len[cand]; t += blockDim.x)
-    D[(long long)c.row[off + t] * n + cand] = c.val[off + t];
+  const long long q = pos ? pos[cand] : cand;  // column of the table
+  double* Dc = D + (q >> 5) * dim * 32 + (q & 31);
+  for (int t = threadIdx.x; t < c.len[cand]; t += blockDim.x) Dc[(long long)c.row[off + t] * 32] = c.val[off + t];
 }
 
 // G[a][b] = merge-dot(left column a, candidate b) for b > a_min(a):
@@ -159,17 +164,17 @@ __global__ void k_dense_cands(Cands c, double* D, long long n) {
 // off the common support, and adding fl(v*0) = +-0 never changes the sum.
 __global__ void k_gram(const int64_t* lptr_off, const int32_t* llen, const int64_t* lptr, int use_ptr,
                        const int32_t* lrow, const double* lval, long long nleft, const double* D,
-                       long long n, double* G, int strictly_upper) {
-  // Warps are ordered column-chunk-major: the warps resident at one time share
-  // a few 32-column chunks of D (dim x 32 doubles each), which stay in L2
-  // while every left vector streams its rows through them.
+                       long long dim, long long n, long long bc0, long long nbc, const int32_t* perm, double* G) {
+  // One warp per (left vector a, 32-column chunk bc of the table), lane =
+  // column (candidate perm[j]).  g[a][b] is the sum over a's entries in order
+  // (the reference's merge order) of x_a[r] * x_b[r]; loads run 4 entries
+  // ahead of the add chain.
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nbw = (n + 31) >> 5;
   const long long a = warp % nleft;
-  const long long bc = warp / nleft;
-  if (bc >= nbw) return;
-  const long long b = bc * 32 + (threadIdx.x & 31);
-  if (strictly_upper && (bc * 32 + 31) <= a) return;  // whole warp below diagonal
+  const long long bc = bc0 + warp / nleft;
+  if (bc >= bc0 + nbc) return;
+  const int lane = threadIdx.x & 31;
+  const long long j = bc * 32 + lane;  // table column
   long long off, len;
   if (use_ptr) {
     off = lptr[a];
@@ -178,14 +183,63 @@ __global__ void k_gram(const int64_t* lptr_off, const int32_t* llen, const int64
     off = lptr_off[a];
     len = llen[a];
   }
+  const double* Dc = D + bc * dim * 32 + lane;
   double s = 0.0;
-  const bool act = b < n && (!strictly_upper || b > a);
-  for (long long t = 0; t < len; ++t) {
-    const int r = lrow[off + t];
-    const double x = lval[off + t];
-    if (act) s = dadd(s, dmul(x, D[(long long)r * n + b]));
+  long long t = 0;
+  for (; t + 4 <= len; t += 4) {
+    const int r0 = lrow[off + t], r1 = lrow[off + t + 1], r2 = lrow[off + t + 2], r3 = lrow[off + t + 3];
+    const double x0 = lval[off + t], x1 = lval[off + t + 1], x2 = lval[off + t + 2], x3 = lval[off + t + 3];
+    const double d0 = Dc[(long long)r0 * 32], d1 = Dc[(long long)r1 * 32];
+    const double d2 = Dc[(long long)r2 * 32], d3 = Dc[(long long)r3 * 32];
+    s = dadd(s, dmul(x0, d0));
+    s = dadd(s, dmul(x1, d1));
+    s = dadd(s, dmul(x2, d2));
+    s = dadd(s, dmul(x3, d3));
   }
-  if (act) G[a * n + b] = s;
+  for (; t < len; ++t) s = dadd(s, dmul(lval[off + t], Dc[(long long)lrow[off + t] * 32]));
+  if (j < n) G[a * n + (perm ? perm[j] : j)] = s;
+}
+
+// The candidate Gram table g[a][b] (a < b), symmetric in its pair: the sum
+// runs over the rows the two fibers share, ascending, of x_a[r] * x_b[r]
+// (both merge orders of the reference visit the same rows in the same order,
+// and rows present in one fiber only add +-0).  So each pair walks the
+// SHORTER fiber: the candidates are ranked by length (perm: rank -> cand, the
+// table's columns in rank order) and warp (i, chunk) walks candidate perm[i]
+// against the 32 ranked columns j > i of the chunk.  The chain of a pair is
+// min(len) long instead of len(a); warps start at the longest i.
+__global__ void k_gram_sym(Cands c, const int32_t* perm, const double* D, long long dim, long long n,
+                           long long nbw, double* G) {
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long i = n - 1 - warp / nbw;
+  const long long bc = warp % nbw;
+  if (i < 0 || bc * 32 + 31 <= i) return;
+  const int lane = threadIdx.x & 31;
+  const long long j = bc * 32 + lane;
+  const int a = perm[i];
+  const long long off = c.off[a], len = c.len[a];
+  const double* Dc = D + bc * dim * 32 + lane;
+  double s = 0.0;
+  long long t = 0;
+  for (; t + 8 <= len; t += 8) {
+    int r[8];
+    double x[8], d[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      r[u] = c.row[off + t + u];
+      x[u] = c.val[off + t + u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) d[u] = Dc[(long long)r[u] * 32];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = dadd(s, dmul(x[u], d[u]));
+  }
+  for (; t < len; ++t) s = dadd(s, dmul(c.val[off + t], Dc[(long long)c.row[off + t] * 32]));
+  if (j < n && j > i) {
+    const long long b = perm[j];
+    const long long lo = a < b ? a : b, hi = a < b ? b : a;
+    G[lo * n + hi] = s;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -328,21 +382,29 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   // ---- per-candidate |x|^2, Gram tables
   Buf<double> xsq(ctx, n);
   LAUNCH(ctx, k_xsq, (unsigned)n, 256, 0, c, xsq.p, ctx->d_flags);
-  Buf<double> D(ctx, (size_t)B.dim * n);
+  // candidates ranked by length (stable): the Gram pairs walk the shorter fiber
+  const long long nbw = (n + 31) / 32;
+  std::vector<int32_t> hlen(n), perm(n), rank(n);
+  ctx->to_host(hlen.data(), c.len, n);
+  ctx->sync();
+  for (int64_t q = 0; q < n; ++q) perm[q] = (int32_t)q;
+  std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) { return hlen[x] < hlen[y]; });
+  for (int64_t q = 0; q < n; ++q) rank[perm[q]] = (int32_t)q;
+  Buf<int32_t> dperm(ctx, n), drank(ctx, n);
+  ctx->to_dev(dperm.p, perm.data(), n);
+  ctx->to_dev(drank.p, rank.data(), n);
+  Buf<double> D(ctx, (size_t)B.dim * nbw * 32);
   D.zero();
-  LAUNCH(ctx, k_dense_cands, (unsigned)n, 128, 0, c, D.p, (long long)n);
+  LAUNCH(ctx, k_dense_cands, (unsigned)n, 128, 0, c, D.p, (long long)B.dim, (const int32_t*)drank.p);
   Buf<double> Gc(ctx, (size_t)n * n);
-  {
-    const long long warps = n * ((n + 31) / 32);
-    LAUNCH(ctx, k_gram, ceil_div(warps * 32, 256), 256, 0, c.off, c.len, (const int64_t*)nullptr, 0,
-           c.row, c.val, (long long)n, D.p, (long long)n, Gc.p, 1);
-  }
+  LAUNCH(ctx, k_gram_sym, ceil_div(n * nbw * 32, 256), 256, 0, c, (const int32_t*)dperm.p, D.p, (long long)B.dim,
+         (long long)n, nbw, Gc.p);
+  // kept fibers x candidates: warp (k, chunk of ranked columns)
   Buf<double> Gb(ctx, K0 > 0 ? (size_t)K0 * n : 1);
-  if (K0 > 0) {
-    const long long warps = K0 * ((n + 31) / 32);
-    LAUNCH(ctx, k_gram, ceil_div(warps * 32, 256), 256, 0, (const int64_t*)nullptr, (const int32_t*)nullptr,
-           B.rptr.p, 1, B.rrow.p, B.rval.p, (long long)K0, D.p, (long long)n, Gb.p, 0);
-  }
+  if (K0 > 0)
+    LAUNCH(ctx, k_gram, ceil_div(K0 * nbw * 32, 256), 256, 0, (const int64_t*)nullptr, (const int32_t*)nullptr,
+           B.rptr.p, 1, B.rrow.p, B.rval.p, (long long)K0, D.p, (long long)B.dim, (long long)n, 0ll, nbw,
+           (const int32_t*)dperm.p, Gb.p);
   D.reset();
   // ---- persistent kernel
   Buf<double> term(ctx, B.dim + 1), term2(ctx, B.dim + 1);
