@@ -107,10 +107,13 @@ __global__ void k_excl_scan_ll(const long long* in, long long n, long long* out)
 
 __global__ void k_copy_rows(const long long* oldbase, const long long* newbase, const int32_t* rowlen,
                             const int32_t* ok, const double* ov, int32_t* nk, double* nv, long long dim) {
-  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  // warp per row, lanes over its entries
+  const long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r >= dim) return;
+  const int lane = threadIdx.x & 31;
   const long long a = oldbase[r], b = newbase[r];
-  for (int t = 0; t < rowlen[r]; ++t) {
+  const int L = rowlen[r];
+  for (int t = lane; t < L; t += 32) {
     nk[b + t] = ok[a + t];
     nv[b + t] = ov[a + t];
   }
@@ -372,7 +375,7 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
     Buf<int32_t> nk(ctx, ncap);
     Buf<double> nv(ctx, ncap);
     if (B.rnnz)
-      LAUNCH(ctx, k_copy_rows, ceil_div(dim, 256), 256, 0, (const long long*)B.rowbase.p,
+      LAUNCH(ctx, k_copy_rows, ceil_div(dim * 32, 256), 256, 0, (const long long*)B.rowbase.p,
              (const long long*)nbase.p, B.rowlen.p, B.rek.p, B.rev.p, nk.p, nv.p, dim);
     B.rowbase = std::move(nbase);
     B.rek = std::move(nk);
