@@ -322,7 +322,7 @@ def run_c4(args, ctx, torch):
     val_t = torch.from_numpy(x.val).to(dev)
     dt = api.DeviceTensor.from_device_ptrs(x.shape, x.nnz, [idx_t[k].data_ptr() for k in range(3)],
                                            val_t.data_ptr(), ctx)
-    ms, info, phases, launches = _time_frontend(ctx, dt, C4, max(1, min(args.steps, 3)), 1, torch)
+    ms, info, phases, launches = _time_frontend(ctx, dt, C4, max(1, min(args.steps, 3)), 2, torch)
     out = {"workload": "C4: CTD-S on 1000x1000x100 at 10% density, planted rank-20 CP + N(0,0.01^2) "
                        "(non-integer fp64), c=5000, eps=1e-6, mode 0",
            "nnz": x.nnz, "ms_per_step": round(ms, 3), "nnz_per_s": round(x.nnz / (ms / 1e3), 1),
@@ -412,7 +412,7 @@ def run_c5(args, ctx, torch):
     nnz = meta["nnz"]
     dt = api.DeviceTensor.from_device_ptrs(C5["shape"], nnz, [idx[k].data_ptr() for k in range(3)],
                                            val.data_ptr(), ctx)
-    ms, info, phases, launches = _time_frontend(ctx, dt, C5, max(1, min(args.steps, 2)), 1, torch)
+    ms, info, phases, launches = _time_frontend(ctx, dt, C5, max(1, min(args.steps, 2)), 2, torch)
     pk, pk_kind = peaks()
     bs = 44 * nnz + 24 * info.n_fibers
     mat_ms = phases.get("matricize")

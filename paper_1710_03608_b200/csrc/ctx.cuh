@@ -2,6 +2,8 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -61,6 +63,7 @@ struct Ctx {
   void* big_alloc(size_t n) {
     n = (n + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
     std::lock_guard<std::mutex> lk(big_mu);
+    // the smallest cached block that fits, if within 25 % (+64 MB)
     auto it = big_free.lower_bound(n);
     if (it != big_free.end() && it->first <= n + n / 4 + (size_t(64) << 20)) {
       void* p = it->second;
@@ -70,12 +73,19 @@ struct Ctx {
       return p;
     }
     void* p = nullptr;
+    static const bool trace = getenv("CTD_ALLOC_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     if (cudaMalloc(&p, n) != cudaSuccess) {
       cudaGetLastError();
       big_trim_locked();  // give the cached blocks and the pool's reserve back, retry
       cudaMemPool_t pool;
       if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
       CUDA_OK(cudaMalloc(&p, n));
+    }
+    if (trace) {
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      if (ms > 1.0) fprintf(stderr, "[alloc] cudaMalloc %zu MB %.2f ms (cached free %zu MB)\n", n >> 20, ms,
+                            big_free_bytes >> 20);
     }
     big_live.emplace(p, n);
     return p;
@@ -123,6 +133,7 @@ struct Ctx {
           if (const char* e = getenv("CTD_GPU_CACHE_GB")) big_cap = (size_t)atoll(e) << 30;
         }
         if (big_free_bytes + n > big_cap) {
+          if (getenv("CTD_ALLOC_TRACE")) fprintf(stderr, "[alloc] over cap: free %zu MB\n", n >> 20);
           cudaStreamSynchronize(stream);  // queued kernels may still use it
           cudaFree(p);
         } else {
