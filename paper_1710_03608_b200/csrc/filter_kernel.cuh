@@ -650,6 +650,12 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         } else if (warp == kChainWarp) {
           // chain warp: z_r = sum_k fl(y_k R[r,k]) in ascending k (fiber_basis.cpp:56-65)
           int q = 0;
+          if (a.trace && blockIdx.x == 0 && lane == 0 && sb0 == 0) {
+            a.trace[(long long)n * kTraceW + 14] = clock64();
+            long long st = 0;
+            for (int g = 0; g < ngr; ++g) st += s_gmx[g];
+            a.trace[(long long)n * kTraceW + 31] = st * 1000 + ngr;
+          }
           for (int g = 0; g < ngr; ++g) {
             const int nchk = s_gch[g], mx = s_gmx[g];
             double z = 0.0;
@@ -677,6 +683,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
               if (z != 0.0 && kfd != kst) atomicExch(&a.slow[n], 1);
             }
           }
+          if (a.trace && blockIdx.x == 0 && lane == 0) a.trace[(long long)n * kTraceW + 15] = clock64();
         }
       }
     }
