@@ -224,6 +224,12 @@ int ctd_gpu_basis_append_batch(ctd_gpu_basis *b, int64_t n, const int64_t *cand_
                                const int64_t *rows, const double *vals, double epsilon,
                                int32_t *accepted, int32_t *degenerate, double *delta);
 /* R of the basis as CSC (size()+1, r_nnz, r_nnz), acceptance order. */
+/* The same with the candidates' rows (int32) and values in DEVICE memory
+ * (e.g. assembled by a device all-gather); cand_ptr stays on the host.  The
+ * row range / ascending checks run on the device. */
+int ctd_gpu_basis_append_batch_device(ctd_gpu_basis *b, int64_t n, const int64_t *cand_ptr,
+                                      const int32_t *rows, const double *vals, double epsilon,
+                                      int32_t *accepted, int32_t *degenerate, double *delta);
 int64_t ctd_gpu_basis_r_nnz(const ctd_gpu_basis *b);
 int ctd_gpu_basis_r(const ctd_gpu_basis *b, int64_t *col_ptr, int64_t *rows, double *vals);
 /* A shard of X bucketed once and kept resident: its fibers' global column
@@ -238,6 +244,10 @@ int ctd_gpu_shard_fibers(const ctd_gpu_shard *s, int64_t *fiber_col, double *sq_
  * Every cols[k] must be a fiber of this shard (ArgumentError otherwise). */
 int ctd_gpu_shard_gather(const ctd_gpu_shard *s, int64_t n, const int64_t *cols,
                          int64_t *cand_ptr, int64_t *rows, double *vals);
+/* The same with rows (int32) / vals written to DEVICE memory (cand_ptr on
+ * the host): the owner's half of a device-resident candidate all-gather. */
+int ctd_gpu_shard_gather_device(const ctd_gpu_shard *s, int64_t n, const int64_t *cols,
+                                int64_t *cand_ptr, int32_t *rows, double *vals);
 int ctd_gpu_shard_error_partials(const ctd_gpu_shard *s, const ctd_gpu_basis *b,
                                  double *x_sq, double *cross);
 int ctd_gpu_shard_destroy(ctd_gpu_shard *s);

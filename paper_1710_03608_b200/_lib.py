@@ -68,6 +68,7 @@ SIGNATURES = [
     ("ctd_gpu_basis_u", _I, [_V, _P]),
     ("ctd_gpu_sample_fibers", _I, [_V, _I64, _P, _P, _I64, _U64, _P, _P, _P]),
     ("ctd_gpu_basis_append_batch", _I, [_V, _I64, _P, _P, _P, _D, _P, _P, _P]),
+    ("ctd_gpu_basis_append_batch_device", _I, [_V, _I64, _P, _P, _P, _D, _P, _P, _P]),
     ("ctd_gpu_basis_r_nnz", _I64, [_V]),
     ("ctd_gpu_basis_r", _I, [_V, _P, _P, _P]),
     ("ctd_gpu_basis_error_partials", _I, [_V, _V, _V, _I, _P, _P]),
@@ -75,6 +76,7 @@ SIGNATURES = [
     ("ctd_gpu_shard_n_fibers", _I64, [_V]),
     ("ctd_gpu_shard_fibers", _I, [_V, _P, _P]),
     ("ctd_gpu_shard_gather", _I, [_V, _I64, _P, _P, _P, _P]),
+    ("ctd_gpu_shard_gather_device", _I, [_V, _I64, _P, _P, _P, _P]),
     ("ctd_gpu_shard_error_partials", _I, [_V, _V, _P, _P]),
     ("ctd_gpu_shard_destroy", _I, [_V]),
     ("ctd_gpu_shard_seq_total", _I, [_V, _D, _P]),

@@ -738,6 +738,76 @@ int ctd_gpu_sample_fibers(ctd_gpu_ctx* ctx, int64_t n_fibers, const int64_t* fib
   });
 }
 
+namespace {
+// device-side candidate checks: rows inside [0, dim) (FLAG_BOUNDS) and
+// strictly ascending within a candidate (FLAG_DUPLICATE: not normalized)
+__global__ void k_check_cands(Cands c, long long dim, unsigned* flags) {
+  const long long k = blockIdx.x;
+  if (k >= c.n) return;
+  const long long off = c.off[k];
+  const int len = c.len[k];
+  bool oob = false, ord = false;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    const int r = c.row[off + i];
+    oob |= r < 0 || r >= dim;
+    if (i > 0) ord |= r <= c.row[off + i - 1];
+  }
+  if (__syncthreads_or(oob) && threadIdx.x == 0) atomicOr(flags, FLAG_BOUNDS);
+  if (__syncthreads_or(ord) && threadIdx.x == 0) atomicOr(flags, FLAG_DUPLICATE);
+}
+}  // namespace
+
+int ctd_gpu_basis_append_batch_device(ctd_gpu_basis* b, int64_t n, const int64_t* cand_ptr, const int32_t* rows,
+                                      const double* vals, double epsilon, int32_t* accepted, int32_t* degenerate,
+                                      double* delta) {
+  return guarded([&] {
+    need(b, "basis");
+    bind_device(b->ctx);
+    if (n < 0) fail(CTD_ERR_ARGUMENT, "negative candidate count");
+    if (n == 0) return;
+    need(cand_ptr, "cand_ptr");
+    Basis& B = *b->b;
+    Ctx* c = b->ctx;
+    if (cand_ptr[0] != 0) fail(CTD_ERR_ARGUMENT, "cand_ptr[0] must be 0");
+    std::vector<int32_t> len(n);
+    std::vector<int64_t> off(n);
+    for (int64_t k = 0; k < n; ++k) {
+      if (cand_ptr[k + 1] < cand_ptr[k]) fail(CTD_ERR_ARGUMENT, "cand_ptr must be non-decreasing");
+      if (cand_ptr[k + 1] - cand_ptr[k] >= (int64_t(1) << 31)) fail(CTD_ERR_ARGUMENT, "candidate too long");
+      off[k] = cand_ptr[k];
+      len[k] = (int32_t)(cand_ptr[k + 1] - cand_ptr[k]);
+    }
+    if (cand_ptr[n] > 0) {
+      need(rows, "rows");
+      need(vals, "vals");
+    }
+    Buf<int32_t> dlen(c, n);
+    Buf<int64_t> doff(c, n);
+    c->to_dev(doff.p, off.data(), n);
+    c->to_dev(dlen.p, len.data(), n);
+    Cands cd;
+    cd.n = n;
+    cd.off = doff.p;
+    cd.len = dlen.p;
+    cd.row = rows;
+    cd.val = vals;
+    // the host path's checks (fiber_basis.cpp:45; rows ascending) on the device
+    LAUNCH(c, k_check_cands, (unsigned)n, 128, 0, cd, (long long)B.dim, c->d_flags);
+    c->check_flags("basis_append_batch_device");
+    BatchOut bo;
+    {
+      PhaseScope ps(c, PH_FILTER);
+      filter_batch(B, cd, epsilon, bo, false);
+    }
+    for (int64_t k = 0; k < n; ++k) {
+      if (accepted) accepted[k] = bo.accepted[k];
+      if (degenerate) degenerate[k] = bo.degenerate[k];
+      if (delta) delta[k] = bo.delta[k];
+    }
+    c->phase_flush();
+  });
+}
+
 int ctd_gpu_basis_append_batch(ctd_gpu_basis* b, int64_t n, const int64_t* cand_ptr, const int64_t* rows,
                                const double* vals, double epsilon, int32_t* accepted, int32_t* degenerate,
                                double* delta) {
@@ -840,6 +910,15 @@ __global__ void k_gather_fibers(const int64_t* src, const int64_t* dst, const in
     oval[d + i] = val[s + i];
   }
 }
+__global__ void k_gather_fibers32(const int64_t* src, const int64_t* dst, const int64_t* len, const int32_t* row,
+                                  const double* val, int32_t* orow, double* oval) {
+  const int k = blockIdx.x;
+  const int64_t s = src[k], d = dst[k], n = len[k];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    orow[d + i] = row[s + i];
+    oval[d + i] = val[s + i];
+  }
+}
 }  // namespace
 
 int ctd_gpu_shard_create(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int mode, ctd_gpu_shard** out) {
@@ -910,6 +989,34 @@ int ctd_gpu_shard_gather(const ctd_gpu_shard* s, int64_t n, const int64_t* cols,
            oval.p);
     c->to_host(rows, orow.p, tot);
     c->to_host(vals, oval.p, tot);
+    c->sync();
+  });
+}
+
+int ctd_gpu_shard_gather_device(const ctd_gpu_shard* s, int64_t n, const int64_t* cols, int64_t* cand_ptr,
+                                int32_t* rows, double* vals) {
+  return guarded([&] {
+    need(s, "shard");
+    bind_device(s->ctx);
+    need(cand_ptr, "cand_ptr");
+    if (n < 0) fail(CTD_ERR_ARGUMENT, "negative count");
+    std::vector<int64_t> src(n), len(n);
+    cand_ptr[0] = 0;
+    for (int64_t k = 0; k < n; ++k) {
+      const auto it = std::lower_bound(s->col.begin(), s->col.end(), cols[k]);
+      if (it == s->col.end() || *it != cols[k]) fail(CTD_ERR_ARGUMENT, "fiber not held by this shard");
+      const int64_t f = it - s->col.begin();
+      src[k] = s->ptr[f];
+      len[k] = s->ptr[f + 1] - s->ptr[f];
+      cand_ptr[k + 1] = cand_ptr[k] + len[k];
+    }
+    if (!rows || !vals || n == 0 || cand_ptr[n] == 0) return;
+    Ctx* c = s->ctx;
+    Buf<int64_t> dsrc(c, n), ddst(c, n), dlen(c, n);
+    c->to_dev(dsrc.p, src.data(), n);
+    c->to_dev(ddst.p, cand_ptr, n);
+    c->to_dev(dlen.p, len.data(), n);
+    LAUNCH(c, k_gather_fibers32, (unsigned)n, 128, 0, dsrc.p, ddst.p, dlen.p, s->fb.row.p, s->fb.val.p, rows, vals);
     c->sync();
   });
 }

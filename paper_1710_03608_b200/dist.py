@@ -114,6 +114,26 @@ class Comm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t.cpu().numpy()
 
+    def allgather_dev(self, t, counts):
+        """Variable-length all-gather of a 1-D DEVICE tensor whose length on rank
+        r is counts[r] (known everywhere); the concatenation in rank order on
+        t's device.  NCCL gathers in place on the device (all_gather_into_tensor);
+        gloo (CPU tests) stages through the host."""
+        torch = self.torch
+        m = max(max(counts), 1)
+        buf = torch.zeros(m, dtype=t.dtype, device=t.device)
+        buf[:t.shape[0]] = t
+        if self.device.type == "cuda":
+            out = torch.empty(self.world * m, dtype=t.dtype, device=t.device)
+            self.dist.all_gather_into_tensor(out, buf, group=self.group)
+            parts = [out[r * m: r * m + counts[r]] for r in range(self.world)]
+        else:
+            cb = buf.cpu()
+            outs = [torch.empty_like(cb) for _ in range(self.world)]
+            self.dist.all_gather(outs, cb, group=self.group)
+            parts = [o[:counts[r]].to(t.device) for r, o in enumerate(outs)]
+        return torch.cat(parts)
+
     def chain(self, fn, start: float = 0.0):
         """Sequential hand-off in rank order: rank r receives the value rank r-1
         produced (rank 0 starts from `start`), applies fn, passes the result on.
@@ -151,7 +171,11 @@ class LocalFibers:
 
 
 class GpuKernels:
-    """Per-rank compute through libctd_gpu (no CPU fallback)."""
+    """Per-rank compute through libctd_gpu (no CPU fallback).  `device_plane`:
+    candidate payloads stay in device memory (owner gather -> device all-gather
+    -> draw-order assembly -> filter), no host round trip."""
+
+    device_plane = True
 
     def __init__(self, ctx: Optional[api.Context] = None):
         self.ctx = ctx or api.default_context()
@@ -209,6 +233,21 @@ class _GpuShard:
         api._check(self.k.L.ctd_gpu_shard_gather(self.h, n, api._p(cols), api._p(ptr), api._p(rows), api._p(vals)))
         return ptr, rows[:ptr[-1]], vals[:ptr[-1]]
 
+    def gather_device(self, cols):
+        """(cand_ptr on the host, rows int32 and vals on the device) of the given
+        local fibers, in the given order."""
+        import torch
+        cols = np.ascontiguousarray(cols, np.int64)
+        n = cols.shape[0]
+        ptr = np.zeros(n + 1, np.int64)
+        api._check(self.k.L.ctd_gpu_shard_gather(self.h, n, api._p(cols), api._p(ptr), None, None))
+        dev = torch.device("cuda", torch.cuda.current_device())
+        rows = torch.empty(max(int(ptr[-1]), 1), dtype=torch.int32, device=dev)
+        vals = torch.empty(max(int(ptr[-1]), 1), dtype=torch.float64, device=dev)
+        api._check(self.k.L.ctd_gpu_shard_gather_device(self.h, n, api._p(cols), api._p(ptr), rows.data_ptr(),
+                                                        vals.data_ptr()))
+        return ptr, rows[:int(ptr[-1])], vals[:int(ptr[-1])]
+
     def error_partials(self, basis):
         xs, cr = C.c_double(), C.c_double()
         api._check(self.k.L.ctd_gpu_shard_error_partials(self.h, basis.h, C.byref(xs), C.byref(cr)))
@@ -263,6 +302,22 @@ class _GpuBasis:
         vals = np.ascontiguousarray(vals, np.float64)
         api._check(self.k.L.ctd_gpu_basis_append_batch(self.h, n, api._p(ptr), api._p(rows), api._p(vals), eps,
                                                        api._p(acc), api._p(deg), api._p(dl)))
+        return acc[:n], deg[:n], dl[:n]
+
+    def append_batch_device(self, ptr, rows, vals, eps):
+        """Candidates in device memory (rows int32, vals fp64 torch tensors)."""
+        import torch
+        n = ptr.shape[0] - 1
+        acc = np.zeros(max(n, 1), np.int32)
+        deg = np.zeros(max(n, 1), np.int32)
+        dl = np.zeros(max(n, 1))
+        ptr = np.ascontiguousarray(ptr, np.int64)
+        rows = rows.to(torch.int32).contiguous()
+        vals = vals.to(torch.float64).contiguous()
+        torch.cuda.current_stream().synchronize()  # the assembly ran on torch's stream
+        api._check(self.k.L.ctd_gpu_basis_append_batch_device(self.h, n, api._p(ptr), rows.data_ptr(),
+                                                              vals.data_ptr(), eps, api._p(acc), api._p(deg),
+                                                              api._p(dl)))
         return acc[:n], deg[:n], dl[:n]
 
     def size(self):
@@ -397,6 +452,61 @@ def _gather_candidates(sh, comm, unique):
     return cptr, crow, cval
 
 
+def _gather_candidates_device(sh, comm, unique):
+    """_gather_candidates with the payload on the device: each owner gathers
+    its candidates into device memory, one variable-length device all-gather
+    per array (NCCL), and the draw-order layout is a device gather.  Only the
+    per-candidate lengths and owners (O(candidates)) cross the host."""
+    import torch
+    pos = np.searchsorted(sh.col, unique)
+    ok = pos < sh.col.shape[0]
+    mine = np.zeros(unique.shape[0], bool)
+    mine[ok] = sh.col[pos[ok]] == unique[ok]
+    which = np.nonzero(mine)[0].astype(np.int64)
+    lptr, lrows, lvals = sh.gather_device(unique[which])
+    g_which = comm.allgather(which)
+    g_lens = comm.allgather(np.diff(lptr).astype(np.int64))
+    counts = [int(ln.sum()) for ln in g_lens]
+    rows_all = comm.allgather_dev(lrows, counts)
+    vals_all = comm.allgather_dev(lvals, counts)
+    n_u = unique.shape[0]
+    owner = np.full(n_u, -1, np.int64)
+    cand_len = np.zeros(n_u, np.int64)
+    src = np.zeros(n_u, np.int64)
+    base = 0
+    for r, (w, ln) in enumerate(zip(g_which, g_lens)):
+        owner[w] = r
+        cand_len[w] = ln
+        if w.size:
+            src[w] = base + np.concatenate([[0], np.cumsum(ln)[:-1]]).astype(np.int64)
+        base += counts[r]
+    if n_u and owner.min() < 0:
+        raise api.CtdError("a drawn fiber has no owner (shards do not cover the fiber space)")
+    cptr = np.concatenate([[0], np.cumsum(cand_len)]).astype(np.int64)
+    total = int(cptr[-1])
+    dev = rows_all.device
+    if total:
+        shift = torch.from_numpy(src - cptr[:-1]).to(dev)
+        idx = torch.repeat_interleave(shift, torch.from_numpy(cand_len).to(dev)) + torch.arange(total, device=dev)
+        crow, cval = rows_all[idx], vals_all[idx]
+    else:
+        crow = torch.zeros(0, dtype=torch.int32, device=dev)
+        cval = torch.zeros(0, dtype=torch.float64, device=dev)
+    return cptr, crow, cval
+
+
+def _candidates_and_filter(sh, comm, k, B, unique, epsilon):
+    """Assemble the candidates (device plane when the kernels have one) and
+    run the replicated filter; (accepted, degenerate, delta, candidate nnz)."""
+    if getattr(k, "device_plane", False):
+        cptr, crow, cval = _gather_candidates_device(sh, comm, unique)
+        acc, deg, dl = B.append_batch_device(cptr, crow, cval, epsilon)
+    else:
+        cptr, crow, cval = _gather_candidates(sh, comm, unique)
+        acc, deg, dl = B.append_batch(cptr, crow, cval, epsilon)
+    return acc, deg, dl, int(cptr[-1])
+
+
 def ctd_s_sharded(shape, local, mode: int, sample_size: int, epsilon: float = 1e-6, seed: int = 42,
                   comm: Optional[Comm] = None, kernels=None, with_error: bool = False) -> ShardedResult:
     """CTD-S front end over fiber-range shards; every rank returns the same
@@ -431,23 +541,22 @@ def ctd_s_sharded(shape, local, mode: int, sample_size: int, epsilon: float = 1e
     # 2. the law, chained across the ranks; draws and dedup
     total, unique = _sample_sharded(sh, comm, k, sample_size, seed)
     mark()
-    # 3. candidate payloads from their owners, assembled in draw order
-    cptr, crow, cval = _gather_candidates(sh, comm, unique)
-    mark()
-    # 4. replicated filter + U recurrence
+    # 3-4. candidate payloads from their owners, assembled in draw order;
+    # replicated filter + U recurrence
     dim = int(shape[mode])
     B = k.basis(dim)
-    acc, deg, dl = B.append_batch(cptr, crow, cval, epsilon)
+    acc, deg, dl, cand_nnz = _candidates_and_filter(sh, comm, k, B, unique, epsilon)
+    mark()
     kept = unique[np.nonzero(acc)[0]]
     U = B.u()
     rp, rr, rv = B.r()
     mark()
     if trace:
-        names = ["shard", "range check", "law+draws", "candidates", "filter+U/R"]
+        names = ["shard", "range check", "law+draws", "candidates+filter", "U/R"]
         print("[dist trace] rank %d: " % comm.rank + " ".join(
             f"{n}={1e3 * (b - a):.1f}ms" for n, a, b in zip(names, tm[:-1], tm[1:])), flush=True)
     res = ShardedResult(kept, U, rp, rr, rv, unique, acc, deg, dl, float(total), None, n_fibers,
-                        {"local_fibers": int(sh.col.shape[0]), "candidate_nnz": int(cptr[-1])})
+                        {"local_fibers": int(sh.col.shape[0]), "candidate_nnz": cand_nnz})
     # 5. error partials, all-reduced
     if with_error:
         xs, cr = sh.error_partials(B)
@@ -485,10 +594,9 @@ class ShardedStream:
         sh = self.k.shard((list(hist_shape), local[0], local[1]), mode)
         _check_ranges(sh, self.comm)
         _, unique = _sample_sharded(sh, self.comm, self.k, sample_size, seed)
-        cptr, crow, cval = _gather_candidates(sh, self.comm, unique)
-        sh.close()
         self.B = self.k.basis(int(hist_shape[mode]))
-        acc, _, _ = self.B.append_batch(cptr, crow, cval, epsilon)
+        acc, _, _, _ = _candidates_and_filter(sh, self.comm, self.k, self.B, unique, epsilon)
+        sh.close()
         self.kept_flat = list(unique[np.nonzero(acc)[0]])
 
     def step(self, local, sample_size: int):
@@ -500,9 +608,8 @@ class ShardedStream:
             sh = self.k.shard((self.slab_shape + [1], idx, val), self.mode)
             _check_ranges(sh, self.comm)
             _, unique = _sample_sharded(sh, self.comm, self.k, sample_size, self.seed ^ self.t)
-            cptr, crow, cval = _gather_candidates(sh, self.comm, unique)
+            acc, _, _, _ = _candidates_and_filter(sh, self.comm, self.k, self.B, unique, self.eps)
             sh.close()
-            acc, _, _ = self.B.append_batch(cptr, crow, cval, self.eps)
             self.kept_flat += [int(j) + self.t * self.slab_cols for j in unique[np.nonzero(acc)[0]]]
         self.t += 1
         return self

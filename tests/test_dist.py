@@ -202,3 +202,41 @@ def test_sharded_stream_gpu_two_ranks(port, tmp_path):
     for r in res:
         assert np.array_equal(r[f"k{x.shape[2] - 3}"], ps.kept_flat())
         assert np.array_equal(r["U"].view(np.int64), ps.U().view(np.int64))
+
+
+@pytest.mark.gpu
+def test_device_candidates_match_host_path(port):
+    """The device-plane entry points (ctd_gpu_shard_gather_device,
+    ctd_gpu_basis_append_batch_device) give the host path's decisions and U
+    bit for bit, and run the host path's input checks on the device."""
+    from paper_1710_03608_b200 import ctd as api
+
+    k = dist.GpuKernels()
+    x = datagen.random_sparse([40, 30, 20], 0.05, 33)
+    sh = k.shard((x.shape, x.idx, x.val), 0)
+    cols = sh.col[::7][:40]
+    ptr_h, rows_h, vals_h = sh.gather(cols)
+    ptr_d, rows_d, vals_d = sh.gather_device(cols)
+    assert np.array_equal(ptr_h, ptr_d)
+    assert np.array_equal(rows_h, rows_d.cpu().numpy().astype(np.int64))
+    assert np.array_equal(vals_h, vals_d.cpu().numpy())
+    Bh, Bd = k.basis(40), k.basis(40)
+    a_h = Bh.append_batch(ptr_h, rows_h, vals_h, 1e-6)
+    a_d = Bd.append_batch_device(ptr_d, rows_d, vals_d, 1e-6)
+    for u, v in zip(a_h, a_d):
+        assert np.array_equal(np.asarray(u).view(np.int64) if u.dtype == np.float64 else u,
+                              np.asarray(v).view(np.int64) if v.dtype == np.float64 else v)
+    assert np.array_equal(Bh.u().view(np.int64), Bd.u().view(np.int64))
+    # checks: a row outside [0, dim) and rows that do not ascend
+    bad = rows_d.clone()
+    bad[0] = 40
+    with pytest.raises(api.ShapeError):
+        k.basis(40).append_batch_device(ptr_d, bad, vals_d, 1e-6)
+    j = int(np.argmax(np.diff(ptr_d) >= 2))
+    bad = rows_d.clone()
+    bad[ptr_d[j] + 1] = bad[ptr_d[j]]
+    with pytest.raises(api.ArgumentError):
+        k.basis(40).append_batch_device(ptr_d, bad, vals_d, 1e-6)
+    for b in (Bh, Bd):
+        b.close()
+    sh.close()
