@@ -614,6 +614,7 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
       fprintf(stderr, " directs=%lld | P1 prod wait=%lld compute=%lld probe=%lld", tr[i * kTraceW + 25],
               tr[i * kTraceW + 28], tr[i * kTraceW + 29], tr[i * kTraceW + 27]);
       fprintf(stderr, " | uncertified div=%lld", tr[i * kTraceW + 30]);
+      fprintf(stderr, " | P2 chain wait=%lld work=%lld", tr[i * kTraceW + 26], tr[i * kTraceW + 27]);
       fprintf(stderr, " | P2 ring: setup=%lld chain=%lld steps=%lld groups=%lld", tr[i * kTraceW + 14] - tr[i * kTraceW + 10],
               tr[i * kTraceW + 15] - tr[i * kTraceW + 14], tr[i * kTraceW + 31] / 1000, tr[i * kTraceW + 31] % 1000);
       fprintf(stderr, "\n");

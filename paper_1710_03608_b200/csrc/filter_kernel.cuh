@@ -38,9 +38,14 @@ constexpr int kWin = 256;  // per-warp window doubles (sizes the shared window a
 #define CTD_RING_SLOTS 3
 #endif
 constexpr int kRingW = CTD_RING_W;         // steps per ring chunk
-constexpr int kRingS = 33;                 // padded lane stride (doubles)
+// Slot layout: row-major, [32 rows][kRingLS] doubles: a producer warp (32
+// consecutive steps of one row) stores 256 contiguous bytes; the chain lane
+// reads its row two steps per 16-byte load (kRingLS = kRingW + 2: 49 16-byte
+// units per row, odd, so the 8 lanes of a load phase hit distinct banks).
+constexpr int kRingLS = CTD_RING_W + 2;
 constexpr int kRingSlots = CTD_RING_SLOTS;
-constexpr int kRingDoubles = kRingSlots * kRingW * kRingS;
+constexpr int kRingSlot = 32 * kRingLS;  // doubles per slot
+constexpr int kRingDoubles = kRingSlots * kRingSlot;
 // (Keeping producers off the chain warp's SM sub-partition measured slower:
 // the producers, not issue-slot sharing, bound the ring.)
 constexpr int kChainWarp = kFThreads / 32 - 1;
@@ -63,6 +68,12 @@ constexpr int kRowPh = kProdThreads / kRingW;
 constexpr int kRowSlots = (32 + kRowPh - 1) / kRowPh;
 static_assert(kRowPh * kRingW == kProdThreads && kRingW % 32 == 0, "ring mapping");
 constexpr int kMeta = kFThreads;           // P2 rows per ring session (one group per warp)
+constexpr int kQuadRank = 160;             // sessions up to this many rows ranked by counting
+// L2 prefetch distance (ring chunks) of the producers' operand streams
+#ifndef CTD_PF_DIST
+#define CTD_PF_DIST 2
+#endif
+constexpr int kPfDist = CTD_PF_DIST;
 constexpr int kWinArea = (kFThreads / 32) * kWin > kRingDoubles ? (kFThreads / 32) * kWin : kRingDoubles;
 
 constexpr size_t kFilterSmem = (size_t)(2 * kVec + kWinArea) * 8;
@@ -74,34 +85,50 @@ __device__ __forceinline__ void nbar_arrive(int id, int cnt) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
 }
 
-// acc <- (((acc + s_0) + s_1) + ... + s_{cnt-1}), s_t = rb[t * kRingS + lane]:
-// 32 independent chains, one per lane, loads 16 steps ahead.
-__device__ __forceinline__ double lane_chain(const double* rb, int lane, int cnt, double acc) {
-  const double* p = rb + lane;
-  if (cnt == kRingW) {
-    // The batch h+1 loads are issued in iteration h of a loop that is NOT
-    // unrolled, so they stay 16 adds (~130 cycles) ahead of their use: fully
-    // unrolled, ptxas re-interleaves them ~4 adds ahead, which the ring's
-    // shared-memory traffic then exposes on every add.
-    double v[16];
+// acc <- (((acc + s_0) + s_1) + ... + s_95), s_t = rb[lane * kRingLS + t]:
+// 32 independent chains, one per lane, over a full chunk (producers write
+// every step of a chunk; steps past a row's end hold +-0.0, which leave a
+// chain that starts at +0.0 unchanged: it never becomes -0.0).  Two steps per
+// 16-byte load, batches of 16 steps loaded one batch ahead, ping-pong
+// registers (no copies: the chain warp shares its sub-partition's issue slots
+// with producer warps, so its instruction count per step is what it pays).
+__device__ __forceinline__ double lane_chain(const double* rb, int lane, double acc) {
+  static_assert(kRingW % 32 == 0, "lane_chain: pairs of 16-step batches");
+  const double2* p = reinterpret_cast<const double2*>(rb + lane * kRingLS);
+  double2 u[8], w[8];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) v[q] = p[q * kRingS];
+  for (int q = 0; q < 8; ++q) u[q] = p[q];
 #pragma unroll 1
-    for (int h = 0; h < kRingW / 16; ++h) {
-      double w[16];
-      const double* pn = p + (h + 1 < kRingW / 16 ? h + 1 : h) * 16 * kRingS;
+  for (int h = 0; h < kRingW / 16; h += 2) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) w[q] = pn[q * kRingS];
+    for (int q = 0; q < 8; ++q) w[q] = p[(h + 1) * 8 + q];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) acc = dadd(acc, v[q]);
-#pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = w[q];
+    for (int q = 0; q < 8; ++q) {
+      acc = dadd(acc, u[q].x);
+      acc = dadd(acc, u[q].y);
     }
-  } else {
-    for (int t = 0; t < cnt; ++t) acc = dadd(acc, p[t * kRingS]);
+    if (h + 2 < kRingW / 16) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) u[q] = p[(h + 2) * 8 + q];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      acc = dadd(acc, w[q].x);
+      acc = dadd(acc, w[q].y);
+    }
   }
   return acc;
 }
+
+// The first cnt steps only (short last chunks: a full chunk costs ~9 cycles
+// per step, this loop ~4x that per step).
+__device__ __forceinline__ double lane_chain_n(const double* rb, int lane, int cnt, double acc) {
+  const double* p = rb + lane * kRingLS;
+#pragma unroll 4
+  for (int t = 0; t < cnt; ++t) acc = dadd(acc, p[t]);
+  return acc;
+}
+constexpr int kShortChunk = 24;
 
 // The residual terms of try_append_fiber in the reference's summation order
 // (fiber_basis.cpp:66-77): x's rows ascending ((x_i - z_i)^2, :69-70), then
@@ -305,8 +332,15 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         if (!ok) qd = ddiv_slow(num, prev_delta);
         return (i < Ko && j < Ko) ? dadd(uo, qd) : qd;
       };
-      // This CTA owns rows i = blockIdx.x + nb * r (r < Rs); groups of 32.
-      const int Rs = ((int)blockIdx.x < Kn) ? (Kn - 1 - (int)blockIdx.x) / (int)nb + 1 : 0;
+      // This CTA owns rows i = blockIdx.x + unb * r (r < Rs); groups of 32.
+      // While one group per CTA suffices, the last CTA owns none: it runs the
+      // ordered append of x_{n-1} above, which the other CTAs' P2 waits for.
+#ifdef CTD_NO_UNB
+      const unsigned unb = nb;
+#else
+      const unsigned unb = (nb > 1 && Kn <= 32 * (int)(nb - 1)) ? nb - 1 : nb;
+#endif
+      const int Rs = ((int)blockIdx.x < Kn && blockIdx.x < unb) ? (Kn - 1 - (int)blockIdx.x) / (int)unb + 1 : 0;
       const int nch = (Kn + kRingW - 1) / kRingW;
       const int Q = ((Rs + 31) / 32) * nch;
       const int warp = threadIdx.x >> 5;
@@ -314,7 +348,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
       if (last) {
         for (long long e = threadIdx.x; e < (long long)Rs * Kn; e += blockDim.x) {
           const int r = (int)(e / Kn), j = (int)(e - (long long)r * Kn);
-          const long long i = blockIdx.x + (long long)nb * r;
+          const long long i = blockIdx.x + (long long)unb * r;
           double* up = a.U + i * LD + j;
           *up = unew(i, j, (i < Ko && j < Ko) ? ldg_cg(up) : 0.0);
         }
@@ -328,7 +362,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         // the chain warp's latency, tools/ubench_ring.cu.)
         const int pi = producer_index(warp, lane);
         const int t = pi % kRingW, rq = pi / kRingW;  // rq is warp-uniform
-        double* ring_t = ring + t * kRingS;
+        double* ring_t = ring + rq * kRingLS + t;  // + slot, + row phase k * kRowPh * kRingLS
         const bool ptr = a.trace && blockIdx.x == 0 && pi == 0;
         long long pwt = 0, pct = 0;
         int q = 0;
@@ -339,7 +373,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
           unsigned inew = 0;
 #pragma unroll
           for (int k = 0; k < NA; ++k) {
-            const long long i = blockIdx.x + (long long)nb * (32 * g + rq + kRowPh * k);
+            const long long i = blockIdx.x + (long long)unb * (32 * g + rq + kRowPh * k);
             up[k] = a.U + i * LD;
             yi[k] = (upd && i < Ko) ? yval(i) : 0.0;
             inew |= (unsigned)(i == Ko) << k;
@@ -358,7 +392,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
           for (int j0 = 0; j0 < Kn; j0 += kRingW, ++q) {
             const int j = j0 + t;
             const int b = q % kRingSlots;
-            double* rb = ring_t + b * (kRingW * kRingS);
+            double* rb = ring_t + b * kRingSlot;
             const long long pt0 = ptr ? clock64() : 0;
             if (q >= kRingSlots) nbar_sync(1 + kRingSlots + b, kRingThreads);
             const long long pt1 = ptr ? clock64() : 0;
@@ -398,7 +432,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
               }
             }
 #pragma unroll
-            for (int k = 0; k < NA; ++k) rb[rq + kRowPh * k] = dmul(un[k], gj);
+            for (int k = 0; k < NA; ++k) rb[kRowPh * k * kRingLS] = dmul(un[k], gj);
             nbar_arrive(1 + b, kRingThreads);
             if (ptr) {
               pwt += pt1 - pt0;
@@ -459,13 +493,15 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
 #endif
           const long long tc0 = clock64();
 #ifndef CTD_EXP_NOCHAIN
-          acc = lane_chain(ring + b * (kRingW * kRingS), lane, cnt, acc);
+          // (steps >= Kn hold +-0.0)
+          acc = cnt > kShortChunk ? lane_chain(ring + b * kRingSlot, lane, acc)
+                                  : lane_chain_n(ring + b * kRingSlot, lane, cnt, acc);
 #endif
           tcc += clock64() - tc0;
           if (q + kRingSlots < Q) nbar_arrive(1 + kRingSlots + b, kRingThreads);
           if (ch == nch - 1) {
             const int r = 32 * g + lane;
-            if (r < Rs) ycur[blockIdx.x + (long long)nb * r] = acc;
+            if (r < Rs) ycur[blockIdx.x + (long long)unb * r] = acc;
             acc = 0.0;
           }
         }
@@ -527,7 +563,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
       int* s_gch = s_pos + kMeta;  // [32] chunks per group
       int* s_gmx = s_gch + 32;     // [32] longest row per group
       long long* s_base = reinterpret_cast<long long*>(s_gmx + 32);
-      int* s_key = reinterpret_cast<int*>(s_base + kMeta);  // lengths by position (ranking)
+      int* s_key = reinterpret_cast<int*>(s_base + kMeta);  // ranking keys
       double* ring = dyn + 2 * kVec;
       const int warp = threadIdx.x >> 5;
       const int Rs2 = ((int)blockIdx.x < srn) ? (srn - 1 - (int)blockIdx.x) / (int)nb + 1 : 0;
@@ -541,21 +577,51 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
             const long long q = blockIdx.x + (long long)nb * (sb0 + r);
             row = ldg_cg(&a.sr_list[q]);
             L = ldg_cg(&a.rowlen[row]);
-            s_key[r] = L;
+          }
+          hist[r] = (uint32_t)row;  // by session position (hist is P3 scratch)
+          // rank by length, longest first, ties by position: bitonic sort of
+          // the keys (2^22 - 1 - L) << 10 | r, one per thread (L < 2^22: K is)
+          // (small sessions, C2: each thread counts the keys below its own,
+          // O(ns) per thread, cheaper than the 45 bitonic stages)
+          uint32_t* kk = reinterpret_cast<uint32_t*>(s_key);
+          static_assert(kMeta == kFThreads && kMeta == 512, "bitonic ranking: one key per thread");
+          const uint32_t mykey = r < ns ? ((uint32_t)(0x3FFFFF - L) << 10) | (uint32_t)r : 0xFFFFFFFFu;
+          kk[r] = mykey;
+          const bool quad = ns <= kQuadRank;
+          if (quad) {
+            __syncthreads();
+            int rank = 0;
+            if (r < ns)
+              for (int u = 0; u < ns; ++u) rank += kk[u] < mykey;
+            __syncthreads();
+            if (r < ns) kk[rank] = mykey;
+          }
+          for (int kb = 2; !quad && kb <= kMeta; kb <<= 1) {
+            for (int j = kb >> 1; j > 0; j >>= 1) {
+              __syncthreads();
+              const int pj = r ^ j;
+              if (pj > r) {
+                const uint32_t x = kk[r], x2 = kk[pj];
+                if ((x > x2) == ((r & kb) == 0)) {
+                  kk[r] = x2;
+                  kk[pj] = x;
+                }
+              }
+            }
           }
           __syncthreads();
           if (r < ns) {
-            int rank = 0;
-            for (int u = 0; u < ns; ++u) {
-              const int Lu = s_key[u];
-              rank += (Lu > L) | ((Lu == L) & (u < r));
-            }
+            const int rank = r;  // slot r of the sorted keys holds the row of rank r
+            const uint32_t key = kk[r];
+            const int src = (int)(key & 1023u);
+            row = (int)hist[src];
+            L = 0x3FFFFF - (int)(key >> 10);
             s_row[rank] = row;
             s_base[rank] = a.rowbase[row];
             s_len[rank] = L;
             s_inx[rank] = ldg_cg(&a.tag[row]) == tg;
             s_tf[rank] = 0x7fffffff;
-            s_pos[rank] = r;
+            s_pos[rank] = src;
           }
           __syncthreads();
           const int Lr = r < ns ? s_len[r] : 0;
@@ -575,7 +641,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
           // (NA active row slots, compile-time as in P1)
           const int pi = producer_index(warp, lane);
           const int t = pi % kRingW, rq = pi / kRingW;
-          double* ring_t = ring + t * kRingS;
+          double* ring_t = ring + rq * kRingLS + t;
           int q = 0;
           auto group = [&](int g, auto na_c) {
             constexpr int NA = decltype(na_c)::value;
@@ -591,28 +657,70 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
             double vv[NA];
             unsigned okm = 0;    // rows with an entry at this step (prefetched chunk)
             unsigned found = 0;  // rows whose first y != 0 entry is known (warp-uniform)
+            const int t0 = t & ~31;  // first step of this warp's 32
             auto load = [&](int te) {
               okm = 0;
 #pragma unroll
               for (int k = 0; k < NA; ++k) {
                 const bool ok = te < slen[k];
+#if defined(CTD_EXP_L2FAKE)
+                kv[k] = ok ? ldg_cg(&a.rek[(sbase[k] & 0xFFFFFll) + te]) : 0;
+                vv[k] = ok ? ldg_cg(&a.rev[(sbase[k] & 0xFFFFFll) + te]) : 0.0;
+#elif defined(CTD_EXP_NOLOAD2)
+                kv[k] = ok ? (te & 1023) : 0;
+                vv[k] = ok ? 1.0 : 0.0;
+#else
                 kv[k] = ok ? ldg_cg(&a.rek[sbase[k] + te]) : 0;
                 vv[k] = ok ? ldg_cg(&a.rev[sbase[k] + te]) : 0.0;
+#endif
                 okm |= (unsigned)ok << k;
               }
             };
+            // R's row index does not fit L2 at C5 scale: per-line L2
+            // prefetches kPfDist chunks ahead (thread pi < 288 takes line
+            // pi / 32 of row pi % 32: 3 lines of k, 6 of values per chunk).
+            // (Bulk cp.async.bulk.prefetch of whole row segments measured
+            // slower; r2 experiments.)
+            const int lr = 32 * g + (pi & 31), ll = pi >> 5;
+            const bool lok = pi < 288 && (pi & 31) < min(32, ns - 32 * g);
+            const int llen = lok ? s_len[lr] : 0;
+            const long long lbase = lok ? s_base[lr] : 0;
+            auto prefetch = [&](int c) {
+              const int e = c * kRingW + (ll < 3 ? ll * 32 : (ll - 3) * 16);
+              if (e >= llen) return;
+              const void* pp = ll < 3 ? (const void*)(a.rek + lbase + e) : (const void*)(a.rev + lbase + e);
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(pp));
+            };
+#ifndef CTD_NO_PF_P2
+            for (int c = 1; c <= kPfDist && c < nchk; ++c) prefetch(c);
+#endif
             load(t);
             for (int ch = 0; ch < nchk; ++ch, ++q) {
               const int b = q % kRingSlots;
-              double* rb = ring_t + b * (kRingW * kRingS);
+              double* rb = ring_t + b * kRingSlot;
               const int te = ch * kRingW + t;
+#ifndef CTD_NO_PF_P2
+              if (ch + 1 + kPfDist < nchk) prefetch(ch + 1 + kPfDist);
+#endif
               if (q >= kRingSlots) nbar_sync(1 + kRingSlots + b, kRingThreads);
+#ifdef CTD_EXP_NOPROD2
+              if (okm != 0xFFFFFFFFu) {
+                nbar_arrive(1 + b, kRingThreads);
+                continue;
+              }
+#endif
 #pragma unroll
               for (int k = 0; k < NA; ++k) {
                 const int r = rq + kRowPh * k;
+                // the warp's steps are te0 .. te0+31 (t0 is a multiple of 32):
+                // past the row's end they only hold +0.0
+                if (ch * kRingW + t0 >= slen[k]) {
+                  rb[kRowPh * k * kRingLS] = 0.0;
+                  continue;
+                }
                 const bool ok = (okm >> k) & 1;
                 const double yk = ok ? (y_fits ? vA[kv[k]] : ldg_cg(&ycur[kv[k]])) : 0.0;
-                rb[r] = dmul(yk, vv[k]);
+                rb[kRowPh * k * kRingLS] = dmul(yk, vv[k]);
                 if (!((found >> k) & 1)) {
                   // first kept column of the row with y != 0 (the touch order)
                   const unsigned nz = __ballot_sync(0xffffffffu, ok && yk != 0.0);
@@ -650,6 +758,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         } else if (warp == kChainWarp) {
           // chain warp: z_r = sum_k fl(y_k R[r,k]) in ascending k (fiber_basis.cpp:56-65)
           int q = 0;
+          long long p2w = 0, p2c = 0;  // trace: cycles waiting for full slots / chaining
           if (a.trace && blockIdx.x == 0 && lane == 0 && sb0 == 0) {
             a.trace[(long long)n * kTraceW + 14] = clock64();
             long long st = 0;
@@ -661,9 +770,19 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
             double z = 0.0;
             for (int ch = 0; ch < nchk; ++ch, ++q) {
               const int b = q % kRingSlots;
+              const long long tw0 = a.trace ? clock64() : 0;
               nbar_sync(1 + b, kRingThreads);
-              // steps past a row's length hold +-0.0, which leave z unchanged
-              z = lane_chain(ring + b * (kRingW * kRingS), lane, min(kRingW, mx - ch * kRingW), z);
+              const long long tw1 = a.trace ? clock64() : 0;
+              // steps past a row's length hold +0.0, which leave z unchanged
+#ifndef CTD_EXP_NOCHAIN2
+              const int cnt = min(kRingW, mx - ch * kRingW);
+              z = cnt > kShortChunk ? lane_chain(ring + b * kRingSlot, lane, z)
+                                    : lane_chain_n(ring + b * kRingSlot, lane, cnt, z);
+#endif
+              if (a.trace) {
+                p2w += tw1 - tw0;
+                p2c += clock64() - tw1;
+              }
               if (q + kRingSlots < Q) nbar_arrive(1 + kRingSlots + b, kRingThreads);
             }
             const int r = 32 * g + lane;
@@ -683,7 +802,11 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
               if (z != 0.0 && kfd != kst) atomicExch(&a.slow[n], 1);
             }
           }
-          if (a.trace && blockIdx.x == 0 && lane == 0) a.trace[(long long)n * kTraceW + 15] = clock64();
+          if (a.trace && blockIdx.x == 0 && lane == 0) {
+            a.trace[(long long)n * kTraceW + 15] = clock64();
+            a.trace[(long long)n * kTraceW + 26] += p2w;  // summed over sessions
+            a.trace[(long long)n * kTraceW + 27] += p2c;
+          }
         }
       }
     }
