@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kCoreThreads) k_core(int pass, const int64_t* 
       const int64_t b = rowbase[r];
       for (int u = threadIdx.x; u < L; u += blockDim.x) {
         const int k = rek[b + u];
+        CTD_CHECK(k >= 0 && k < K);
         acc[k] = dadd(acc[k], dmul(rev[b + u], x));  // mv[u] * xv[t] (tensor_ops.cpp:45)
       }
       __syncthreads();

@@ -306,6 +306,7 @@ struct FArgs {
   int prev_n0;       // last exactly processed candidate before n_begin (a rejection), or -1
   int exit_run;      // return after this many consecutive rejections (0: never)
   int* next_out;     // first unprocessed candidate (n_u when done)
+  long long* chk;    // [grid][2] checked builds: per-CTA (K, rnnz) after grid barrier 1
 };
 
 constexpr int kTraceW = 32;  // clock64 slots per candidate
@@ -515,6 +516,8 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
     const int gv = atoi(ge);
     if (gv > 0 && gv < (int)grid) grid = (unsigned)gv;
   }
+  Buf<long long> chk(ctx, 2 * (size_t)grid);  // read only by checked builds
+  fa.chk = chk.p;
   void* args[] = {&fa};
   // Exact kernel segments; after kSpecRun consecutive rejections the kernel
   // returns and the following candidates are certified in batches

@@ -275,6 +275,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           if (nw[u]) {
+            CTD_CHECK(rr[u] >= 0 && rr[u] < a.dim && srn + pos < a.dim);
             a.sr_list[srn + pos] = rr[u];
             a.sr_pos[rr[u]] = srn + pos;
             ++pos;
@@ -375,6 +376,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
           for (int k = 0; k < NA; ++k) {
             const long long i = blockIdx.x + (long long)unb * (32 * g + rq + kRowPh * k);
             up[k] = a.U + i * LD;
+            CTD_CHECK(32 * g + rq + kRowPh * k >= Rs || i < Kn);
             yi[k] = (upd && i < Ko) ? yval(i) : 0.0;
             inew |= (unsigned)(i == Ko) << k;
           }
@@ -529,6 +531,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
         a.rval[rnnz + t] = v;
         const int L = ldg_cg(&a.rowlen[r]);
         const long long p = a.rowbase[r] + L;
+        CTD_CHECK(r >= 0 && r < a.dim && p < a.rowbase[r + 1]);  // the row's capacity (k_row_caps)
         a.rek[p] = Ko;
         a.rev[p] = v;
         a.rowlen[r] = L + 1;
@@ -540,6 +543,13 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     stamp(a.trace, n, 3);
     grid_barrier(a.bar, nb);
     stamp(a.trace, n, 4);
+#ifdef CTD_CHECKED
+    // every CTA took the same decisions: the basis size and R's entry count agree
+    if (threadIdx.x == 0) {
+      a.chk[blockIdx.x * 2] = K;
+      a.chk[blockIdx.x * 2 + 1] = rnnz;
+    }
+#endif
     // ---------------- P2: z over R's rows, residual terms ---------------------
     const int srn = ldg_cg(a.sr_n);
     const bool y_fits = K <= a.kvec;
@@ -719,6 +729,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
                   continue;
                 }
                 const bool ok = (okm >> k) & 1;
+                CTD_CHECK(!ok || (kv[k] >= 0 && kv[k] < K));
                 const double yk = ok ? (y_fits ? vA[kv[k]] : ldg_cg(&ycur[kv[k]])) : 0.0;
                 rb[kRowPh * k * kRingLS] = dmul(yk, vv[k]);
                 if (!((found >> k) & 1)) {
@@ -793,6 +804,8 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
               const int tf = s_tf[r];
               const int kfd = tf < L ? ldg_cg(&a.rek[b0 + tf]) : -1;
               const int kst = L > 0 ? ldg_cg(&a.rek[b0]) : -1;
+              CTD_CHECK(row >= 0 && row < a.dim && K < a.Wld + (a.W ? 0 : K + 1));
+              CTD_CHECK(blockIdx.x + (long long)nb * (sb0 + s_pos[r]) < srn);
               zdn[row] = z;
               if (a.W) a.W[(long long)row * a.Wld + K] = -z;  // W's column K on R's rows (relerr.cu)
               a.kf[row] = kfd;
@@ -813,6 +826,12 @@ __global__ void __launch_bounds__(kFThreads, 1) k_filter(FArgs a) {
     stamp(a.trace, n, 5);
     grid_barrier(a.bar, nb);
     stamp(a.trace, n, 6);
+#ifdef CTD_CHECKED
+    if (threadIdx.x == 0) {
+      const unsigned o = (blockIdx.x + 1) % nb;
+      CTD_CHECK(__ldcg(&a.chk[o * 2]) == K && __ldcg(&a.chk[o * 2 + 1]) == rnnz);
+    }
+#endif
     // ---------------- P3: exact residual, decision (every CTA) ---------------
     const bool slow = ldg_cg(&a.slow[n]) != 0;
     long long nterm = srn;

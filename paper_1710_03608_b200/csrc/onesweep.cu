@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
       }
       atomicExch(st, kInc | (prefix + tot));
       gbase[d] = a.digit_base[d] + prefix;
+      CTD_CHECK(prefix + tot <= (unsigned long long)a.n);  // look-back total within the pass
     }
   }
   __syncthreads();
@@ -254,6 +255,7 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
     if (i < a.n) {
       const unsigned d = (jv[r] >> a.shift) & mask;
       const unsigned pos = doff[d] + whist[warp * bins + d] + lr[r];
+      CTD_CHECK(pos < (unsigned)kOsTile);
       tj[pos] = jv[r];
       tr[pos] = a.first ? rv[r] : __ldcs(a.rin + i);
       tv[pos] = a.first ? a.c.val[i] : __ldcs(a.vin + i);
@@ -266,6 +268,7 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
     const uint32_t j = tj[s];
     const unsigned d = (j >> a.shift) & mask;
     const unsigned long long gp = gbase[d] + (unsigned long long)(s - (int)doff[d]);
+    CTD_CHECK(gp < (unsigned long long)a.n && s >= (int)doff[d]);
     if (a.last) {  // read next by the heads / norms (and, at C2 size, from L2)
       a.jout[gp] = j;
       a.rout[gp] = tr[s];
@@ -340,6 +343,7 @@ __global__ void k_os_heads_write(const uint32_t* j, long long n, const unsigned 
   for (int u = 0; u < kPer; ++u) {
     const long long p = p0 + u;
     if (p < n && os_head(j, p)) {
+      CTD_CHECK(base + f < (unsigned long long)n);
       fcol[base + f] = j[p];
       fptr[base + f] = p;
       ++f;

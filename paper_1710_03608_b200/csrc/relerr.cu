@@ -47,6 +47,7 @@ __global__ void k_cdw(const int64_t* fptr, long long F, const int32_t* row, cons
 #pragma unroll 4
       for (long long t = b; t < e; ++t) {
         const double v = __ldcs(val + t);
+        CTD_CHECK(__ldcs(row + t) >= 0);
         const double* ww = W + (long long)__ldcs(row + t) * LD;
 #pragma unroll
         for (int u = 0; u < kCW; ++u) {

@@ -72,6 +72,7 @@ __global__ void k_draw(const uint64_t* raw, long long count, const double* cum, 
     if (u < cum[mid]) hi = mid;
     else lo = mid + 1;
   }
+  CTD_CHECK(lo < F);  // the clamped CDF ends at 1.0 > u
   fiber_out[k] = (int32_t)lo;
 }
 
@@ -104,7 +105,10 @@ __global__ void __launch_bounds__(kDedupThreads) k_dedup(const int32_t* drawn, i
   int tot;
   int pos = block_excl_sum<int>(nk, shi, &tot);
   for (int p = c0; p < c1; ++p)
-    if (keep[p]) unique_out[pos++] = drawn[p];
+    if (keep[p]) {
+      CTD_CHECK(pos < count);
+      unique_out[pos++] = drawn[p];
+    }
   if (threadIdx.x == 0) *n_unique = tot;
 }
 
