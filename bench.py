@@ -620,11 +620,12 @@ def ncu_traffic(phase):
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_kernels.json")))
     if not kern or not files:
         return None
-    rows = [d for d in json.load(open(files[-1])) if d.get("kernel") == kern
-            and d.get("dram_read") is not None and d.get("dram_write") is not None]
-    if not rows:
-        return None
-    return int(sum(d["dram_read"] + d["dram_write"] for d in rows) / len(rows))
+    for f in reversed(files):  # the newest capture that has this kernel
+        rows = [d for d in json.load(open(f)) if d.get("kernel") == kern
+                and d.get("dram_read") is not None and d.get("dram_write") is not None]
+        if rows:
+            return int(sum(d["dram_read"] + d["dram_write"] for d in rows) / len(rows))
+    return None
 
 
 def run_sharded(args, rank, world, local_rank):

@@ -275,39 +275,58 @@ void core_from_static(Ctx* ctx, const Core& c, DevCore& out) {
   }
 }
 
-void* CoreArena::take(Ctx*, size_t bytes) {
+void* CoreArena::take(Ctx* ctx, size_t bytes) {
   bytes = (bytes + 255) & ~size_t(255);
+  static const bool trace = getenv("CTD_ARENA_TRACE") != nullptr;
   if (chunks.empty() || used + bytes > chunks.back().second) {
-    // geometric growth: O(log) cudaMalloc calls over a long stream (each can
-    // stall the step by tens of ms under load)
+    // geometric growth: O(log) allocations over a long stream
     const size_t n = std::max({bytes, chunk_bytes, this->bytes() / 2});
-    void* p = nullptr;
-    static const bool trace = getenv("CTD_ARENA_TRACE") != nullptr;
+    std::pair<char*, size_t> c{nullptr, 0};
     const auto t0 = std::chrono::steady_clock::now();
-    CUDA_OK(cudaMalloc(&p, n));
-    if (trace) {
-      cudaMemPool_t pool;
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetDefaultMemPool(&pool, dev);
-      uint64_t res = 0, used_b = 0;
-      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
-      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used_b);
-      size_t fr = 0, tot = 0;
-      cudaMemGetInfo(&fr, &tot);
-      fprintf(stderr, "[arena] chunk %zu MB in %.2f ms (%zu chunks) pool reserved %.1f GB used %.1f GB free %.1f GB\n",
-              n >> 20, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
-              chunks.size() + 1, res / 1e9, used_b / 1e9, fr / 1e9);
+    if (next.valid()) {
+      c = next.get();
+      if (c.first && c.second < bytes) {
+        cudaFree(c.first);
+        c = {nullptr, 0};
+      }
     }
-    chunks.emplace_back(static_cast<char*>(p), n);
+    const bool pre = c.first != nullptr;
+    if (!pre) {
+      void* p = nullptr;
+      CUDA_OK(cudaMalloc(&p, n));
+      c = {static_cast<char*>(p), n};
+    }
+    if (trace)
+      fprintf(stderr, "[arena] chunk %zu MB (%s) waited %.2f ms (%zu chunks)\n", c.second >> 20,
+              pre ? "prefetched" : "inline",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+              chunks.size() + 1);
+    chunks.push_back(c);
     used = 0;
   }
   void* p = chunks.back().first + used;
   used += bytes;
+  if (!next.valid() && used * 2 > chunks.back().second) {
+    const size_t n2 = std::max(chunk_bytes, (this->bytes() + chunks.back().second) / 2);
+    const int dev = ctx->device;
+    next = std::async(std::launch::async, [n2, dev]() -> std::pair<char*, size_t> {
+      cudaSetDevice(dev);
+      void* q = nullptr;
+      if (cudaMalloc(&q, n2) != cudaSuccess) {
+        cudaGetLastError();  // this thread's error state only; take() allocates inline instead
+        return {nullptr, 0};
+      }
+      return {static_cast<char*>(q), n2};
+    });
+  }
   return p;
 }
 
 void CoreArena::clear() {
+  if (next.valid()) {
+    auto c = next.get();
+    if (c.first) cudaFree(c.first);
+  }
   for (auto& c : chunks) cudaFree(c.first);
   chunks.clear();
   used = 0;

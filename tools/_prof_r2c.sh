@@ -1,0 +1,17 @@
+#!/bin/bash
+# Round-2 (session c) measurements under gpurun: the default bench line, the C2
+# step's launch list, --set full captures of the top kernels, the C5 launch list.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+timeout 1200 python bench.py > gpurun_out/bench_r2c.json 2> gpurun_out/bench_r2c.err || { echo "bench failed"; tail gpurun_out/bench_r2c.err; }
+tail -c 600 gpurun_out/bench_r2c.json
+B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-ctdd --no-c4 --no-c5"
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_r2c.csv $B > /dev/null 2>&1
+B1="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-ctdd --no-c4 --no-c5"
+for k in k_filter k_os_pass k_cdw; do
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"$k" -c 1 -f -o gpurun_out/r2c_$k $B1 > /dev/null 2>&1
+done
+C5_ITERS=1 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k regex:"^k_" --csv --log-file gpurun_out/launches_c5_r2c.csv python tools/c5_diag.py > /dev/null 2>&1
+ls -la gpurun_out/*r2c*

@@ -34,7 +34,7 @@ for k, d in enumerate(dev):
     ph = {kk: v[0] for kk, v in ctx.phase_times(reset=True).items() if v[1]}
     for kk, v in ph.items():
         agg[kk] = agg.get(kk, 0.0) + v
-    if k % 50 == 0 or ms > 60:
+    if k % 50 == 0 or ms > float(os.environ.get("SPIKE_MS", "60")):
         print(f"t={H + k} step {ms:.2f} ms  phases {({kk: round(v, 2) for kk, v in ph.items()})}", flush=True)
 lat = np.array(lat)
 print(f"p50 {np.percentile(lat, 50):.2f} p99 {np.percentile(lat, 99):.2f} mean {lat.mean():.2f} ms; "
