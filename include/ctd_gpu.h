@@ -251,6 +251,15 @@ int ctd_gpu_shard_gather_device(const ctd_gpu_shard *s, int64_t n, const int64_t
 int ctd_gpu_shard_error_partials(const ctd_gpu_shard *s, const ctd_gpu_basis *b,
                                  double *x_sq, double *cross);
 int ctd_gpu_shard_destroy(ctd_gpu_shard *s);
+/* The core columns of this shard's fibers, C_p = R^T X_p (compute_core,
+ * ctd_static.cpp:12-17, tensor_ops.cpp:27-59): C is column-sharded exactly like
+ * X (a core column j is fiber j's), so every rank computes its own columns from
+ * the replicated basis with no exchange.  The shard
+ * keeps C_p resident; _core_copy exports it like ctd_gpu_factors_core (column
+ * ids ascending, rows = kept-column index ascending within a column). */
+int ctd_gpu_shard_core(ctd_gpu_shard *s, const ctd_gpu_basis *b, int64_t *c_cols, int64_t *c_nnz);
+int ctd_gpu_shard_core_copy(const ctd_gpu_shard *s, int64_t *col_id, int64_t *col_ptr, int64_t *rows,
+                            double *vals);
 /* The sampling law chained across the shards' ascending fiber ranges instead
  * of all-gathering every fiber (column_distribution / sample_with_replacement,
  * sampling.cpp:21-64, whose sums are sequential over the columns):

@@ -78,6 +78,8 @@ SIGNATURES = [
     ("ctd_gpu_shard_gather", _I, [_V, _I64, _P, _P, _P, _P]),
     ("ctd_gpu_shard_gather_device", _I, [_V, _I64, _P, _P, _P, _P]),
     ("ctd_gpu_shard_error_partials", _I, [_V, _V, _P, _P]),
+    ("ctd_gpu_shard_core", _I, [_V, _V, _P, _P]),
+    ("ctd_gpu_shard_core_copy", _I, [_V, _P, _P, _P, _P]),
     ("ctd_gpu_shard_destroy", _I, [_V]),
     ("ctd_gpu_shard_seq_total", _I, [_V, _D, _P]),
     ("ctd_gpu_shard_cdf", _I, [_V, _D, _D, _P, _P]),

@@ -37,6 +37,8 @@ struct ctd_gpu_shard {
   Buf<double> cum;                 // this shard's segment of the global CDF (ctd_gpu_shard_cdf)
   Buf<int> last_pos;               // last fiber with p > 0, or -1
   double cum_lo = 0.0, cum_hi = 0.0;
+  Core core;                       // this shard's core columns (ctd_gpu_shard_core)
+  bool has_core = false;
 };
 
 namespace {
@@ -1032,6 +1034,40 @@ int ctd_gpu_shard_error_partials(const ctd_gpu_shard* s, const ctd_gpu_basis* b,
     if (s->fb.rows != b->b->dim) fail(CTD_ERR_SHAPE, "fiber length does not match basis");
     PhaseScope ps(s->ctx, PH_ERROR);
     error_partials(s->ctx, s->fb, *b->b, x_sq, cross);
+  });
+}
+
+int ctd_gpu_shard_core(ctd_gpu_shard* s, const ctd_gpu_basis* b, int64_t* c_cols, int64_t* c_nnz) {
+  return guarded([&] {
+    need(s, "shard");
+    bind_device(s->ctx);
+    need(b, "basis");
+    if (s->fb.rows != b->b->dim) fail(CTD_ERR_SHAPE, "fiber length does not match basis");
+    PhaseScope ps(s->ctx, PH_CORE);
+    s->core = Core{};
+    compute_core(s->ctx, s->fb, *b->b, s->core);
+    s->has_core = true;
+    if (c_cols) *c_cols = s->core.cols;
+    if (c_nnz) *c_nnz = s->core.nnz;
+  });
+}
+
+int ctd_gpu_shard_core_copy(const ctd_gpu_shard* s, int64_t* col_id, int64_t* col_ptr, int64_t* rows,
+                            double* vals) {
+  return guarded([&] {
+    need(s, "shard");
+    bind_device(s->ctx);
+    if (!s->has_core) fail(CTD_ERR_ARGUMENT, "ctd_gpu_shard_core was not called on this shard");
+    const Core& c = s->core;
+    if (col_id && c.cols) std::memcpy(col_id, c.col_id.data(), c.cols * sizeof(int64_t));
+    if (col_ptr) std::memcpy(col_ptr, c.ptr.data(), (c.cols + 1) * sizeof(int64_t));
+    if (c.nnz && (rows || vals)) {
+      if (vals) s->ctx->to_host(vals, c.val.p, c.nnz);
+      std::vector<int32_t> r32(rows ? c.nnz : 0);
+      if (rows) s->ctx->to_host(r32.data(), c.row.p, c.nnz);
+      s->ctx->sync();
+      for (int64_t i = 0; rows && i < c.nnz; ++i) rows[i] = r32[i];
+    }
   });
 }
 

@@ -253,6 +253,21 @@ class _GpuShard:
         api._check(self.k.L.ctd_gpu_shard_error_partials(self.h, basis.h, C.byref(xs), C.byref(cr)))
         return xs.value, cr.value
 
+    def nnz_local(self):
+        return int(self.x.nnz)
+
+    def core(self, basis):
+        """This shard's core columns C_p = R^T X_p from the replicated basis
+        (compute_core, ctd_static.cpp:12-17): (col_id, col_ptr, rows, vals)."""
+        nc, nz = C.c_int64(), C.c_int64()
+        api._check(self.k.L.ctd_gpu_shard_core(self.h, basis.h, C.byref(nc), C.byref(nz)))
+        col = np.zeros(max(nc.value, 1), np.int64)
+        ptr = np.zeros(nc.value + 1, np.int64)
+        rows = np.zeros(max(nz.value, 1), np.int64)
+        vals = np.zeros(max(nz.value, 1))
+        api._check(self.k.L.ctd_gpu_shard_core_copy(self.h, api._p(col), api._p(ptr), api._p(rows), api._p(vals)))
+        return col[:nc.value], ptr, rows[:nz.value], vals[:nz.value]
+
     # the chained sampling law (ctd_gpu_shard_seq_total / _cdf / _clamp / _draw)
     def seq_total(self, start):
         out = C.c_double()
@@ -369,6 +384,11 @@ class ShardedResult:
     relative_error: Optional[float] = None
     n_fibers: int = 0
     stats: dict = field(default_factory=dict)
+    # with_core: this rank's core columns (col_id, col_ptr, rows, vals) -- C is
+    # column-sharded like X -- and the global nnz(C) / memory_usage
+    core: Optional[tuple] = None
+    core_nnz: int = 0
+    memory_usage: Optional[float] = None
 
 
 def _check_ranges(sh, comm) -> int:
@@ -508,11 +528,15 @@ def _candidates_and_filter(sh, comm, k, B, unique, epsilon):
 
 
 def ctd_s_sharded(shape, local, mode: int, sample_size: int, epsilon: float = 1e-6, seed: int = 42,
-                  comm: Optional[Comm] = None, kernels=None, with_error: bool = False) -> ShardedResult:
+                  comm: Optional[Comm] = None, kernels=None, with_error: bool = False,
+                  with_core: bool = False) -> ShardedResult:
     """CTD-S front end over fiber-range shards; every rank returns the same
     (replicated) kept ids, U and R.  `local` is this rank's part of X in the
     GLOBAL index space (see `shard`): a DeviceTensor or (idx, val) host arrays.
-    Mirrors ctd_s (ctd_static.cpp:19-50) without compute_core."""
+    Mirrors ctd_s (ctd_static.cpp:19-50); with_core adds compute_core
+    (ctd_static.cpp:12-17, :47) as this rank's columns of C (no exchange: a
+    core column is the same fiber's) and the global nnz(C) for memory_usage
+    (evaluation.cpp:124-129, one all-reduce)."""
     comm = comm or Comm()
     k = kernels or GpuKernels()
     if sample_size < 1:
@@ -557,7 +581,16 @@ def ctd_s_sharded(shape, local, mode: int, sample_size: int, epsilon: float = 1e
             f"{n}={1e3 * (b - a):.1f}ms" for n, a, b in zip(names, tm[:-1], tm[1:])), flush=True)
     res = ShardedResult(kept, U, rp, rr, rv, unique, acc, deg, dl, float(total), None, n_fibers,
                         {"local_fibers": int(sh.col.shape[0]), "candidate_nnz": cand_nnz})
-    # 5. error partials, all-reduced
+    # 5. the core, column-sharded like X
+    if with_core:
+        res.core = sh.core(B)
+        nl = np.array([res.core[2].shape[0], sh.nnz_local()], dtype=np.int64)
+        tot = comm.allreduce_sum(nl)
+        res.core_nnz = int(tot[0])
+        # memory_usage: (nnz(C) + nnz(U) + nnz(R)) / nnz(X), U's exact non-zeros
+        # (dense_matrix.cpp:24-29)
+        res.memory_usage = float(res.core_nnz + int(np.count_nonzero(U)) + int(rr.shape[0])) / float(tot[1])
+    # 6. error partials, all-reduced
     if with_error:
         xs, cr = sh.error_partials(B)
         s = comm.allreduce_sum(np.array([xs, cr], dtype=np.float64))

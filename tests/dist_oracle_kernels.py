@@ -37,6 +37,7 @@ class _OracleShard:
     def __init__(self, P, shape, idx, val, mode):
         self.P = P
         m = P.matricize(shape, np.asarray(idx).reshape(-1), val, mode)
+        self.m = m
         counts = np.diff(m.col_ptr)
         cols = np.nonzero(counts > 0)[0].astype(np.int64)
         sel = np.concatenate([np.arange(m.col_ptr[c], m.col_ptr[c + 1]) for c in cols]) if cols.size else \
@@ -101,6 +102,22 @@ class _OracleShard:
             g = Rd[lf.row[lf.ptr[f]:lf.ptr[f + 1]]].T @ lf.val[lf.ptr[f]:lf.ptr[f + 1]]
             cross += float(g @ (U @ g))
         return xs, cross
+
+    def nnz_local(self):
+        return int(self.m.nnz)
+
+    def core(self, basis):
+        # compute_core on this shard's columns (ctd_static.cpp:12-17) by the oracle
+        from oracle.bindings import Csc
+        cp, rr, rv = basis.r()
+        R = Csc(self.m.rows, basis.size(), np.asarray(cp, np.int64), np.asarray(rr, np.int64), np.asarray(rv))
+        c = self.P.core_matricized(self.m, R)
+        counts = np.diff(c.col_ptr)
+        cols = np.nonzero(counts > 0)[0].astype(np.int64)
+        sel = np.concatenate([np.arange(c.col_ptr[j], c.col_ptr[j + 1]) for j in cols]) if cols.size else \
+            np.zeros(0, np.int64)
+        ptr = np.concatenate([[0], np.cumsum(counts[cols])]).astype(np.int64)
+        return cols, ptr, np.asarray(c.row, np.int64)[sel], np.asarray(c.val)[sel]
 
     def close(self):
         pass

@@ -46,10 +46,12 @@ def _worker(rank, world, port, case, mode, s, backend, out):
         else:
             k = dist.GpuKernels()
         r = dist.ctd_s_sharded(x.shape, (il, vl), mode, s, 1e-6, 42, comm=dist.Comm(), kernels=k,
-                               with_error=True)
+                               with_error=True, with_core=True)
+        cc, cptr, crow, cval = r.core
         np.savez(os.path.join(out, f"r{rank}.npz"), kept=r.kept_flat, U=r.U, acc=r.accepted, deg=r.degenerate,
                  delta=r.delta, unique=r.unique, rel=r.relative_error, total=r.total_sq_norm,
-                 cp=r.R_col_ptr, rr=r.R_row, rv=r.R_val)
+                 cp=r.R_col_ptr, rr=r.R_row, rv=r.R_val, ccol=cc, cptr=cptr, crow=crow, cval=cval,
+                 cnnz=r.core_nnz, mem=r.memory_usage)
     finally:
         tdist.destroy_process_group()
 
@@ -103,6 +105,43 @@ def test_sharded_equals_single_process_oracle(case, mode, s, port, tmp_path):
         assert abs(want - rel) <= 1e-9 * max(1.0, abs(rel))
 
 
+def _merged_core(res):
+    """The ranks' column shards of C concatenated in rank order (their fiber
+    ranges ascend): (col ids, col_ptr, rows, vals)."""
+    cols, rows, vals, ptr = [], [], [], [0]
+    for r in res:
+        cols.append(r["ccol"])
+        rows.append(r["crow"])
+        vals.append(r["cval"])
+        ptr.extend((np.asarray(r["cptr"][1:]) + ptr[-1]).tolist())
+    return (np.concatenate(cols), np.asarray(ptr, np.int64), np.concatenate(rows), np.concatenate(vals))
+
+
+def _nonempty_cols(c):
+    counts = np.diff(c.col_ptr)
+    cols = np.nonzero(counts > 0)[0]
+    sel = np.concatenate([np.arange(c.col_ptr[j], c.col_ptr[j + 1]) for j in cols]) if cols.size else \
+        np.zeros(0, np.int64)
+    return cols, np.concatenate([[0], np.cumsum(counts[cols])]), np.asarray(c.row)[sel], np.asarray(c.val)[sel]
+
+
+@pytest.mark.parametrize("case,mode,s", [("c1", 0, 200), ("traffic", 0, 300)])
+def test_sharded_core_equals_single_process_oracle(case, mode, s, port, tmp_path):
+    """compute_core over fiber-range shards (gloo, two ranks, oracle kernels):
+    the ranks' column shards of C, in rank order, are the single-process core
+    bit for bit, and every rank reports the same global nnz(C) / memory_usage."""
+    res = _run(case, mode, s, "oracle", tmp_path)
+    x = CASES[case]()
+    fe, core, _ = port.ctd_s_error(x.shape, x.idx.reshape(-1), x.val, mode, s, 1e-6, 42)
+    want = _nonempty_cols(core)
+    got = _merged_core(res)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+    assert np.array_equal(got[2], want[2]) and np.array_equal(got[3].view(np.int64), want[3].view(np.int64))
+    for r in res:
+        assert int(r["cnnz"]) == core.nnz
+        assert float(r["mem"]) == (core.nnz + np.count_nonzero(fe.U) + fe.R.nnz) / x.nnz
+
+
 def _gram_identity_error(port, x, mode, R, U):
     m = port.matricize(x.shape, x.idx.reshape(-1), x.val, mode)
     K = U.shape[0]
@@ -130,6 +169,11 @@ def test_sharded_gpu_two_ranks_equal_single_gpu(case, mode, s, tmp_path):
         assert np.array_equal(r["kept"], f.kept_flat)
         assert np.array_equal(r["U"].view(np.int64), f.U.view(np.int64))
         assert abs(float(r["rel"]) - f.relative_error) <= 1e-9 * max(1.0, abs(f.relative_error))
+    # the core, column-sharded: the ranks' shards in rank order are the single-GPU core
+    fc = ctd.ctd_s(ctd.SparseTensor.from_datagen(x), mode, s, 1e-6, 42, with_core=True)
+    got = _merged_core(res)
+    assert np.array_equal(got[0], fc.C_col) and np.array_equal(got[1], fc.C_ptr)
+    assert np.array_equal(got[2], fc.C_row) and np.array_equal(got[3].view(np.int64), fc.C_val.view(np.int64))
 
 
 def _stream_worker(rank, world, port, backend, out):
