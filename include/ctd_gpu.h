@@ -258,6 +258,23 @@ int ctd_gpu_shard_destroy(ctd_gpu_shard *s);
  * keeps C_p resident; _core_copy exports it like ctd_gpu_factors_core (column
  * ids ascending, rows = kept-column index ascending within a column). */
 int ctd_gpu_shard_core(ctd_gpu_shard *s, const ctd_gpu_basis *b, int64_t *c_cols, int64_t *c_nnz);
+/* The CTD-D core over fiber-range shards (core tiles stay
+ * column-sharded): a rank's columns of StreamState::core (ctd_dynamic.hpp:18-39).
+ * _create: init_stream's core of the rank's history shard (ctd_dynamic.cpp:
+ * 129-147); per ctd_d_step (:149-229): _begin before the filter (snapshots U^(t),
+ * :165-167), _step after it (Eq. 13: the old columns gain the bottom-left rows
+ * chain_product(dR, R, U, C) (:190-222, :231-269), the slab's columns are
+ * R_new^T dX_p (transpose_times, :188,:219); dR is read from the replicated
+ * basis).  Every column of the stream's core is computed by exactly one rank,
+ * from its own data and the replicated basis: no exchange. */
+typedef struct ctd_gpu_core_shard ctd_gpu_core_shard;
+int ctd_gpu_core_shard_create(ctd_gpu_shard *hist, const ctd_gpu_basis *b, ctd_gpu_core_shard **out);
+int ctd_gpu_core_shard_begin(ctd_gpu_core_shard *c, const ctd_gpu_basis *b);
+int ctd_gpu_core_shard_step(ctd_gpu_core_shard *c, const ctd_gpu_shard *slab, const ctd_gpu_basis *b,
+                            int64_t col_offset);
+int ctd_gpu_core_shard_copy(const ctd_gpu_core_shard *c, int64_t *c_cols, int64_t *c_nnz, int64_t *col_id,
+                            int64_t *col_ptr, int64_t *rows, double *vals);
+int ctd_gpu_core_shard_destroy(ctd_gpu_core_shard *c);
 int ctd_gpu_shard_core_copy(const ctd_gpu_shard *s, int64_t *col_id, int64_t *col_ptr, int64_t *rows,
                             double *vals);
 /* The sampling law chained across the shards' ascending fiber ranges instead

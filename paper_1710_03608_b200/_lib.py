@@ -80,6 +80,11 @@ SIGNATURES = [
     ("ctd_gpu_shard_error_partials", _I, [_V, _V, _P, _P]),
     ("ctd_gpu_shard_core", _I, [_V, _V, _P, _P]),
     ("ctd_gpu_shard_core_copy", _I, [_V, _P, _P, _P, _P]),
+    ("ctd_gpu_core_shard_create", _I, [_V, _V, _PV]),
+    ("ctd_gpu_core_shard_begin", _I, [_V, _V]),
+    ("ctd_gpu_core_shard_step", _I, [_V, _V, _V, _I64]),
+    ("ctd_gpu_core_shard_copy", _I, [_V, _P, _P, _P, _P, _P, _P]),
+    ("ctd_gpu_core_shard_destroy", _I, [_V]),
     ("ctd_gpu_shard_destroy", _I, [_V]),
     ("ctd_gpu_shard_seq_total", _I, [_V, _D, _P]),
     ("ctd_gpu_shard_cdf", _I, [_V, _D, _D, _P, _P]),

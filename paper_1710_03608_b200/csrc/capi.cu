@@ -40,6 +40,12 @@ struct ctd_gpu_shard {
   Core core;                       // this shard's core columns (ctd_gpu_shard_core)
   bool has_core = false;
 };
+struct ctd_gpu_core_shard {
+  Ctx* ctx;
+  DevCore core;       // this rank's columns of the stream's Eq. 13 core
+  Buf<double> uold;   // U^(t) snapshot (Kold x Kold) taken by _begin
+  int64_t Kold = -1;
+};
 
 namespace {
 
@@ -1068,6 +1074,87 @@ int ctd_gpu_shard_core_copy(const ctd_gpu_shard* s, int64_t* col_id, int64_t* co
       s->ctx->sync();
       for (int64_t i = 0; rows && i < c.nnz; ++i) rows[i] = r32[i];
     }
+  });
+}
+
+// ---- CTD-D core over fiber-range shards ---------------------------------------
+int ctd_gpu_core_shard_create(ctd_gpu_shard* hist, const ctd_gpu_basis* b, ctd_gpu_core_shard** out) {
+  return guarded([&] {
+    need(hist, "shard");
+    need(b, "basis");
+    need(out, "out");
+    bind_device(hist->ctx);
+    if (hist->fb.rows != b->b->dim) fail(CTD_ERR_SHAPE, "fiber length does not match basis");
+    PhaseScope ps(hist->ctx, PH_CORE);
+    auto c = std::make_unique<ctd_gpu_core_shard>();
+    c->ctx = hist->ctx;
+    Core st;
+    compute_core(hist->ctx, hist->fb, *b->b, st);  // init_stream's core (ctd_dynamic.cpp:129-147)
+    core_from_static(hist->ctx, st, c->core);
+    *out = c.release();
+  });
+}
+
+int ctd_gpu_core_shard_begin(ctd_gpu_core_shard* c, const ctd_gpu_basis* b) {
+  return guarded([&] {
+    need(c, "core shard");
+    need(b, "basis");
+    bind_device(c->ctx);
+    const Basis& B = *b->b;
+    c->Kold = B.K;
+    if (B.K) {
+      if (c->uold.n < (size_t)B.K * B.K) c->uold.alloc(c->ctx, (size_t)B.K * B.K * 3 / 2 + 1);
+      CUDA_OK(cudaMemcpy2DAsync(c->uold.p, B.K * sizeof(double), B.U.p, B.LD * sizeof(double), B.K * sizeof(double),
+                                B.K, cudaMemcpyDeviceToDevice, c->ctx->stream));
+    }
+  });
+}
+
+int ctd_gpu_core_shard_step(ctd_gpu_core_shard* c, const ctd_gpu_shard* slab, const ctd_gpu_basis* b,
+                            int64_t col_offset) {
+  return guarded([&] {
+    need(c, "core shard");
+    need(slab, "shard");
+    need(b, "basis");
+    bind_device(c->ctx);
+    if (c->Kold < 0) fail(CTD_ERR_ARGUMENT, "ctd_gpu_core_shard_begin was not called before this step");
+    if (slab->fb.rows != b->b->dim) fail(CTD_ERR_SHAPE, "fiber length does not match basis");
+    if (b->b->K < c->Kold) fail(CTD_ERR_ARGUMENT, "the basis shrank since ctd_gpu_core_shard_begin");
+    PhaseScope ps(c->ctx, PH_CORE);
+    // Eq. 13 on this rank's columns: its old columns gain the bottom-left rows
+    // ((dR^T R) U) C, its slab columns are R_new^T dX_p; dR from the basis
+    core_step(c->ctx, c->core, slab->fb, *b->b, c->Kold, c->uold.p, {}, col_offset, true);
+    c->Kold = -1;
+  });
+}
+
+int ctd_gpu_core_shard_copy(const ctd_gpu_core_shard* c, int64_t* c_cols, int64_t* c_nnz, int64_t* col_id,
+                            int64_t* col_ptr, int64_t* rows, double* vals) {
+  return guarded([&] {
+    need(c, "core shard");
+    bind_device(c->ctx);
+    const DevCore& d = c->core;
+    if (c_cols) *c_cols = d.cols;
+    if (c_nnz) *c_nnz = d.nnz;
+    Ctx* cx = c->ctx;
+    if (col_id && d.cols) cx->to_host(col_id, d.col.p, d.cols);
+    if (col_ptr) cx->to_host(col_ptr, d.ptr.p, d.cols + 1);
+    if (d.nnz && (rows || vals)) {
+      if (vals) cx->to_host(vals, d.val.p, d.nnz);
+      std::vector<int32_t> r32(rows ? d.nnz : 0);
+      if (rows) cx->to_host(r32.data(), d.row.p, d.nnz);
+      cx->sync();
+      for (int64_t i = 0; rows && i < d.nnz; ++i) rows[i] = r32[i];
+    }
+    cx->sync();
+  });
+}
+
+int ctd_gpu_core_shard_destroy(ctd_gpu_core_shard* c) {
+  return guarded([&] {
+    if (!c) return;
+    bind_device(c->ctx);
+    delete c;
   });
 }
 

@@ -340,8 +340,8 @@ size_t CoreArena::bytes() const {
 
 void core_record(Ctx* ctx, const Fibers& fb, const Basis& B, int64_t Kold, const double* uold,
                  const std::vector<int32_t>& appended_fib, int64_t col_offset, CoreArena* arena,
-                 CoreRecord& rec) {
-  const int A = (int)appended_fib.size();
+                 CoreRecord& rec, bool dr_from_basis) {
+  const int A = dr_from_basis ? (int)(B.K - Kold) : (int)appended_fib.size();
   rec.A = A;
   rec.Kold = Kold;
   rec.col_offset = col_offset;
@@ -389,21 +389,28 @@ void core_record(Ctx* ctx, const Fibers& fb, const Basis& B, int64_t Kold, const
     }
     rec.left = left;
     Buf<int32_t> fib(ctx, A);
-    ctx->to_dev(fib.p, appended_fib.data(), A);
+    // dR's columns: fibers of fb, or the basis's own columns Kold..K-1
+    std::vector<int32_t> bcols;
+    if (dr_from_basis)
+      for (int a = 0; a < A; ++a) bcols.push_back((int32_t)(Kold + a));
+    ctx->to_dev(fib.p, dr_from_basis ? bcols.data() : appended_fib.data(), A);
+    const int64_t* dptr = dr_from_basis ? B.rptr.p : fb.ptr.p;
+    const int32_t* drow = dr_from_basis ? B.rrow.p : fb.row.p;
+    const double* dval = dr_from_basis ? B.rval.p : fb.val.p;
     Buf<double> gram(ctx, (size_t)A * Kold);
     const size_t xsmem = (size_t)B.dim * sizeof(double);
     if (xsmem <= 96 * 1024 && !getenv("CTD_CORE_LEGACY")) {
       if (xsmem > 48 * 1024)
         CUDA_OK(cudaFuncSetAttribute(k_gram_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem));
       const dim3 grid(ceil_div((uint64_t)Kold, 256), A);
-      LAUNCH(ctx, k_gram_cols, grid, 256, xsmem, fib.p, fb.ptr.p, fb.row.p, fb.val.p, (int)B.dim, B.rptr.p,
-             B.rrow.p, B.rval.p, (int)Kold, gram.p);
+      LAUNCH(ctx, k_gram_cols, grid, 256, xsmem, fib.p, dptr, drow, dval, (int)B.dim, B.rptr.p, B.rrow.p,
+             B.rval.p, (int)Kold, gram.p);
     } else {
       const size_t smem = (size_t)Kold * sizeof(double);
       if (smem > 200 * 1024) fail(CTD_ERR_ARGUMENT, "core update supports at most 25600 kept fibers");
       CUDA_OK(cudaFuncSetAttribute(k_gram_old, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      LAUNCH(ctx, k_gram_old, (unsigned)std::min(A, ctx->sm_count * 4), 256, smem, fib.p, A, fb.ptr.p, fb.row.p,
-             fb.val.p, B.rowbase.p, B.rowlen.p, B.rek.p, B.rev.p, (int)Kold, gram.p);
+      LAUNCH(ctx, k_gram_old, (unsigned)std::min(A, ctx->sm_count * 4), 256, smem, fib.p, A, dptr, drow, dval,
+             B.rowbase.p, B.rowlen.p, B.rek.p, B.rev.p, (int)Kold, gram.p);
     }
     if (!getenv("CTD_CORE_LEGACY")) {
       Buf<int32_t> nzj(ctx, (size_t)A * Kold);
@@ -477,9 +484,9 @@ void core_apply(Ctx* ctx, DevCore& core, const CoreRecord& rec) {
 }
 
 void core_step(Ctx* ctx, DevCore& core, const Fibers& fb, const Basis& B, int64_t Kold, const double* uold,
-               const std::vector<int32_t>& appended_fib, int64_t col_offset) {
+               const std::vector<int32_t>& appended_fib, int64_t col_offset, bool dr_from_basis) {
   CoreRecord rec;
-  core_record(ctx, fb, B, Kold, uold, appended_fib, col_offset, nullptr, rec);
+  core_record(ctx, fb, B, Kold, uold, appended_fib, col_offset, nullptr, rec, dr_from_basis);
   core_apply(ctx, core, rec);
 }
 

@@ -60,9 +60,12 @@ struct CoreRecord {
   int64_t Kold = 0;
   int64_t col_offset = 0;
 };
+// dr_from_basis: the appended fibers dR are read from the basis itself (its
+// columns Kold..K-1, identical data) instead of fb -- a rank of a sharded
+// stream owns only its part of the slab, while the basis is replicated.
 void core_record(Ctx* ctx, const Fibers& fb, const Basis& B, int64_t Kold, const double* uold,
                  const std::vector<int32_t>& appended_fib, int64_t col_offset, CoreArena* arena,
-                 CoreRecord& out);
+                 CoreRecord& out, bool dr_from_basis = false);
 void core_apply(Ctx* ctx, DevCore& core, const CoreRecord& rec);
 
 // One ctd_d_step core update (Eq. 13) = core_record + core_apply.  B is the basis after this step's
@@ -70,7 +73,7 @@ void core_apply(Ctx* ctx, DevCore& core, const CoreRecord& rec);
 // before them; appended_fib the appended candidates' fiber indices into fb in
 // acceptance order; col_offset = t * slab_columns.
 void core_step(Ctx* ctx, DevCore& core, const Fibers& fb, const Basis& B, int64_t Kold, const double* uold,
-               const std::vector<int32_t>& appended_fib, int64_t col_offset);
+               const std::vector<int32_t>& appended_fib, int64_t col_offset, bool dr_from_basis = false);
 
 // exact_core variant (ctd_dynamic.cpp:207-211): the bottom-left block is
 // dR^T X_hist (transpose_times over the retained history's matricization hf,

@@ -210,6 +210,47 @@ class GpuKernels:
     def basis(self, dim):
         return _GpuBasis(self, dim)
 
+    def core_shard(self, hist_shard, basis):
+        return _GpuCoreShard(self, hist_shard, basis)
+
+
+class _GpuCoreShard:
+    """This rank's columns of a sharded stream's Eq. 13 core (ctd_gpu_core_shard)."""
+
+    def __init__(self, k, hist_shard, basis):
+        self.k = k
+        h = C.c_void_p()
+        api._check(k.L.ctd_gpu_core_shard_create(hist_shard.h, basis.h, C.byref(h)))
+        self.h = h
+
+    def begin(self, basis):
+        api._check(self.k.L.ctd_gpu_core_shard_begin(self.h, basis.h))
+
+    def step(self, slab_shard, basis, col_offset: int):
+        api._check(self.k.L.ctd_gpu_core_shard_step(self.h, slab_shard.h, basis.h, int(col_offset)))
+
+    def columns(self):
+        nc, nz = C.c_int64(), C.c_int64()
+        api._check(self.k.L.ctd_gpu_core_shard_copy(self.h, C.byref(nc), C.byref(nz), None, None, None, None))
+        col = np.zeros(max(nc.value, 1), np.int64)
+        ptr = np.zeros(nc.value + 1, np.int64)
+        rows = np.zeros(max(nz.value, 1), np.int64)
+        vals = np.zeros(max(nz.value, 1))
+        api._check(self.k.L.ctd_gpu_core_shard_copy(self.h, C.byref(nc), C.byref(nz), api._p(col), api._p(ptr),
+                                                    api._p(rows), api._p(vals)))
+        return col[:nc.value], ptr, rows[:nz.value], vals[:nz.value]
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.k.L.ctd_gpu_core_shard_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
 
 class _GpuShard:
     def __init__(self, k: GpuKernels, x: "api.DeviceTensor", mode: int):
@@ -611,11 +652,13 @@ class ShardedStream:
     slab, runs the chained law with seed ^ t (:177), gathers the candidates and
     filters them against the replicated basis (:178-187).  Every rank holds the
     same kept ids (flat ids j + t * slab_columns on the grown shape, :184-185),
-    R and U.  The Eq. 13 core is not maintained (the front end of the step,
-    as the C3 latency line measures it)."""
+    R and U.  with_core: every rank also maintains ITS columns of the Eq. 13
+    core (ctd_dynamic.cpp:188-222) -- the columns of its history shard and of
+    its part of every slab -- from its own data and the replicated basis, so
+    the core stays column-sharded with no exchange."""
 
     def __init__(self, hist_shape, local, mode: int, sample_size: int, epsilon: float = 1e-6, seed: int = 42,
-                 comm: Optional[Comm] = None, kernels=None):
+                 comm: Optional[Comm] = None, kernels=None, with_core: bool = False):
         self.comm = comm or Comm()
         self.k = kernels or GpuKernels()
         if len(hist_shape) < 2 or not (0 <= mode < len(hist_shape) - 1):
@@ -629,6 +672,7 @@ class ShardedStream:
         _, unique = _sample_sharded(sh, self.comm, self.k, sample_size, seed)
         self.B = self.k.basis(int(hist_shape[mode]))
         acc, _, _, _ = _candidates_and_filter(sh, self.comm, self.k, self.B, unique, epsilon)
+        self.core = self.k.core_shard(sh, self.B) if with_core else None  # init_stream's core (:129-147)
         sh.close()
         self.kept_flat = list(unique[np.nonzero(acc)[0]])
 
@@ -641,7 +685,11 @@ class ShardedStream:
             sh = self.k.shard((self.slab_shape + [1], idx, val), self.mode)
             _check_ranges(sh, self.comm)
             _, unique = _sample_sharded(sh, self.comm, self.k, sample_size, self.seed ^ self.t)
+            if self.core is not None:
+                self.core.begin(self.B)  # U^(t), R^(t) before this step's appends (:165-167)
             acc, _, _, _ = _candidates_and_filter(sh, self.comm, self.k, self.B, unique, self.eps)
+            if self.core is not None:
+                self.core.step(sh, self.B, self.t * self.slab_cols)
             sh.close()
             self.kept_flat += [int(j) + self.t * self.slab_cols for j in unique[np.nonzero(acc)[0]]]
         self.t += 1
@@ -650,5 +698,13 @@ class ShardedStream:
     def U(self):
         return self.B.u()
 
+    def core_columns(self):
+        """This rank's columns of the core: (col ids ascending, col_ptr, rows, vals)."""
+        if self.core is None:
+            raise api.ArgumentError("the stream was created without with_core")
+        return self.core.columns()
+
     def close(self):
+        if self.core is not None:
+            self.core.close()
         self.B.close()

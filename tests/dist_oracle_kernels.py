@@ -32,6 +32,9 @@ class OracleKernels:
     def basis(self, dim):
         return _OracleBasis(self.P.basis(dim))
 
+    def core_shard(self, hist_shard, basis):
+        return _OracleCoreShard(self.P, hist_shard, basis)
+
 
 class _OracleShard:
     def __init__(self, P, shape, idx, val, mode):
@@ -152,6 +155,68 @@ class _OracleBasis:
         rows = np.concatenate([c[0] for c in self.cols]) if self.cols else np.zeros(0, np.int64)
         vals = np.concatenate([c[1] for c in self.cols]) if self.cols else np.zeros(0)
         return cp, rows, vals
+
+    def close(self):
+        pass
+
+
+class _OracleCoreShard:
+    """A rank's columns of the stream core (ctd_dynamic.cpp:188-222) restated
+    in numpy in the reference's operation order: transpose_times merges
+    (:53-85), chain_product (:231-269), compute_core for the slab columns."""
+
+    def __init__(self, P, hist_shard, basis):
+        self.P = P
+        self.cols = {}  # global column id -> (rows, vals)
+        self._add(hist_shard.core(basis), 0)
+
+    def _add(self, core, offset):
+        cols, ptr, rows, vals = core
+        for q, j in enumerate(cols):
+            self.cols[int(j) + offset] = (rows[ptr[q]:ptr[q + 1]].copy(), vals[ptr[q]:ptr[q + 1]].copy())
+
+    def begin(self, basis):
+        self.Kold = basis.size()
+        self.Rold = basis.r()
+        self.Uold = basis.u() if self.Kold else np.zeros((0, 0))
+
+    def step(self, slab_shard, basis, col_offset):
+        K, Kold = basis.size(), self.Kold
+        cp, rr, rv = basis.r()
+        A = K - Kold
+        if A > 0 and Kold > 0:
+            ocp, orr, orv = self.Rold
+            gram = np.zeros((A, Kold))
+            for a in range(A):
+                ar, av = rr[cp[Kold + a]:cp[Kold + a + 1]], rv[cp[Kold + a]:cp[Kold + a + 1]]
+                for j in range(Kold):
+                    br, bv = orr[ocp[j]:ocp[j + 1]], orv[ocp[j]:ocp[j + 1]]
+                    _, ia, ib = np.intersect1d(ar, br, assume_unique=True, return_indices=True)
+                    acc = 0.0
+                    for x, y in zip(av[ia], bv[ib]):  # ascending common rows, sequential
+                        acc += float(x) * float(y)
+                    if abs(acc) >= 1e-14:
+                        gram[a, j] = acc
+            left = np.zeros((A, Kold))
+            for j in range(Kold):
+                for i in np.nonzero(gram[:, j])[0]:
+                    left[i, :] += gram[i, j] * self.Uold[j, :]
+            for c, (crow, cval) in list(self.cols.items()):
+                acc = np.zeros(A)
+                for r, v in zip(crow, cval):
+                    acc += left[:, r] * v
+                keep = np.nonzero(np.abs(acc) >= 1e-14)[0]
+                if keep.size:
+                    self.cols[c] = (np.concatenate([crow, Kold + keep]), np.concatenate([cval, acc[keep]]))
+        self._add(slab_shard.core(basis), int(col_offset))
+        self.Kold = -1
+
+    def columns(self):
+        ids = np.array(sorted(self.cols), dtype=np.int64)
+        ptr = np.concatenate([[0], np.cumsum([self.cols[int(j)][0].shape[0] for j in ids])]).astype(np.int64)
+        rows = np.concatenate([self.cols[int(j)][0] for j in ids]) if ids.size else np.zeros(0, np.int64)
+        vals = np.concatenate([self.cols[int(j)][1] for j in ids]) if ids.size else np.zeros(0)
+        return ids, ptr, rows.astype(np.int64), vals
 
     def close(self):
         pass

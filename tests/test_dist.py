@@ -194,14 +194,15 @@ def _stream_worker(rank, world, port, backend, out):
         comm = dist.Comm()
         hb = dist.fiber_range_bounds(hist.shape, 0, hist.idx, world)
         st = dist.ShardedStream(hist.shape, dist.shard(hist.shape, hist.idx, hist.val, 0, hb, rank), 0, 120, 1e-6,
-                                7, comm=comm, kernels=k)
+                                7, comm=comm, kernels=k, with_core=True)
         kept = [np.array(st.kept_flat, np.int64)]
         for t in range(3, x.shape[2]):
             sl = x.time_slab(t, t + 1)
             sb = dist.fiber_range_bounds(sl.shape, 0, sl.idx, world)
             st.step(dist.shard(sl.shape, sl.idx, sl.val, 0, sb, rank), 40)
             kept.append(np.array(st.kept_flat, np.int64))
-        np.savez(os.path.join(out, f"s{rank}.npz"), U=st.U(), t=st.t,
+        cc, cptr, crow, cval = st.core_columns()
+        np.savez(os.path.join(out, f"s{rank}.npz"), U=st.U(), t=st.t, ccol=cc, cptr=cptr, crow=crow, cval=cval,
                  **{f"k{i}": k_ for i, k_ in enumerate(kept)})
         st.close()
     finally:
@@ -217,11 +218,12 @@ def _run_stream(backend, tmp_path, world=2):
 def test_sharded_stream_equals_single_process(port, tmp_path):
     """CTD-D with every slab split by fiber range over two ranks (gloo, CPU
     kernels): kept ids after every step and U equal the single-process
-    restatement's stream (front end; the core is not kept on either side)."""
+    restatement's stream, and the ranks' column shards of the Eq. 13 core, in
+    rank order per slab, are its core bit for bit."""
     res = _run_stream("oracle", tmp_path)
     x = datagen.c3_stream(seed=5, n_steps=3, slices_per_step=3, draws_per_slice=2500, n=300, planted_step=2, block=20)
     hist = x.time_slab(0, 3)
-    ps = port.stream(hist.shape, hist.flat_idx(), hist.val, 0, 120, 1e-6, 7, core=False)
+    ps = port.stream(hist.shape, hist.flat_idx(), hist.val, 0, 120, 1e-6, 7, core=True)
     want = [ps.kept_flat()]
     for t in range(3, x.shape[2]):
         sl = x.time_slab(t, t + 1)
@@ -232,6 +234,34 @@ def test_sharded_stream_equals_single_process(port, tmp_path):
             assert np.array_equal(r[f"k{i}"], w), i
         assert int(r["t"]) == x.shape[2]
         assert np.array_equal(r["U"].view(np.int64), ps.U().view(np.int64))
+    _check_sharded_stream_core(res, ps.core())
+
+
+def _check_sharded_stream_core(res, core):
+    """Every core column is held by exactly one rank; together they are the
+    single-process core (nonempty columns), bit for bit."""
+    want = _nonempty_cols(core)
+    cols = np.concatenate([r["ccol"] for r in res])
+    assert np.unique(cols).shape[0] == cols.shape[0]
+    order = np.argsort(cols, kind="stable")
+    got_rows, got_vals, ptr = [], [], [0]
+    flat = [(r, q) for r in res for q in range(r["ccol"].shape[0])]
+    for o in order:
+        r, q = flat[o]
+        a, b = r["cptr"][q], r["cptr"][q + 1]
+        got_rows.append(r["crow"][a:b])
+        got_vals.append(r["cval"][a:b])
+        ptr.append(ptr[-1] + (b - a))
+    assert np.array_equal(cols[order], want[0])
+    assert np.array_equal(np.asarray(ptr), want[1])
+    assert np.array_equal(np.concatenate(got_rows), want[2])
+    assert np.array_equal(np.concatenate(got_vals).view(np.int64), want[3].view(np.int64))
+    # the bottom-left block (chain_product) was exercised: some history column
+    # holds a row of a fiber kept after init_stream
+    k0 = res[0]["k0"].shape[0]
+    hist_cols = want[0] < 3 * 300  # the 3 history slices (slab columns: 300 dst ids)
+    rows_of = [want[2][want[1][q]:want[1][q + 1]] for q in np.nonzero(hist_cols)[0]]
+    assert any((rr >= k0).any() for rr in rows_of)
 
 
 @pytest.mark.gpu
@@ -239,13 +269,14 @@ def test_sharded_stream_gpu_two_ranks(port, tmp_path):
     res = _run_stream("gpu", tmp_path)
     x = datagen.c3_stream(seed=5, n_steps=3, slices_per_step=3, draws_per_slice=2500, n=300, planted_step=2, block=20)
     hist = x.time_slab(0, 3)
-    ps = port.stream(hist.shape, hist.flat_idx(), hist.val, 0, 120, 1e-6, 7, core=False)
+    ps = port.stream(hist.shape, hist.flat_idx(), hist.val, 0, 120, 1e-6, 7, core=True)
     for t in range(3, x.shape[2]):
         sl = x.time_slab(t, t + 1)
         ps.step(sl.shape, sl.flat_idx(), sl.val, 40)
     for r in res:
         assert np.array_equal(r[f"k{x.shape[2] - 3}"], ps.kept_flat())
         assert np.array_equal(r["U"].view(np.int64), ps.U().view(np.int64))
+    _check_sharded_stream_core(res, ps.core())
 
 
 @pytest.mark.gpu
