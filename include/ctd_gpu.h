@@ -258,6 +258,27 @@ int ctd_gpu_shard_destroy(ctd_gpu_shard *s);
  * keeps C_p resident; _core_copy exports it like ctd_gpu_factors_core (column
  * ids ascending, rows = kept-column index ascending within a column). */
 int ctd_gpu_shard_core(ctd_gpu_shard *s, const ctd_gpu_basis *b, int64_t *c_cols, int64_t *c_nnz);
+/* compute_core (ctd_static.hpp:28, ctd_static.cpp:12-17) for a caller-given R
+ * (CSC, r_cols columns over r_rows = x's extent in `mode`, rows ascending):
+ * C_(mode) = R^T X_(mode), entries with |c| < 1e-14 dropped.  The result is a
+ * ctd_gpu_csc: K = r_cols rows, only the columns of X_(mode) that keep an
+ * entry (their ids j); fold it with the reference's fold() for the tensor. */
+typedef struct ctd_gpu_csc ctd_gpu_csc;
+int ctd_gpu_compute_core(ctd_gpu_ctx *ctx, const ctd_gpu_tensor *x, int mode, int64_t r_rows, int64_t r_cols,
+                         const int64_t *r_col_ptr, const int64_t *r_row, const double *r_val, ctd_gpu_csc **out);
+/* chain_product (ctd_dynamic.hpp:61-62, ctd_dynamic.cpp:231-269):
+ * ((dR^T R) U) C for dR (a_cols columns), R (k columns; both over `dim` rows),
+ * U (k x k row-major) and C (k rows, c_cols columns): a_cols x c_cols, only the
+ * columns that keep an entry (ids = C's column index), |v| < 1e-14 dropped, in
+ * the reference's operation order. */
+int ctd_gpu_chain_product(ctd_gpu_ctx *ctx, int64_t dim, int64_t a_cols, const int64_t *dr_col_ptr,
+                          const int64_t *dr_row, const double *dr_val, int64_t k, const int64_t *r_col_ptr,
+                          const int64_t *r_row, const double *r_val, const double *u, int64_t c_cols,
+                          const int64_t *c_col_ptr, const int64_t *c_row, const double *c_val, ctd_gpu_csc **out);
+int ctd_gpu_csc_info(const ctd_gpu_csc *m, int64_t *rows, int64_t *n_cols, int64_t *nnz);
+int ctd_gpu_csc_copy(const ctd_gpu_csc *m, int64_t *col_id, int64_t *col_ptr, int64_t *rows, double *vals);
+int ctd_gpu_csc_destroy(ctd_gpu_csc *m);
+
 /* The CTD-D core over fiber-range shards (core tiles stay
  * column-sharded): a rank's columns of StreamState::core (ctd_dynamic.hpp:18-39).
  * _create: init_stream's core of the rank's history shard (ctd_dynamic.cpp:

@@ -447,6 +447,13 @@ class Ref:
             L.ref_run_stream.argtypes = [v, i32, i64, i64, f64, f64, C.c_uint64, i32, C.POINTER(i64), v, v, v,
                                          v, v, v]
             L.ref_tsv_line.argtypes = [i64, f64, f64, f64, i64, C.c_char_p, i64]
+        if hasattr(L, "ref_compute_core"):
+            L.ref_compute_core.argtypes = [v, i32, i64, i64, v, v, v, C.POINTER(v)]
+            L.ref_chain_product.argtypes = [i64, i64, v, v, v, i64, i64, v, v, v, i64, i64, v, i64, i64, v, v, v,
+                                            C.POINTER(v)]
+            L.ref_matrix_free.argtypes = [v]
+            L.ref_matrix_shape.argtypes = [v, v, v, v]
+            L.ref_matrix_data.argtypes = [v, v, v, v]
         if hasattr(L, "ref_save_factors"):
             L.ref_save_factors.argtypes = [v, C.c_char_p]
             L.ref_load_factors.argtypes = [C.c_char_p, C.POINTER(v)]
@@ -459,6 +466,41 @@ class Ref:
 
     def tensor(self, shape, idx, val):
         return _RefTensor(self, shape, idx, val)
+
+    def compute_core(self, t: "_RefTensor", r: Csc, mode: int):
+        """ctd::compute_core (ctd_static.hpp:28) -> (shape, flat indices, values) of C."""
+        h = C.c_void_p()
+        cp, rr, rv = _i64(r.col_ptr), _i64(r.row), _f64(r.val)  # held across the call
+        self._chk(self.L.ref_compute_core(t.h, mode, r.rows, r.cols, _p(cp), _p(rr), _p(rv), C.byref(h)),
+                  "compute_core")
+        out = _RefTensor.__new__(_RefTensor)
+        out.R, out.h = self, h
+        out.nnz = int(self.L.ref_tensor_nnz(h))
+        shape = list(t.shape)
+        shape[mode] = r.cols
+        out.shape = shape
+        return out
+
+    def chain_product(self, dr: Csc, r: Csc, u: np.ndarray, core: Csc) -> Csc:
+        """ctd::chain_product (ctd_dynamic.hpp:61-62)."""
+        h = C.c_void_p()
+        uu = np.ascontiguousarray(u, np.float64)
+        a = (_i64(dr.col_ptr), _i64(dr.row), _f64(dr.val))  # held across the call
+        b = (_i64(r.col_ptr), _i64(r.row), _f64(r.val))
+        c = (_i64(core.col_ptr), _i64(core.row), _f64(core.val))
+        self._chk(self.L.ref_chain_product(dr.rows, dr.cols, _p(a[0]), _p(a[1]), _p(a[2]), r.rows, r.cols,
+                                           _p(b[0]), _p(b[1]), _p(b[2]), uu.shape[0], uu.shape[1], _p(uu), core.rows,
+                                           core.cols, _p(c[0]), _p(c[1]), _p(c[2]), C.byref(h)), "chain_product")
+        try:
+            rows, cols, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+            self.L.ref_matrix_shape(h, C.byref(rows), C.byref(cols), C.byref(nnz))
+            cp = np.zeros(cols.value + 1, np.int64)
+            rr = np.zeros(max(nnz.value, 1), np.int64)
+            vv = np.zeros(max(nnz.value, 1))
+            self.L.ref_matrix_data(h, _p(cp), _p(rr), _p(vv))
+            return Csc(rows.value, cols.value, cp, rr[:nnz.value], vv[:nnz.value])
+        finally:
+            self.L.ref_matrix_free(h)
 
     def matricize(self, t: "_RefTensor", mode: int):
         shape = t.shape

@@ -393,3 +393,59 @@ int ref_decompose_online(void* t, int mode, int64_t d, double eps, uint64_t seed
 }
 
 }  // extern "C"
+
+// compute_core / chain_product on caller-given operands (test driver for the
+// drop-in's compute_core and chain_product wrappers)
+namespace {
+SparseMatrix csc_of(int64_t rows, int64_t cols, const int64_t* cp, const int64_t* r, const double* v) {
+  std::vector<index_t> ri, ci;
+  std::vector<double> vv;
+  for (int64_t j = 0; j < cols; ++j)
+    for (int64_t t = cp[j]; t < cp[j + 1]; ++t) {
+      ri.push_back(r[t]);
+      ci.push_back(j);
+      vv.push_back(v[t]);
+    }
+  return SparseMatrix(rows, cols, std::move(ri), std::move(ci), std::move(vv));
+}
+}  // namespace
+
+extern "C" {
+int ref_compute_core(void* t, int mode, int64_t r_rows, int64_t r_cols, const int64_t* cp, const int64_t* rows,
+                     const double* vals, void** out) {
+  return guard([&] {
+    const SparseMatrix R = csc_of(r_rows, r_cols, cp, rows, vals);
+    *out = new SparseTensor(compute_core(*static_cast<SparseTensor*>(t), R, mode));
+  });
+}
+int ref_chain_product(int64_t dr_rows, int64_t a, const int64_t* dcp, const int64_t* drow, const double* dval,
+                      int64_t r_rows, int64_t k, const int64_t* rcp, const int64_t* rrow, const double* rval,
+                      int64_t u_rows, int64_t u_cols, const double* u, int64_t c_rows, int64_t c_cols,
+                      const int64_t* ccp, const int64_t* crow, const double* cval, void** out) {
+  return guard([&] {
+    const SparseMatrix dR = csc_of(dr_rows, a, dcp, drow, dval);
+    const SparseMatrix R = csc_of(r_rows, k, rcp, rrow, rval);
+    DenseMatrix U(u_rows, u_cols);
+    for (int64_t i = 0; i < u_rows; ++i)
+      for (int64_t j = 0; j < u_cols; ++j) U.at(i, j) = u[i * u_cols + j];
+    const SparseMatrix Cm = csc_of(c_rows, c_cols, ccp, crow, cval);
+    *out = new SparseMatrix(chain_product(dR, R, U, Cm));
+  });
+}
+void ref_matrix_free(void* m) { delete static_cast<SparseMatrix*>(m); }
+void ref_matrix_shape(void* m, int64_t* rows, int64_t* cols, int64_t* nnz) {
+  const auto* M = static_cast<SparseMatrix*>(m);
+  *rows = M->rows();
+  *cols = M->cols();
+  *nnz = M->nnz();
+}
+void ref_matrix_data(void* m, int64_t* col_ptr, int64_t* rows, double* vals) {
+  const auto* M = static_cast<SparseMatrix*>(m);
+  const auto& cp = M->column_pointers();
+  for (size_t j = 0; j < cp.size(); ++j) col_ptr[j] = (int64_t)cp[j];
+  for (size_t t = 0; t < M->row_indices().size(); ++t) {
+    rows[t] = M->row_indices()[t];
+    vals[t] = M->values()[t];
+  }
+}
+}

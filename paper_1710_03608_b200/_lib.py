@@ -80,6 +80,11 @@ SIGNATURES = [
     ("ctd_gpu_shard_error_partials", _I, [_V, _V, _P, _P]),
     ("ctd_gpu_shard_core", _I, [_V, _V, _P, _P]),
     ("ctd_gpu_shard_core_copy", _I, [_V, _P, _P, _P, _P]),
+    ("ctd_gpu_compute_core", _I, [_V, _V, _I, _I64, _I64, _P, _P, _P, _PV]),
+    ("ctd_gpu_chain_product", _I, [_V, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _PV]),
+    ("ctd_gpu_csc_info", _I, [_V, _P, _P, _P]),
+    ("ctd_gpu_csc_copy", _I, [_V, _P, _P, _P, _P]),
+    ("ctd_gpu_csc_destroy", _I, [_V]),
     ("ctd_gpu_core_shard_create", _I, [_V, _V, _PV]),
     ("ctd_gpu_core_shard_begin", _I, [_V, _V]),
     ("ctd_gpu_core_shard_step", _I, [_V, _V, _V, _I64]),

@@ -40,6 +40,11 @@ struct ctd_gpu_shard {
   Core core;                       // this shard's core columns (ctd_gpu_shard_core)
   bool has_core = false;
 };
+struct ctd_gpu_csc {
+  Ctx* ctx;
+  Core c;               // columns with entries; row/val on the device
+  int32_t row_shift = 0;  // subtracted from the stored rows on export
+};
 struct ctd_gpu_core_shard {
   Ctx* ctx;
   DevCore core;       // this rank's columns of the stream's Eq. 13 core
@@ -1074,6 +1079,129 @@ int ctd_gpu_shard_core_copy(const ctd_gpu_shard* s, int64_t* col_id, int64_t* co
       s->ctx->sync();
       for (int64_t i = 0; rows && i < c.nnz; ++i) rows[i] = r32[i];
     }
+  });
+}
+
+// ---- compute_core / chain_product on caller-provided operands ----------------
+int ctd_gpu_compute_core(ctd_gpu_ctx* ctx, const ctd_gpu_tensor* x, int mode, int64_t r_rows, int64_t r_cols,
+                         const int64_t* r_col_ptr, const int64_t* r_row, const double* r_val, ctd_gpu_csc** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    bind_device(&ctx->c);
+    need(x, "x");
+    need(out, "out");
+    need(r_col_ptr, "r_col_ptr");
+    Ctx* c = &ctx->c;
+    if (mode < 0 || mode >= x->t.order) fail(CTD_ERR_ARGUMENT, "mode out of range");
+    // ctd_static.cpp:14-15
+    if (r_rows != x->t.shape[mode]) fail(CTD_ERR_SHAPE, "fiber matrix rows do not match the tensor extent");
+    if (r_cols < 0) fail(CTD_ERR_ARGUMENT, "negative column count");
+    PhaseScope ps(c, PH_CORE);
+    Fibers fb;
+    matricize(c, x->t, mode, fb);
+    Basis B(c, r_rows);
+    basis_load(B, r_cols, r_col_ptr, r_row, r_val, nullptr);
+    auto h = std::make_unique<ctd_gpu_csc>();
+    h->ctx = c;
+    compute_core(c, fb, B, h->c);
+    *out = h.release();
+  });
+}
+
+int ctd_gpu_chain_product(ctd_gpu_ctx* ctx, int64_t dim, int64_t a_cols, const int64_t* dr_col_ptr,
+                          const int64_t* dr_row, const double* dr_val, int64_t k, const int64_t* r_col_ptr,
+                          const int64_t* r_row, const double* r_val, const double* u, int64_t c_cols,
+                          const int64_t* c_col_ptr, const int64_t* c_row, const double* c_val, ctd_gpu_csc** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    bind_device(&ctx->c);
+    need(out, "out");
+    need(dr_col_ptr, "dr_col_ptr");
+    need(r_col_ptr, "r_col_ptr");
+    need(c_col_ptr, "c_col_ptr");
+    Ctx* c = &ctx->c;
+    if (dim < 0 || a_cols < 0 || k < 0 || c_cols < 0) fail(CTD_ERR_ARGUMENT, "negative extent");
+    if (k > 0) need(u, "u");
+    if (a_cols >= (1ll << 31)) fail(CTD_ERR_ARGUMENT, "too many appended columns");
+    PhaseScope ps(c, PH_CORE);
+    Basis B(c, dim);
+    basis_load(B, k, r_col_ptr, r_row, r_val, u);
+    // dR on the device (rows ascending within a column, inside dim)
+    const int64_t dn = dr_col_ptr[a_cols];
+    std::vector<int32_t> d32(dn > 0 ? dn : 1);
+    for (int64_t a = 0; a < a_cols; ++a)
+      for (int64_t t = dr_col_ptr[a]; t < dr_col_ptr[a + 1]; ++t) {
+        if (dr_row[t] < 0 || dr_row[t] >= dim) fail(CTD_ERR_SHAPE, "dR row outside the fiber length");
+        d32[t] = (int32_t)dr_row[t];
+      }
+    Buf<int64_t> dptr(c, a_cols + 1);
+    Buf<int32_t> drow(c, dn + 1);
+    Buf<double> dval(c, dn + 1);
+    c->to_dev(dptr.p, dr_col_ptr, a_cols + 1);
+    if (dn) {
+      c->to_dev(drow.p, d32.data(), dn);
+      c->to_dev(dval.p, dr_val, dn);
+    }
+    // C on the device (k rows)
+    const int64_t cn = c_col_ptr[c_cols];
+    std::vector<int32_t> c32(cn > 0 ? cn : 1);
+    for (int64_t t = 0; t < cn; ++t) {
+      if (c_row[t] < 0 || c_row[t] >= k) fail(CTD_ERR_SHAPE, "core row outside the basis size");
+      c32[t] = (int32_t)c_row[t];
+    }
+    DevCore core;
+    core.cols = c_cols;
+    core.nnz = cn;
+    core.ptr.alloc(c, c_cols + 1);
+    core.row.alloc(c, cn + 1);
+    core.val.alloc(c, cn + 1);
+    c->to_dev(core.ptr.p, c_col_ptr, c_cols + 1);
+    if (cn) {
+      c->to_dev(core.row.p, c32.data(), cn);
+      c->to_dev(core.val.p, c_val, cn);
+    }
+    Buf<double> ud(c, k > 0 ? (size_t)k * k : 1);
+    if (k) c->to_dev(ud.p, u, (size_t)k * k);
+    auto h = std::make_unique<ctd_gpu_csc>();
+    h->ctx = c;
+    h->row_shift = (int32_t)k;  // chain_product stores the rows as k + a
+    chain_product(c, B, ud.p, (int)a_cols, dptr.p, drow.p, dval.p, core, h->c);
+    c->sync();
+    *out = h.release();
+  });
+}
+
+int ctd_gpu_csc_info(const ctd_gpu_csc* m, int64_t* rows, int64_t* n_cols, int64_t* nnz) {
+  return guarded([&] {
+    need(m, "csc");
+    if (rows) *rows = m->c.rows;
+    if (n_cols) *n_cols = m->c.cols;
+    if (nnz) *nnz = m->c.nnz;
+  });
+}
+
+int ctd_gpu_csc_copy(const ctd_gpu_csc* m, int64_t* col_id, int64_t* col_ptr, int64_t* rows, double* vals) {
+  return guarded([&] {
+    need(m, "csc");
+    bind_device(m->ctx);
+    const Core& c = m->c;
+    if (col_id && c.cols) std::memcpy(col_id, c.col_id.data(), c.cols * sizeof(int64_t));
+    if (col_ptr) std::memcpy(col_ptr, c.ptr.data(), (c.cols + 1) * sizeof(int64_t));
+    if (c.nnz && (rows || vals)) {
+      if (vals) m->ctx->to_host(vals, c.val.p, c.nnz);
+      std::vector<int32_t> r32(rows ? c.nnz : 0);
+      if (rows) m->ctx->to_host(r32.data(), c.row.p, c.nnz);
+      m->ctx->sync();
+      for (int64_t i = 0; rows && i < c.nnz; ++i) rows[i] = (int64_t)r32[i] - m->row_shift;
+    }
+  });
+}
+
+int ctd_gpu_csc_destroy(ctd_gpu_csc* m) {
+  return guarded([&] {
+    if (!m) return;
+    bind_device(m->ctx);
+    delete m;
   });
 }
 

@@ -51,6 +51,65 @@ Basis::Basis(Ctx* c, int64_t d) : ctx(c), dim(d) {
   rptr.zero();
 }
 
+void basis_load(Basis& B, int64_t K, const int64_t* col_ptr, const int64_t* rows, const double* vals,
+                const double* u) {
+  Ctx* ctx = B.ctx;
+  if (B.K != 0) fail(CTD_ERR_ARGUMENT, "basis_load needs an empty basis");
+  const int64_t nnz = col_ptr[K], dim = B.dim;
+  if (col_ptr[0] != 0 || nnz < 0) fail(CTD_ERR_ARGUMENT, "malformed column pointers");
+  // R's CSC
+  B.kcap = K;
+  B.rptr.alloc(ctx, K + 1);
+  ctx->to_dev(B.rptr.p, col_ptr, K + 1);
+  std::vector<int32_t> r32(nnz > 0 ? nnz : 1);
+  std::vector<int32_t> cnt(dim + 1, 0);
+  for (int64_t k = 0; k < K; ++k) {
+    if (col_ptr[k + 1] < col_ptr[k]) fail(CTD_ERR_ARGUMENT, "malformed column pointers");
+    for (int64_t t = col_ptr[k]; t < col_ptr[k + 1]; ++t) {
+      if (rows[t] < 0 || rows[t] >= dim) fail(CTD_ERR_SHAPE, "row index outside the fiber length");
+      if (t > col_ptr[k] && rows[t] <= rows[t - 1]) fail(CTD_ERR_ARGUMENT, "rows must ascend within a column");
+      r32[t] = (int32_t)rows[t];
+      ++cnt[rows[t]];
+    }
+  }
+  B.rcap = std::max<int64_t>(nnz, 1);
+  B.rrow.alloc(ctx, B.rcap);
+  B.rval.alloc(ctx, B.rcap);
+  if (nnz) {
+    ctx->to_dev(B.rrow.p, r32.data(), nnz);
+    ctx->to_dev(B.rval.p, vals, nnz);
+  }
+  B.rnnz = nnz;
+  // row index: per row, the columns containing it in ascending k
+  std::vector<int64_t> base(dim + 1, 0);
+  for (int64_t r = 0; r < dim; ++r) base[r + 1] = base[r] + ((cnt[r] + 3) & ~3);
+  const int64_t ricap = base[dim] + 4;
+  std::vector<int32_t> ek(ricap, 0), fill(dim, 0);
+  std::vector<double> ev(ricap, 0.0);
+  for (int64_t k = 0; k < K; ++k)
+    for (int64_t t = col_ptr[k]; t < col_ptr[k + 1]; ++t) {
+      const int64_t r = rows[t], p = base[r] + fill[r]++;
+      ek[p] = (int32_t)k;
+      ev[p] = vals[t];
+    }
+  B.ricap = ricap;
+  B.rek.alloc(ctx, ricap);
+  B.rev.alloc(ctx, ricap);
+  ctx->to_dev(B.rek.p, ek.data(), ricap);
+  ctx->to_dev(B.rev.p, ev.data(), ricap);
+  ctx->to_dev(B.rowbase.p, base.data(), dim + 1);
+  ctx->to_dev(B.rowlen.p, cnt.data(), dim);
+  // U
+  B.LD = (K + 2) & ~int64_t(1);
+  if (u && K) {
+    B.U.alloc(ctx, (size_t)B.LD * B.LD);
+    CUDA_OK(cudaMemcpy2DAsync(B.U.p, B.LD * sizeof(double), u, K * sizeof(double), K * sizeof(double), K,
+                              cudaMemcpyHostToDevice, ctx->stream));
+  }
+  B.K = K;
+  ctx->sync();
+}
+
 namespace {
 
 template <typename T>

@@ -93,6 +93,13 @@ int64_t spec_certify(Basis& B, const Cands& c, const double* xsq, const double* 
                      const int* kept_cand, int64_t K0, int64_t K, int64_t pos, int64_t b, double eps, int32_t* acc,
                      int32_t* deg, double* dl, double* res_out);
 
+// Loads a given R (host CSC: K columns over B.dim rows, rows ascending within
+// a column) and optionally U (K x K row-major) into an empty basis, with R's
+// row index: the operand form compute_core / chain_product read (read-only
+// use; the filter's first-appearance bookkeeping is not rebuilt).
+void basis_load(Basis& B, int64_t K, const int64_t* col_ptr, const int64_t* rows, const double* vals,
+                const double* u);
+
 // Host copies of the basis.
 void basis_u(const Basis& B, double* u /* K*K row-major */);
 void basis_r(const Basis& B, int64_t* col_ptr, int64_t* rows, double* vals);

@@ -338,6 +338,38 @@ size_t CoreArena::bytes() const {
   return b;
 }
 
+// left = (dR^T R_old) U_old (A x Kold, row-major): the chain product's dense
+// left factor (ctd_dynamic.cpp:234-246), dR = columns fib[0..A) of (fptr,
+// frow, fval), R_old = B's first Kold columns.
+void chain_left(Ctx* ctx, const int32_t* fib, int A, const int64_t* dptr, const int32_t* drow, const double* dval,
+                const Basis& B, int64_t Kold, const double* uold, double* left) {
+    Buf<double> gram(ctx, (size_t)A * Kold);
+    const size_t xsmem = (size_t)B.dim * sizeof(double);
+    if (xsmem <= 96 * 1024 && !getenv("CTD_CORE_LEGACY")) {
+      if (xsmem > 48 * 1024)
+        CUDA_OK(cudaFuncSetAttribute(k_gram_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem));
+      const dim3 grid(ceil_div((uint64_t)Kold, 256), A);
+      LAUNCH(ctx, k_gram_cols, grid, 256, xsmem, fib, dptr, drow, dval, (int)B.dim, B.rptr.p, B.rrow.p,
+             B.rval.p, (int)Kold, gram.p);
+    } else {
+      const size_t smem = (size_t)Kold * sizeof(double);
+      if (smem > 200 * 1024) fail(CTD_ERR_ARGUMENT, "core update supports at most 25600 kept fibers");
+      CUDA_OK(cudaFuncSetAttribute(k_gram_old, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      LAUNCH(ctx, k_gram_old, (unsigned)std::min(A, ctx->sm_count * 4), 256, smem, fib, A, dptr, drow, dval,
+             B.rowbase.p, B.rowlen.p, B.rek.p, B.rev.p, (int)Kold, gram.p);
+    }
+    if (!getenv("CTD_CORE_LEGACY")) {
+      Buf<int32_t> nzj(ctx, (size_t)A * Kold);
+      Buf<double> nzg(ctx, (size_t)A * Kold);
+      Buf<int> nzn(ctx, A);
+      LAUNCH(ctx, k_gram_compact, A, 256, 0, gram.p, (int)Kold, nzj.p, nzg.p, nzn.p);
+      const dim3 grid(A, ceil_div((uint64_t)Kold, 256));
+      LAUNCH(ctx, k_left_nz, grid, 256, 0, nzj.p, nzg.p, nzn.p, (int)Kold, uold, left);
+    } else {
+      LAUNCH(ctx, k_left, ceil_div((uint64_t)A * Kold, 256), 256, 0, gram.p, A, (int)Kold, uold, left);
+    }
+}
+
 void core_record(Ctx* ctx, const Fibers& fb, const Basis& B, int64_t Kold, const double* uold,
                  const std::vector<int32_t>& appended_fib, int64_t col_offset, CoreArena* arena,
                  CoreRecord& rec, bool dr_from_basis) {
@@ -397,31 +429,7 @@ void core_record(Ctx* ctx, const Fibers& fb, const Basis& B, int64_t Kold, const
     const int64_t* dptr = dr_from_basis ? B.rptr.p : fb.ptr.p;
     const int32_t* drow = dr_from_basis ? B.rrow.p : fb.row.p;
     const double* dval = dr_from_basis ? B.rval.p : fb.val.p;
-    Buf<double> gram(ctx, (size_t)A * Kold);
-    const size_t xsmem = (size_t)B.dim * sizeof(double);
-    if (xsmem <= 96 * 1024 && !getenv("CTD_CORE_LEGACY")) {
-      if (xsmem > 48 * 1024)
-        CUDA_OK(cudaFuncSetAttribute(k_gram_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem));
-      const dim3 grid(ceil_div((uint64_t)Kold, 256), A);
-      LAUNCH(ctx, k_gram_cols, grid, 256, xsmem, fib.p, dptr, drow, dval, (int)B.dim, B.rptr.p, B.rrow.p,
-             B.rval.p, (int)Kold, gram.p);
-    } else {
-      const size_t smem = (size_t)Kold * sizeof(double);
-      if (smem > 200 * 1024) fail(CTD_ERR_ARGUMENT, "core update supports at most 25600 kept fibers");
-      CUDA_OK(cudaFuncSetAttribute(k_gram_old, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      LAUNCH(ctx, k_gram_old, (unsigned)std::min(A, ctx->sm_count * 4), 256, smem, fib.p, A, dptr, drow, dval,
-             B.rowbase.p, B.rowlen.p, B.rek.p, B.rev.p, (int)Kold, gram.p);
-    }
-    if (!getenv("CTD_CORE_LEGACY")) {
-      Buf<int32_t> nzj(ctx, (size_t)A * Kold);
-      Buf<double> nzg(ctx, (size_t)A * Kold);
-      Buf<int> nzn(ctx, A);
-      LAUNCH(ctx, k_gram_compact, A, 256, 0, gram.p, (int)Kold, nzj.p, nzg.p, nzn.p);
-      const dim3 grid(A, ceil_div((uint64_t)Kold, 256));
-      LAUNCH(ctx, k_left_nz, grid, 256, 0, nzj.p, nzg.p, nzn.p, (int)Kold, uold, left);
-    } else {
-      LAUNCH(ctx, k_left, ceil_div((uint64_t)A * Kold, 256), 256, 0, gram.p, A, (int)Kold, uold, left);
-    }
+    chain_left(ctx, fib.p, A, dptr, drow, dval, B, Kold, uold, left);
     lap(2);
   }
   if (trace && tm[0] + tm[1] + tm[2] > 10.0)
@@ -633,6 +641,60 @@ double core_drift(Ctx* ctx, const DevCore& core, const Fibers& hf, const Basis& 
   ctx->sync();
   ctx->check_flags("core_drift");
   return std::sqrt(sq);
+}
+
+}  // namespace ctdgpu
+
+namespace ctdgpu {
+
+void chain_product(Ctx* ctx, const Basis& B, const double* u, int A, const int64_t* dptr, const int32_t* drow,
+                   const double* dval, const DevCore& core, Core& out) {
+  const int64_t K = B.K;
+  const long long oc = core.cols;
+  out = Core{};
+  out.rows = A;
+  if (A == 0 || K == 0 || oc == 0) return;
+  Buf<double> left(ctx, (size_t)A * K);
+  std::vector<int32_t> f(A);
+  for (int a = 0; a < A; ++a) f[a] = a;
+  Buf<int32_t> fib(ctx, A);
+  ctx->to_dev(fib.p, f.data(), A);
+  chain_left(ctx, fib.p, A, dptr, drow, dval, B, K, u, left.p);
+  // ((dR^T R) U) C column by column (ctd_dynamic.cpp:249-267): counts, then
+  // the entries at their offsets (k_bottom_left writes row K + a at
+  // nptr[w] + (column length) + rank, so nptr is shifted back by the length)
+  Buf<long long> blc(ctx, oc + 1);
+  const unsigned wgrid = ceil_div((uint64_t)oc * 32, 256);
+  LAUNCH(ctx, k_bottom_left, wgrid, 256, 0, 0, core.ptr.p, core.row.p, core.val.p, oc, left.p, A, (int)K, blc.p,
+         (const int64_t*)nullptr, (int32_t*)nullptr, (double*)nullptr);
+  std::vector<long long> cnt(oc);
+  std::vector<int64_t> optr(oc + 1);
+  ctx->to_host(cnt.data(), blc.p, oc);
+  ctx->to_host(optr.data(), core.ptr.p, oc + 1);
+  ctx->sync();
+  std::vector<int64_t> adj(oc + 1);
+  int64_t tot = 0;
+  out.ptr.push_back(0);
+  for (long long w = 0; w < oc; ++w) {
+    adj[w] = tot - (optr[w + 1] - optr[w]);
+    if (cnt[w]) {
+      out.col_id.push_back(w);
+      out.ptr.push_back(tot + cnt[w]);
+    }
+    tot += cnt[w];
+  }
+  adj[oc] = tot;
+  out.cols = (int64_t)out.col_id.size();
+  out.nnz = tot;
+  out.row.alloc(ctx, tot + 1);
+  out.val.alloc(ctx, tot + 1);
+  if (tot) {
+    Buf<int64_t> nptr(ctx, oc + 1);
+    ctx->to_dev(nptr.p, adj.data(), oc + 1);
+    LAUNCH(ctx, k_bottom_left, wgrid, 256, 0, 1, core.ptr.p, core.row.p, core.val.p, oc, left.p, A, (int)K,
+           (long long*)nullptr, nptr.p, out.row.p, out.val.p);
+    ctx->sync();
+  }
 }
 
 }  // namespace ctdgpu

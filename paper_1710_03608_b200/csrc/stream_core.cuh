@@ -68,6 +68,14 @@ void core_record(Ctx* ctx, const Fibers& fb, const Basis& B, int64_t Kold, const
                  CoreRecord& out, bool dr_from_basis = false);
 void core_apply(Ctx* ctx, DevCore& core, const CoreRecord& rec);
 
+// chain_product(dR, R, U, C) (ctd_dynamic.cpp:231-269) on its own: B holds R
+// (its K columns and row index) and u U (K x K row-major, device), dR is A
+// columns (dptr/drow/dval, device CSC over B.dim rows), core is C (K rows).
+// out: the A x core.cols product over the columns that keep an entry; its
+// rows are stored as K + a (the bottom-left block's rows in the grown core).
+void chain_product(Ctx* ctx, const Basis& B, const double* u, int A, const int64_t* dptr, const int32_t* drow,
+                   const double* dval, const DevCore& core, Core& out);
+
 // One ctd_d_step core update (Eq. 13) = core_record + core_apply.  B is the basis after this step's
 // appends, Kold its size before them and uold (Kold x Kold, row-major) U
 // before them; appended_fib the appended candidates' fiber indices into fb in

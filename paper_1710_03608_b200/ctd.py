@@ -523,6 +523,62 @@ def ctd_s(x, mode: int, sample_size: int, epsilon: float = 1e-6, seed: int = 42,
     return _read_factors(ctx, h, d.shape, mode)
 
 
+@dataclass
+class Csc:
+    """A compressed sparse matrix: only the columns that keep an entry (col_id)."""
+    rows: int
+    col_id: np.ndarray
+    col_ptr: np.ndarray
+    row: np.ndarray
+    val: np.ndarray
+
+
+def _read_csc(ctx: Context, h) -> Csc:
+    try:
+        r, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(ctx.L.ctd_gpu_csc_info(h, C.byref(r), C.byref(nc), C.byref(nz)))
+        col = np.zeros(max(nc.value, 1), np.int64)
+        ptr = np.zeros(nc.value + 1, np.int64)
+        row = np.zeros(max(nz.value, 1), np.int64)
+        val = np.zeros(max(nz.value, 1))
+        _check(ctx.L.ctd_gpu_csc_copy(h, _p(col), _p(ptr), _p(row), _p(val)))
+        return Csc(r.value, col[:nc.value], ptr, row[:nz.value], val[:nz.value])
+    finally:
+        ctx.L.ctd_gpu_csc_destroy(h)
+
+
+def compute_core(x, r_col_ptr, r_row, r_val, r_cols: int, mode: int, ctx: Optional[Context] = None) -> Csc:
+    """compute_core (ctd_static.hpp:28): C_(mode) = R^T X_(mode) for a given R
+    (CSC over x's extent in `mode`), on the device."""
+    ctx = ctx or default_context()
+    d = _dev(x, ctx)
+    cp = np.ascontiguousarray(r_col_ptr, np.int64)
+    rr = np.ascontiguousarray(r_row, np.int64)
+    rv = np.ascontiguousarray(r_val, np.float64)
+    h = C.c_void_p()
+    _check(ctx.L.ctd_gpu_compute_core(ctx.h, d.h, mode, int(d.shape[mode]), int(r_cols), _p(cp), _p(rr), _p(rv),
+                                      C.byref(h)))
+    return _read_csc(ctx, h)
+
+
+def chain_product(dim: int, dr, r, u, c, c_cols: int, ctx: Optional[Context] = None) -> Csc:
+    """chain_product (ctd_dynamic.hpp:61-62): ((dR^T R) U) C on the device.
+    dr, r, c: (col_ptr, rows, vals) CSC triples (dr, r over `dim` rows; c with
+    one row per column of r), u: k x k."""
+    ctx = ctx or default_context()
+    a = [np.ascontiguousarray(v) for v in dr]
+    b = [np.ascontiguousarray(v) for v in r]
+    cc = [np.ascontiguousarray(v) for v in c]
+    a[0], a[1], b[0], b[1], cc[0], cc[1] = (np.asarray(v, np.int64) for v in (a[0], a[1], b[0], b[1], cc[0], cc[1]))
+    uu = np.ascontiguousarray(u, np.float64)
+    k = b[0].shape[0] - 1
+    h = C.c_void_p()
+    _check(ctx.L.ctd_gpu_chain_product(ctx.h, int(dim), a[0].shape[0] - 1, _p(a[0]), _p(a[1]), _p(a[2]), k, _p(b[0]),
+                                       _p(b[1]), _p(b[2]), _p(uu), int(c_cols), _p(cc[0]), _p(cc[1]), _p(cc[2]),
+                                       C.byref(h)))
+    return _read_csc(ctx, h)
+
+
 def memory_usage(x, f: LRFactors, ctx: Optional[Context] = None) -> float:
     """memory_usage (evaluation.cpp:124-129): (nnz(C) + nnz(U) + nnz(R)) / nnz(X);
     the factors must carry C (``ctd_s(..., with_core=True)``)."""

@@ -18,6 +18,11 @@
 //   column_distribution      sampling.hpp:20        (src/sampling.cpp:21-31)
 //   sample_with_replacement  sampling.hpp:27-28     (src/sampling.cpp:33-64)
 //   unique_first_occurrence  sampling.hpp:31        (src/sampling.cpp:66-78)
+//   compute_core             ctd_static.hpp:28      (src/ctd_static.cpp:12-17)
+//   chain_product            ctd_dynamic.hpp:61-62  (src/ctd_dynamic.cpp:231-269)
+// FiberBasis stays reference code: callers drive it one candidate at a time
+// and read its STL members directly; the batched GPU filter is reached
+// through ctd_s / init_stream / ctd_d_step above.
 // memory_usage (evaluation.cpp:124-129) stays reference code: it counts the
 // nonzeros of host objects the caller already holds.
 //
@@ -432,6 +437,65 @@ std::vector<index_t> __wrap__ZN3ctd23unique_first_occurrenceESt4spanIKlLm1844674
   rethrow(ctd_gpu_unique_first_occurrence(context(), drawn.data(), (int64_t)drawn.size(), out.data(), &n));
   out.resize((size_t)n);
   return out;
+}
+
+namespace {
+// A ctd_gpu_csc result as a reference SparseMatrix with `rows` x `cols`.
+SparseMatrix from_csc(ctd_gpu_csc* h, index_t rows, index_t cols) {
+  struct Guard {
+    ctd_gpu_csc* h;
+    ~Guard() { ctd_gpu_csc_destroy(h); }
+  } g{h};
+  int64_t r = 0, nc = 0, nz = 0;
+  rethrow(ctd_gpu_csc_info(h, &r, &nc, &nz));
+  std::vector<int64_t> col(nc), ptr(nc + 1), rr(nz);
+  std::vector<double> vals(nz);
+  rethrow(ctd_gpu_csc_copy(h, col.data(), ptr.data(), rr.data(), vals.data()));
+  std::vector<index_t> ri(rr.begin(), rr.end()), ci;
+  ci.reserve(nz);
+  for (int64_t c = 0; c < nc; ++c)
+    for (int64_t t = ptr[c]; t < ptr[c + 1]; ++t) ci.push_back(col[c]);
+  return SparseMatrix(rows, cols, std::move(ri), std::move(ci), std::move(vals));
+}
+std::vector<int64_t> ptr64(const SparseMatrix& m) {
+  const auto& cp = m.column_pointers();
+  return std::vector<int64_t>(cp.begin(), cp.end());
+}
+}  // namespace
+
+SparseTensor __wrap__ZN3ctd12compute_coreERKNS_12SparseTensorERKNS_12SparseMatrixEi(const SparseTensor& x,
+                                                                                 const SparseMatrix& r, int mode) {
+  if (mode < 0 || mode >= x.order())
+    throw ArgumentError("mode " + std::to_string(mode) + " out of range for order " + std::to_string(x.order()));
+  if (r.rows() != x.extent(mode)) throw ShapeError("fiber matrix rows do not match the tensor extent");  // :14-15
+  Tensor t(x);
+  const auto cp = ptr64(r);
+  ctd_gpu_csc* h = nullptr;
+  rethrow(ctd_gpu_compute_core(context(), t.h, mode, r.rows(), r.cols(), cp.data(), r.row_indices().data(),
+                               r.values().data(), &h));
+  std::vector<index_t> cshape = x.shape();
+  cshape[(size_t)mode] = r.cols();
+  return fold(from_csc(h, r.cols(), other_extents(x.shape(), mode)), mode, cshape);
+}
+
+SparseMatrix __wrap__ZN3ctd13chain_productERKNS_12SparseMatrixES2_RKNS_11DenseMatrixES2_(const SparseMatrix& delta_r,
+                                                                                      const SparseMatrix& r,
+                                                                                      const DenseMatrix& u,
+                                                                                      const SparseMatrix& core) {
+  if (delta_r.rows() != r.rows()) throw ShapeError("inner dimensions differ");  // transpose_times, :55
+  if (r.cols() != u.rows() || u.cols() != core.rows())
+    throw ShapeError("chain product dimension mismatch");  // :234-235
+  const index_t k = r.cols();
+  std::vector<double> uf((size_t)k * (size_t)k);
+  for (index_t i = 0; i < k; ++i)
+    for (index_t j = 0; j < k; ++j) uf[(size_t)i * (size_t)k + (size_t)j] = u.at(i, j);
+  const auto dcp = ptr64(delta_r), rcp = ptr64(r), ccp = ptr64(core);
+  ctd_gpu_csc* h = nullptr;
+  rethrow(ctd_gpu_chain_product(context(), r.rows(), delta_r.cols(), dcp.data(), delta_r.row_indices().data(),
+                                delta_r.values().data(), k, rcp.data(), r.row_indices().data(), r.values().data(),
+                                uf.data(), core.cols(), ccp.data(), core.row_indices().data(), core.values().data(),
+                                &h));
+  return from_csc(h, delta_r.cols(), core.cols());
 }
 
 // For callers that read StreamState::basis / core / history directly (the

@@ -26,7 +26,9 @@ WRAPPED = ("_ZN3ctd5ctd_sERKNS_12SparseTensorEildm",
            "_ZN3ctd15column_sq_normsERKNS_12SparseMatrixE",
            "_ZN3ctd19column_distributionERKNS_12SparseMatrixE",
            "_ZN3ctd23sample_with_replacementERKNS_18ColumnDistributionElm",
-           "_ZN3ctd23unique_first_occurrenceESt4spanIKlLm18446744073709551615EE")
+           "_ZN3ctd23unique_first_occurrenceESt4spanIKlLm18446744073709551615EE",
+           "_ZN3ctd12compute_coreERKNS_12SparseTensorERKNS_12SparseMatrixEi",
+           "_ZN3ctd13chain_productERKNS_12SparseMatrixES2_RKNS_11DenseMatrixES2_")
 
 needs_dropin = pytest.mark.skipif(not os.path.exists(DROPIN),
                                   reason="drop-in not built (make -C paper_1710_03608_b200/shim)")
@@ -191,3 +193,75 @@ def test_dropin_run_stream(ref, dropin):
     assert np.array_equal(a["memory_usage"], b["memory_usage"])
     for ea, eb in zip(a["relative_error"], b["relative_error"]):
         assert abs(ea - eb) <= 1e-9 * max(1.0, abs(ea)), (ea, eb)
+
+
+def _cols(m, lo, hi):
+    """Columns [lo, hi) of a Csc."""
+    from oracle.bindings import Csc
+    a, b = m.col_ptr[lo], m.col_ptr[hi]
+    return Csc(m.rows, hi - lo, (m.col_ptr[lo:hi + 1] - a).astype(np.int64), m.row[a:b].copy(), m.val[a:b].copy())
+
+
+@pytest.mark.gpu
+@needs_dropin
+@pytest.mark.parametrize("name", list(CASES))
+def test_dropin_compute_core_and_chain_product(ref, dropin, name):
+    """compute_core (ctd_static.hpp:28) and chain_product (ctd_dynamic.hpp:61-62)
+    called by the reference's own driver code: bit-identical results through the
+    drop-in, and the reference's ShapeError on mismatched operands."""
+    from oracle.bindings import Csc, OracleError
+    make, mode, s = CASES[name]
+    x = make()
+    ta, tb = ref.tensor(x.shape, x.flat_idx(), x.val), dropin.tensor(x.shape, x.flat_idx(), x.val)
+    fe = ref.frontend(ta, mode, s)
+    ca, cb = ref.compute_core(ta, fe.R, mode), dropin.compute_core(tb, fe.R, mode)
+    (ia, va), (ib, vb) = ca.data(), cb.data()
+    assert ca.shape == cb.shape and np.array_equal(ia, ib)
+    assert np.array_equal(va.view(np.int64), vb.view(np.int64))
+    # chain_product((dR, R_old, U_old, C_old)): the last A kept fibers against the others
+    K = fe.R.cols
+    A = max(1, min(6, K // 3))
+    r_old, d_r = _cols(fe.R, 0, K - A), _cols(fe.R, K - A, K)
+    u_old = np.ascontiguousarray(fe.U[:K - A, :K - A])
+    core_t = ref.compute_core(ta, r_old, mode)
+    core_m, _ = ref.matricize(core_t, mode)
+    pa, pb = ref.chain_product(d_r, r_old, u_old, core_m), dropin.chain_product(d_r, r_old, u_old, core_m)
+    assert (pa.rows, pa.cols) == (pb.rows, pb.cols) == (A, core_m.cols)
+    assert pa.col_ptr[-1] > 0
+    assert np.array_equal(pa.col_ptr, pb.col_ptr) and np.array_equal(pa.row, pb.row)
+    assert np.array_equal(pa.val.view(np.int64), pb.val.view(np.int64))
+    for lib in (ref, dropin):
+        with pytest.raises(OracleError) as e:  # U's size differs from R's column count
+            lib.chain_product(d_r, r_old, np.ascontiguousarray(u_old[:-1, :-1]), core_m)
+        assert e.value.code == 2  # ShapeError
+        with pytest.raises(OracleError) as e:  # dR and R over different fiber lengths
+            lib.chain_product(Csc(d_r.rows + 1, d_r.cols, d_r.col_ptr, d_r.row, d_r.val), r_old, u_old, core_m)
+        assert e.value.code == 2
+        bad = Csc(fe.R.rows + 1, fe.R.cols, fe.R.col_ptr, fe.R.row, fe.R.val)  # rows != the tensor extent
+        with pytest.raises(OracleError) as e:
+            lib.compute_core(ta if lib is ref else tb, bad, mode)
+        assert e.value.code == 2
+
+
+@pytest.mark.gpu
+def test_python_compute_core_and_chain_product(ref):
+    """The Python mirror's compute_core / chain_product on the device against
+    the compiled reference."""
+    from paper_1710_03608_b200 import ctd
+    x = g.traffic([300, 300, 20], 12000, 3)
+    ta = ref.tensor(x.shape, x.flat_idx(), x.val)
+    fe = ref.frontend(ta, 0, 200)
+    got = ctd.compute_core(ctd.SparseTensor.from_datagen(x), fe.R.col_ptr, fe.R.row, fe.R.val, fe.R.cols, 0)
+    want, _ = ref.matricize(ref.compute_core(ta, fe.R, 0), 0)
+    cols = np.nonzero(np.diff(want.col_ptr))[0]
+    assert np.array_equal(got.col_id, cols)
+    assert np.array_equal(got.row, want.row) and np.array_equal(got.val.view(np.int64), want.val.view(np.int64))
+    K = fe.R.cols
+    r_old, d_r = _cols(fe.R, 0, K - 4), _cols(fe.R, K - 4, K)
+    core_m, _ = ref.matricize(ref.compute_core(ta, r_old, 0), 0)
+    u = np.ascontiguousarray(fe.U[:K - 4, :K - 4])
+    pa = ref.chain_product(d_r, r_old, u, core_m)
+    pb = ctd.chain_product(fe.R.rows, (d_r.col_ptr, d_r.row, d_r.val), (r_old.col_ptr, r_old.row, r_old.val), u,
+                           (core_m.col_ptr, core_m.row, core_m.val), core_m.cols)
+    assert np.array_equal(pb.col_id, np.nonzero(np.diff(pa.col_ptr))[0])
+    assert np.array_equal(pb.row, pa.row) and np.array_equal(pb.val.view(np.int64), pa.val.view(np.int64))
