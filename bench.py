@@ -658,8 +658,18 @@ def run_sharded(args, rank, world, local_rank):
     dt = api.DeviceTensor.from_device_ptrs(gshape, nnz_local, [idx_t[k].data_ptr() for k in range(3)],
                                            val_t.data_ptr(), ctx)
     c, eps, seed, mode = C2["c"], C2["eps"], C2["seed"], C2["mode"]
+    # default: the orchestration inside the library (ctd_gpu_ctd_s_sharded, C++;
+    # NCCL communicator of its own, or host callbacks when the ranks share a GPU
+    # over gloo); CTD_BENCH_DIST=py: the Python orchestrator (dist.ctd_s_sharded)
+    native = os.environ.get("CTD_BENCH_DIST", "native") != "py"
+    if native:
+        ncomm = dist.NativeComm(ctx, "nccl" if torch.distributed.get_backend() == "nccl" else "host")
 
     def step(src=dt, err=False):
+        if native:
+            local = src if isinstance(src, api.DeviceTensor) else api.DeviceTensor(
+                api.SparseTensor(gshape, src[0], src[1]), ctx)
+            return dist.ctd_s_sharded_native(local, mode, c, eps, seed, comm=ncomm, with_error=err)
         return dist.ctd_s_sharded(gshape, src, mode, c, eps, seed, comm=comm, kernels=kern, with_error=err)
 
     for _ in range(args.warmup):
@@ -714,6 +724,9 @@ def run_sharded(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded splitmix64 generator, SURVEY §8d)",
         "config": bench_config(world),
+        "orchestration": ("C++ in libctd_gpu (ctd_gpu_ctd_s_sharded), "
+                          + ("NCCL all-reduces on device buffers" if torch.distributed.get_backend() == "nccl"
+                             else "host-callback all-reduces (gloo)")) if native else "Python (dist.ctd_s_sharded)",
         "result": {"nnz_global": nnz, "global_shape": gshape,
                    "kept": int(r.kept_flat.shape[0]), "unique_sampled": int(r.unique.shape[0]),
                    "relative_error": rel, "fibers_global": r.n_fibers},

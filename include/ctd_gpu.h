@@ -320,6 +320,74 @@ int ctd_gpu_shard_draw(const ctd_gpu_shard *s, int64_t count, uint64_t seed, int
 int ctd_gpu_basis_error_partials(ctd_gpu_ctx *ctx, const ctd_gpu_basis *b,
                                  const ctd_gpu_tensor *x, int mode, double *x_sq,
                                  double *cross);
+/* pos[k] = the shard-local fiber index of global column cols[k], or -1 when
+ * this shard does not hold it (owner lookup for the candidate exchange). */
+int ctd_gpu_shard_find(const ctd_gpu_shard *s, int64_t n, const int64_t *cols, int64_t *pos);
+/* Owner-side candidate gather straight into a draw-order layout in DEVICE
+ * memory: fiber cols[k] (held by this shard) is written to rows/vals
+ * [dst_off[k], dst_off[k] + its length).  dst_off stays on the host. */
+int ctd_gpu_shard_gather_into(const ctd_gpu_shard *s, int64_t n, const int64_t *cols,
+                              const int64_t *dst_off, int32_t *rows, double *vals);
+
+/* ---- multi-GPU CTD-S driven from C++  -------------------------
+ * ctd_s (ctd_static.cpp:19-50) over fiber-range shards with the whole host
+ * orchestration inside this library: one process (or thread) per GPU, each
+ * holding its fiber range of X in the GLOBAL index space.  Every exchange is
+ * an in-place all-reduce (sum) of a DEVICE buffer on the context's stream:
+ *   - range check and global fiber count (a slot per rank);
+ *   - the sequential law, chained rank to rank (one double per hop);
+ *   - the draws (each is resolved by exactly one owner; others add 0);
+ *   - candidate lengths and payload, written by the owners into the
+ *     draw-order layout (others add 0: integer sums of bit patterns, exact);
+ *   - relative_error's partials, summed in rank order on the host.
+ * The filter then runs replicated, so every rank ends with the same kept
+ * ids, R and U, bit-identical to ctd_gpu_ctd_s on the whole tensor.
+ * Communicators:
+ *   - NCCL (libnccl.so.2 is dlopen'ed on first use, preferring the copy the
+ *     process already loaded): rank 0 makes the 128-byte id, the caller
+ *     ships it to the other ranks by any means, each rank calls _nccl_create;
+ *   - host callbacks (gloo, MPI, tests): allreduce_sum receives a HOST copy
+ *     of the buffer (dtype 0 = int32, 1 = int64) and sums it in place over
+ *     the ranks; return 0 on success. */
+typedef struct ctd_gpu_comm ctd_gpu_comm;
+typedef int (*ctd_gpu_allreduce_fn)(void *user, void *buf, int64_t n, int dtype);
+int ctd_gpu_comm_nccl_unique_id(unsigned char id[128]);
+int ctd_gpu_comm_nccl_create(ctd_gpu_ctx *ctx, int world, int rank, const unsigned char id[128],
+                             ctd_gpu_comm **out);
+int ctd_gpu_comm_host_create(ctd_gpu_ctx *ctx, int world, int rank, ctd_gpu_allreduce_fn allreduce_sum,
+                             void *user, ctd_gpu_comm **out);
+int ctd_gpu_comm_world(const ctd_gpu_comm *c, int *world, int *rank);
+int ctd_gpu_comm_destroy(ctd_gpu_comm *c);
+
+typedef struct ctd_gpu_sharded ctd_gpu_sharded;
+typedef struct {
+  int64_t n_fibers;      /* global nonempty fibers */
+  int64_t n_unique;      /* unique drawn fibers (candidates) */
+  int64_t n_kept;        /* accepted candidates = kept_fibers.size() */
+  int64_t r_nnz;         /* nnz(R) */
+  int64_t cand_nnz;      /* entries of the candidate layout */
+  int64_t local_fibers;  /* this rank's nonempty fibers */
+  int64_t core_cols;     /* CTD_GPU_WITH_CORE: this rank's core columns and entries */
+  int64_t core_nnz;
+  double total_sq_norm;  /* |X|^2 in the law's sequential order */
+  double relative_error; /* CTD_GPU_WITH_ERROR, else NaN */
+} ctd_gpu_sharded_info;
+/* flags: CTD_GPU_WITH_ERROR; CTD_GPU_WITH_CORE keeps this rank's core
+ * columns on the shard (ctd_gpu_sharded_shard + ctd_gpu_shard_core_copy). */
+int ctd_gpu_ctd_s_sharded(ctd_gpu_ctx *ctx, ctd_gpu_comm *comm, const ctd_gpu_tensor *local, int mode,
+                          int64_t sample_size, double epsilon, uint64_t seed, unsigned flags,
+                          ctd_gpu_sharded **out);
+int ctd_gpu_sharded_info_get(const ctd_gpu_sharded *r, ctd_gpu_sharded_info *info);
+/* kept[n_kept] (acceptance order); unique[n_unique] with per-candidate
+ * accepted / degenerate / delta (any may be NULL). */
+int ctd_gpu_sharded_kept(const ctd_gpu_sharded *r, int64_t *kept);
+int ctd_gpu_sharded_trace(const ctd_gpu_sharded *r, int64_t *unique, int32_t *accepted,
+                          int32_t *degenerate, double *delta);
+/* Borrowed handles owned by the result: the replicated basis (R, U via
+ * ctd_gpu_basis_r / ctd_gpu_basis_u) and this rank's shard. */
+ctd_gpu_basis *ctd_gpu_sharded_basis(ctd_gpu_sharded *r);
+ctd_gpu_shard *ctd_gpu_sharded_shard(ctd_gpu_sharded *r);
+int ctd_gpu_sharded_destroy(ctd_gpu_sharded *r);
 
 /* ---- CTD-D (ctd_dynamic.hpp:42-58) -------------------------------------- */
 int ctd_gpu_stream_init(ctd_gpu_ctx *ctx, const ctd_gpu_tensor *historical,

@@ -15,6 +15,17 @@ LIB_PATH = os.environ.get("CTD_GPU_LIB") or os.path.join(HERE, "libctd_gpu.so")
 _lib = None
 
 
+class ShardedInfo(C.Structure):
+    _fields_ = [("n_fibers", C.c_int64), ("n_unique", C.c_int64), ("n_kept", C.c_int64),
+                ("r_nnz", C.c_int64), ("cand_nnz", C.c_int64), ("local_fibers", C.c_int64),
+                ("core_cols", C.c_int64), ("core_nnz", C.c_int64),
+                ("total_sq_norm", C.c_double), ("relative_error", C.c_double)]
+
+
+# int (*)(void *user, void *buf, int64_t n, int dtype): the host all-reduce callback
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int)
+
+
 class FactorsInfo(C.Structure):
     _fields_ = [("kept", C.c_int64), ("r_rows", C.c_int64), ("r_nnz", C.c_int64),
                 ("c_nnz", C.c_int64), ("n_drawn", C.c_int64), ("n_unique", C.c_int64),
@@ -95,6 +106,20 @@ SIGNATURES = [
     ("ctd_gpu_shard_cdf", _I, [_V, _D, _D, _P, _P]),
     ("ctd_gpu_shard_clamp", _I, [_V]),
     ("ctd_gpu_shard_draw", _I, [_V, _I64, _U64, _P]),
+    ("ctd_gpu_shard_find", _I, [_V, _I64, _P, _P]),
+    ("ctd_gpu_shard_gather_into", _I, [_V, _I64, _P, _P, _P, _P]),
+    ("ctd_gpu_comm_nccl_unique_id", _I, [_P]),
+    ("ctd_gpu_comm_nccl_create", _I, [_V, _I, _I, _P, _PV]),
+    ("ctd_gpu_comm_host_create", _I, [_V, _I, _I, ALLREDUCE_FN, _V, _PV]),
+    ("ctd_gpu_comm_world", _I, [_V, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("ctd_gpu_comm_destroy", _I, [_V]),
+    ("ctd_gpu_ctd_s_sharded", _I, [_V, _V, _V, _I, _I64, _D, _U64, C.c_uint, _PV]),
+    ("ctd_gpu_sharded_info_get", _I, [_V, C.POINTER(ShardedInfo)]),
+    ("ctd_gpu_sharded_kept", _I, [_V, _P]),
+    ("ctd_gpu_sharded_trace", _I, [_V, _P, _P, _P, _P]),
+    ("ctd_gpu_sharded_basis", _V, [_V]),
+    ("ctd_gpu_sharded_shard", _V, [_V]),
+    ("ctd_gpu_sharded_destroy", _I, [_V]),
     ("ctd_gpu_stream_init", _I, [_V, _V, _I, _I64, _D, _U64, C.c_uint, _PV]),
     ("ctd_gpu_stream_step", _I, [_V, _V, _I64]),
     ("ctd_gpu_stream_t", _I64, [_V]),

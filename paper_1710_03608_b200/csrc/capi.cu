@@ -109,6 +109,23 @@ void check_shape(int order, const int64_t* shape) {
 
 namespace ctdgpu {
 
+// dist.cu's view of the boundary objects (its own entry points report
+// through the same thread-local message as every other entry point).
+Ctx* ctx_of(ctd_gpu_ctx* c) { return c ? &c->c : nullptr; }
+int report_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int64_t tensor_extent(const ctd_gpu_tensor* t, int mode) {
+  return (t && mode >= 0 && mode < t->t.order) ? t->t.shape[mode] : -1;
+}
+bool shard_col_range(const ctd_gpu_shard* s, int64_t* first, int64_t* last) {
+  if (!s || s->col.empty()) return false;
+  *first = s->col.front();
+  *last = s->col.back();
+  return true;
+}
+
 void Ctx::check_flags(const char* where) {
   unsigned f = 0;
   CUDA_OK(cudaMemcpyAsync(&f, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, stream));
@@ -1028,6 +1045,53 @@ int ctd_gpu_shard_gather_device(const ctd_gpu_shard* s, int64_t n, const int64_t
     Buf<int64_t> dsrc(c, n), ddst(c, n), dlen(c, n);
     c->to_dev(dsrc.p, src.data(), n);
     c->to_dev(ddst.p, cand_ptr, n);
+    c->to_dev(dlen.p, len.data(), n);
+    LAUNCH(c, k_gather_fibers32, (unsigned)n, 128, 0, dsrc.p, ddst.p, dlen.p, s->fb.row.p, s->fb.val.p, rows, vals);
+    c->sync();
+  });
+}
+
+int ctd_gpu_shard_find(const ctd_gpu_shard* s, int64_t n, const int64_t* cols, int64_t* pos) {
+  return guarded([&] {
+    need(s, "shard");
+    if (n < 0) fail(CTD_ERR_ARGUMENT, "negative count");
+    if (n == 0) return;
+    need(cols, "cols");
+    need(pos, "pos");
+    for (int64_t k = 0; k < n; ++k) {
+      const auto it = std::lower_bound(s->col.begin(), s->col.end(), cols[k]);
+      pos[k] = (it != s->col.end() && *it == cols[k]) ? (int64_t)(it - s->col.begin()) : -1;
+    }
+  });
+}
+
+int ctd_gpu_shard_gather_into(const ctd_gpu_shard* s, int64_t n, const int64_t* cols, const int64_t* dst_off,
+                              int32_t* rows, double* vals) {
+  return guarded([&] {
+    need(s, "shard");
+    bind_device(s->ctx);
+    if (n < 0) fail(CTD_ERR_ARGUMENT, "negative count");
+    if (n == 0) return;
+    need(cols, "cols");
+    need(dst_off, "dst_off");
+    std::vector<int64_t> src(n), len(n);
+    int64_t tot = 0;
+    for (int64_t k = 0; k < n; ++k) {
+      const auto it = std::lower_bound(s->col.begin(), s->col.end(), cols[k]);
+      if (it == s->col.end() || *it != cols[k]) fail(CTD_ERR_ARGUMENT, "fiber not held by this shard");
+      if (dst_off[k] < 0) fail(CTD_ERR_ARGUMENT, "negative destination offset");
+      const int64_t f = it - s->col.begin();
+      src[k] = s->ptr[f];
+      len[k] = s->ptr[f + 1] - s->ptr[f];
+      tot += len[k];
+    }
+    if (tot == 0) return;
+    need(rows, "rows");
+    need(vals, "vals");
+    Ctx* c = s->ctx;
+    Buf<int64_t> dsrc(c, n), ddst(c, n), dlen(c, n);
+    c->to_dev(dsrc.p, src.data(), n);
+    c->to_dev(ddst.p, dst_off, n);
     c->to_dev(dlen.p, len.data(), n);
     LAUNCH(c, k_gather_fibers32, (unsigned)n, 128, 0, dsrc.p, ddst.p, dlen.p, s->fb.row.p, s->fb.val.p, rows, vals);
     c->sync();

@@ -644,6 +644,117 @@ def ctd_s_sharded(shape, local, mode: int, sample_size: int, epsilon: float = 1e
 
 
 # ---------------------------------------------------------------------------
+# the same front end with the orchestration inside the library (C++, dist.cu)
+
+class NativeComm:
+    """A `ctd_gpu_comm` for `ctd_s_sharded_native`: the library's own NCCL
+    communicator (rank 0's 128-byte id is broadcast over torch.distributed,
+    then every exchange is an ncclAllReduce on the library's stream), or,
+    with backend="host", the host-callback communicator over torch.distributed
+    (gloo: CPU tests and several ranks sharing one GPU)."""
+
+    def __init__(self, ctx: "api.Context", backend: str = "nccl", group=None):
+        import torch
+        import torch.distributed as tdist
+        from . import _lib
+        self.L, self.ctx = ctx.L, ctx
+        self.rank, self.world = tdist.get_rank(group), tdist.get_world_size(group)
+        h = C.c_void_p()
+        if backend == "nccl":
+            idb = (C.c_ubyte * 128)()
+            if self.rank == 0:
+                api._check(self.L.ctd_gpu_comm_nccl_unique_id(idb))
+            box = [bytes(idb)]
+            src = 0 if group is None else tdist.get_global_rank(group, 0)
+            tdist.broadcast_object_list(box, src=src, group=group)
+            idb = (C.c_ubyte * 128).from_buffer_copy(box[0])
+            api._check(self.L.ctd_gpu_comm_nccl_create(ctx.h, self.world, self.rank, idb, C.byref(h)))
+        elif backend == "host":
+            def allreduce(user, buf, n, dtype):
+                try:
+                    ct = C.c_int64 if dtype else C.c_int32
+                    a = np.ctypeslib.as_array((ct * n).from_address(buf))
+                    t = torch.from_numpy(a.copy())
+                    tdist.all_reduce(t, op=tdist.ReduceOp.SUM, group=group)
+                    a[:] = t.numpy()
+                    return 0
+                except Exception:  # reported by the library as a device error
+                    return 1
+            self._cb = _lib.ALLREDUCE_FN(allreduce)  # kept alive with the communicator
+            api._check(self.L.ctd_gpu_comm_host_create(ctx.h, self.world, self.rank, self._cb, None, C.byref(h)))
+        else:
+            raise api.ArgumentError(f"unknown communicator backend {backend!r}")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.ctd_gpu_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def ctd_s_sharded_native(local: "api.DeviceTensor", mode: int, sample_size: int, epsilon: float = 1e-6,
+                         seed: int = 42, comm: Optional[NativeComm] = None, with_error: bool = False,
+                         with_core: bool = False) -> ShardedResult:
+    """ctd_s over fiber-range shards through `ctd_gpu_ctd_s_sharded`: the
+    whole host orchestration (range check, chained law, draws, candidate
+    exchange, replicated filter, error partials) runs in the library, with
+    every exchange an all-reduce of a device buffer.  Same contract and
+    results as `ctd_s_sharded` (`local` is this rank's part of X in the
+    global index space, on the context's device)."""
+    if comm is None:
+        raise api.ArgumentError("ctd_s_sharded_native needs a NativeComm")
+    L = comm.L
+    flags = (1 if with_error else 0) | (2 if with_core else 0)
+    h = C.c_void_p()
+    api._check(L.ctd_gpu_ctd_s_sharded(comm.ctx.h, comm.h, local.h, mode, sample_size, C.c_double(epsilon),
+                                       C.c_uint64(seed), flags, C.byref(h)))
+    try:
+        from . import _lib
+        info = _lib.ShardedInfo()
+        api._check(L.ctd_gpu_sharded_info_get(h, C.byref(info)))
+        nk, nu = int(info.n_kept), int(info.n_unique)
+        kept = np.zeros(max(nk, 1), np.int64)
+        api._check(L.ctd_gpu_sharded_kept(h, api._p(kept)))
+        uniq = np.zeros(max(nu, 1), np.int64)
+        acc = np.zeros(max(nu, 1), np.int32)
+        deg = np.zeros(max(nu, 1), np.int32)
+        dl = np.zeros(max(nu, 1))
+        api._check(L.ctd_gpu_sharded_trace(h, api._p(uniq), api._p(acc), api._p(deg), api._p(dl)))
+        b = L.ctd_gpu_sharded_basis(h)
+        K = int(L.ctd_gpu_basis_size(b))
+        U = np.zeros((K, K))
+        if K:
+            api._check(L.ctd_gpu_basis_u(b, api._p(U)))
+        rp = np.zeros(K + 1, np.int64)
+        rr = np.zeros(max(int(info.r_nnz), 1), np.int64)
+        rv = np.zeros(max(int(info.r_nnz), 1))
+        api._check(L.ctd_gpu_basis_r(b, api._p(rp), api._p(rr), api._p(rv)))
+        res = ShardedResult(kept[:nk], U, rp, rr[:info.r_nnz], rv[:info.r_nnz], uniq[:nu], acc[:nu], deg[:nu],
+                            dl[:nu], float(info.total_sq_norm),
+                            float(info.relative_error) if with_error else None, int(info.n_fibers),
+                            {"local_fibers": int(info.local_fibers), "candidate_nnz": int(info.cand_nnz),
+                             "native": True})
+        if with_core:
+            nc, nz = int(info.core_cols), int(info.core_nnz)
+            col = np.zeros(max(nc, 1), np.int64)
+            ptr = np.zeros(nc + 1, np.int64)
+            rows = np.zeros(max(nz, 1), np.int64)
+            vals = np.zeros(max(nz, 1))
+            api._check(L.ctd_gpu_shard_core_copy(L.ctd_gpu_sharded_shard(h), api._p(col), api._p(ptr),
+                                                 api._p(rows), api._p(vals)))
+            res.core = (col[:nc], ptr, rows[:nz], vals[:nz])
+        return res
+    finally:
+        L.ctd_gpu_sharded_destroy(h)
+
+
+# ---------------------------------------------------------------------------
 # CTD-D over fiber-range shards (SURVEY §8e item 5)
 
 class ShardedStream:
