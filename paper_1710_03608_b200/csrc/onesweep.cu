@@ -128,8 +128,232 @@ struct PassArgs {
   const unsigned long long* digit_base;  // [bins] global start of each digit
   unsigned long long* status;            // [tiles][bins] look-back words
   unsigned* ticket;
+  int bulk;  // every source array 16-byte aligned: full tiles arrive by bulk copy
 };
 
+#ifndef CTD_OS_LEGACY
+// 1-D bulk copies (TMA, cp.async.bulk) completing on a shared-memory mbarrier:
+// the whole tile (keys, rows, values) is in flight from the CTA's first
+// instruction, no registers held, one memory latency per tile.
+__device__ __forceinline__ uint32_t os_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void os_mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(os_smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void os_mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(os_smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void os_bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   os_smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(os_smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void os_mbar_wait(uint64_t* bar, unsigned parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(os_smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+__global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int bins = 1 << a.dbits;
+  // the tile in INPUT order (bulk-copied), permuted on the way out through sidx
+  double* sv = reinterpret_cast<double*>(smem);                                      // [tile]
+  uint32_t* sj = reinterpret_cast<uint32_t*>(sv + kOsTile);                          // [tile]
+  int32_t* sr = reinterpret_cast<int32_t*>(sj + kOsTile);                            // [tile]
+  unsigned long long* gbase = reinterpret_cast<unsigned long long*>(sr + kOsTile);   // [bins]
+  unsigned* whist = reinterpret_cast<unsigned*>(gbase + bins);                       // [warps][bins]
+  unsigned* doff = whist + kOsWarps * bins;                                          // [bins]
+  uint16_t* sidx = reinterpret_cast<uint16_t*>(doff + bins);                         // [tile] slot -> item
+  __shared__ long long s_tile;
+  __shared__ unsigned sh32[33];
+  __shared__ __align__(8) uint64_t s_bar;
+  if (threadIdx.x == 0) {
+    const long long t0 = atomicAdd(a.ticket, 1u);
+    s_tile = t0;
+    const long long st0 = t0 * kOsTile;
+    if (a.bulk && a.n - st0 >= kOsTile) {
+      os_mbar_init(&s_bar, 1);
+      os_mbar_expect_tx(&s_bar, a.first ? kOsTile * 8u : kOsTile * 16u);
+      os_bulk_load(sv, (a.first ? a.c.val : a.vin) + st0, kOsTile * 8u, &s_bar);
+      if (!a.first) {
+        os_bulk_load(sj, a.jin + st0, kOsTile * 4u, &s_bar);
+        os_bulk_load(sr, a.rin + st0, kOsTile * 4u, &s_bar);
+      }
+    }
+  }
+  for (int t = threadIdx.x; t < kOsWarps * bins; t += blockDim.x) whist[t] = 0u;
+  __syncthreads();
+  const long long tile = s_tile;
+  const long long start = tile * kOsTile;
+  const int tn = (int)min((long long)kOsTile, a.n - start);
+  const bool bulk = a.bulk && tn == kOsTile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned mask = (unsigned)bins - 1u;
+  unsigned* wh = whist + warp * bins;
+  uint32_t jv[kOsItems];
+  unsigned lr[kOsItems];
+  // warp w owns the contiguous items [w*256, w*256+256) of the tile, 32 per
+  // round: ranks follow the item order (stable).
+  const int li0 = warp * (32 * kOsItems) + lane;
+  if (a.first) {
+    // keys and rows from the COO's index columns (all rounds in flight)
+#pragma unroll
+    for (int r = 0; r < kOsItems; ++r) {
+      const int li = li0 + r * 32;
+      uint32_t j = 0;
+      int row = 0;
+      if (li < tn) {
+        bool oob;
+        j = coo_col(a.c, start + li, &row, &oob);
+      }
+      jv[r] = j;
+      sj[li] = j;
+      sr[li] = row;
+    }
+    if (!bulk)
+      for (int s = threadIdx.x; s < tn; s += blockDim.x) sv[s] = __ldcs(a.c.val + start + s);
+  } else if (!bulk) {
+    for (int s = threadIdx.x; s < tn; s += blockDim.x) {
+      sj[s] = __ldcs(a.jin + start + s);
+      sr[s] = __ldcs(a.rin + start + s);
+      sv[s] = __ldcs(a.vin + start + s);
+    }
+    __syncthreads();
+  }
+  if (bulk) os_mbar_wait(&s_bar, 0);
+  if (!a.first) {
+#pragma unroll
+    for (int r = 0; r < kOsItems; ++r) jv[r] = sj[li0 + r * 32];
+  }
+#pragma unroll
+  for (int r = 0; r < kOsItems; ++r) {
+    const bool act = li0 + r * 32 < tn;
+    const unsigned amask = __ballot_sync(0xffffffffu, act);
+    if (act) {
+      const unsigned d = (jv[r] >> a.shift) & mask;
+      // lanes with the same digit: one ballot per digit bit (cheaper than
+      // MATCH.ANY on this part)
+      // (all kOsMaxBits bits, unrolled: the bits above dbits are 0 in every
+      // lane and leave peers unchanged)
+      unsigned peers = amask;
+#pragma unroll
+      for (int b = 0; b < kOsMaxBits; ++b) {
+        const bool bit = (d >> b) & 1u;
+        const unsigned bal = __ballot_sync(amask, bit);
+        peers &= bal ^ (bit ? 0u : 0xffffffffu);
+      }
+      const unsigned b0 = wh[d];
+      lr[r] = b0 + __popc(peers & ((1u << lane) - 1u));
+      __syncwarp(amask);
+      if (lane == __ffs(peers) - 1) wh[d] = b0 + __popc(peers);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive offsets of the warps, and the tile's total
+  unsigned tot = 0;
+  if ((int)threadIdx.x < bins) {
+    const int d = threadIdx.x;
+    for (int w = 0; w < kOsWarps; ++w) {
+      const unsigned cnt = whist[w * bins + d];
+      whist[w * bins + d] = tot;
+      tot += cnt;
+    }
+  }
+  const unsigned excl = block_excl_sum<unsigned>(tot, sh32, nullptr);
+  if ((int)threadIdx.x < bins) {
+    const int d = threadIdx.x;
+    doff[d] = excl;
+    // decoupled look-back over the tiles' counts of digit d
+    const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = kAgg - 1ull;
+    unsigned long long* st = a.status + tile * bins + d;
+    if (tile == 0) {
+      atomicExch(st, kInc | (unsigned long long)tot);
+      gbase[d] = a.digit_base[d];
+    } else {
+      atomicExch(st, kAgg | (unsigned long long)tot);
+      // walk back 8 tiles per round trip (independent loads): a wave of
+      // resident tiles otherwise serializes on one load latency per tile
+      unsigned long long prefix = 0;
+      long long i = tile - 1;
+      bool done = false;
+      while (!done) {
+        unsigned long long w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          w[k] = (i - k >= 0) ? *((volatile unsigned long long*)(a.status + (i - k) * bins + d)) : kInc;
+        // common case: all 8 published their aggregate only
+        unsigned long long andw = w[0], orw = w[0], sum = w[0] & kVal;
+#pragma unroll
+        for (int k = 1; k < 8; ++k) {
+          andw &= w[k];
+          orw |= w[k];
+          sum += w[k] & kVal;
+        }
+        if ((andw >> 62) == 1ull && (orw >> 62) == 1ull) {
+          prefix += sum;
+          i -= 8;
+          continue;
+        }
+        int k = 0;
+        for (; k < 8; ++k) {
+          const unsigned long long f = w[k] >> 62;
+          if (f == 0) break;  // not published yet: re-read from this tile
+          prefix += w[k] & kVal;
+          if (f == 2) {
+            done = true;
+            break;
+          }
+        }
+        if (!done) {
+          i -= k;
+          if (k < 8) __nanosleep(32);
+        }
+      }
+      atomicExch(st, kInc | (prefix + tot));
+      gbase[d] = a.digit_base[d] + prefix;
+      CTD_CHECK(prefix + tot <= (unsigned long long)a.n);  // look-back total within the pass
+    }
+  }
+  __syncthreads();
+  // slot -> item map of the tile reordered by digit (stable)
+#pragma unroll
+  for (int r = 0; r < kOsItems; ++r) {
+    const int li = li0 + r * 32;
+    if (li < tn) {
+      const unsigned d = (jv[r] >> a.shift) & mask;
+      const unsigned pos = doff[d] + whist[warp * bins + d] + lr[r];
+      CTD_CHECK(pos < (unsigned)kOsTile);
+      sidx[pos] = (uint16_t)li;
+    }
+  }
+  __syncthreads();
+  // contiguous per-digit runs to global memory
+  for (int s = threadIdx.x; s < tn; s += blockDim.x) {
+    const int src = sidx[s];
+    const uint32_t j = sj[src];
+    const unsigned d = (j >> a.shift) & mask;
+    const unsigned long long gp = gbase[d] + (unsigned long long)(s - (int)doff[d]);
+    CTD_CHECK(gp < (unsigned long long)a.n && s >= (int)doff[d]);
+    if (a.last) {  // read next by the heads / norms (and, at C2 size, from L2)
+      a.jout[gp] = j;
+      a.rout[gp] = sr[src];
+      a.vout[gp] = sv[src];
+    } else {  // consumed by the next pass only: streaming stores
+      __stcs(a.jout + gp, j);
+      __stcs(a.rout + gp, sr[src]);
+      __stcs(a.vout + gp, sv[src]);
+    }
+  }
+}
+#else  // CTD_OS_LEGACY: register/LDG staging (round-2 A/B baseline)
 __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int bins = 1 << a.dbits;
@@ -280,6 +504,8 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
     }
   }
 }
+
+#endif  // CTD_OS_LEGACY
 
 // Fiber heads: a head where j changes.  Inside a column rows must strictly
 // ascend: equal -> duplicate coordinates, descending -> the input was not
@@ -490,10 +716,15 @@ bool matricize_onesweep(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
   const long long tiles = (nnz + kOsTile - 1) / kOsTile;
   Buf<unsigned long long> status(ctx, (size_t)tiles * bins);
   Buf<unsigned> ticket(ctx, 1);
-  const size_t smem = (size_t)kOsTile * (8 + 4 + 4) + (size_t)bins * 8 + (size_t)(kOsWarps + 1) * bins * 4;
+#ifndef CTD_OS_LEGACY
+  constexpr size_t kOsSlot = 2;  // the slot -> item map
+#else
+  constexpr size_t kOsSlot = 0;
+#endif
+  const size_t smem = (size_t)kOsTile * (8 + 4 + 4 + kOsSlot) + (size_t)bins * 8 + (size_t)(kOsWarps + 1) * bins * 4;
   static unsigned long long attr_done = 0;
   if (first_on_device(&attr_done, ctx->device)) {
-    const size_t smax = (size_t)kOsTile * 16 + ((size_t)1 << kOsMaxBits) * (8 + (kOsWarps + 1) * 4);
+    const size_t smax = (size_t)kOsTile * (16 + kOsSlot) + ((size_t)1 << kOsMaxBits) * (8 + (kOsWarps + 1) * 4);
     CUDA_OK(cudaFuncSetAttribute(k_os_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
   }
   for (int p = 0; p < npass; ++p) {
@@ -519,6 +750,7 @@ bool matricize_onesweep(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
     pa.digit_base = dbase.p + (size_t)p * bins;
     pa.status = status.p;
     pa.ticket = ticket.p;
+    pa.bulk = (((uintptr_t)(pa.first ? (const void*)c.val : (const void*)pa.vin) | (uintptr_t)pa.jin | (uintptr_t)pa.rin) & 15) == 0;
     status.zero();
     ticket.zero();
     LAUNCH(ctx, k_os_pass, (unsigned)tiles, kOsThreads, smem, pa);
