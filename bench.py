@@ -322,7 +322,7 @@ def run_c4(args, ctx, torch):
     val_t = torch.from_numpy(x.val).to(dev)
     dt = api.DeviceTensor.from_device_ptrs(x.shape, x.nnz, [idx_t[k].data_ptr() for k in range(3)],
                                            val_t.data_ptr(), ctx)
-    ms, info, phases, launches = _time_frontend(ctx, dt, C4, max(1, min(args.steps, 3)), 2, torch)
+    ms, info, phases, launches = _time_frontend(ctx, dt, C4, max(1, min(args.steps, 3)), 3, torch)
     out = {"workload": "C4: CTD-S on 1000x1000x100 at 10% density, planted rank-20 CP + N(0,0.01^2) "
                        "(non-integer fp64), c=5000, eps=1e-6, mode 0",
            "nnz": x.nnz, "ms_per_step": round(ms, 3), "nnz_per_s": round(x.nnz / (ms / 1e3), 1),
@@ -876,6 +876,10 @@ def run_ours(args, rank, world, local_rank):
 
     c4 = c5 = full = None
     if rank == 0 and world == 1 and not args.no_c4:
+        # the C3 stream's record arena (tens of GB) goes back to the driver first:
+        # a cudaFree of that size still in progress stalls C4's first allocations
+        ctx.trim()
+        torch.cuda.synchronize()
         c4 = run_c4(args, ctx, torch)
         try:
             full = run_full_ctd_s(args, ctx, torch)

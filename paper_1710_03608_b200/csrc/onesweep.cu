@@ -128,7 +128,9 @@ struct PassArgs {
   const unsigned long long* digit_base;  // [bins] global start of each digit
   unsigned long long* status;            // [tiles][bins] look-back words
   unsigned* ticket;
-  int bulk;  // every source array 16-byte aligned: full tiles arrive by bulk copy
+  int bulk;  // 1: every source array 16-byte aligned, full tiles arrive by bulk copy; 2: also the COO index columns
+  int ka, kb;     // first pass, order 3: the two non-mode coordinates, j = i_ka + i_kb * mulb
+  uint32_t mulb;
 };
 
 #ifndef CTD_OS_LEGACY
@@ -180,20 +182,28 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
     const long long st0 = t0 * kOsTile;
     if (a.bulk && a.n - st0 >= kOsTile) {
       os_mbar_init(&s_bar, 1);
-      os_mbar_expect_tx(&s_bar, a.first ? kOsTile * 8u : kOsTile * 16u);
-      os_bulk_load(sv, (a.first ? a.c.val : a.vin) + st0, kOsTile * 8u, &s_bar);
+      const bool c3 = a.first && a.bulk == 2;  // order-3 COO: the index columns come by bulk copy too
+      os_mbar_expect_tx(&s_bar, a.first ? (c3 ? kOsTile * 12u : kOsTile * 8u) : kOsTile * 16u);
+      if (!c3) os_bulk_load(sv, (a.first ? a.c.val : a.vin) + st0, kOsTile * 8u, &s_bar);
       if (!a.first) {
         os_bulk_load(sj, a.jin + st0, kOsTile * 4u, &s_bar);
         os_bulk_load(sr, a.rin + st0, kOsTile * 4u, &s_bar);
+      } else if (c3) {
+        os_bulk_load(sr, a.c.idx[a.c.mode] + st0, kOsTile * 4u, &s_bar);
+        os_bulk_load(sj, a.c.idx[a.ka] + st0, kOsTile * 4u, &s_bar);
+        os_bulk_load(sv, a.c.idx[a.kb] + st0, kOsTile * 4u, &s_bar);  // parked in the value area; values follow
       }
     }
   }
+  // (the counters are cleared while thread 0's ticket and copies are in flight;
+  // scalar stores: 16-byte zeroing measured slower at C5, 15.2 vs 13.5 ms per pass)
   for (int t = threadIdx.x; t < kOsWarps * bins; t += blockDim.x) whist[t] = 0u;
   __syncthreads();
   const long long tile = s_tile;
   const long long start = tile * kOsTile;
   const int tn = (int)min((long long)kOsTile, a.n - start);
   const bool bulk = a.bulk && tn == kOsTile;
+  const bool c3 = bulk && a.first && a.bulk == 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned mask = (unsigned)bins - 1u;
   unsigned* wh = whist + warp * bins;
@@ -202,7 +212,29 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
   // warp w owns the contiguous items [w*256, w*256+256) of the tile, 32 per
   // round: ranks follow the item order (stable).
   const int li0 = warp * (32 * kOsItems) + lane;
-  if (a.first) {
+  if (c3) {
+    // j = i_a + i_b * shape_a (fiber_strides, tensor_ops.cpp:106-116; < 2^32)
+    // (one warp polls the mbarrier, the others sleep at the CTA barrier: 512
+    // polling threads cost the co-resident CTA its issue slots)
+    if (warp == 0) os_mbar_wait(&s_bar, 0);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kOsItems; ++r) {
+      const int li = li0 + r * 32;
+      jv[r] = sj[li] + reinterpret_cast<const uint32_t*>(sv)[li] * a.mulb;
+      sj[li] = jv[r];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // the values, second phase of the mbarrier (waited for before the write-out)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      os_mbar_expect_tx(&s_bar, kOsTile * 8u);
+      os_bulk_load(sv, a.c.val + start, kOsTile * 8u, &s_bar);
+    }
+  } else if (bulk) {
+    if (warp == 0) os_mbar_wait(&s_bar, 0);
+    __syncthreads();
+  }
+  if (a.first && !c3) {
     // keys and rows from the COO's index columns (all rounds in flight)
 #pragma unroll
     for (int r = 0; r < kOsItems; ++r) {
@@ -219,7 +251,7 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
     }
     if (!bulk)
       for (int s = threadIdx.x; s < tn; s += blockDim.x) sv[s] = __ldcs(a.c.val + start + s);
-  } else if (!bulk) {
+  } else if (!a.first && !bulk) {
     for (int s = threadIdx.x; s < tn; s += blockDim.x) {
       sj[s] = __ldcs(a.jin + start + s);
       sr[s] = __ldcs(a.rin + start + s);
@@ -227,7 +259,6 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
     }
     __syncthreads();
   }
-  if (bulk) os_mbar_wait(&s_bar, 0);
   if (!a.first) {
 #pragma unroll
     for (int r = 0; r < kOsItems; ++r) jv[r] = sj[li0 + r * 32];
@@ -276,7 +307,7 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
     unsigned long long* st = a.status + tile * bins + d;
     if (tile == 0) {
       atomicExch(st, kInc | (unsigned long long)tot);
-      gbase[d] = a.digit_base[d];
+      gbase[d] = a.digit_base[d] - excl;  // global start of the digit's run minus its tile offset
     } else {
       atomicExch(st, kAgg | (unsigned long long)tot);
       // walk back 8 tiles per round trip (independent loads): a wave of
@@ -318,7 +349,7 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
         }
       }
       atomicExch(st, kInc | (prefix + tot));
-      gbase[d] = a.digit_base[d] + prefix;
+      gbase[d] = a.digit_base[d] + prefix - excl;
       CTD_CHECK(prefix + tot <= (unsigned long long)a.n);  // look-back total within the pass
     }
   }
@@ -334,13 +365,14 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
       sidx[pos] = (uint16_t)li;
     }
   }
+  if (c3 && warp == 0) os_mbar_wait(&s_bar, 1);
   __syncthreads();
   // contiguous per-digit runs to global memory
   for (int s = threadIdx.x; s < tn; s += blockDim.x) {
     const int src = sidx[s];
     const uint32_t j = sj[src];
     const unsigned d = (j >> a.shift) & mask;
-    const unsigned long long gp = gbase[d] + (unsigned long long)(s - (int)doff[d]);
+    const unsigned long long gp = gbase[d] + (unsigned long long)s;
     CTD_CHECK(gp < (unsigned long long)a.n && s >= (int)doff[d]);
     if (a.last) {  // read next by the heads / norms (and, at C2 size, from L2)
       a.jout[gp] = j;
@@ -598,9 +630,18 @@ __global__ void k_os_norms(const int64_t* fptr, const long long* F_in, const dou
 
 // A warp per listed fiber: 32 values loaded per round (the next round's in
 // flight), then added in order by every lane through shuffles.
+// Integer-exact tensors (every |v| <= 2^26 integral and sum v^2 < 2^52, from
+// k_os_hist): every partial sum of squares is an exactly representable
+// integer, so ANY summation order gives the reference's sequential result bit
+// for bit; the mid / long kernels then reduce in parallel.
+__device__ __forceinline__ bool os_int_exact(const int* intok, const double* sumsq) {
+  return intok != nullptr && *intok != 0 && *sumsq < 4503599627370496.0;
+}
+
 __global__ void k_os_norms_mid(const int64_t* fptr, const int* list, const int* nlist, const double* val,
-                               double* norm, int* longl, int* nlong) {
+                               double* norm, int* longl, int* nlong, const int* intok, const double* sumsq) {
   const int nl = *nlist;
+  const bool exact = os_int_exact(intok, sumsq);
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -609,6 +650,21 @@ __global__ void k_os_norms_mid(const int64_t* fptr, const int* list, const int* 
     const long long b = fptr[f], e = fptr[f + 1];
     if (e - b > kOsLong) {
       if (lane == 0) longl[atomicAdd(nlong, 1)] = (int)f;
+      continue;
+    }
+    if (exact) {
+      double p = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+      long long q = b + lane;
+      for (; q + 96 < e; q += 128) {  // four loads in flight per lane
+        const double v0 = val[q], v1 = val[q + 32], v2 = val[q + 64], v3 = val[q + 96];
+        p = dadd(p, dsqr(v0));
+        p1 = dadd(p1, dsqr(v1));
+        p2 = dadd(p2, dsqr(v2));
+        p3 = dadd(p3, dsqr(v3));
+      }
+      for (; q < e; q += 32) p = dadd(p, dsqr(val[q]));
+      p = warp_sum(dadd(dadd(p, p1), dadd(p2, p3)));
+      if (lane == 0) norm[f] = p;
       continue;
     }
     double s = 0.0;
@@ -625,12 +681,39 @@ __global__ void k_os_norms_mid(const int64_t* fptr, const int* list, const int* 
 }
 
 __global__ void __launch_bounds__(256) k_os_norms_long(const int64_t* fptr, const int* longl, const int* nlong,
-                                                       const double* val, double* norm, unsigned* flags) {
+                                                       const double* val, double* norm, unsigned* flags,
+                                                       const int* intok, const double* sumsq) {
   __shared__ SeqSumSmem S;
+  __shared__ double s_part[8];
   const int nl = *nlong;
+  const bool exact = os_int_exact(intok, sumsq);
   for (int q = blockIdx.x; q < nl; q += gridDim.x) {
     const long long f = longl[q];
     const double* v = val + fptr[f];
+    if (exact) {
+      const long long len = fptr[f + 1] - fptr[f];
+      double p = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+      long long i = threadIdx.x;
+      const long long B = blockDim.x;
+      for (; i + 3 * B < len; i += 4 * B) {  // four loads in flight per thread
+        const double v0 = v[i], v1 = v[i + B], v2 = v[i + 2 * B], v3 = v[i + 3 * B];
+        p = dadd(p, dsqr(v0));
+        p1 = dadd(p1, dsqr(v1));
+        p2 = dadd(p2, dsqr(v2));
+        p3 = dadd(p3, dsqr(v3));
+      }
+      for (; i < len; i += B) p = dadd(p, dsqr(v[i]));
+      p = warp_sum(dadd(dadd(p, p1), dadd(p2, p3)));
+      if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = p;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = dadd(t, s_part[w]);
+        norm[f] = t;
+      }
+      __syncthreads();
+      continue;
+    }
     auto get = [v](long long i) { return dsqr(v[i]); };
     bool bad = false;
     const double s = block_exact_sum(get, fptr[f + 1] - fptr[f], S, &bad);
@@ -662,9 +745,9 @@ void fiber_norms(Ctx* ctx, Fibers& fb) {
   const unsigned ngrid = (unsigned)std::min<long long>((F + 255) / 256, (long long)ctx->sm_count * 16);
   LAUNCH(ctx, k_os_norms, ngrid, 256, 0, fb.ptr.p, dF.p, fb.val.p, fb.norm.p, midl.p, nmid.p);
   LAUNCH(ctx, k_os_norms_mid, (unsigned)ctx->sm_count * 8, 256, 0, fb.ptr.p, midl.p, nmid.p, fb.val.p, fb.norm.p,
-         longl.p, nlong.p);
+         longl.p, nlong.p, (const int*)nullptr, (const double*)nullptr);
   LAUNCH(ctx, k_os_norms_long, (unsigned)ctx->sm_count * 4, 256, 0, fb.ptr.p, longl.p, nlong.p, fb.val.p, fb.norm.p,
-         ctx->d_flags);
+         ctx->d_flags, (const int*)nullptr, (const double*)nullptr);
 }
 
 bool matricize_onesweep(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
@@ -751,6 +834,13 @@ bool matricize_onesweep(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
     pa.status = status.p;
     pa.ticket = ticket.p;
     pa.bulk = (((uintptr_t)(pa.first ? (const void*)c.val : (const void*)pa.vin) | (uintptr_t)pa.jin | (uintptr_t)pa.rin) & 15) == 0;
+    if (pa.first && pa.bulk && c.order == 3 &&
+        (((uintptr_t)c.idx[0] | (uintptr_t)c.idx[1] | (uintptr_t)c.idx[2]) & 15) == 0) {
+      pa.ka = mode == 0 ? 1 : 0;
+      pa.kb = mode == 2 ? 1 : 2;
+      pa.mulb = (uint32_t)c.shape[pa.ka];
+      pa.bulk = 2;
+    }
     status.zero();
     ticket.zero();
     LAUNCH(ctx, k_os_pass, (unsigned)tiles, kOsThreads, smem, pa);
@@ -774,9 +864,9 @@ bool matricize_onesweep(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
   const unsigned ngrid = (unsigned)std::min<long long>((nnz + 255) / 256, (long long)ctx->sm_count * 16);
   LAUNCH(ctx, k_os_norms, ngrid, 256, 0, out.ptr.p, dF.p, out.val.p, out.norm.p, midl.p, nmid.p);
   LAUNCH(ctx, k_os_norms_mid, (unsigned)ctx->sm_count * 8, 256, 0, out.ptr.p, midl.p, nmid.p, out.val.p, out.norm.p,
-         longl.p, nlong.p);
+         longl.p, nlong.p, (const int*)intok.p, (const double*)sumsq.p);
   LAUNCH(ctx, k_os_norms_long, (unsigned)ctx->sm_count * 4, 256, 0, out.ptr.p, longl.p, nlong.p, out.val.p,
-         out.norm.p, ctx->d_flags);
+         out.norm.p, ctx->d_flags, (const int*)intok.p, (const double*)sumsq.p);
   long long F = 0;
   int iok = 0;
   double ssq = 0.0;

@@ -53,6 +53,63 @@ def test_matricize_bitexact(ctx, port, name, mode):
     assert np.array_equal(m.dense_norms(), port.column_sq_norms(o))
 
 
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_matricize_wide_columns(ctx, port, mode):
+    """>= 2^17 columns in every mode: 9-bit digits, so the first onesweep pass takes
+    its order-3 path (index columns by bulk copy, j = i_a + i_b * shape_a), on
+    full tiles and a ragged tail."""
+    x = g.random_sparse([300, 400, 500], 5e-4, 21, integer=(mode == 1))
+    assert x.nnz > 3 * 4096 and x.nnz % 4096 != 0
+    m = ctd.matricize(_st(x), mode, ctx)
+    o = port.matricize(x.shape, x.flat_idx(), x.val, mode)
+    assert np.array_equal(m.dense_col_ptr(), o.col_ptr)
+    assert np.array_equal(m.row.astype(np.int64), o.row)
+    assert np.array_equal(m.val, o.val)
+    assert np.array_equal(m.dense_norms(), port.column_sq_norms(o))
+
+
+def test_norms_integer_exact_parallel(ctx, port):
+    """Integer-valued tensor with mid (33..1024) and long (> 1024) fibers: the
+    norms kernels reduce in parallel (any order is exact below 2^52) and must
+    still equal the reference's sequential sums bit for bit."""
+    x = _heavy_fibers()
+    x.val = np.floor(np.abs(x.val) * 5.0) + 1.0
+    m = ctd.matricize(_st(x), 0, ctx)
+    o = port.matricize(x.shape, x.flat_idx(), x.val, 0)
+    lens = np.diff(o.col_ptr)
+    assert (lens > 1024).any() and ((lens > 32) & (lens <= 1024)).any()
+    assert np.array_equal(m.val, o.val)
+    assert np.array_equal(m.dense_norms(), port.column_sq_norms(o))
+
+
+def test_matricize_unaligned_device_pointers(ctx, port):
+    """Borrowed device arrays that are only element-aligned (not 16 bytes): the
+    onesweep pass must take its non-bulk staging path and give the same result."""
+    import torch
+    x = CASES["c1"]()
+    dev = torch.device("cuda", 0)
+    idx = np.ascontiguousarray(x.idx.T.astype(np.int32))
+    hold = []
+    ptrs = []
+    for k in range(3):
+        t = torch.zeros(x.nnz + 1, dtype=torch.int32, device=dev)
+        t[1:] = torch.from_numpy(idx[k]).to(dev)
+        hold.append(t)
+        ptrs.append(t.data_ptr() + 4)
+    v = torch.zeros(x.nnz + 1, dtype=torch.float64, device=dev)
+    v[1:] = torch.from_numpy(x.val).to(dev)
+    torch.cuda.synchronize()
+    assert (v.data_ptr() + 8) % 16 != 0
+    d = api.DeviceTensor.from_device_ptrs(x.shape, x.nnz, ptrs, v.data_ptr() + 8, ctx)
+    for mode in (0, 1):
+        m = ctd.matricize(d, mode, ctx)
+        o = port.matricize(x.shape, x.flat_idx(), x.val, mode)
+        assert np.array_equal(m.dense_col_ptr(), o.col_ptr)
+        assert np.array_equal(m.row.astype(np.int64), o.row)
+        assert np.array_equal(m.val, o.val)
+        assert np.array_equal(m.dense_norms(), port.column_sq_norms(o))
+
+
 @pytest.mark.parametrize("name", list(CASES))
 def test_distribution_and_cdf_bitexact(ctx, port, name):
     x = CASES[name]()
