@@ -270,37 +270,83 @@ __global__ void k_gram(const int64_t* lptr_off, const int32_t* llen, const int64
 // table's columns in rank order) and warp (i, chunk) walks candidate perm[i]
 // against the 32 ranked columns j > i of the chunk.  The chain of a pair is
 // min(len) long instead of len(a); warps start at the longest i.
-__global__ void k_gram_sym(Cands c, const int32_t* perm, const double* D, long long dim, long long n,
+__global__ void __launch_bounds__(256, 4) k_gram_sym(Cands c, const int32_t* perm, const double* D, long long dim, long long n,
                            long long nbw, double* G) {
-  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long i = n - 1 - warp / nbw;
-  const long long bc = warp % nbw;
-  if (i < 0 || bc * 32 + 31 <= i) return;
+  // Chunk-major: blockIdx.y picks a PAIR of 32-column chunks (the widest-ranked,
+  // i.e. those with the most and longest partners, first) and blockIdx.x the
+  // walked fibers i < their columns, longest first.  All resident warps then
+  // gather from a few chunks (dim x 32 doubles each, 25.6 MB at C5), which
+  // stay in L2, instead of sweeping the whole table per walked fiber.
+  // The kernel is bound by L1 wavefronts (ncu at C5: l1tex 91 %, DRAM 14 %): a
+  // walked entry costs its warp-uniform row/value loads plus two wavefronts
+  // per 256-byte gather.  So a warp feeds TWO chunks from one walk, and the
+  // walked entries arrive eight at a time by 16-byte uniform loads (2 + 4
+  // wavefronts per eight entries instead of 16).
+  const long long bc1 = nbw - 1 - 2 * (long long)blockIdx.y;  // upper chunk
+  const long long bc0 = bc1 - 1;                              // lower chunk (absent when bc1 == 0)
+  const long long ni = bc1 * 32 + 31 < n ? bc1 * 32 + 31 : n;  // i < the upper chunk's last column
+  const long long i = ni - 1 - (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (i < 0) return;
+  const bool lower = bc0 >= 0 && i < bc0 * 32 + 31;  // the lower chunk has columns above i too
   const int lane = threadIdx.x & 31;
-  const long long j = bc * 32 + lane;
   const int a = perm[i];
   const long long off = c.off[a], len = c.len[a];
-  const double* Dc = D + bc * dim * 32 + lane;
-  double s = 0.0;
+  const int32_t* __restrict__ cr = c.row + off;
+  const double* __restrict__ cv = c.val + off;
+  const double* D1 = D + bc1 * dim * 32 + lane;
+  const double* D0 = lower ? D + bc0 * dim * 32 + lane : D1;
+  double s1 = 0.0, s0 = 0.0;
   long long t = 0;
-  for (; t + 8 <= len; t += 8) {
+  // entries up to the first 16-byte aligned row index; the vector loop runs only
+  // if the values are 16-byte aligned there as well (always, for the library's
+  // own 256-byte aligned arrays; else every entry takes the scalar loop)
+  const long long pre = min(len, (long long)((4 - (((uintptr_t)cr >> 2) & 3)) & 3));
+  const bool vec = (((uintptr_t)(cv + pre)) & 15) == 0;
+  for (; t < pre; ++t) {
+    const long long r = (long long)cr[t] * 32;
+    const double x = cv[t];
+    s1 = dadd(s1, dmul(x, D1[r]));
+    if (lower) s0 = dadd(s0, dmul(x, D0[r]));
+  }
+  for (; vec && t + 8 <= len; t += 8) {
     int r[8];
     double x[8], d[8];
+    const int4 ra = *reinterpret_cast<const int4*>(cr + t), rb = *reinterpret_cast<const int4*>(cr + t + 4);
+    r[0] = ra.x, r[1] = ra.y, r[2] = ra.z, r[3] = ra.w, r[4] = rb.x, r[5] = rb.y, r[6] = rb.z, r[7] = rb.w;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      r[u] = c.row[off + t + u];
-      x[u] = c.val[off + t + u];
+    for (int u = 0; u < 8; u += 2) {
+      const double2 xv = *reinterpret_cast<const double2*>(cv + t + u);
+      x[u] = xv.x, x[u + 1] = xv.y;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) d[u] = Dc[(long long)r[u] * 32];
+    for (int u = 0; u < 8; ++u) d[u] = D1[(long long)r[u] * 32];
+    if (lower) {
+      double e[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) s = dadd(s, dmul(x[u], d[u]));
+      for (int u = 0; u < 8; ++u) e[u] = D0[(long long)r[u] * 32];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s0 = dadd(s0, dmul(x[u], e[u]));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s1 = dadd(s1, dmul(x[u], d[u]));
   }
-  for (; t < len; ++t) s = dadd(s, dmul(c.val[off + t], Dc[(long long)c.row[off + t] * 32]));
-  if (j < n && j > i) {
-    const long long b = perm[j];
+  for (; t < len; ++t) {
+    const long long r = (long long)cr[t] * 32;
+    const double x = cv[t];
+    s1 = dadd(s1, dmul(x, D1[r]));
+    if (lower) s0 = dadd(s0, dmul(x, D0[r]));
+  }
+  const long long j1 = bc1 * 32 + lane;
+  if (j1 < n && j1 > i) {
+    const long long b = perm[j1];
     const long long lo = a < b ? a : b, hi = a < b ? b : a;
-    G[lo * n + hi] = s;
+    G[lo * n + hi] = s1;
+  }
+  const long long j0 = bc0 * 32 + lane;
+  if (lower && j0 > i) {
+    const long long b = perm[j0];
+    const long long lo = a < b ? a : b, hi = a < b ? b : a;
+    G[lo * n + hi] = s0;
   }
 }
 
@@ -460,8 +506,8 @@ void filter_batch(Basis& B, const Cands& c, double eps, BatchOut& out, bool want
   D.zero();
   LAUNCH(ctx, k_dense_cands, (unsigned)n, 128, 0, c, D.p, (long long)B.dim, (const int32_t*)drank.p);
   Buf<double> Gc(ctx, (size_t)n * n);
-  LAUNCH(ctx, k_gram_sym, ceil_div(n * nbw * 32, 256), 256, 0, c, (const int32_t*)dperm.p, D.p, (long long)B.dim,
-         (long long)n, nbw, Gc.p);
+  LAUNCH(ctx, k_gram_sym, dim3(ceil_div(n * 32, 256), (unsigned)((nbw + 1) / 2)), 256, 0, c, (const int32_t*)dperm.p, D.p,
+         (long long)B.dim, (long long)n, nbw, Gc.p);
   // kept fibers x candidates: warp (k, chunk of ranked columns)
   Buf<double> Gb(ctx, K0 > 0 ? (size_t)K0 * n : 1);
   if (K0 > 0)

@@ -231,8 +231,12 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_os_pass(PassArgs a) {
       os_bulk_load(sv, a.c.val + start, kOsTile * 8u, &s_bar);
     }
   } else if (bulk) {
+#ifdef CTD_OS_ALLPOLL
+    os_mbar_wait(&s_bar, 0);
+#else
     if (warp == 0) os_mbar_wait(&s_bar, 0);
     __syncthreads();
+#endif
   }
   if (a.first && !c3) {
     // keys and rows from the COO's index columns (all rounds in flight)
