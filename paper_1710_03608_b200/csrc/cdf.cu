@@ -410,18 +410,30 @@ void seq_cumsum(Ctx* ctx, const double* x, int64_t n, double* cum, double* d_tot
 // Sampling law.
 namespace {
 
+// (grid-stride; the last positive position is reduced per thread and per warp,
+// one atomicMax per warp at the end -- one per element serialises 8e7 atomics
+// on a single address at C5)
 __global__ void k_probs(const double* __restrict__ norms, long long F, const double* total,
                         double* probs, int* last_pos) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= F) return;
-  const double p = ddiv(norms[i], *total);  // sampling.cpp:29
-  probs[i] = p;
-  if (p > 0.0) atomicMax(last_pos, (int)i);
+  const double tot = *total;
+  int lp = -1;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < F;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double p = ddiv(norms[i], tot);  // sampling.cpp:29
+    probs[i] = p;
+    if (p > 0.0) lp = (int)i;  // i ascends per thread
+  }
+  lp = __reduce_max_sync(0xffffffffu, lp);
+  if ((threadIdx.x & 31) == 0 && lp >= 0) atomicMax(last_pos, lp);
 }
 
 __global__ void k_lastpos(const double* probs, long long n, int* last_pos) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && probs[i] > 0.0) atomicMax(last_pos, (int)i);
+  int lp = -1;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (probs[i] > 0.0) lp = (int)i;
+  lp = __reduce_max_sync(0xffffffffu, lp);
+  if ((threadIdx.x & 31) == 0 && lp >= 0) atomicMax(last_pos, lp);
 }
 
 __global__ void k_clamp(double* cum, long long F, const int* last_pos, unsigned* flags) {
@@ -442,7 +454,7 @@ void sampling_law(Ctx* ctx, const double* norms, int64_t F, double* d_total, dou
   seq_cumsum(ctx, norms, F, scratch.p, d_total);  // T: sequential over columns
   Buf<int> lp(ctx, 1);
   CUDA_OK(cudaMemsetAsync(lp.p, 0xff, sizeof(int), ctx->stream));
-  if (F > 0) LAUNCH(ctx, k_probs, ceil_div(F, 256), 256, 0, norms, (long long)F, d_total, probs, lp.p);
+  if (F > 0) LAUNCH(ctx, k_probs, std::min<unsigned>(ceil_div(F, 256), (unsigned)ctx->sm_count * 16), 256, 0, norms, (long long)F, d_total, probs, lp.p);
   Buf<double> t2(ctx, 1);
   seq_cumsum(ctx, probs, F, cum, t2.p);
   LAUNCH(ctx, k_clamp, ceil_div(F > 0 ? F : 1, 256), 256, 0, cum, (long long)F, lp.p, d_law_flags);
@@ -451,7 +463,7 @@ void sampling_law(Ctx* ctx, const double* norms, int64_t F, double* d_total, dou
 void probs_from_norms(Ctx* ctx, const double* norms, int64_t F, const double* d_total, double* probs,
                       int* d_last_pos) {
   CUDA_OK(cudaMemsetAsync(d_last_pos, 0xff, sizeof(int), ctx->stream));
-  if (F > 0) LAUNCH(ctx, k_probs, ceil_div(F, 256), 256, 0, norms, (long long)F, d_total, probs, d_last_pos);
+  if (F > 0) LAUNCH(ctx, k_probs, std::min<unsigned>(ceil_div(F, 256), (unsigned)ctx->sm_count * 16), 256, 0, norms, (long long)F, d_total, probs, d_last_pos);
 }
 
 void clamp_from(Ctx* ctx, double* cum, int64_t n, const int* d_last_pos) {
@@ -465,7 +477,7 @@ void clamped_cdf(Ctx* ctx, const double* probs, int64_t n, double* cum, unsigned
   CUDA_OK(cudaMemsetAsync(lp.p, 0xff, sizeof(int), ctx->stream));
   Buf<double> t(ctx, 1);
   seq_cumsum(ctx, probs, n, cum, t.p);
-  if (n > 0) LAUNCH(ctx, k_lastpos, ceil_div(n, 256), 256, 0, probs, (long long)n, lp.p);
+  if (n > 0) LAUNCH(ctx, k_lastpos, std::min<unsigned>(ceil_div(n, 256), (unsigned)ctx->sm_count * 16), 256, 0, probs, (long long)n, lp.p);
   LAUNCH(ctx, k_clamp, ceil_div(n > 0 ? n : 1, 256), 256, 0, cum, (long long)n, lp.p, d_flags);
 }
 

@@ -620,12 +620,23 @@ __global__ void k_os_heads_write(const uint32_t* j, long long n, const unsigned 
 __global__ void k_os_norms(const int64_t* fptr, const long long* F_in, const double* val, double* norm, int* midl,
                            int* nmid) {
   const long long F = *F_in;
-  for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < F; f += (long long)gridDim.x * blockDim.x) {
-    const long long b = fptr[f], e = fptr[f + 1];
-    if (e - b > kOsShort) {
-      midl[atomicAdd(nmid, 1)] = (int)f;
-      continue;
+  const int lane = threadIdx.x & 31;
+  // whole warps iterate together: the list of longer fibers is appended to once
+  // per warp (one atomic per listed fiber serialises on nmid at C5)
+  for (long long f0 = (long long)blockIdx.x * blockDim.x + threadIdx.x - lane; f0 < F;
+       f0 += (long long)gridDim.x * blockDim.x) {
+    const long long f = f0 + lane;
+    const bool valid = f < F;
+    const long long b = valid ? fptr[f] : 0, e = valid ? fptr[f + 1] : 0;
+    const bool mid = e - b > kOsShort;
+    const unsigned m = __ballot_sync(0xffffffffu, mid);
+    if (m) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(nmid, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (mid) midl[base + __popc(m & ((1u << lane) - 1u))] = (int)f;
     }
+    if (!valid || mid) continue;
     double s = 0.0;
     for (long long q = b; q < e; ++q) s = dadd(s, dsqr(val[q]));
     norm[f] = s;
@@ -634,24 +645,39 @@ __global__ void k_os_norms(const int64_t* fptr, const long long* F_in, const dou
 
 // A warp per listed fiber: 32 values loaded per round (the next round's in
 // flight), then added in order by every lane through shuffles.
-// Integer-exact tensors (every |v| <= 2^26 integral and sum v^2 < 2^52, from
-// k_os_hist): every partial sum of squares is an exactly representable
-// integer, so ANY summation order gives the reference's sequential result bit
-// for bit; the mid / long kernels then reduce in parallel.
-__device__ __forceinline__ bool os_int_exact(const int* intok, const double* sumsq) {
-  return intok != nullptr && *intok != 0 && *sumsq < 4503599627370496.0;
-}
+// Integer tensors (every |v| <= 2^26 and integral, from k_os_hist): squares are
+// exact integers, and because they are non-negative every partial sum in ANY
+// order is at most the fiber's total.  A fiber whose parallel sum comes out
+// below 2^52 therefore had only exactly representable partial sums: the
+// result equals the reference's sequential sum bit for bit.  (A true total of
+// 2^52 or more cannot round to less, so such fibers are always caught and take
+// the sequential path.)  The tensor-wide sum of squares need not be small:
+// C5's is ~1e16, its heaviest fiber's ~1e13.
+constexpr double kOsExactLimit = 4503599627370496.0;  // 2^52
+__device__ __forceinline__ bool os_int_exact(const int* intok) { return intok != nullptr && *intok != 0; }
 
 __global__ void k_os_norms_mid(const int64_t* fptr, const int* list, const int* nlist, const double* val,
-                               double* norm, int* longl, int* nlong, const int* intok, const double* sumsq) {
+                               double* norm, int* longl, int* nlong, const int* intok) {
   const int nl = *nlist;
-  const bool exact = os_int_exact(intok, sumsq);
+  const bool exact = os_int_exact(intok);
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
+  // the next fiber's bounds are fetched while this one is summed (list -> ptr ->
+  // values is three dependent latencies per fiber otherwise)
+  long long fn = 0, bn = 0, en = 0;
+  if (warp < nl) {
+    fn = list[warp];
+    bn = fptr[fn];
+    en = fptr[fn + 1];
+  }
   for (long long q0 = warp; q0 < nl; q0 += nw) {
-    const long long f = list[q0];
-    const long long b = fptr[f], e = fptr[f + 1];
+    const long long f = fn, b = bn, e = en;
+    if (q0 + nw < nl) {
+      fn = list[q0 + nw];
+      bn = fptr[fn];
+      en = fptr[fn + 1];
+    }
     if (e - b > kOsLong) {
       if (lane == 0) longl[atomicAdd(nlong, 1)] = (int)f;
       continue;
@@ -668,8 +694,10 @@ __global__ void k_os_norms_mid(const int64_t* fptr, const int* list, const int* 
       }
       for (; q < e; q += 32) p = dadd(p, dsqr(val[q]));
       p = warp_sum(dadd(dadd(p, p1), dadd(p2, p3)));
-      if (lane == 0) norm[f] = p;
-      continue;
+      if (p < kOsExactLimit) {  // warp-uniform
+        if (lane == 0) norm[f] = p;
+        continue;
+      }
     }
     double s = 0.0;
     double cur = (b + lane < e) ? val[b + lane] : 0.0;
@@ -684,40 +712,52 @@ __global__ void k_os_norms_mid(const int64_t* fptr, const int* list, const int* 
   }
 }
 
+// Integer-exact long fibers (see os_int_exact): a block per fiber, any order.
+__global__ void __launch_bounds__(256, 8) k_os_norms_long_int(const int64_t* fptr, const int* longl, const int* nlong,
+                                                              const double* val, double* norm, const int* intok,
+                                                              int* longl2, int* nlong2) {
+  __shared__ double s_part[2][8];
+  if (!os_int_exact(intok)) return;
+  const int nl = *nlong;
+  int par = 0;
+  for (int q = blockIdx.x; q < nl; q += gridDim.x, par ^= 1) {
+    const long long f = longl[q];
+    const long long b = fptr[f], len = fptr[f + 1] - b;
+    const double* v = val + b;
+    double p = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+    long long i = threadIdx.x;
+    const long long B = blockDim.x;
+    for (; i + 3 * B < len; i += 4 * B) {  // four loads in flight per thread
+      const double v0 = v[i], v1 = v[i + B], v2 = v[i + 2 * B], v3 = v[i + 3 * B];
+      p = dadd(p, dsqr(v0));
+      p1 = dadd(p1, dsqr(v1));
+      p2 = dadd(p2, dsqr(v2));
+      p3 = dadd(p3, dsqr(v3));
+    }
+    for (; i < len; i += B) p = dadd(p, dsqr(v[i]));
+    p = warp_sum(dadd(dadd(p, p1), dadd(p2, p3)));
+    if ((threadIdx.x & 31) == 0) s_part[par][threadIdx.x >> 5] = p;
+    __syncthreads();  // (the slots alternate, so one barrier per fiber is enough)
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = dadd(t, s_part[par][w]);
+      if (t < kOsExactLimit) norm[f] = t;
+      else longl2[atomicAdd(nlong2, 1)] = (int)f;  // sequential path (k_os_norms_long)
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_os_norms_long(const int64_t* fptr, const int* longl, const int* nlong,
                                                        const double* val, double* norm, unsigned* flags,
-                                                       const int* intok, const double* sumsq) {
+                                                       const int* intok, const int* longl2, const int* nlong2) {
   __shared__ SeqSumSmem S;
-  __shared__ double s_part[8];
-  const int nl = *nlong;
-  const bool exact = os_int_exact(intok, sumsq);
+  // integer tensors: only the fibers k_os_norms_long_int passed on
+  const bool ints = os_int_exact(intok);
+  if (ints) longl = longl2;
+  const int nl = ints ? *nlong2 : *nlong;
   for (int q = blockIdx.x; q < nl; q += gridDim.x) {
     const long long f = longl[q];
     const double* v = val + fptr[f];
-    if (exact) {
-      const long long len = fptr[f + 1] - fptr[f];
-      double p = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-      long long i = threadIdx.x;
-      const long long B = blockDim.x;
-      for (; i + 3 * B < len; i += 4 * B) {  // four loads in flight per thread
-        const double v0 = v[i], v1 = v[i + B], v2 = v[i + 2 * B], v3 = v[i + 3 * B];
-        p = dadd(p, dsqr(v0));
-        p1 = dadd(p1, dsqr(v1));
-        p2 = dadd(p2, dsqr(v2));
-        p3 = dadd(p3, dsqr(v3));
-      }
-      for (; i < len; i += B) p = dadd(p, dsqr(v[i]));
-      p = warp_sum(dadd(dadd(p, p1), dadd(p2, p3)));
-      if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = p;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = dadd(t, s_part[w]);
-        norm[f] = t;
-      }
-      __syncthreads();
-      continue;
-    }
     auto get = [v](long long i) { return dsqr(v[i]); };
     bool bad = false;
     const double s = block_exact_sum(get, fptr[f + 1] - fptr[f], S, &bad);
@@ -749,9 +789,9 @@ void fiber_norms(Ctx* ctx, Fibers& fb) {
   const unsigned ngrid = (unsigned)std::min<long long>((F + 255) / 256, (long long)ctx->sm_count * 16);
   LAUNCH(ctx, k_os_norms, ngrid, 256, 0, fb.ptr.p, dF.p, fb.val.p, fb.norm.p, midl.p, nmid.p);
   LAUNCH(ctx, k_os_norms_mid, (unsigned)ctx->sm_count * 8, 256, 0, fb.ptr.p, midl.p, nmid.p, fb.val.p, fb.norm.p,
-         longl.p, nlong.p, (const int*)nullptr, (const double*)nullptr);
+         longl.p, nlong.p, (const int*)nullptr);
   LAUNCH(ctx, k_os_norms_long, (unsigned)ctx->sm_count * 4, 256, 0, fb.ptr.p, longl.p, nlong.p, fb.val.p, fb.norm.p,
-         ctx->d_flags, (const int*)nullptr, (const double*)nullptr);
+         ctx->d_flags, (const int*)nullptr, (const int*)nullptr, (const int*)nullptr);
 }
 
 bool matricize_onesweep(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
@@ -863,14 +903,18 @@ bool matricize_onesweep(Ctx* ctx, const Tensor& x, int mode, Fibers& out) {
   LAUNCH(ctx, k_os_scan_blocks, 1, 1024, 0, bcnt.p, hb, bbase.p, dF.p, out.ptr.p, nnz);
   LAUNCH(ctx, k_os_heads_write, (unsigned)hb, 256, 0, jf, nnz, bbase.p, out.col.p, out.ptr.p);
   Buf<int> midl(ctx, nnz / kOsShort + 2), nmid(ctx, 1), longl(ctx, nnz / kOsLong + 2), nlong(ctx, 1);
+  Buf<int> longl2(ctx, nnz / kOsLong + 2), nlong2(ctx, 1);
   nmid.zero();
   nlong.zero();
+  nlong2.zero();
   const unsigned ngrid = (unsigned)std::min<long long>((nnz + 255) / 256, (long long)ctx->sm_count * 16);
   LAUNCH(ctx, k_os_norms, ngrid, 256, 0, out.ptr.p, dF.p, out.val.p, out.norm.p, midl.p, nmid.p);
   LAUNCH(ctx, k_os_norms_mid, (unsigned)ctx->sm_count * 8, 256, 0, out.ptr.p, midl.p, nmid.p, out.val.p, out.norm.p,
-         longl.p, nlong.p, (const int*)intok.p, (const double*)sumsq.p);
+         longl.p, nlong.p, (const int*)intok.p);
+  LAUNCH(ctx, k_os_norms_long_int, (unsigned)ctx->sm_count * 8, 256, 0, out.ptr.p, longl.p, nlong.p, out.val.p,
+         out.norm.p, (const int*)intok.p, longl2.p, nlong2.p);
   LAUNCH(ctx, k_os_norms_long, (unsigned)ctx->sm_count * 4, 256, 0, out.ptr.p, longl.p, nlong.p, out.val.p,
-         out.norm.p, ctx->d_flags, (const int*)intok.p, (const double*)sumsq.p);
+         out.norm.p, ctx->d_flags, (const int*)intok.p, (const int*)longl2.p, (const int*)nlong2.p);
   long long F = 0;
   int iok = 0;
   double ssq = 0.0;

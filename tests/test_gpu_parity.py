@@ -82,6 +82,21 @@ def test_norms_integer_exact_parallel(ctx, port):
     assert np.array_equal(m.dense_norms(), port.column_sq_norms(o))
 
 
+def test_norms_integer_large_take_sequential_path(ctx, port):
+    """Integer values near 2^26: a fiber's sum of squares passes 2^52 after two
+    entries, so partial sums round and only the reference's order gives its
+    bits; the parallel reduction must detect that per fiber and fall back."""
+    x = _heavy_fibers()
+    x.val = 67108864.0 - np.floor(np.abs(x.val) * 1000.0) % 4096.0
+    assert (x.val == np.rint(x.val)).all() and x.val.max() <= 67108864.0 and x.val.min() >= 1.0
+    m = ctd.matricize(_st(x), 0, ctx)
+    o = port.matricize(x.shape, x.flat_idx(), x.val, 0)
+    ref = port.column_sq_norms(o)
+    assert (ref >= 2.0 ** 52).any()
+    assert np.array_equal(m.val, o.val)
+    assert np.array_equal(m.dense_norms(), ref)
+
+
 def test_matricize_unaligned_device_pointers(ctx, port):
     """Borrowed device arrays that are only element-aligned (not 16 bytes): the
     onesweep pass must take its non-bulk staging path and give the same result."""
