@@ -870,16 +870,11 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(x)
 
-    ctdd = None
-    if rank == 0 and world == 1 and not args.no_ctdd:
-        ctdd = run_ctd_d(args, ctx, torch)
-
+    # The C3 stream runs last: its record arena (tens of GB, chunks allocated on a
+    # helper thread) going back to the driver stalls whatever allocates next
+    # (measured: C4 filter prep 1.4 -> 7 ms, C5 step + 300 ms when they followed it)
     c4 = c5 = full = None
     if rank == 0 and world == 1 and not args.no_c4:
-        # the C3 stream's record arena (tens of GB) goes back to the driver first:
-        # a cudaFree of that size still in progress stalls C4's first allocations
-        ctx.trim()
-        torch.cuda.synchronize()
         c4 = run_c4(args, ctx, torch)
         try:
             full = run_full_ctd_s(args, ctx, torch)
@@ -891,6 +886,11 @@ def run_ours(args, rank, world, local_rank):
         ctx.trim()  # the library's cached blocks back to the driver for the C5 generator
         torch.cuda.empty_cache()
         c5 = run_c5(args, ctx, torch)
+        ctx.trim()
+        torch.cuda.empty_cache()
+    ctdd = None
+    if rank == 0 and world == 1 and not args.no_ctdd:
+        ctdd = run_ctd_d(args, ctx, torch)
 
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
@@ -944,10 +944,12 @@ def run_e2e(args, ctx, x, torch):
     c, eps, seed, mode = C2["c"], C2["eps"], C2["seed"], C2["mode"]
     shape = np.asarray(x.shape, dtype=np.int64)
 
+    u_h = torch.empty(c * c, dtype=torch.float64).pin_memory().numpy()   # the caller's result buffer
+
     def step():
         t = api.DeviceTensor.from_host_ptrs(x.shape, nnz, idx_h.data_ptr(), val_h.data_ptr(), ctx)
         h, info = api.ctd_s_raw(t, mode, c, eps, seed, with_error=False, ctx=ctx)
-        kept, u = api.factors_result(ctx, h, info)   # D2H: kept ids + U
+        kept, u = api.factors_result(ctx, h, info, u_out=u_h)   # D2H: kept ids + U
         api.free_factors(ctx, h)
         t.close()
         return info, kept, u

@@ -632,12 +632,20 @@ def factors_trace(ctx: Context, h, info) -> dict:
             "r_rows": rows[:int(cp[-1])]}
 
 
-def factors_result(ctx: Context, h, info):
-    """The decomposition's result on the host: kept fiber ids and U."""
+def factors_result(ctx: Context, h, info, u_out=None):
+    """The decomposition's result on the host: kept fiber ids and U.  `u_out`: a
+    caller-owned float64 array of at least kept^2 elements to receive U (e.g. a
+    view of pinned memory, which the copy then reaches directly)."""
     k = info.kept
     kept = np.zeros(max(k, 1), dtype=np.int64)
     _check(ctx.L.ctd_gpu_factors_kept_flat(h, _p(kept)))
-    u = np.zeros(max(k * k, 1))
+    if u_out is None:
+        u = np.empty(max(k * k, 1))
+    else:
+        u = u_out
+        if u.dtype != np.float64 or not u.flags.c_contiguous or u.size < max(k * k, 1):
+            raise ValueError("u_out must be a contiguous float64 array of at least kept^2 elements")
+        u = u.reshape(-1)
     _check(ctx.L.ctd_gpu_factors_u(h, _p(u)))
     return kept[:k], u[:k * k].reshape(k, k)
 
