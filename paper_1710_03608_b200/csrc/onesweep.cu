@@ -78,27 +78,8 @@ __global__ void k_os_hist(Coo c, int npass, int dbits, unsigned long long* hist,
   __syncthreads();
   double sq = 0.0;
   bool iok = true, oobf = false, zf = false;
-  // two entries per thread per round (their loads in flight together: one entry
-  // is 20 bytes per thread, too little outstanding to cover HBM latency at C5)
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + stride < c.nnz; i += 2 * stride) {
-    int row0, row1;
-    bool oob0, oob1;
-    const uint32_t j0 = coo_col(c, i, &row0, &oob0);
-    const uint32_t j1 = coo_col(c, i + stride, &row1, &oob1);
-    const double v0 = c.val[i], v1 = c.val[i + stride];
-    oobf |= oob0 | oob1;
-    zf |= (v0 == 0.0) | (v1 == 0.0);
-    iok &= (v0 == rint(v0)) && (fabs(v0) <= 67108864.0) && (v1 == rint(v1)) && (fabs(v1) <= 67108864.0);
-    sq += v0 * v0;
-    sq += v1 * v1;
-    for (int p = 0; p < npass; ++p) {
-      atomicAdd(&sh[p * bins + ((j0 >> (p * dbits)) & (bins - 1))], 1u);
-      atomicAdd(&sh[p * bins + ((j1 >> (p * dbits)) & (bins - 1))], 1u);
-    }
-  }
-  if (i < c.nnz) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < c.nnz;
+       i += (long long)gridDim.x * blockDim.x) {
     int row;
     bool oob;
     const uint32_t j = coo_col(c, i, &row, &oob);
