@@ -270,7 +270,7 @@ __global__ void k_gram(const int64_t* lptr_off, const int32_t* llen, const int64
 // table's columns in rank order) and warp (i, chunk) walks candidate perm[i]
 // against the 32 ranked columns j > i of the chunk.  The chain of a pair is
 // min(len) long instead of len(a); warps start at the longest i.
-__global__ void __launch_bounds__(256, 4) k_gram_sym(Cands c, const int32_t* perm, const double* D, long long dim, long long n,
+__global__ void __launch_bounds__(256, 3) k_gram_sym(Cands c, const int32_t* perm, const double* D, long long dim, long long n,
                            long long nbw, double* G) {
   // Chunk-major: blockIdx.y picks a PAIR of 32-column chunks (the widest-ranked,
   // i.e. those with the most and longest partners, first) and blockIdx.x the
@@ -296,45 +296,39 @@ __global__ void __launch_bounds__(256, 4) k_gram_sym(Cands c, const int32_t* per
   const double* D1 = D + bc1 * dim * 32 + lane;
   const double* D0 = lower ? D + bc0 * dim * 32 + lane : D1;
   double s1 = 0.0, s0 = 0.0;
-  long long t = 0;
-  // entries up to the first 16-byte aligned row index; the vector loop runs only
-  // if the values are 16-byte aligned there as well (always, for the library's
-  // own 256-byte aligned arrays; else every entry takes the scalar loop)
-  const long long pre = min(len, (long long)((4 - (((uintptr_t)cr >> 2) & 3)) & 3));
-  const bool vec = (((uintptr_t)(cv + pre)) & 15) == 0;
-  for (; t < pre; ++t) {
-    const long long r = (long long)cr[t] * 32;
-    const double x = cv[t];
-    s1 = dadd(s1, dmul(x, D1[r]));
-    if (lower) s0 = dadd(s0, dmul(x, D0[r]));
-  }
-  for (; vec && t + 8 <= len; t += 8) {
-    int r[8];
-    double x[8], d[8];
-    const int4 ra = *reinterpret_cast<const int4*>(cr + t), rb = *reinterpret_cast<const int4*>(cr + t + 4);
-    r[0] = ra.x, r[1] = ra.y, r[2] = ra.z, r[3] = ra.w, r[4] = rb.x, r[5] = rb.y, r[6] = rb.z, r[7] = rb.w;
+  // 32 walked entries per round: lane u loads entry t + u (coalesced), and the
+  // entries reach every lane in order by shuffles, eight gathers in flight per chunk
+  for (long long t = 0; t < len; t += 32) {
+    const int rem = (int)min(32ll, len - t);
+    const int rl = lane < rem ? cr[t + lane] : 0;
+    const double xl = lane < rem ? cv[t + lane] : 0.0;
+    int u0 = 0;
+    for (; u0 + 8 <= rem; u0 += 8) {
+      int r[8];
+      double x[8], d[8];
 #pragma unroll
-    for (int u = 0; u < 8; u += 2) {
-      const double2 xv = *reinterpret_cast<const double2*>(cv + t + u);
-      x[u] = xv.x, x[u + 1] = xv.y;
+      for (int u = 0; u < 8; ++u) {
+        r[u] = __shfl_sync(0xffffffffu, rl, u0 + u);
+        x[u] = __shfl_sync(0xffffffffu, xl, u0 + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) d[u] = D1[(long long)r[u] * 32];
+      if (lower) {
+        double e[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) e[u] = D0[(long long)r[u] * 32];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s0 = dadd(s0, dmul(x[u], e[u]));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s1 = dadd(s1, dmul(x[u], d[u]));
     }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) d[u] = D1[(long long)r[u] * 32];
-    if (lower) {
-      double e[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) e[u] = D0[(long long)r[u] * 32];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) s0 = dadd(s0, dmul(x[u], e[u]));
+    for (; u0 < rem; ++u0) {
+      const long long r = (long long)__shfl_sync(0xffffffffu, rl, u0) * 32;
+      const double x = __shfl_sync(0xffffffffu, xl, u0);
+      s1 = dadd(s1, dmul(x, D1[r]));
+      if (lower) s0 = dadd(s0, dmul(x, D0[r]));
     }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s1 = dadd(s1, dmul(x[u], d[u]));
-  }
-  for (; t < len; ++t) {
-    const long long r = (long long)cr[t] * 32;
-    const double x = cv[t];
-    s1 = dadd(s1, dmul(x, D1[r]));
-    if (lower) s0 = dadd(s0, dmul(x, D0[r]));
   }
   const long long j1 = bc1 * 32 + lane;
   if (j1 < n && j1 > i) {
