@@ -277,11 +277,11 @@ __global__ void __launch_bounds__(256, 3) k_gram_sym(Cands c, const int32_t* per
   // walked fibers i < their columns, longest first.  All resident warps then
   // gather from a few chunks (dim x 32 doubles each, 25.6 MB at C5), which
   // stay in L2, instead of sweeping the whole table per walked fiber.
-  // The kernel is bound by L1 wavefronts (ncu at C5: l1tex 91 %, DRAM 14 %): a
-  // walked entry costs its warp-uniform row/value loads plus two wavefronts
-  // per 256-byte gather.  So a warp feeds TWO chunks from one walk, and the
-  // walked entries arrive eight at a time by 16-byte uniform loads (2 + 4
-  // wavefronts per eight entries instead of 16).
+  // The kernel is bound by L1 wavefronts / LSU write-back (ncu at C5: l1tex
+  // 83-91 %, DRAM 9-14 %): a walked entry costs three write-back cycles for its
+  // row and value however they reach the 32 lanes (uniform loads and shuffles
+  // measured the same) plus two per 256-byte gather.  So a warp feeds TWO
+  // chunks from one walk.
   const long long bc1 = nbw - 1 - 2 * (long long)blockIdx.y;  // upper chunk
   const long long bc0 = bc1 - 1;                              // lower chunk (absent when bc1 == 0)
   const long long ni = bc1 * 32 + 31 < n ? bc1 * 32 + 31 : n;  // i < the upper chunk's last column
